@@ -1,0 +1,145 @@
+/*
+ * boltz_cuda.h -- C ABI of the B200 (sm_100a) collision path.
+ *
+ * Drop-in boundary for the reference's per-cell collision step (SURVEY.md
+ * §8b).  Each entry point replaces one reference operation, batched over
+ * cells; no torch or C++ types cross the boundary, no exceptions escape.
+ *
+ *   reference operation                                   | entry point
+ *   ------------------------------------------------------+-------------------------------
+ *   SpectralTransform(grid)           fourier.hpp:31       | boltz_create (+ table upload)
+ *   ~SpectralTransform                fourier.hpp:32       | boltz_destroy
+ *   SpectralTransform::forward        fourier.hpp:36       | boltz_forward_batch
+ *   SpectralTransform::inverse        fourier.hpp:38-41    | boltz_inverse_batch
+ *   evaluate_qhat                     SPEC.md:186-194      | boltz_qhat_batch
+ *   conserve                          SPEC.md:204-212      | boltz_conserve_batch
+ *   collide                           SPEC.md:195-203      | boltz_collide_batch
+ *   collision_rk2                     SPEC.md:383-391      | boltz_rk2_batch
+ *   generate_table                    SPEC.md:126-134      | boltz_generate_table (host)
+ *   save_table / load_table           SPEC.md:135-143      | boltz_save_table / boltz_load_table
+ *   transport_step (+ ghost fill)     SPEC.md:342-350      | boltz_transport_step
+ *   boltz::Error{category}            errors.hpp:8-35      | return codes + boltz_last_error
+ *
+ * Layouts at the boundary are the reference's: a batch of `ncells` cells is
+ * `ncells` consecutive N^3 blocks, flat index (i1*N+i2)*N+i3
+ * (velocity_grid.hpp:30-32); complex arrays are interleaved (re, im) doubles
+ * (std::complex<double>, fourier.hpp:36).  The weight table is the dense
+ * zeta-major N^6 array G[k][m].
+ *
+ * `mem`: BOLTZ_MEM_HOST (pointers are host memory; the call copies in/out
+ * and is synchronous) or BOLTZ_MEM_DEVICE (pointers are device memory on the
+ * context's device; the call is ordered on `stream` and synchronises it
+ * before returning so that numeric errors can be reported).  `stream` may be
+ * NULL (the context's own stream).
+ *
+ * Threading mirrors SpectralTransform (fourier.hpp:24-25): a context is not
+ * thread-safe; distinct contexts may be used concurrently.
+ */
+#ifndef BOLTZ_CUDA_H
+#define BOLTZ_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes: 0 ok; 2/3/4 mirror boltz::ErrorCategory (errors.hpp:8-13) */
+#define BOLTZ_OK 0
+#define BOLTZ_ERR_CONFIG 2
+#define BOLTZ_ERR_IO 3
+#define BOLTZ_ERR_NUMERIC 4
+#define BOLTZ_ERR_CUDA 5 /* CUDA / NCCL failure (new; no reference counterpart) */
+
+#define BOLTZ_MEM_HOST 0
+#define BOLTZ_MEM_DEVICE 1
+
+typedef struct boltz_ctx boltz_ctx;
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* boltz_last_error(void);
+
+/* Library build information (compute capability, supported N list). */
+const char* boltz_build_info(void);
+
+/*
+ * Create a context on `device` for the grid (n, L) (VelocityGrid::create,
+ * velocity_grid.cpp:11-32: n even >= 4, L > 0) and kernel (lambda, beta, r0)
+ * (KernelSpec).  `G_host` is the caller's dense zeta-major
+ * table (n^6 doubles); it is COPIED (and re-laid out) into device memory and
+ * may be freed after the call.  Errors: 2 for an invalid grid/kernel or an
+ * unsupported n, 5 for CUDA failures (e.g. out of device memory).
+ */
+int boltz_create(int n, double L, double lambda, double beta, double r0, const double* G_host, int device,
+                 boltz_ctx** out);
+int boltz_destroy(boltz_ctx* ctx);
+
+/* Device bytes held by the context (folded table + workspace). */
+int boltz_memory_bytes(const boltz_ctx* ctx, int64_t* table_bytes, int64_t* workspace_bytes);
+
+/* forward: f (ncells x N^3 real) -> fhat (ncells x N^3 complex) */
+int boltz_forward_batch(boltz_ctx* ctx, const double* f, double* fhat, int64_t ncells, int mem, void* stream);
+
+/* inverse: g (complex) -> f (real); max_imag (ncells doubles, nullable) */
+int boltz_inverse_batch(boltz_ctx* ctx, const double* g, double* f, double* max_imag, int64_t ncells, int mem,
+                        void* stream);
+
+/* evaluate_qhat: fhat (complex) -> qhat (complex), raw K2 for parity tests */
+int boltz_qhat_batch(boltz_ctx* ctx, const double* fhat, double* qhat, int64_t ncells, int mem, void* stream);
+
+/* conserve: q_raw (real) -> q (real) */
+int boltz_conserve_batch(boltz_ctx* ctx, const double* q_raw, double* q, int64_t ncells, int mem, void* stream);
+
+/*
+ * collide: q = (1/eps) P_N(inverse(evaluate_qhat(forward(f)))) per cell.
+ * inv_eps = 1/epsilon.  max_imag (ncells, nullable): inverse-transform
+ * imaginary residue (fourier.hpp:38-41).  Non-finite f -> 4.
+ */
+int boltz_collide_batch(boltz_ctx* ctx, const double* f, double* q, int64_t ncells, double inv_eps,
+                        double* max_imag, int mem, void* stream);
+
+/*
+ * collision_rk2 in place: f* = f + dt/2 collide(f); f <- f + dt collide(f*).
+ * Non-finite input or stage -> 4.
+ */
+int boltz_rk2_batch(boltz_ctx* ctx, double* f, int64_t ncells, double dt, double inv_eps, int mem, void* stream);
+
+/*
+ * transport_step on a device field of (ncl + 4) cells x
+ * N^3 (2 ghost cells per side) whose ghosts are already filled
+ * (halo exchange / boltz_fill_boundary).  x_ext, dx_ext: DEVICE arrays of the
+ * ncl+4 cell centres/widths.  wall_left/right: zero slope at a wall
+ * (SPEC.md:336,359).  `out` (device, same shape) receives the updated field;
+ * its ghost cells are copied through.
+ */
+int boltz_transport_step(boltz_ctx* ctx, const double* field, double* out, int64_t ncl, const double* x_ext,
+                         const double* dx_ext, double dt, int wall_left, int wall_right, void* stream);
+
+/*
+ * Ghost fill at a physical end (side 0 = left, 1 = right) of a device field:
+ * kind 0 = linear extrapolation, kind 1 = diffuse wall with
+ * T_w, V_w.  x_ext is a DEVICE array.  sigma_w (host
+ * double, nullable) receives the wall's re-emission factor.
+ */
+int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double* x_ext, int side, int kind,
+                        double Tw, const double* Vw_host3, double* sigma_w, void* stream);
+
+/* ---- host-side weight table (the hot path's input) ---- */
+
+/* generate the dense zeta-major table (n^6 doubles) on the host; lambda in
+ * {0,1} closed form, else composite Gauss-Legendre with `panels` panels. */
+int boltz_generate_table(int n, double L, double lambda, double beta, double r0, int panels, double* G,
+                         int nthreads);
+double boltz_weight(double lambda, double beta, double r0, const double xi[3], const double zeta[3], int panels);
+
+/* cache file: header (magic, version, N, L, lambda, beta, r0, panels) + LE doubles */
+int boltz_save_table(const char* path, int n, double L, double lambda, double beta, double r0, int panels,
+                     const double* G);
+/* expected parameters must match the header exactly; G must hold n^6 doubles */
+int boltz_load_table(const char* path, int n, double L, double lambda, double beta, double r0, int panels,
+                     double* G);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BOLTZ_CUDA_H */

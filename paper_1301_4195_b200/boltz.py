@@ -1,0 +1,376 @@
+"""Python mirror of the reference's collision-path API over the C ABI.
+
+The reference is C++ (proj/include/boltz/*.hpp + SPEC.md); this module keeps
+its names, argument meanings and error categories so the parity tests and
+the benchmark read like the reference's own tests:
+
+  VelocityGrid.create(n, L)        velocity_grid.hpp:17-47 / velocity_grid.cpp:11-32
+  KernelSpec(lam, beta, r0)
+  generate_table / save_table /
+    load_table                     SPEC.md:126-143 (host, C++ in libboltz_cuda.so)
+  CollisionOperator                SpectralTransform (fourier.hpp:28-52) +
+                                   evaluate_qhat / conserve / collide
+                                   + collision_rk2, batched
+  transport_step / fill_boundary
+  ConfigError / IoError /
+    NumericError                   errors.hpp:8-35 (categories 2/3/4)
+
+Every compute call goes to libboltz_cuda.so (sm_100a kernels).  There is no
+CPU fallback: a missing library raises ImportError-like RuntimeError.
+Arrays may be numpy (host memory: the call stages H2D/D2H) or torch CUDA
+tensors (device memory: ordered on the current torch stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from .build import LIB as _LIB_PATH
+
+MEM_HOST, MEM_DEVICE = 0, 1
+
+
+class BoltzError(RuntimeError):
+    category = 0
+
+    def __init__(self, msg, category=None):
+        super().__init__(msg)
+        if category is not None:
+            self.category = category
+
+
+class ConfigError(BoltzError):
+    category = 2
+
+
+class IoError(BoltzError):
+    category = 3
+
+
+class NumericError(BoltzError):
+    category = 4
+
+
+class CudaError(BoltzError):
+    category = 5
+
+
+_ERR = {2: ConfigError, 3: IoError, 4: NumericError, 5: CudaError}
+_lib = None
+
+
+def lib():
+    """Load libboltz_cuda.so (built in-tree by paper_1301_4195_b200.build)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise RuntimeError(
+                f"{_LIB_PATH} is missing: run `python -m paper_1301_4195_b200.build` "
+                "(there is no CPU fallback for the collision path)")
+        L = C.CDLL(str(_LIB_PATH))
+        vp, i, d, i64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
+        dp = C.POINTER(C.c_double)
+        sig = {
+            "boltz_last_error": (C.c_char_p, []),
+            "boltz_build_info": (C.c_char_p, []),
+            "boltz_create": (i, [i, d, d, d, d, vp, i, C.POINTER(vp)]),
+            "boltz_destroy": (i, [vp]),
+            "boltz_memory_bytes": (i, [vp, C.POINTER(i64), C.POINTER(i64)]),
+            "boltz_forward_batch": (i, [vp, vp, vp, i64, i, vp]),
+            "boltz_inverse_batch": (i, [vp, vp, vp, vp, i64, i, vp]),
+            "boltz_qhat_batch": (i, [vp, vp, vp, i64, i, vp]),
+            "boltz_conserve_batch": (i, [vp, vp, vp, i64, i, vp]),
+            "boltz_collide_batch": (i, [vp, vp, vp, i64, d, vp, i, vp]),
+            "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
+            "boltz_transport_step": (i, [vp, vp, vp, i64, vp, vp, d, i, i, vp]),
+            "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
+            "boltz_generate_table": (i, [i, d, d, d, d, i, vp, i]),
+            "boltz_weight": (d, [d, d, d, vp, vp, i]),
+            "boltz_save_table": (i, [C.c_char_p, i, d, d, d, d, i, vp]),
+            "boltz_load_table": (i, [C.c_char_p, i, d, d, d, d, i, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc:
+        msg = lib().boltz_last_error().decode()
+        raise _ERR.get(rc, BoltzError)(msg, rc)
+
+
+# ----------------------------------------------------------------- grid
+@dataclass
+class VelocityGrid:
+    """Cubic velocity lattice + Fourier dual (velocity_grid.hpp:8-47)."""
+    n: int
+    half_width: float
+    dv: float
+    dzeta: float
+    v_nodes: np.ndarray
+    zeta_nodes: np.ndarray
+    axis_coeff: np.ndarray
+
+    @staticmethod
+    def create(n: int, half_width: float) -> "VelocityGrid":
+        # velocity_grid.cpp:11-32
+        if n < 4 or n % 2 != 0:
+            raise ConfigError(f"velocity grid: N must be even and >= 4, got {n}")
+        if not half_width > 0.0:
+            raise ConfigError(f"velocity grid: L must be positive, got {half_width}")
+        dv = 2.0 * half_width / n
+        dz = math.pi / half_width
+        k = np.arange(n)
+        coeff = np.ones(n)
+        coeff[0] = coeff[-1] = 0.5
+        return VelocityGrid(n, float(half_width), dv, dz, dv * (k - n // 2), dz * (k - n // 2), coeff)
+
+    def size(self) -> int:
+        return self.n ** 3
+
+    def flat(self, i, j, k) -> int:
+        return (i * self.n + j) * self.n + k
+
+    def coeff3(self, i, j, k) -> float:
+        return self.axis_coeff[i] * self.axis_coeff[j] * self.axis_coeff[k]
+
+    def vel_weight(self, i, j, k) -> float:
+        return self.coeff3(i, j, k) * self.dv ** 3
+
+    def fourier_weight(self, i, j, k) -> float:
+        return self.coeff3(i, j, k) * self.dzeta ** 3
+
+    def velocities(self) -> np.ndarray:
+        """(N^3, 3) node velocities in flat order."""
+        v = self.v_nodes
+        V1, V2, V3 = np.meshgrid(v, v, v, indexing="ij")
+        return np.stack([V1.ravel(), V2.ravel(), V3.ravel()], axis=1)
+
+    def vel_weights(self) -> np.ndarray:
+        c = self.axis_coeff
+        return (c[:, None, None] * c[None, :, None] * c[None, None, :]).ravel() * self.dv ** 3
+
+
+@dataclass
+class KernelSpec:
+    """Collision kernel |u|^lambda, isotropic b = 1/(4 pi)."""
+    lam: float = 1.0
+    beta: float = 1.0
+    r0: Optional[float] = None
+    panels: int = 64  # Gauss-Legendre panels for 0 < lambda < 1
+
+    def radius(self, grid: VelocityGrid) -> float:
+        return grid.half_width if self.r0 is None else self.r0  # r0 = L
+
+
+# ------------------------------------------------------------- weights
+def weight(kernel: KernelSpec, xi, zeta, r0: float) -> float:
+    xi = np.ascontiguousarray(xi, dtype=np.float64)
+    zeta = np.ascontiguousarray(zeta, dtype=np.float64)
+    return lib().boltz_weight(kernel.lam, kernel.beta, r0, xi.ctypes.data, zeta.ctypes.data, kernel.panels)
+
+
+def generate_table(grid: VelocityGrid, kernel: KernelSpec, nthreads: int = 0) -> np.ndarray:
+    """Dense zeta-major table G[k][m], N^6 doubles."""
+    n = grid.n
+    G = np.empty(n ** 6, dtype=np.float64)
+    _check(lib().boltz_generate_table(n, grid.half_width, kernel.lam, kernel.beta, kernel.radius(grid),
+                                      kernel.panels, G.ctypes.data, nthreads))
+    return G
+
+
+def save_table(path, grid: VelocityGrid, kernel: KernelSpec, G: np.ndarray) -> None:
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    _check(lib().boltz_save_table(str(path).encode(), grid.n, grid.half_width, kernel.lam, kernel.beta,
+                                  kernel.radius(grid), kernel.panels, G.ctypes.data))
+
+
+def load_table(path, grid: VelocityGrid, kernel: KernelSpec) -> np.ndarray:
+    G = np.empty(grid.n ** 6, dtype=np.float64)
+    _check(lib().boltz_load_table(str(path).encode(), grid.n, grid.half_width, kernel.lam, kernel.beta,
+                                  kernel.radius(grid), kernel.panels, G.ctypes.data))
+    return G
+
+
+# ------------------------------------------------------------ operator
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+class CollisionOperator:
+    """Batched GPU collision operator on one device.
+
+    Replaces, for a batch of spatial cells, the reference's
+    SpectralTransform (forward/inverse, fourier.hpp:36-41), evaluate_qhat,
+    conserve and collide and collision_rk2
+    (SPEC.md:383-391).  A batch is (ncells, N^3) real / complex, flat index
+    (i1*N+i2)*N+i3.  The table is copied to HBM (folded, pair-symmetric
+    layout) at construction; the host copy may be dropped afterwards.
+    Not thread-safe (like SpectralTransform, fourier.hpp:24-25).
+    """
+
+    def __init__(self, grid: VelocityGrid, kernel: KernelSpec, table: np.ndarray, device: int = 0):
+        self.grid, self.kernel, self.device = grid, kernel, device
+        table = np.ascontiguousarray(table, dtype=np.float64)
+        if table.size != grid.n ** 6:
+            raise ConfigError(f"weight table has {table.size} entries, expected N^6 = {grid.n ** 6}")
+        h = C.c_void_p()
+        _check(lib().boltz_create(grid.n, grid.half_width, kernel.lam, kernel.beta, kernel.radius(grid),
+                                  table.ctypes.data, device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().boltz_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def memory_bytes(self):
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().boltz_memory_bytes(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    # -- argument plumbing
+    def _ncells(self, x, per_cell):
+        n = x.numel() if _is_torch(x) else x.size
+        if n % per_cell:
+            raise ConfigError(f"array of {n} values is not a whole number of cells ({per_cell} per cell)")
+        return n // per_cell
+
+    def _args(self, *arrays):
+        if all(_is_torch(a) for a in arrays):
+            import torch
+            for a in arrays:
+                if not (a.is_cuda and a.is_contiguous() and a.dtype in (torch.float64, torch.complex128)):
+                    raise ConfigError("device arrays must be contiguous float64/complex128 CUDA tensors")
+            return [a.data_ptr() for a in arrays], MEM_DEVICE, torch.cuda.current_stream(arrays[0].device).cuda_stream
+        if any(_is_torch(a) for a in arrays):
+            raise ConfigError("mix of host and device arrays")
+        return [a.ctypes.data for a in arrays], MEM_HOST, None
+
+    def _alloc_like(self, x, shape, complex_=False):
+        if _is_torch(x):
+            import torch
+            return torch.empty(shape, dtype=torch.complex128 if complex_ else torch.float64, device=x.device)
+        return np.empty(shape, dtype=np.complex128 if complex_ else np.float64)
+
+    @staticmethod
+    def _host(x, dtype):
+        return np.ascontiguousarray(x, dtype=dtype)
+
+    def _prep(self, x, complex_=False):
+        if _is_torch(x):
+            return x.contiguous()
+        return self._host(x, np.complex128 if complex_ else np.float64)
+
+    # -- reference operations, batched
+    def forward(self, f):
+        """SpectralTransform::forward (fourier.hpp:36): real -> complex."""
+        f = self._prep(f)
+        n3 = self.grid.size()
+        nc = self._ncells(f, n3)
+        out = self._alloc_like(f, (nc, n3), complex_=True)
+        (pf, po), mem, s = self._args(f, out)
+        _check(lib().boltz_forward_batch(self._h, pf, po, nc, mem, s))
+        return out
+
+    def inverse(self, g):
+        """SpectralTransform::inverse (fourier.hpp:38-41) -> (real, max_imag per cell)."""
+        g = self._prep(g, complex_=True)
+        n3 = self.grid.size()
+        nc = self._ncells(g, n3)
+        out = self._alloc_like(g, (nc, n3))
+        mi = self._alloc_like(g, (nc,))
+        (pg, po, pm), mem, s = self._args(g, out, mi)
+        _check(lib().boltz_inverse_batch(self._h, pg, po, pm, nc, mem, s))
+        return out, mi
+
+    def evaluate_qhat(self, fhat):
+        """evaluate_qhat, complex -> complex."""
+        fhat = self._prep(fhat, complex_=True)
+        n3 = self.grid.size()
+        nc = self._ncells(fhat, n3)
+        out = self._alloc_like(fhat, (nc, n3), complex_=True)
+        (pf, po), mem, s = self._args(fhat, out)
+        _check(lib().boltz_qhat_batch(self._h, pf, po, nc, mem, s))
+        return out
+
+    def conserve(self, q_raw):
+        """conserve."""
+        q_raw = self._prep(q_raw)
+        n3 = self.grid.size()
+        nc = self._ncells(q_raw, n3)
+        out = self._alloc_like(q_raw, (nc, n3))
+        (pq, po), mem, s = self._args(q_raw, out)
+        _check(lib().boltz_conserve_batch(self._h, pq, po, nc, mem, s))
+        return out
+
+    def collide(self, f, epsilon: float = 1.0, with_max_imag: bool = False):
+        """collide: (1/eps) P_N(inverse(qhat(forward(f))))."""
+        if not epsilon > 0.0:
+            raise ConfigError("collide: epsilon must be positive")
+        f = self._prep(f)
+        n3 = self.grid.size()
+        nc = self._ncells(f, n3)
+        out = self._alloc_like(f, (nc, n3))
+        if with_max_imag:
+            mi = self._alloc_like(f, (nc,))
+            (pf, po, pm), mem, s = self._args(f, out, mi)
+        else:
+            mi = None
+            (pf, po), mem, s = self._args(f, out)
+            pm = None
+        _check(lib().boltz_collide_batch(self._h, pf, po, nc, 1.0 / epsilon, pm, mem, s))
+        return (out, mi) if with_max_imag else out
+
+    def collision_rk2(self, f, dt: float, epsilon: float = 1.0):
+        """collision_rk2, IN PLACE on f (numpy or torch)."""
+        if not dt > 0.0 or not epsilon > 0.0:
+            raise ConfigError("collision_rk2: dt and epsilon must be positive")
+        if not _is_torch(f) and not (isinstance(f, np.ndarray) and f.dtype == np.float64 and f.flags.c_contiguous):
+            raise ConfigError("collision_rk2 works in place: pass a C-contiguous float64 array")
+        n3 = self.grid.size()
+        nc = self._ncells(f, n3)
+        (pf,), mem, s = self._args(f)
+        _check(lib().boltz_rk2_batch(self._h, pf, nc, dt, 1.0 / epsilon, mem, s))
+        return f
+
+    # -- transport (device tensors only)
+    def transport_step(self, field, out, x_ext, dx_ext, dt, wall_left=False, wall_right=False):
+        """transport_step on a (ncl+4, N^3) device field."""
+        ncl = field.shape[0] - 4
+        (pf, po, px, pd), mem, s = self._args(field, out, x_ext, dx_ext)
+        if mem != MEM_DEVICE:
+            raise ConfigError("transport_step takes CUDA tensors")
+        _check(lib().boltz_transport_step(self._h, pf, po, ncl, px, pd, dt, int(wall_left), int(wall_right), s))
+        return out
+
+    def fill_boundary(self, field, x_ext, side, kind, Tw=1.0, Vw=(0.0, 0.0, 0.0)):
+        """Ghost fill at a physical end: kind 0 extrapolation, 1 diffuse wall. Returns sigma_w."""
+        ncl = field.shape[0] - 4
+        (pf, px), mem, s = self._args(field, x_ext)
+        if mem != MEM_DEVICE:
+            raise ConfigError("fill_boundary takes CUDA tensors")
+        vw = np.ascontiguousarray(Vw, dtype=np.float64)
+        sig = C.c_double()
+        _check(lib().boltz_fill_boundary(self._h, pf, ncl, px, side, kind, Tw, vw.ctypes.data, C.byref(sig), s))
+        return sig.value

@@ -1,0 +1,612 @@
+// boltz_cuda.cu -- context object and C ABI (include/boltz_cuda.h) of the
+// B200 collision path.  Host orchestration only; the kernels live in
+// transforms.cuh (K1/K3), conv.cuh (K2) and transport.cuh (K4).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/boltz_cuda.h"
+#include "common.cuh"
+#include "conv.cuh"
+#include "fft.cuh"
+#include "transforms.cuh"
+#include "transport.cuh"
+
+namespace boltz_gpu {
+
+
+thread_local std::string g_err;
+void set_error(const std::string& s) { g_err = s; }
+
+struct CudaError {
+    std::string msg;
+};
+
+#define CK(call)                                                                                      \
+    do {                                                                                              \
+        cudaError_t e_ = (call);                                                                      \
+        if (e_ != cudaSuccess)                                                                        \
+            throw CudaError{std::string(#call) + ": " + cudaGetErrorString(e_) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")"};                                          \
+    } while (0)
+
+static bool supported_n(int n) {
+#define BOLTZ_SUP(N) if (n == N) return true;
+    BOLTZ_FOR_EACH_N(BOLTZ_SUP)
+#undef BOLTZ_SUP
+    return false;
+}
+
+}  // namespace boltz_gpu
+
+using namespace boltz_gpu;
+
+struct boltz_ctx {
+    int n = 0;
+    double L = 0, lambda = 0, beta = 0, r0 = 0;
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    // folded convolution table (conv.cuh)
+    double* dH = nullptr;
+    int2* dEnt = nullptr;
+    int* dRowStart = nullptr;
+    int nent = 0, slab = 0;
+    // workspace (group layout), capacity in cells (multiple of 32)
+    int64_t cap = 0;
+    double2* dA = nullptr;
+    double2* dB = nullptr;
+    double* dFs = nullptr;   // RK2 stage (user layout)
+    double* dIn = nullptr;   // host-call staging (user layout, complex-sized)
+    double* dOut = nullptr;
+    unsigned long long* dMaxIm = nullptr;
+    int* dFlag = nullptr;
+    int* hFlag = nullptr;    // pinned
+    ProjConst pc{};
+    int64_t table_bytes = 0, ws_bytes = 0;
+};
+
+namespace {
+
+int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
+
+void fill_twiddles() {
+    std::vector<double2> tw(kTwTotal);
+    const int ns[] = {4, 6, 8, 12, 16, 24, 32};
+    for (int n : ns)
+        for (int j = 0; j < n; ++j) {
+            long double ang = -2.0L * 3.14159265358979323846264338327950288L * j / n;
+            tw[tw_offset(n) + j] = make_double2((double)cosl(ang), (double)sinl(ang));
+        }
+    CK(cudaMemcpyToSymbol(c_tw, tw.data(), sizeof(double2) * kTwTotal));
+}
+
+// (C C^T)^{-1} for the projection; long double accumulation.
+void build_projection(boltz_ctx* c) {
+    const int n = c->n;
+    const long double dv = 2.0L * c->L / n;
+    long double A[5][5] = {};
+    for (int i1 = 0; i1 < n; ++i1)
+        for (int i2 = 0; i2 < n; ++i2)
+            for (int i3 = 0; i3 < n; ++i3) {
+                long double cc = (long double)axis_coeff(n, i1) * axis_coeff(n, i2) * axis_coeff(n, i3);
+                long double w = cc * dv * dv * dv;
+                long double v1 = dv * (i1 - n / 2), v2 = dv * (i2 - n / 2), v3 = dv * (i3 - n / 2);
+                long double r[5] = {w, v1 * w, v2 * w, v3 * w, (v1 * v1 + v2 * v2 + v3 * v3) * w};
+                for (int a = 0; a < 5; ++a)
+                    for (int b = 0; b < 5; ++b) A[a][b] += r[a] * r[b];
+            }
+    // Gauss-Jordan inverse (SPD, well conditioned at these sizes)
+    long double M[5][10] = {};
+    for (int a = 0; a < 5; ++a) {
+        for (int b = 0; b < 5; ++b) M[a][b] = A[a][b];
+        M[a][5 + a] = 1.0L;
+    }
+    for (int col = 0; col < 5; ++col) {
+        int piv = col;
+        for (int r = col + 1; r < 5; ++r)
+            if (fabsl(M[r][col]) > fabsl(M[piv][col])) piv = r;
+        for (int k = 0; k < 10; ++k) std::swap(M[col][k], M[piv][k]);
+        long double d = M[col][col];
+        for (int k = 0; k < 10; ++k) M[col][k] /= d;
+        for (int r = 0; r < 5; ++r)
+            if (r != col) {
+                long double f = M[r][col];
+                for (int k = 0; k < 10; ++k) M[r][k] -= f * M[col][k];
+            }
+    }
+    for (int a = 0; a < 5; ++a)
+        for (int b = 0; b < 5; ++b) c->pc.ginv[a * 5 + b] = (double)M[a][5 + b];
+    c->pc.dv = 2.0 * c->L / n;
+    c->pc.half = n / 2;
+}
+
+// Build the folded, pair-symmetric table H (conv.cuh) from the host G, one
+// k1-plane (N^5 doubles) at a time so the dense N^6 table is never resident.
+void build_table(boltz_ctx* c, const double* G_host) {
+    const int n = c->n, h = n / 2;
+    const int t = conv_tile(n), nk = n / t;
+    const int slab_kc = band_slab_kc(n, t);
+    c->slab = nk * slab_kc;
+    // slab term order (must match conv_rows)
+    std::vector<short2> term(c->slab, make_short2(-1, -1));
+    for (int kc = 0; kc < nk; ++kc) {
+        int pos = kc * slab_kc;
+        for (int sc = 0; sc < nk; ++sc)
+            for (int m3 = 0; m3 < n; ++m3)
+                for (int kk = 0; kk < t; ++kk)
+                    if (band_term(n, t, kc, sc, m3, kk)) term[pos++] = make_short2((short)(kc * t + kk), (short)m3);
+    }
+    // entries: output row (k1,k2) x representative input row (m1,m2)
+    std::vector<int2> ent;
+    std::vector<int4> entk;
+    std::vector<int> row_start(n * n + 1, 0);
+    for (int k1 = 0; k1 < n; ++k1)
+        for (int k2 = 0; k2 < n; ++k2) {
+            row_start[k1 * n + k2] = (int)ent.size();
+            for (int m1 = std::max(0, k1 - h + 1); m1 <= std::min(n - 1, k1 + h); ++m1)
+                for (int m2 = std::max(0, k2 - h + 1); m2 <= std::min(n - 1, k2 + h); ++m2) {
+                    const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+                    if (m1 < s1 || (m1 == s1 && m2 <= s2)) {
+                        ent.push_back(make_int2((m1 * n + m2) * n, (s1 * n + s2) * n));
+                        entk.push_back(make_int4(k1, k2, m1, m2));
+                    }
+                }
+        }
+    row_start[n * n] = (int)ent.size();
+    c->nent = (int)ent.size();
+    const size_t hbytes = (size_t)c->nent * c->slab * sizeof(double);
+    CK(cudaMalloc(&c->dH, hbytes));
+    CK(cudaMalloc(&c->dEnt, ent.size() * sizeof(int2)));
+    CK(cudaMalloc(&c->dRowStart, row_start.size() * sizeof(int)));
+    CK(cudaMemcpy(c->dEnt, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dRowStart, row_start.data(), row_start.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->table_bytes = (int64_t)hbytes + (int64_t)ent.size() * 8 + (int64_t)row_start.size() * 4;
+
+    int4* dEntK = nullptr;
+    short2* dTerm = nullptr;
+    double* dPlane = nullptr;
+    const size_t n3 = (size_t)n * n * n, plane = (size_t)n * n * n3;
+    try {
+        CK(cudaMalloc(&dEntK, entk.size() * sizeof(int4)));
+        CK(cudaMalloc(&dTerm, term.size() * sizeof(short2)));
+        CK(cudaMalloc(&dPlane, plane * sizeof(double)));
+        CK(cudaMemcpy(dEntK, entk.data(), entk.size() * sizeof(int4), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dTerm, term.data(), term.size() * sizeof(short2), cudaMemcpyHostToDevice));
+        const double dz = kPi / c->L, w3 = dz * dz * dz;
+        for (int k1 = 0; k1 < n; ++k1) {
+            CK(cudaMemcpy(dPlane, G_host + (size_t)k1 * plane, plane * sizeof(double), cudaMemcpyHostToDevice));
+            const int e0 = row_start[k1 * n], e1 = row_start[k1 * n + n];
+            const long long total = (long long)(e1 - e0) * c->slab;
+            const int blk = 256;
+            k_build_H<<<(unsigned)((total + blk - 1) / blk), blk>>>(dPlane, c->dH, dEntK, dTerm, e0, e1, c->slab, n,
+                                                                     w3);
+            CK(cudaGetLastError());
+        }
+        CK(cudaDeviceSynchronize());
+    } catch (...) {
+        cudaFree(dEntK);
+        cudaFree(dTerm);
+        cudaFree(dPlane);
+        throw;
+    }
+    cudaFree(dEntK);
+    cudaFree(dTerm);
+    cudaFree(dPlane);
+}
+
+void ensure_workspace(boltz_ctx* c, int64_t cells) {
+    int64_t want = (cells + kLanes - 1) / kLanes * kLanes;
+    // default capacity: up to ~2 GiB of workspace per context
+    const int64_t n3 = n3_of(c);
+    const int64_t per_cell = n3 * (16 + 16 + 8 + 16 + 16) + 8;
+    int64_t lim = std::max<int64_t>(kLanes, ((int64_t)2 << 30) / per_cell / kLanes * kLanes);
+    want = std::min(want, lim);
+    if (want <= c->cap) return;
+    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut); cudaFree(c->dMaxIm);
+    c->dA = c->dB = nullptr; c->dFs = c->dIn = c->dOut = nullptr; c->dMaxIm = nullptr; c->cap = 0;
+    CK(cudaMalloc(&c->dA, (size_t)want * n3 * 16));
+    CK(cudaMalloc(&c->dB, (size_t)want * n3 * 16));
+    CK(cudaMalloc(&c->dFs, (size_t)want * n3 * 8));
+    CK(cudaMalloc(&c->dIn, (size_t)want * n3 * 16));
+    CK(cudaMalloc(&c->dOut, (size_t)want * n3 * 16));
+    CK(cudaMalloc(&c->dMaxIm, (size_t)want * 8));
+    c->cap = want;
+    c->ws_bytes = want * per_cell;
+}
+
+// ---------------------------------------------------------------- launchers
+template <int N>
+struct Launch {
+    static constexpr int N3 = N * N * N;
+    static dim3 pass_grid(int64_t ngroups) { return dim3((N * N + 7) / 8, (unsigned)ngroups); }
+
+    // user real f (device, nc cells) -> group complex fhat in c->dA
+    static void forward(boltz_ctx* c, const double* f, int64_t nc, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
+        const double par = ((N / 2) & 1) ? -1.0 : 1.0;  // ((-1)^{N/2})^3
+        const double scale = sv * sv * sv * par;
+        dim3 blk(32, 8);
+        k_fft_pass<N, 2, -1, PASS_PACK_FWD><<<pass_grid(ng), blk, 0, s>>>(f, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0);
+        k_fft_pass<N, 1, -1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0);
+        k_fft_pass<N, 0, -1, PASS_FWD_LAST><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc,
+                                                                           scale);
+        CK(cudaGetLastError());
+    }
+    // group complex c->dA -> group complex (s_k * Qhat) in c->dB
+    static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        constexpr int NK = N / conv_tile(N);
+        dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+        k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+        CK(cudaGetLastError());
+    }
+    // group complex c->dB (already * s_m) -> group real Qt in (double*)c->dA; max|Im| per cell
+    static void inverse(boltz_ctx* c, int64_t nc, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        const double dz = kPi / c->L;
+        const double sz = dz / std::sqrt(2.0 * kPi);
+        const double par = ((N / 2) & 1) ? -1.0 : 1.0;
+        const double scale = sz * sz * sz;
+        dim3 blk(32, 8);
+        CK(cudaMemsetAsync(c->dMaxIm, 0, (size_t)nc * 8, s));
+        k_fft_pass<N, 2, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0);
+        k_fft_pass<N, 1, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0);
+        // the INV_LAST pass folds par into the sign of its scale; max|Im| uses |scale|
+        k_fft_pass<N, 0, +1, PASS_INV_LAST><<<pass_grid(ng), blk, 0, s>>>(
+            nullptr, c->dB, reinterpret_cast<double*>(c->dA), c->dMaxIm, c->dFlag, nc, scale * par);
+        CK(cudaGetLastError());
+    }
+    // group real Qt in (double*)c->dA -> out = base + coef * P_N(Qt)  (user layout)
+    static void project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        k_project<N><<<(unsigned)ng, 256, 0, s>>>(reinterpret_cast<const double*>(c->dA), base, out, nc, coef, c->pc,
+                                                  c->dFlag);
+        CK(cudaGetLastError());
+    }
+    static void pack_complex(const double* in, double2* dst, int64_t nc, int sign, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
+        k_pack_complex<N><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(in), dst, nc, sign);
+        CK(cudaGetLastError());
+    }
+    static void unpack_complex(const double2* src, double* out, int64_t nc, int sign, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
+        k_unpack_complex<N><<<grid, 256, 0, s>>>(src, reinterpret_cast<double2*>(out), nc, sign);
+        CK(cudaGetLastError());
+    }
+    static void unpack_real(const double* src, double* out, int64_t nc, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
+        k_unpack_real<N><<<grid, 256, 0, s>>>(src, out, nc);
+        CK(cudaGetLastError());
+    }
+    static void pack_real(const double* in, double* dst, int64_t nc, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
+        k_pack_real<N><<<grid, 256, 0, s>>>(in, dst, nc);
+        CK(cudaGetLastError());
+    }
+};
+
+template <typename F>
+void dispatch(int n, F&& f) {
+    switch (n) {
+#define BOLTZ_CASE(N) \
+    case N: f(Launch<N>{}); break;
+        BOLTZ_FOR_EACH_N(BOLTZ_CASE)
+#undef BOLTZ_CASE
+        default: throw CudaError{"unsupported N"};
+    }
+}
+
+int guard_ctx(boltz_ctx* c) {
+    if (!c) {
+        set_error("null context");
+        return BOLTZ_ERR_CONFIG;
+    }
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) {
+        set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+        return BOLTZ_ERR_CUDA;
+    }
+    return BOLTZ_OK;
+}
+
+// Runs fn(chunk_in, chunk_out, cells, stream) over chunks of the batch, staging
+// host memory through the context buffers when mem == HOST.  in_elems /
+// out_elems: doubles per cell of the user-layout input / output.
+template <typename Fn>
+int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems, int mem,
+                void* stream, double* max_imag, Fn&& fn) {
+    if (ncells < 0 || (ncells > 0 && (!in || !out))) {
+        set_error("invalid batch arguments (null pointer or negative count)");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (mem != BOLTZ_MEM_HOST && mem != BOLTZ_MEM_DEVICE) {
+        set_error("mem must be BOLTZ_MEM_HOST or BOLTZ_MEM_DEVICE");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (ncells == 0) return BOLTZ_OK;
+    cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+    ensure_workspace(c, ncells);
+    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
+    for (int64_t c0 = 0; c0 < ncells; c0 += c->cap) {
+        const int64_t nc = std::min<int64_t>(c->cap, ncells - c0);
+        const double* din = in + c0 * in_elems;
+        double* dout = out + c0 * out_elems;
+        if (mem == BOLTZ_MEM_HOST) {
+            CK(cudaMemcpyAsync(c->dIn, din, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice, s));
+            din = c->dIn;
+            dout = c->dOut;
+        }
+        fn(din, dout, nc, s);
+        if (mem == BOLTZ_MEM_HOST) {
+            CK(cudaMemcpyAsync(out + c0 * out_elems, c->dOut, (size_t)nc * out_elems * 8, cudaMemcpyDeviceToHost, s));
+        }
+        if (max_imag) {
+            std::vector<unsigned long long> tmp(nc);
+            CK(cudaMemcpyAsync(tmp.data(), c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (mem == BOLTZ_MEM_HOST) {
+                std::memcpy(max_imag + c0, tmp.data(), (size_t)nc * 8);
+            } else {
+                CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToDevice, s));
+            }
+        }
+    }
+    CK(cudaMemcpyAsync(c->hFlag, c->dFlag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (*c->hFlag & 1) {
+        set_error("NumericError: non-finite value in the input distribution");
+        return BOLTZ_ERR_NUMERIC;
+    }
+    if (*c->hFlag & 2) {
+        set_error("NumericError: non-finite value produced (collision output / RK2 stage)");
+        return BOLTZ_ERR_NUMERIC;
+    }
+    return BOLTZ_OK;
+}
+
+template <typename Body>
+int api(boltz_ctx* c, Body&& body) {
+    int rc = guard_ctx(c);
+    if (rc) return rc;
+    try {
+        return body();
+    } catch (const CudaError& e) {
+        set_error(e.msg);
+        return BOLTZ_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return BOLTZ_ERR_CUDA;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* boltz_last_error(void) { return g_err.c_str(); }
+
+const char* boltz_build_info(void) {
+    return "boltz_cuda sm_100a; N in {4,6,8,12,16,24,32}; conv: pair-symmetric folded table, lane=cell group layout";
+}
+
+int boltz_create(int n, double L, double lambda, double beta, double r0, const double* G_host, int device,
+                 boltz_ctx** out) {
+    if (!out) {
+        set_error("boltz_create: out is null");
+        return BOLTZ_ERR_CONFIG;
+    }
+    *out = nullptr;
+    if (n < 4 || n % 2 != 0) {
+        set_error("velocity grid: N must be even and >= 4, got " + std::to_string(n));
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!(L > 0.0)) {
+        set_error("velocity grid: L must be positive, got " + std::to_string(L));
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!supported_n(n)) {
+        set_error("boltz_create: N=" + std::to_string(n) + " has no compiled kernel (supported 4,6,8,12,16,24,32)");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!(lambda >= 0.0 && lambda <= 1.0) || !(beta > 0.0 && beta <= 1.0) || !(r0 > 0.0)) {
+        set_error("kernel spec: need 0<=lambda<=1, 0<beta<=1, r0>0");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!G_host) {
+        set_error("boltz_create: weight table is null");
+        return BOLTZ_ERR_CONFIG;
+    }
+    boltz_ctx* c = new boltz_ctx();
+    c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device;
+    try {
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        CK(cudaMalloc(&c->dFlag, sizeof(int)));
+        CK(cudaMallocHost(&c->hFlag, sizeof(int)));
+        fill_twiddles();
+        build_projection(c);
+        build_table(c, G_host);
+    } catch (const CudaError& e) {
+        set_error(e.msg);
+        boltz_destroy(c);
+        return BOLTZ_ERR_CUDA;
+    }
+    *out = c;
+    return BOLTZ_OK;
+}
+
+int boltz_destroy(boltz_ctx* c) {
+    if (!c) return BOLTZ_OK;
+    cudaSetDevice(c->device);
+    cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
+    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut);
+    cudaFree(c->dMaxIm); cudaFree(c->dFlag);
+    if (c->hFlag) cudaFreeHost(c->hFlag);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return BOLTZ_OK;
+}
+
+int boltz_memory_bytes(const boltz_ctx* c, int64_t* table_bytes, int64_t* workspace_bytes) {
+    if (!c) return BOLTZ_ERR_CONFIG;
+    if (table_bytes) *table_bytes = c->table_bytes;
+    if (workspace_bytes) *workspace_bytes = c->ws_bytes;
+    return BOLTZ_OK;
+}
+
+int boltz_forward_batch(boltz_ctx* c, const double* f, double* fhat, int64_t ncells, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, f, fhat, ncells, (int)n3, (int)(2 * n3), mem, stream, nullptr,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   Lx::forward(c, in, nc, s);
+                                   Lx::unpack_complex(c->dA, out, nc, 0, s);
+                               });
+                           });
+    });
+}
+
+int boltz_inverse_batch(boltz_ctx* c, const double* g, double* f, double* max_imag, int64_t ncells, int mem,
+                        void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, g, f, ncells, (int)(2 * n3), (int)n3, mem, stream, max_imag,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   Lx::pack_complex(in, c->dB, nc, 1, s);
+                                   Lx::inverse(c, nc, s);
+                                   Lx::unpack_real(reinterpret_cast<const double*>(c->dA), out, nc, s);
+                               });
+                           });
+    });
+}
+
+int boltz_qhat_batch(boltz_ctx* c, const double* fhat, double* qhat, int64_t ncells, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, fhat, qhat, ncells, (int)(2 * n3), (int)(2 * n3), mem, stream, nullptr,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   Lx::pack_complex(in, c->dA, nc, 0, s);
+                                   Lx::conv(c, nc, s);
+                                   Lx::unpack_complex(c->dB, out, nc, 1, s);
+                               });
+                           });
+    });
+}
+
+int boltz_conserve_batch(boltz_ctx* c, const double* q_raw, double* q, int64_t ncells, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, q_raw, q, ncells, (int)n3, (int)n3, mem, stream, nullptr,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   Lx::pack_real(in, reinterpret_cast<double*>(c->dA), nc, s);
+                                   Lx::project(c, nullptr, out, nc, 1.0, s);
+                               });
+                           });
+    });
+}
+
+int boltz_collide_batch(boltz_ctx* c, const double* f, double* q, int64_t ncells, double inv_eps, double* max_imag,
+                        int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, f, q, ncells, (int)n3, (int)n3, mem, stream, max_imag,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   Lx::forward(c, in, nc, s);
+                                   Lx::conv(c, nc, s);
+                                   Lx::inverse(c, nc, s);
+                                   Lx::project(c, nullptr, out, nc, inv_eps, s);
+                               });
+                           });
+    });
+}
+
+int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double inv_eps, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, f, f, ncells, (int)n3, (int)n3, mem, stream, nullptr,
+                           [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
+                               // host staging: in = dIn, out = dOut; copy base through
+                               if (in != out) CK(cudaMemcpyAsync(out, in, (size_t)nc * n3 * 8,
+                                                                 cudaMemcpyDeviceToDevice, s));
+                               dispatch(c->n, [&](auto L) {
+                                   using Lx = decltype(L);
+                                   // stage 1: f* = f + dt/2 * collide(f)
+                                   Lx::forward(c, out, nc, s);
+                                   Lx::conv(c, nc, s);
+                                   Lx::inverse(c, nc, s);
+                                   Lx::project(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
+                                   // stage 2: f <- f + dt * collide(f*)
+                                   Lx::forward(c, c->dFs, nc, s);
+                                   Lx::conv(c, nc, s);
+                                   Lx::inverse(c, nc, s);
+                                   Lx::project(c, out, out, nc, dt * inv_eps, s);
+                               });
+                           });
+    });
+}
+
+int boltz_transport_step(boltz_ctx* c, const double* field, double* out, int64_t ncl, const double* x_ext,
+                         const double* dx_ext, double dt, int wall_left, int wall_right, void* stream) {
+    return api(c, [&] {
+        if (ncl < 1 || !field || !out || !x_ext || !dx_ext) {
+            set_error("transport_step: invalid arguments");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+        launch_transport(c->n, field, out, ncl, x_ext, dx_ext, dt, wall_left, wall_right, c->pc.dv, s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
+        return BOLTZ_OK;
+    });
+}
+
+int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* x_ext, int side, int kind, double Tw,
+                        const double* Vw_host3, double* sigma_w, void* stream) {
+    return api(c, [&] {
+        if (ncl < 2 || !field || !x_ext || (side != 0 && side != 1) || (kind != 0 && kind != 1)) {
+            set_error("fill_boundary: invalid arguments (need >= 2 interior cells)");
+            return BOLTZ_ERR_CONFIG;
+        }
+        if (kind == 1 && !(Tw > 0.0)) {
+            set_error("fill_boundary: wall temperature must be positive");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+        double vw[3] = {0, 0, 0};
+        if (Vw_host3) std::memcpy(vw, Vw_host3, sizeof vw);
+        double* dsig = reinterpret_cast<double*>(c->dMaxIm);
+        if (!dsig) {
+            ensure_workspace(c, kLanes);
+            dsig = reinterpret_cast<double*>(c->dMaxIm);
+        }
+        launch_fill_boundary(c->n, field, ncl, x_ext, side, kind, Tw, vw[0], vw[1], vw[2], c->pc.dv, dsig, s);
+        CK(cudaGetLastError());
+        double hs = 0.0;
+        CK(cudaMemcpyAsync(&hs, dsig, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (sigma_w) *sigma_w = hs;
+        return BOLTZ_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// transport.cuh -- K4: second-order finite-volume transport on a non-uniform
+// 1D grid and the physical-end ghost fill
+// (linear extrapolation SPEC.md:318; diffuse Maxwell wall SPEC.md:333-341).
+// Elementwise over (cell, velocity node); user layout field[cell][N^3] with
+// two ghost cells per side, so consecutive threads touch
+// consecutive nodes of one cell (coalesced).  HBM-bound.
+#pragma once
+#include "common.cuh"
+
+namespace boltz_gpu {
+
+__device__ __forceinline__ double minmod3(double a, double b, double c) {
+    if (a > 0 && b > 0 && c > 0) return fmin(a, fmin(b, c));
+    if (a < 0 && b < 0 && c < 0) return fmax(a, fmax(b, c));
+    return 0.0;
+}
+
+// grid = (ceil(N^3/256), ncl + 4); ghosts are copied through.
+template <int N>
+__global__ void __launch_bounds__(256)
+k_transport(const double* __restrict__ f, double* __restrict__ out, long long ncl, const double* __restrict__ x,
+            const double* __restrict__ dx, double dt, int wl, int wr, double dv) {
+    constexpr int N3 = N * N * N;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long ce = blockIdx.y;
+    if (j >= N3) return;
+    if (ce < 2 || ce > ncl + 1) {
+        out[ce * N3 + j] = f[ce * N3 + j];
+        return;
+    }
+    const double v1 = dv * (j / (N * N) - N / 2);
+    double fv[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) fv[d] = f[(ce - 2 + d) * N3 + j];
+    double sg[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const long long c = ce - 1 + d;
+        const double fm = fv[d], f0 = fv[d + 1], fp = fv[d + 2];
+        double s = minmod3((fp - f0) / (x[c + 1] - x[c]), (f0 - fm) / (x[c] - x[c - 1]),
+                           (fp - fm) / (x[c + 1] - x[c - 1]));
+        if (wl && (c == 1 || c == 2)) s = 0.0;
+        if (wr && (c == ncl + 2 || c == ncl + 1)) s = 0.0;
+        sg[d] = s;
+    }
+    double Fl, Fr;
+    if (v1 >= 0.0) {
+        Fl = v1 * (fv[1] + 0.5 * dx[ce - 1] * sg[0]);
+        Fr = v1 * (fv[2] + 0.5 * dx[ce] * sg[1]);
+    } else {
+        Fl = v1 * (fv[2] - 0.5 * dx[ce] * sg[1]);
+        Fr = v1 * (fv[3] - 0.5 * dx[ce + 1] * sg[2]);
+    }
+    out[ce * N3 + j] = fv[2] - dt / dx[ce] * (Fr - Fl);
+}
+
+// one block of 256 threads; sigma_w written to sig[0]
+template <int N>
+__global__ void __launch_bounds__(256)
+k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict__ x, int side, int kind, double Tw,
+                double vw0, double vw1, double vw2, double dv, double* __restrict__ sig) {
+    constexpr int N3 = N * N * N;
+    const long long g0 = side == 0 ? 1 : ncl + 2, g1 = side == 0 ? 0 : ncl + 3;
+    const long long i0 = side == 0 ? 2 : ncl + 1, i1 = side == 0 ? 3 : ncl;
+    double* G0 = f + g0 * N3;
+    double* G1 = f + g1 * N3;
+    const double* I0 = f + i0 * N3;
+    const double* I1 = f + i1 * N3;
+    if (kind == 0) {
+        const double xa = x[i0], xb = x[i1];
+        for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+            const double slope = (I0[j] - I1[j]) / (xa - xb);
+            G0[j] = I0[j] + slope * (x[g0] - xa);
+            G1[j] = I0[j] + slope * (x[g1] - xa);
+        }
+        if (threadIdx.x == 0) sig[0] = 0.0;
+        return;
+    }
+    const double nrm = side == 0 ? 1.0 : -1.0;
+    __shared__ double red[256];
+    double part = 0.0;
+    for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+        const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
+        const double un = (dv * (a1 - N / 2) - vw0) * nrm;
+        if (un <= 0.0) part += un * I0[j] * (axis_coeff(N, a1) * axis_coeff(N, a2) * axis_coeff(N, a3) * dv * dv * dv);
+    }
+    red[threadIdx.x] = part;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double sw = -sqrt(2.0 * kPi / Tw) * red[0];
+    const double norm = sw / pow(2.0 * kPi * Tw, 1.5);
+    for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+        const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
+        const double c1 = dv * (a1 - N / 2) - vw0, c2 = dv * (a2 - N / 2) - vw1, c3 = dv * (a3 - N / 2) - vw2;
+        const double val = (c1 * nrm > 0.0) ? norm * exp(-(c1 * c1 + c2 * c2 + c3 * c3) / (2.0 * Tw)) : 0.0;
+        G0[j] = val;
+        G1[j] = val;
+    }
+    if (threadIdx.x == 0) sig[0] = sw;
+}
+
+inline void launch_transport(int n, const double* f, double* out, long long ncl, const double* x, const double* dx,
+                             double dt, int wl, int wr, double dv, cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_TR(N)                                                                                        \
+    case N: {                                                                                              \
+        dim3 grid((N * N * N + 255) / 256, (unsigned)(ncl + 4));                                          \
+        k_transport<N><<<grid, 256, 0, s>>>(f, out, ncl, x, dx, dt, wl, wr, dv);                           \
+    } break;
+        BOLTZ_FOR_EACH_N(BOLTZ_TR)
+#undef BOLTZ_TR
+        default: break;
+    }
+}
+
+inline void launch_fill_boundary(int n, double* f, long long ncl, const double* x, int side, int kind, double Tw,
+                                 double vw0, double vw1, double vw2, double dv, double* sig, cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_FB(N) \
+    case N: k_fill_boundary<N><<<1, 256, 0, s>>>(f, ncl, x, side, kind, Tw, vw0, vw1, vw2, dv, sig); break;
+        BOLTZ_FOR_EACH_N(BOLTZ_FB)
+#undef BOLTZ_FB
+        default: break;
+    }
+}
+
+}  // namespace boltz_gpu

@@ -1,0 +1,119 @@
+"""GPU collision path vs the CPU oracle (tests/conftest.py `O`), through the
+C ABI.  Bar (BASELINE.json north_star): ||dQ||_inf/||Q||_inf <= 1e-10 per
+cell in FP64; conservation <= 1e-12 relative to rho."""
+import numpy as np
+import pytest
+
+from conftest import rel_max, table
+from paper_1301_4195_b200 import CollisionOperator, KernelSpec, NumericError, VelocityGrid, scenarios
+
+pytestmark = pytest.mark.gpu
+
+TOL_Q = 1e-10
+TOL_CONS = 1e-12
+
+
+def _op(n, L, lam=1.0):
+    return CollisionOperator(VelocityGrid.create(n, L), KernelSpec(lam), table(n, L, lam))
+
+
+@pytest.mark.parametrize("n,L", [(4, 3.0), (6, 4.0), (8, 5.0), (12, 6.0), (16, 6.0)])
+def test_forward_inverse_vs_oracle(gpu, O, n, L):
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 5, seed=7)
+    with _op(n, L) as op:
+        fh = op.forward(f)
+        back, mi = op.inverse(fh)
+    for c in range(5):
+        ref = O.forward(n, L, f[c])
+        assert rel_max(fh[c], ref) < 1e-12
+        rb, rmi = O.inverse(n, L, ref)
+        assert rel_max(back[c], rb) < 1e-12
+        assert abs(mi[c] - rmi) <= 1e-12 * np.abs(rb).max() + 1e-300
+
+
+@pytest.mark.parametrize("n,L", [(4, 3.0), (6, 4.0), (8, 5.0), (12, 6.0), (16, 6.0)])
+def test_qhat_vs_oracle(gpu, O, n, L):
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 3, seed=11)
+    G = table(n, L)
+    with _op(n, L) as op:
+        fh = op.forward(f)
+        qh = op.evaluate_qhat(fh)
+    for c in range(3):
+        ref = O.evaluate_qhat(n, L, G, fh[c])
+        assert rel_max(qh[c], ref) < TOL_Q
+
+
+@pytest.mark.parametrize("n,L,lam", [(8, 5.0, 1.0), (8, 5.0, 0.0), (16, 6.0, 1.0), (12, 6.0, 0.0)])
+def test_collide_vs_oracle(gpu, O, n, L, lam):
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 4, seed=3)
+    G = table(n, L, lam)
+    with _op(n, L, lam) as op:
+        q, mi = op.collide(f, 1.0, with_max_imag=True)
+    for c in range(4):
+        ref, rmi = O.collide(n, L, G, f[c])
+        assert rel_max(q[c], ref) < TOL_Q
+        assert abs(mi[c] - rmi) <= 1e-9 * rmi + 1e-300
+        m = O.moments(n, L, q[c])
+        rho = O.moments(n, L, f[c])[0]
+        assert np.abs(m[:5]).max() < TOL_CONS * rho
+
+
+def test_config1_rk2_vs_oracle(gpu, O):
+    n, L = 16, 6.0
+    grid = VelocityGrid.create(n, L)
+    f0 = scenarios.config1_initial(grid)
+    G = table(n, L)
+    f = f0.copy().reshape(1, -1)
+    with _op(n, L) as op:
+        for _ in range(3):
+            op.collision_rk2(f, 0.01)
+    ref = f0.copy()
+    for _ in range(3):
+        ref = O.collision_rk2(n, L, G, ref.reshape(1, -1), 0.01)
+    assert rel_max(f[0] - f0, ref.ravel() - f0) < 1e-9
+    m0, m1 = O.moments(n, L, f0), O.moments(n, L, f[0])
+    assert np.abs(m1[:5] - m0[:5]).max() < TOL_CONS * m0[0]
+
+
+def test_batch_composition_bitwise(gpu):
+    """A cell's result does not depend on its batch neighbours or position."""
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 70, seed=5)
+    with _op(n, L) as op:
+        q_all = op.collide(f)
+        q_one = op.collide(f[37:38])
+        q_perm = op.collide(f[::-1].copy())
+    assert np.array_equal(q_all[37], q_one[0])
+    assert np.array_equal(q_all[::-1], q_perm)
+
+
+def test_nonfinite_rejected(gpu):
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 3, seed=5)
+    f[1, 17] = np.nan
+    with _op(n, L) as op:
+        with pytest.raises(NumericError):
+            op.collide(f)
+        g = f.copy()
+        g[1, 17] = np.inf
+        with pytest.raises(NumericError):
+            op.collision_rk2(g, 0.01)
+        assert np.isfinite(op.collide(f[[0, 2]])).all()
+
+
+def test_empty_and_ragged_batches(gpu, O):
+    n, L = 6, 4.0
+    grid = VelocityGrid.create(n, L)
+    G = table(n, L)
+    with _op(n, L) as op:
+        assert op.collide(np.zeros((0, n ** 3))).shape == (0, n ** 3)
+        f = scenarios.mixture_cells(grid, 33, seed=9)
+        q = op.collide(f)
+        for c in (0, 31, 32):
+            assert rel_max(q[c], O.collide(n, L, G, f[c])[0]) < TOL_Q
+        assert np.abs(op.collide(np.zeros((2, n ** 3)))).max() == 0.0
