@@ -124,6 +124,17 @@ int boltz_transport_step(boltz_ctx* ctx, const double* field, double* out, int64
 int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double* x_ext, int side, int kind,
                         double Tw, const double* Vw_host3, double* sigma_w, void* stream);
 
+/* ---- measurement hooks (bench.py; no reference counterpart) ---- */
+
+/* Enable CUDA-event bracketing of every kernel launch on its stream.  Kinds:
+ * 0 convolution (K2), 1 FFT passes (K1/K3), 2 projection/RK2 epilogue (K3),
+ * 3 layout conversion, 4 transport (K4).  Launch counts are always kept. */
+int boltz_set_timing(boltz_ctx* ctx, int enable);
+/* ms[k], launches[k] for k < nkinds (nullable); reset != 0 zeroes them */
+int boltz_get_timing(boltz_ctx* ctx, double* ms, int64_t* launches, int nkinds, int reset);
+/* FP64 (DFMA) throughput of `device` in TFLOP/s, best over ~`seconds` */
+int boltz_fp64_peak(int device, double seconds, double* tflops);
+
 /* ---- host-side weight table (the hot path's input) ---- */
 
 /* generate the dense zeta-major table (n^6 doubles) on the host; lambda in

@@ -88,6 +88,9 @@ def lib():
             "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
             "boltz_transport_step": (i, [vp, vp, vp, i64, vp, vp, d, i, i, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
+            "boltz_set_timing": (i, [vp, i]),
+            "boltz_get_timing": (i, [vp, vp, vp, i, i]),
+            "boltz_fp64_peak": (i, [i, d, dp]),
             "boltz_generate_table": (i, [i, d, d, d, d, i, vp, i]),
             "boltz_weight": (d, [d, d, d, vp, vp, i]),
             "boltz_save_table": (i, [C.c_char_p, i, d, d, d, d, i, vp]),
@@ -200,6 +203,13 @@ def load_table(path, grid: VelocityGrid, kernel: KernelSpec) -> np.ndarray:
     return G
 
 
+def fp64_peak(device: int = 0, seconds: float = 0.5) -> float:
+    """Measured DFMA throughput of the device (TFLOP/s)."""
+    t = C.c_double()
+    _check(lib().boltz_fp64_peak(device, seconds, C.byref(t)))
+    return t.value
+
+
 # ------------------------------------------------------------ operator
 def _is_torch(x):
     return type(x).__module__.startswith("torch")
@@ -248,6 +258,19 @@ class CollisionOperator:
         a, b = C.c_int64(), C.c_int64()
         _check(lib().boltz_memory_bytes(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    # -- measurement hooks (bench.py)
+    KINDS = ("conv", "fft", "project", "layout", "transport")
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().boltz_set_timing(self._h, int(enable)))
+
+    def timing(self, reset: bool = False):
+        """({kind: ms}, {kind: launches}) accumulated since the last reset."""
+        ms = np.zeros(5)
+        cnt = np.zeros(5, dtype=np.int64)
+        _check(lib().boltz_get_timing(self._h, ms.ctypes.data, cnt.ctypes.data, 5, int(reset)))
+        return dict(zip(self.KINDS, ms.tolist())), dict(zip(self.KINDS, cnt.tolist()))
 
     # -- argument plumbing
     def _ncells(self, x, per_cell):

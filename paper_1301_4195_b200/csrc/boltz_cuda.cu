@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -16,6 +17,7 @@
 #include "fft.cuh"
 #include "transforms.cuh"
 #include "transport.cuh"
+#include "probe.cuh"
 
 namespace boltz_gpu {
 
@@ -46,6 +48,9 @@ static bool supported_n(int n) {
 
 using namespace boltz_gpu;
 
+// kernel classes for timing / launch counting
+enum Kind : int { KIND_CONV = 0, KIND_FFT = 1, KIND_PROJECT = 2, KIND_LAYOUT = 3, KIND_TRANSPORT = 4, kKinds = 5 };
+
 struct boltz_ctx {
     int n = 0;
     double L = 0, lambda = 0, beta = 0, r0 = 0;
@@ -68,11 +73,53 @@ struct boltz_ctx {
     int* hFlag = nullptr;    // pinned
     ProjConst pc{};
     int64_t table_bytes = 0, ws_bytes = 0;
+    // per-kernel-class CUDA-event timing (bench.py roofline) and launch counts
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<int> ev_kind;
+    double ms[kKinds] = {0, 0, 0, 0, 0};
+    int64_t launches[kKinds] = {0, 0, 0, 0, 0};
 };
 
 namespace {
 
 int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
+
+// Brackets one kernel launch with CUDA events on its stream when timing is on.
+struct Timed {
+    boltz_ctx* c;
+    cudaStream_t s;
+    Timed(boltz_ctx* c_, int kind, cudaStream_t s_) : c(c_), s(s_) {
+        c->launches[kind]++;
+        if (!c->timing) return;
+        if (c->ev_used + 2 > c->ev_pool.size()) {
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                c->ev_pool.push_back(e);
+            }
+        }
+        c->ev_kind.push_back(kind);
+        CK(cudaEventRecord(c->ev_pool[c->ev_used], s));
+    }
+    ~Timed() {
+        if (!c->timing) return;
+        cudaEventRecord(c->ev_pool[c->ev_used + 1], s);
+        c->ev_used += 2;
+    }
+};
+
+// after a stream sync: fold the recorded event pairs into the per-kind totals
+void collect_timing(boltz_ctx* c) {
+    for (size_t i = 0; i < c->ev_kind.size(); ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]) == cudaSuccess)
+            c->ms[c->ev_kind[i]] += ms;
+    }
+    c->ev_kind.clear();
+    c->ev_used = 0;
+}
 
 void fill_twiddles() {
     std::vector<double2> tw(kTwTotal);
@@ -201,10 +248,12 @@ void build_table(boltz_ctx* c, const double* G_host) {
 
 void ensure_workspace(boltz_ctx* c, int64_t cells) {
     int64_t want = (cells + kLanes - 1) / kLanes * kLanes;
-    // default capacity: up to ~2 GiB of workspace per context
+    // capacity: up to BOLTZ_WORKSPACE_GB (default 8) GiB of workspace per context
     const int64_t n3 = n3_of(c);
     const int64_t per_cell = n3 * (16 + 16 + 8 + 16 + 16) + 8;
-    int64_t lim = std::max<int64_t>(kLanes, ((int64_t)2 << 30) / per_cell / kLanes * kLanes);
+    double gb = 8.0;
+    if (const char* e = std::getenv("BOLTZ_WORKSPACE_GB")) gb = std::max(0.01, std::atof(e));
+    int64_t lim = std::max<int64_t>(kLanes, (int64_t)(gb * (1 << 30)) / per_cell / kLanes * kLanes);
     want = std::min(want, lim);
     if (want <= c->cap) return;
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut); cudaFree(c->dMaxIm);
@@ -232,10 +281,10 @@ struct Launch {
         const double par = ((N / 2) & 1) ? -1.0 : 1.0;  // ((-1)^{N/2})^3
         const double scale = sv * sv * sv * par;
         dim3 blk(32, 8);
-        k_fft_pass<N, 2, -1, PASS_PACK_FWD><<<pass_grid(ng), blk, 0, s>>>(f, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0);
-        k_fft_pass<N, 1, -1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0);
-        k_fft_pass<N, 0, -1, PASS_FWD_LAST><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc,
-                                                                           scale);
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 2, -1, PASS_PACK_FWD><<<pass_grid(ng), blk, 0, s>>>(f, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0); }
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 1, -1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0); }
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 0, -1, PASS_FWD_LAST><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc,
+                                                                           scale); }
         CK(cudaGetLastError());
     }
     // group complex c->dA -> group complex (s_k * Qhat) in c->dB
@@ -243,7 +292,7 @@ struct Launch {
         const int64_t ng = (nc + 31) / 32;
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-        k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+        { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng); }
         CK(cudaGetLastError());
     }
     // group complex c->dB (already * s_m) -> group real Qt in (double*)c->dA; max|Im| per cell
@@ -255,45 +304,78 @@ struct Launch {
         const double scale = sz * sz * sz;
         dim3 blk(32, 8);
         CK(cudaMemsetAsync(c->dMaxIm, 0, (size_t)nc * 8, s));
-        k_fft_pass<N, 2, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0);
-        k_fft_pass<N, 1, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0);
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 2, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0); }
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 1, +1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dB, nullptr, nullptr, c->dFlag, nc, 1.0); }
         // the INV_LAST pass folds par into the sign of its scale; max|Im| uses |scale|
-        k_fft_pass<N, 0, +1, PASS_INV_LAST><<<pass_grid(ng), blk, 0, s>>>(
-            nullptr, c->dB, reinterpret_cast<double*>(c->dA), c->dMaxIm, c->dFlag, nc, scale * par);
+        { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 0, +1, PASS_INV_LAST><<<pass_grid(ng), blk, 0, s>>>(
+            nullptr, c->dB, reinterpret_cast<double*>(c->dA), c->dMaxIm, c->dFlag, nc, scale * par); }
         CK(cudaGetLastError());
     }
     // group real Qt in (double*)c->dA -> out = base + coef * P_N(Qt)  (user layout)
     static void project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
-        k_project<N><<<(unsigned)ng, 256, 0, s>>>(reinterpret_cast<const double*>(c->dA), base, out, nc, coef, c->pc,
-                                                  c->dFlag);
+        { Timed t_(c, KIND_PROJECT, s); k_project<N><<<(unsigned)ng, 256, 0, s>>>(reinterpret_cast<const double*>(c->dA), base, out, nc, coef, c->pc,
+                                                  c->dFlag); }
         CK(cudaGetLastError());
     }
-    static void pack_complex(const double* in, double2* dst, int64_t nc, int sign, cudaStream_t s) {
+    static void pack_complex(boltz_ctx* c, const double* in, double2* dst, int64_t nc, int sign, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
         dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
-        k_pack_complex<N><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(in), dst, nc, sign);
+        { Timed t_(c, KIND_LAYOUT, s); k_pack_complex<N><<<grid, 256, 0, s>>>(reinterpret_cast<const double2*>(in), dst, nc, sign); }
         CK(cudaGetLastError());
     }
-    static void unpack_complex(const double2* src, double* out, int64_t nc, int sign, cudaStream_t s) {
+    static void unpack_complex(boltz_ctx* c, const double2* src, double* out, int64_t nc, int sign, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
         dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
-        k_unpack_complex<N><<<grid, 256, 0, s>>>(src, reinterpret_cast<double2*>(out), nc, sign);
+        { Timed t_(c, KIND_LAYOUT, s); k_unpack_complex<N><<<grid, 256, 0, s>>>(src, reinterpret_cast<double2*>(out), nc, sign); }
         CK(cudaGetLastError());
     }
-    static void unpack_real(const double* src, double* out, int64_t nc, cudaStream_t s) {
+    static void unpack_real(boltz_ctx* c, const double* src, double* out, int64_t nc, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
         dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
-        k_unpack_real<N><<<grid, 256, 0, s>>>(src, out, nc);
+        { Timed t_(c, KIND_LAYOUT, s); k_unpack_real<N><<<grid, 256, 0, s>>>(src, out, nc); }
         CK(cudaGetLastError());
     }
-    static void pack_real(const double* in, double* dst, int64_t nc, cudaStream_t s) {
+    static void pack_real(boltz_ctx* c, const double* in, double* dst, int64_t nc, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
         dim3 grid((unsigned)std::min<int64_t>((N3 + 7) / 8, 512), (unsigned)ng);
-        k_pack_real<N><<<grid, 256, 0, s>>>(in, dst, nc);
+        { Timed t_(c, KIND_LAYOUT, s); k_pack_real<N><<<grid, 256, 0, s>>>(in, dst, nc); }
         CK(cudaGetLastError());
     }
 };
+
+// DFMA throughput of the whole device, TFLOP/s (2 flops per DFMA)
+double fp64_peak_probe(double seconds) {
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* d = nullptr;
+    CK(cudaMalloc(&d, 8));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = sms * 4, threads = 256;
+    int iters = 1 << 14;
+    double best = 0.0, spent = 0.0;
+    k_dfma_probe<<<blocks, threads>>>(d, iters, 0.999999, 1e-6);  // warm-up
+    CK(cudaDeviceSynchronize());
+    while (spent < seconds * 1e3) {
+        CK(cudaEventRecord(e0));
+        k_dfma_probe<<<blocks, threads>>>(d, iters, 0.999999, 1e-6);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        spent += ms;
+        const double tf = 2.0 * 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+        best = std::max(best, tf);
+        if (ms < 50.0f) iters *= 2;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return best;
+}
 
 template <typename F>
 void dispatch(int n, F&& f) {
@@ -363,6 +445,7 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
     }
     CK(cudaMemcpyAsync(c->hFlag, c->dFlag, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (c->timing) collect_timing(c);
     if (*c->hFlag & 1) {
         set_error("NumericError: non-finite value in the input distribution");
         return BOLTZ_ERR_NUMERIC;
@@ -453,6 +536,7 @@ int boltz_destroy(boltz_ctx* c) {
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     if (c->hFlag) cudaFreeHost(c->hFlag);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return BOLTZ_OK;
 }
@@ -472,7 +556,7 @@ int boltz_forward_batch(boltz_ctx* c, const double* f, double* fhat, int64_t nce
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
                                    Lx::forward(c, in, nc, s);
-                                   Lx::unpack_complex(c->dA, out, nc, 0, s);
+                                   Lx::unpack_complex(c, c->dA, out, nc, 0, s);
                                });
                            });
     });
@@ -486,9 +570,9 @@ int boltz_inverse_batch(boltz_ctx* c, const double* g, double* f, double* max_im
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
-                                   Lx::pack_complex(in, c->dB, nc, 1, s);
+                                   Lx::pack_complex(c, in, c->dB, nc, 1, s);
                                    Lx::inverse(c, nc, s);
-                                   Lx::unpack_real(reinterpret_cast<const double*>(c->dA), out, nc, s);
+                                   Lx::unpack_real(c, reinterpret_cast<const double*>(c->dA), out, nc, s);
                                });
                            });
     });
@@ -501,9 +585,9 @@ int boltz_qhat_batch(boltz_ctx* c, const double* fhat, double* qhat, int64_t nce
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
-                                   Lx::pack_complex(in, c->dA, nc, 0, s);
+                                   Lx::pack_complex(c, in, c->dA, nc, 0, s);
                                    Lx::conv(c, nc, s);
-                                   Lx::unpack_complex(c->dB, out, nc, 1, s);
+                                   Lx::unpack_complex(c, c->dB, out, nc, 1, s);
                                });
                            });
     });
@@ -516,7 +600,7 @@ int boltz_conserve_batch(boltz_ctx* c, const double* q_raw, double* q, int64_t n
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
-                                   Lx::pack_real(in, reinterpret_cast<double*>(c->dA), nc, s);
+                                   Lx::pack_real(c, in, reinterpret_cast<double*>(c->dA), nc, s);
                                    Lx::project(c, nullptr, out, nc, 1.0, s);
                                });
                            });
@@ -573,9 +657,13 @@ int boltz_transport_step(boltz_ctx* c, const double* field, double* out, int64_t
             return BOLTZ_ERR_CONFIG;
         }
         cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
-        launch_transport(c->n, field, out, ncl, x_ext, dx_ext, dt, wall_left, wall_right, c->pc.dv, s);
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_transport(c->n, field, out, ncl, x_ext, dx_ext, dt, wall_left, wall_right, c->pc.dv, s);
+        }
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
+        if (c->timing) collect_timing(c);
         return BOLTZ_OK;
     });
 }
@@ -599,14 +687,49 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
             ensure_workspace(c, kLanes);
             dsig = reinterpret_cast<double*>(c->dMaxIm);
         }
-        launch_fill_boundary(c->n, field, ncl, x_ext, side, kind, Tw, vw[0], vw[1], vw[2], c->pc.dv, dsig, s);
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_fill_boundary(c->n, field, ncl, x_ext, side, kind, Tw, vw[0], vw[1], vw[2], c->pc.dv, dsig, s);
+        }
         CK(cudaGetLastError());
         double hs = 0.0;
         CK(cudaMemcpyAsync(&hs, dsig, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (c->timing) collect_timing(c);
         if (sigma_w) *sigma_w = hs;
         return BOLTZ_OK;
     });
+}
+
+int boltz_set_timing(boltz_ctx* c, int enable) {
+    if (!c) return BOLTZ_ERR_CONFIG;
+    c->timing = enable != 0;
+    return BOLTZ_OK;
+}
+
+int boltz_get_timing(boltz_ctx* c, double* ms, int64_t* launches, int nkinds, int reset) {
+    if (!c || nkinds < 0) return BOLTZ_ERR_CONFIG;
+    for (int k = 0; k < nkinds && k < kKinds; ++k) {
+        if (ms) ms[k] = c->ms[k];
+        if (launches) launches[k] = c->launches[k];
+    }
+    if (reset)
+        for (int k = 0; k < kKinds; ++k) {
+            c->ms[k] = 0.0;
+            c->launches[k] = 0;
+        }
+    return BOLTZ_OK;
+}
+
+int boltz_fp64_peak(int device, double seconds, double* tflops) {
+    try {
+        CK(cudaSetDevice(device));
+        *tflops = fp64_peak_probe(seconds);
+        return BOLTZ_OK;
+    } catch (const CudaError& e) {
+        set_error(e.msg);
+        return BOLTZ_ERR_CUDA;
+    }
 }
 
 }  // extern "C"
