@@ -109,11 +109,14 @@ int boltz_rk2_batch(boltz_ctx* ctx, double* f, int64_t ncells, double dt, double
  * N^3 (2 ghost cells per side) whose ghosts are already filled
  * (halo exchange / boltz_fill_boundary).  x_ext, dx_ext: DEVICE arrays of the
  * ncl+4 cell centres/widths.  wall_left/right: zero slope at a wall
- * (SPEC.md:336,359).  `out` (device, same shape) receives the updated field;
- * its ghost cells are copied through.
+ * (SPEC.md:336,359).  `out` (device, same shape, not aliasing field/base)
+ * receives alpha*base + (1-alpha)*step(field) on interior cells (base NULL:
+ * the plain step), its ghost cells are copied through.  base/alpha fuse the
+ * second stage of the SSP-RK2 transport sub-step.
  */
-int boltz_transport_step(boltz_ctx* ctx, const double* field, double* out, int64_t ncl, const double* x_ext,
-                         const double* dx_ext, double dt, int wall_left, int wall_right, void* stream);
+int boltz_transport_step(boltz_ctx* ctx, const double* field, const double* base, double alpha, double* out,
+                         int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                         int wall_right, void* stream);
 
 /*
  * Ghost fill at a physical end (side 0 = left, 1 = right) of a device field:

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -71,7 +72,8 @@ def lib():
             raise RuntimeError(
                 f"{_LIB_PATH} is missing: run `python -m paper_1301_4195_b200.build` "
                 "(there is no CPU fallback for the collision path)")
-        L = C.CDLL(str(_LIB_PATH))
+        path = os.environ.get("BOLTZ_LIB_VARIANT") or str(_LIB_PATH)  # dev: A/B kernel variants
+        L = C.CDLL(path)
         vp, i, d, i64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
         dp = C.POINTER(C.c_double)
         sig = {
@@ -86,7 +88,7 @@ def lib():
             "boltz_conserve_batch": (i, [vp, vp, vp, i64, i, vp]),
             "boltz_collide_batch": (i, [vp, vp, vp, i64, d, vp, i, vp]),
             "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
-            "boltz_transport_step": (i, [vp, vp, vp, i64, vp, vp, d, i, i, vp]),
+            "boltz_transport_step": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
             "boltz_set_timing": (i, [vp, i]),
             "boltz_get_timing": (i, [vp, vp, vp, i, i]),
@@ -378,13 +380,18 @@ class CollisionOperator:
         return f
 
     # -- transport (device tensors only)
-    def transport_step(self, field, out, x_ext, dx_ext, dt, wall_left=False, wall_right=False):
-        """transport_step on a (ncl+4, N^3) device field."""
+    def transport_step(self, field, out, x_ext, dx_ext, dt, wall_left=False, wall_right=False, base=None,
+                       alpha=0.0):
+        """transport_step on a (ncl+4, N^3) device field:
+        out = alpha*base + (1-alpha)*step(field) (base=None: the plain step)."""
         ncl = field.shape[0] - 4
-        (pf, po, px, pd), mem, s = self._args(field, out, x_ext, dx_ext)
+        arrs = (field, out, x_ext, dx_ext) + ((base,) if base is not None else ())
+        ptrs, mem, s = self._args(*arrs)
         if mem != MEM_DEVICE:
             raise ConfigError("transport_step takes CUDA tensors")
-        _check(lib().boltz_transport_step(self._h, pf, po, ncl, px, pd, dt, int(wall_left), int(wall_right), s))
+        pb = ptrs[4] if base is not None else None
+        _check(lib().boltz_transport_step(self._h, ptrs[0], pb, alpha, ptrs[1], ncl, ptrs[2], ptrs[3], dt,
+                                          int(wall_left), int(wall_right), s))
         return out
 
     def fill_boundary(self, field, x_ext, side, kind, Tw=1.0, Vw=(0.0, 0.0, 0.0)):

@@ -35,12 +35,14 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _inputs())
 
 
-def build(verbose: bool = False, force: bool = False) -> pathlib.Path:
-    if not force and up_to_date():
+def build(verbose: bool = False, force: bool = False, out: pathlib.Path = LIB, defines=()) -> pathlib.Path:
+    """Compile libboltz_cuda.so (or a development variant with extra -D defines)."""
+    if not force and out == LIB and up_to_date():
         return LIB
+    out.parent.mkdir(parents=True, exist_ok=True)
     cmd = [
         _nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC,-fopenmp",
-        "-ccbin", "/usr/bin/g++", "-o", str(LIB), *map(str, SOURCES), "-lgomp",
+        "-ccbin", "/usr/bin/g++", *[f"-D{d}" for d in defines], "-o", str(out), *map(str, SOURCES), "-lgomp",
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -649,17 +649,19 @@ int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double i
     });
 }
 
-int boltz_transport_step(boltz_ctx* c, const double* field, double* out, int64_t ncl, const double* x_ext,
-                         const double* dx_ext, double dt, int wall_left, int wall_right, void* stream) {
+int boltz_transport_step(boltz_ctx* c, const double* field, const double* base, double alpha, double* out,
+                         int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                         int wall_right, void* stream) {
     return api(c, [&] {
-        if (ncl < 1 || !field || !out || !x_ext || !dx_ext) {
-            set_error("transport_step: invalid arguments");
+        if (ncl < 1 || !field || !out || !x_ext || !dx_ext || out == field || (base && out == base)) {
+            set_error("transport_step: invalid arguments (out must not alias field/base)");
             return BOLTZ_ERR_CONFIG;
         }
         cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
         {
             Timed t_(c, KIND_TRANSPORT, s);
-            launch_transport(c->n, field, out, ncl, x_ext, dx_ext, dt, wall_left, wall_right, c->pc.dv, s);
+            launch_transport(c->n, field, base, base ? alpha : 0.0, out, ncl, x_ext, dx_ext, dt, wall_left,
+                             wall_right, c->pc.dv, s);
         }
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));

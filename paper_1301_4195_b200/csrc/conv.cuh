@@ -47,7 +47,16 @@ __host__ __device__ constexpr int band_slab_kc(int n, int t) {
 
 // register tile width per N (accumulators + y window = 8T registers)
 __host__ __device__ constexpr int conv_tile(int n) { return n == 24 ? 12 : (n == 32 ? 16 : n); }
-constexpr int kConvWarps = 4;  // cell groups per CTA (share the H stream via L1)
+#ifndef BOLTZ_CONV_WARPS
+#define BOLTZ_CONV_WARPS 4
+#endif
+#ifndef BOLTZ_CONV_MINB
+#define BOLTZ_CONV_MINB 1
+#endif
+#ifndef BOLTZ_CONV_PREFETCH
+#define BOLTZ_CONV_PREFETCH 0
+#endif
+constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the H stream via L1)
 
 template <int N, int T, int KC>
 __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const double* __restrict__ H,
@@ -57,6 +66,18 @@ __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const 
     constexpr int SLAB = NK * SLAB_KC;
     for (int e = e0; e < e1; ++e) {
         const int2 en = __ldg(ent + e);
+#if BOLTZ_CONV_PREFETCH
+        if (e + 1 < e1) {  // pull the next row pair into L1 while this one computes
+            const int2 nx = __ldg(ent + e + 1);
+            const double2* Xn = Ag + (size_t)nx.x * kLanes;
+            const double2* Yn = Ag + (size_t)nx.y * kLanes;
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + (size_t)j * kLanes));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(Yn + (size_t)j * kLanes));
+            }
+        }
+#endif
         const double2* X = Ag + (size_t)en.x * kLanes;
         const double2* Y = Ag + (size_t)en.y * kLanes;
         const double2* Hs = reinterpret_cast<const double2*>(H + (size_t)e * SLAB + KC * SLAB_KC);
@@ -95,7 +116,7 @@ __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const 
 // grid = (N*N*NK, ceil(ngroups / W)); block = 32*W.  Output B carries the
 // inverse transform's input sign s_k (transforms.cuh).
 template <int N>
-__global__ void __launch_bounds__(kLanes* kConvWarps)
+__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_CONV_MINB)
 k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
        const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
     constexpr int T = conv_tile(N);

@@ -16,10 +16,13 @@ __device__ __forceinline__ double minmod3(double a, double b, double c) {
 }
 
 // grid = (ceil(N^3/256), ncl + 4); ghosts are copied through.
+// out = alpha*base + (1-alpha)*(f - dt/dx (F_{j+1/2} - F_{j-1/2}))   (base may be null)
+// -- the second stage of the SSP-RK2 transport sub-step fused in.
 template <int N>
 __global__ void __launch_bounds__(256)
-k_transport(const double* __restrict__ f, double* __restrict__ out, long long ncl, const double* __restrict__ x,
-            const double* __restrict__ dx, double dt, int wl, int wr, double dv) {
+k_transport(const double* __restrict__ f, const double* __restrict__ base, double alpha, double* __restrict__ out,
+            long long ncl, const double* __restrict__ x, const double* __restrict__ dx, double dt, int wl, int wr,
+            double dv) {
     constexpr int N3 = N * N * N;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const long long ce = blockIdx.y;
@@ -51,7 +54,8 @@ k_transport(const double* __restrict__ f, double* __restrict__ out, long long nc
         Fl = v1 * (fv[2] - 0.5 * dx[ce] * sg[1]);
         Fr = v1 * (fv[3] - 0.5 * dx[ce + 1] * sg[2]);
     }
-    out[ce * N3 + j] = fv[2] - dt / dx[ce] * (Fr - Fl);
+    const double upd = fv[2] - dt / dx[ce] * (Fr - Fl);
+    out[ce * N3 + j] = base ? alpha * base[ce * N3 + j] + (1.0 - alpha) * upd : upd;
 }
 
 // one block of 256 threads; sigma_w written to sig[0]
@@ -102,13 +106,14 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
     if (threadIdx.x == 0) sig[0] = sw;
 }
 
-inline void launch_transport(int n, const double* f, double* out, long long ncl, const double* x, const double* dx,
-                             double dt, int wl, int wr, double dv, cudaStream_t s) {
+inline void launch_transport(int n, const double* f, const double* base, double alpha, double* out, long long ncl,
+                             const double* x, const double* dx, double dt, int wl, int wr, double dv,
+                             cudaStream_t s) {
     switch (n) {
 #define BOLTZ_TR(N)                                                                                        \
     case N: {                                                                                              \
         dim3 grid((N * N * N + 255) / 256, (unsigned)(ncl + 4));                                          \
-        k_transport<N><<<grid, 256, 0, s>>>(f, out, ncl, x, dx, dt, wl, wr, dv);                           \
+        k_transport<N><<<grid, 256, 0, s>>>(f, base, alpha, out, ncl, x, dx, dt, wl, wr, dv);              \
     } break;
         BOLTZ_FOR_EACH_N(BOLTZ_TR)
 #undef BOLTZ_TR

@@ -1,0 +1,202 @@
+"""Space-inhomogeneous driver: Strang splitting of second-order FV transport
+and the GPU collision RK2, with the spatial domain sharded across ranks
+(SPEC.md:372-481).
+
+    strang_step(dt) = T(dt/2) o C_RK2(dt) o T(dt/2)
+    T(h): ghost fill (halo exchange / wall / extrapolation), then one explicit
+          FV step -- single stage, SURVEY Appendix A.4
+    C_RK2(dt): boltz_rk2_batch over the rank's interior cells -- cell-local,
+          no communication
+
+Decomposition: contiguous cell ranges balanced to +-1.
+Halo: each transport sub-step refreshes 2 ghost cells per side
+(SPEC.md:296,448,471); the two edge cells of a rank are one contiguous
+2*N^3 block, so one send + one recv per neighbour (grouped P2P via
+torch.distributed -- NCCL over NVLink on GPUs, gloo on CPU), with no
+even/odd ordering needed.  LoopbackHalo runs n virtual
+ranks in one process (the SPEC's required in-process backend).
+
+The field layout is the reference's DistributionField: (n_local + 4) x N^3,
+ghosts at 0,1 and n_local+2, n_local+3.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from .boltz import CollisionOperator, ConfigError, NumericError
+from .scenarios import extend_ghosts
+
+
+def plan_decomposition(ncells: int, nranks: int) -> List[Tuple[int, int]]:
+    """(start, count) per rank; contiguous, ordered, |count_r - count_s| <= 1,
+    larger ranges first.  More ranks than cells -> error."""
+    if nranks < 1 or ncells < nranks:
+        raise ConfigError(f"plan_decomposition: {nranks} ranks for {ncells} cells")
+    base, rem = divmod(ncells, nranks)
+    out, s = [], 0
+    for r in range(nranks):
+        c = base + (1 if r < rem else 0)
+        out.append((s, c))
+        s += c
+    return out
+
+
+@dataclass
+class Boundary:
+    """Physical end condition: kind 'extrap' (linear extrapolation,
+    SPEC.md:318) or 'wall' (diffuse Maxwell wall)."""
+    kind: str = "extrap"
+    Tw: float = 1.0
+    Vw: Tuple[float, float, float] = (0.0, 0.0, 0.0)
+
+    def code(self) -> int:
+        if self.kind not in ("extrap", "wall"):
+            raise ConfigError(f"unknown boundary kind {self.kind!r}")
+        return 1 if self.kind == "wall" else 0
+
+
+class TorchHalo:
+    """Two-ghost-cell exchange with the left/right neighbour ranks over
+    torch.distributed (NCCL on GPUs, gloo on CPU).  Works on any (ncl+4, M)
+    tensor whose rows are cells."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.rank, self.world, self.group = rank, world, group
+
+    def exchange(self, field) -> int:
+        import torch.distributed as dist
+        ncl = field.shape[0] - 4
+        ops = []
+        if self.rank > 0:
+            ops.append(dist.P2POp(dist.isend, field[2:4].contiguous(), self.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, field[0:2], self.rank - 1, self.group))
+        if self.rank < self.world - 1:
+            ops.append(dist.P2POp(dist.isend, field[ncl:ncl + 2].contiguous(), self.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, field[ncl + 2:ncl + 4], self.rank + 1, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return len(ops) // 2
+
+
+class LoopbackHalo:
+    """In-process backend over a list of per-rank fields."""
+
+    @staticmethod
+    def exchange_all(fields: Sequence) -> None:
+        for r in range(len(fields) - 1):
+            a, b = fields[r], fields[r + 1]
+            ncl = a.shape[0] - 4
+            a[ncl + 2:ncl + 4] = b[2:4]   # right ghosts of r = first two interior of r+1
+            b[0:2] = a[ncl:ncl + 2]       # left ghosts of r+1 = last two interior of r
+
+
+class Solver1D:
+    """One rank's share of a 1D-in-space kinetic problem on the GPU.
+
+    x, dx: global cell centres / widths (Nx); f0: global initial field
+    (Nx, N^3) or a callable(start, count) -> (count, N^3) (so ranks only
+    build their own cells).
+    """
+
+    def __init__(self, op: CollisionOperator, x: np.ndarray, dx: np.ndarray, f0, *, rank: int = 0,
+                 world: int = 1, left: Boundary = Boundary(), right: Boundary = Boundary(),
+                 epsilon: float = 1.0, halo=None, device=None, plan=None):
+        import torch
+        self.op, self.rank, self.world, self.eps = op, rank, world, epsilon
+        self.left, self.right = left, right
+        self.n3 = op.grid.size()
+        plan = plan or plan_decomposition(len(x), world)
+        self.start, self.ncl = plan[rank]
+        if self.ncl < 2:
+            raise ConfigError("each rank needs at least 2 cells (2-cell halo, SPEC.md:438)")
+        xe, dxe = extend_ghosts(np.asarray(x, float), np.asarray(dx, float))
+        self.x_glob, self.dx_glob = np.asarray(x, float), np.asarray(dx, float)
+        sl = slice(self.start, self.start + self.ncl + 4)
+        self.device = device if device is not None else torch.device("cuda", op.device)
+        self.x_ext = torch.from_numpy(xe[sl].copy()).to(self.device)
+        self.dx_ext = torch.from_numpy(dxe[sl].copy()).to(self.device)
+        self.field = torch.zeros((self.ncl + 4, self.n3), dtype=torch.float64, device=self.device)
+        init = f0(self.start, self.ncl) if callable(f0) else np.asarray(f0)[self.start:self.start + self.ncl]
+        self.field[2:self.ncl + 2] = torch.from_numpy(np.ascontiguousarray(init, dtype=np.float64)).to(self.device)
+        self._tmp = torch.empty_like(self.field)
+        self._tmp2 = torch.empty_like(self.field)
+        self.halo = halo if halo is not None else (TorchHalo(rank, world) if world > 1 else None)
+        self.is_left_end = rank == 0
+        self.is_right_end = rank == world - 1
+        self.sigma_w = {}
+        self.t = 0.0
+
+    @property
+    def interior(self):
+        return self.field[2:self.ncl + 2]
+
+    def cfl_dt(self, cfl: float = 0.9) -> float:
+        """dt <= cfl * min dx / L; global min."""
+        return cfl * float(self.dx_glob.min()) / self.op.grid.half_width
+
+    def fill_ghosts(self, exchange: bool = True) -> None:
+        if exchange and self.halo is not None:
+            self.halo.exchange(self.field)
+        if self.is_left_end:
+            self.sigma_w[0] = self.op.fill_boundary(self.field, self.x_ext, 0, self.left.code(), self.left.Tw,
+                                                    self.left.Vw)
+        if self.is_right_end:
+            self.sigma_w[1] = self.op.fill_boundary(self.field, self.x_ext, 1, self.right.code(), self.right.Tw,
+                                                    self.right.Vw)
+
+    def _walls(self):
+        return (self.is_left_end and self.left.kind == "wall", self.is_right_end and self.right.kind == "wall")
+
+    def transport_stage(self, stage: int, dt: float, exchange: bool = True) -> None:
+        """SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
+        stage 1: f <- f/2 + S(t1)/2, S = one FV step after a
+        ghost refresh of its input."""
+        wl, wr = self._walls()
+        if stage == 0:
+            self.fill_ghosts(exchange)
+            self.op.transport_step(self.field, self._tmp, self.x_ext, self.dx_ext, dt, wl, wr)
+        else:
+            self.field, self._tmp = self._tmp, self.field  # field = t1, _tmp = f^n
+            self.fill_ghosts(exchange)
+            out = self._tmp2
+            self.op.transport_step(self.field, out, self.x_ext, self.dx_ext, dt, wl, wr, base=self._tmp, alpha=0.5)
+            self._tmp2 = self.field
+            self.field = out
+
+    def transport(self, dt: float, exchange: bool = True) -> None:
+        """Transport sub-step T(dt): SSP-RK2 of the FV step."""
+        if dt * self.op.grid.half_width > float(self.dx_glob.min()) * (1 + 1e-12):
+            raise ConfigError("transport: CFL violated (dt * L > min dx)")
+        self.transport_stage(0, dt, exchange)
+        self.transport_stage(1, dt, exchange)
+
+    def collide(self, dt: float) -> None:
+        interior = self.field[2:self.ncl + 2]  # contiguous rows -> in place on device
+        self.op.collision_rk2(interior, dt, self.eps)
+
+    def strang_step(self, dt: float) -> None:
+        self.transport(0.5 * dt)
+        self.collide(dt)
+        self.transport(0.5 * dt)
+        self.t += dt
+
+
+def strang_step_loopback(solvers: Sequence[Solver1D], dt: float) -> None:
+    """One Strang step of n virtual ranks in one process (LoopbackHalo)."""
+    for half in (0, 1):
+        for stage in (0, 1):
+            if stage == 1:  # the stage-1 input t1 lives in _tmp until transport_stage swaps it in
+                LoopbackHalo.exchange_all([s._tmp for s in solvers])
+            else:
+                LoopbackHalo.exchange_all([s.field for s in solvers])
+            for s in solvers:
+                s.transport_stage(stage, 0.5 * dt, exchange=False)
+        if half == 0:
+            for s in solvers:
+                s.collide(dt)
+    for s in solvers:
+        s.t += dt

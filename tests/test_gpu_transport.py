@@ -1,0 +1,138 @@
+"""K4 transport / ghost fill and the Strang driver vs the CPU oracle (GPU)."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_max, table
+from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, scenarios
+from paper_1301_4195_b200.solver import Boundary, Solver1D, plan_decomposition, strang_step_loopback
+
+pytestmark = pytest.mark.gpu
+
+
+def _op(n, L):
+    return CollisionOperator(VelocityGrid.create(n, L), KernelSpec(1.0), table(n, L))
+
+
+@pytest.mark.parametrize("wl,wr", [(0, 0), (1, 0), (1, 1)])
+def test_transport_step_vs_oracle(gpu, O, wl, wr):
+    n, L, nx = 8, 5.0, 12
+    x, dx = scenarios.geometric_grid(nx, 3.0, 1.15)
+    xe, dxe = scenarios.extend_ghosts(x, dx)
+    rng = np.random.default_rng(1)
+    field = rng.random((nx + 4, n ** 3))
+    base = rng.random((nx + 4, n ** 3))
+    dt = 0.8 * dx.min() / L
+    ref = O.transport_step(n, L, field, xe, dxe, dt, wl, wr)
+    with _op(n, L) as op:
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(gpu)  # noqa: E731
+        out = torch.empty_like(d(field))
+        op.transport_step(d(field), out, d(xe), d(dxe), dt, wl, wr)
+        assert rel_max(out.cpu().numpy(), ref) < 1e-13
+        out2 = torch.empty_like(out)
+        op.transport_step(d(field), out2, d(xe), d(dxe), dt, wl, wr, base=d(base), alpha=0.5)
+        exp = ref.copy()
+        exp[2:nx + 2] = 0.5 * base[2:nx + 2] + 0.5 * ref[2:nx + 2]
+        assert rel_max(out2.cpu().numpy(), exp) < 1e-13
+
+
+@pytest.mark.parametrize("side,kind", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_fill_boundary_vs_oracle(gpu, O, side, kind):
+    n, L, nx = 8, 5.0, 6
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    xe, _ = scenarios.extend_ghosts(x, dx)
+    rng = np.random.default_rng(2)
+    field = rng.random((nx + 4, n ** 3))
+    ref = field.copy()
+    sref = O.fill_boundary(n, L, ref, xe, side, kind, Tw=2.0, Vw=(0.1, 0.0, 0.0))
+    with _op(n, L) as op:
+        f = torch.from_numpy(field).to(gpu)
+        s = op.fill_boundary(f, torch.from_numpy(xe).to(gpu), side, kind, Tw=2.0, Vw=(0.1, 0.0, 0.0))
+    assert rel_max(f.cpu().numpy(), ref) < 1e-13
+    assert abs(s - sref) <= 1e-13 * max(1.0, abs(sref))
+
+
+def _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, steps):
+    """Strang step composed from the oracle's primitives,
+    transport sub-step = SSP-RK2 of the FV step."""
+    nx = field.shape[0] - 4
+
+    def fill(f):
+        O.fill_boundary(n, L, f, xe, 0, 1, Tw=Tw)
+        O.fill_boundary(n, L, f, xe, 1, 0)
+
+    def T(f, h):
+        fill(f)
+        t1 = O.transport_step(n, L, f, xe, dxe, h, 1, 0)
+        fill(t1)
+        t2 = O.transport_step(n, L, t1, xe, dxe, h, 1, 0)
+        out = t1.copy()
+        out[2:nx + 2] = 0.5 * f[2:nx + 2] + 0.5 * t2[2:nx + 2]
+        return out
+
+    for _ in range(steps):
+        field = T(field, 0.5 * dt)
+        field[2:nx + 2] = O.collision_rk2(n, L, G, field[2:nx + 2], dt)
+        field = T(field, 0.5 * dt)
+    return field
+
+
+def test_strang_wall_problem_vs_oracle(gpu, O):
+    """cfg3 in miniature: gas at rest, diffuse wall T_w=2 at x=0, geometric grid."""
+    n, L, nx, Tw = 8, 5.0, 10, 2.0
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    xe, dxe = scenarios.extend_ghosts(x, dx)
+    grid = VelocityGrid.create(n, L)
+    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (nx, 1))
+    G = table(n, L)
+    with _op(n, L) as op:
+        s = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw), right=Boundary("extrap"))
+        dt = s.cfl_dt()
+        for _ in range(4):
+            s.strang_step(dt)
+        got = s.interior.cpu().numpy()
+    field = np.zeros((nx + 4, n ** 3))
+    field[2:nx + 2] = f0
+    ref = _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, 4)[2:nx + 2]
+    assert rel_max(got - f0, ref - f0) < 1e-9
+    assert np.abs(got - f0).max() > 1e-6  # the wall did something
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_decomposition_transparency_bitwise(gpu, nranks):
+    """N=8, M_x=8 wall-heating trajectories for n ranks are
+    bit-identical to n=1 (loopback backend, one GPU)."""
+    n, L, nx, Tw = 8, 5.0, 8, 2.0
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.05)
+    grid = VelocityGrid.create(n, L)
+    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (nx, 1))
+    with _op(n, L) as op:
+        single = [Solver1D(op, x, dx, f0, left=Boundary("wall", Tw))]
+        plan = plan_decomposition(nx, nranks)
+        multi = [Solver1D(op, x, dx, f0, rank=r, world=nranks, left=Boundary("wall", Tw), plan=plan, halo=False)
+                 for r in range(nranks)]
+        for m in multi:
+            m.halo = None
+        dt = single[0].cfl_dt()
+        for _ in range(5):
+            strang_step_loopback(single, dt)
+            strang_step_loopback(multi, dt)
+        a = single[0].interior.cpu().numpy()
+        b = np.concatenate([m.interior.cpu().numpy() for m in multi])
+    assert np.array_equal(a, b)
+
+
+def test_uniform_equilibrium_is_quiescent(gpu):
+    """wall at the gas temperature, uniform equilibrium -> stays
+    near equilibrium (bounded by the discrete equilibrium residual)."""
+    n, L, nx = 8, 5.0, 8
+    x, dx = scenarios.uniform_grid(nx, 0.0, 4.0)
+    grid = VelocityGrid.create(n, L)
+    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (nx, 1))
+    with _op(n, L) as op:
+        s = Solver1D(op, x, dx, f0, left=Boundary("wall", 1.0), right=Boundary("extrap"))
+        dt = s.cfl_dt()
+        for _ in range(10):
+            s.strang_step(dt)
+        got = s.interior.cpu().numpy()
+    assert np.abs(got - f0).max() < 5e-2 * f0.max()
