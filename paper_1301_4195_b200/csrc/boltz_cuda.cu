@@ -292,6 +292,20 @@ struct Launch {
         const int64_t ng = (nc + 31) / 32;
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+#if BOLTZ_CONV_PIPE
+        if constexpr (NK == 1) {
+            const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
+            static bool configured = false;  // per process; attributes apply to every device
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_conv_pipe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                CK(cudaFuncSetAttribute(k_conv_pipe<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                configured = true;
+            }
+            Timed t_(c, KIND_CONV, s);
+            k_conv_pipe<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
+                                                                    (int)ng);
+        } else
+#endif
         { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng); }
         CK(cudaGetLastError());
     }

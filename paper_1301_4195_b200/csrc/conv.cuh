@@ -56,6 +56,9 @@ __host__ __device__ constexpr int conv_tile(int n) { return n == 24 ? 12 : (n ==
 #ifndef BOLTZ_CONV_PREFETCH
 #define BOLTZ_CONV_PREFETCH 0
 #endif
+#ifndef BOLTZ_CONV_PIPE
+#define BOLTZ_CONV_PIPE 1  // cp.async-pipelined kernel for N <= 16
+#endif
 constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the H stream via L1)
 
 template <int N, int T, int KC>
@@ -141,6 +144,116 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
         const int k3 = kc * T + kk;
         const double s = ((k1 + k2 + k3) & 1) ? -1.0 : 1.0;
         Bg[(size_t)k3 * kLanes] = make_double2(s * acc[kk].x, s * acc[kk].y);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2, pipelined variant for a single register tile (T == N, i.e. N <= 16).
+// Each warp owns a private shared-memory ring: while row pair e is computed
+// from registers (y, accumulators) and shared memory (x, H), cp.async streams
+// row pair e+1's x row, y row and H slab in behind it, so no global-memory
+// latency is exposed at row boundaries (the stall that bounded k_conv).
+//   per warp: x[2][N][32] + y[N][32] double2, H[2][SLAB] double
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <int N>
+struct PipeLayout {
+    static constexpr int SLAB = band_slab_kc(N, N);                   // doubles, even
+    static constexpr int X_BYTES = N * kLanes * 16;                   // one row of 32 cells
+    static constexpr int H_BYTES = SLAB * 8;
+    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES;      // x[2], y, H[2]
+};
+
+template <int N>
+__device__ __forceinline__ void pipe_issue(char* wsm, int buf, const double2* __restrict__ Ag, const double* H,
+                                           int2 en, int e, int lane) {
+    using PL = PipeLayout<N>;
+    double2* xs = reinterpret_cast<double2*>(wsm + buf * PL::X_BYTES);
+    double2* ys = reinterpret_cast<double2*>(wsm + 2 * PL::X_BYTES);
+    char* hs = wsm + 3 * PL::X_BYTES + buf * PL::H_BYTES;
+    const double2* X = Ag + (size_t)en.x * kLanes;
+    const double2* Y = Ag + (size_t)en.y * kLanes;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        cp_async16(xs + j * kLanes + lane, X + (size_t)j * kLanes);
+        cp_async16(ys + j * kLanes + lane, Y + (size_t)j * kLanes);
+    }
+    const char* hg = reinterpret_cast<const char*>(H + (size_t)e * PL::SLAB);
+    for (int o = lane * 16; o < PL::H_BYTES; o += kLanes * 16) cp_async16(hs + o, hg + o);
+    cp_async_commit();
+}
+
+template <int N>
+__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
+k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+            const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+    using PL = PipeLayout<N>;
+    constexpr int N3 = N * N * N;
+    extern __shared__ __align__(16) char smem[];
+    const int row = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * kConvWarps + wid;
+    if (g >= ngroups) return;  // whole warp exits together; warps never sync across each other
+    char* wsm = smem + wid * PL::WARP_BYTES;
+    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
+    const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
+    double2 acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) acc[i] = make_double2(0.0, 0.0);
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    double2 y[N];
+    if (e0 < e1) {
+        pipe_issue<N>(wsm, 0, Ag, H, __ldg(ent + e0), e0, lane);
+        cp_async_wait_all();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < N; ++j) y[j] = ys[j * kLanes + lane];
+    }
+    for (int e = e0; e < e1; ++e) {
+        const int cur = (e - e0) & 1;
+        __syncwarp();  // every lane is done reading the buffers the next issue overwrites
+        if (e + 1 < e1) pipe_issue<N>(wsm, cur ^ 1, Ag, H, __ldg(ent + e + 1), e + 1, lane);
+        const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
+        const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
+        int p = 0;
+        double2 hb = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int m3 = 0; m3 < N; ++m3) {
+            const double2 xm = xs[m3 * kLanes + lane];
+#pragma unroll
+            for (int kk = 0; kk < N; ++kk) {
+                if (!band_term(N, N, 0, 0, m3, kk)) continue;
+                const int j = kk - m3 + N / 2;
+                double h;
+                if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
+                else h = hb.y;
+                ++p;
+                const double tr = fma(xm.x, y[j].x, -xm.y * y[j].y);
+                const double ti = fma(xm.x, y[j].y, xm.y * y[j].x);
+                acc[kk].x = fma(h, tr, acc[kk].x);
+                acc[kk].y = fma(h, ti, acc[kk].y);
+            }
+        }
+        if (e + 1 < e1) {
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < N; ++j) y[j] = ys[j * kLanes + lane];
+        }
+    }
+    const int k1 = row / N, k2 = row % N;
+    double2* Bg = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk) {
+        const double s = ((k1 + k2 + kk) & 1) ? -1.0 : 1.0;
+        Bg[(size_t)kk * kLanes] = make_double2(s * acc[kk].x, s * acc[kk].y);
     }
 }
 
