@@ -18,6 +18,11 @@
 #include "transforms.cuh"
 #include "transport.cuh"
 #include "probe.cuh"
+#include "fused.cuh"
+
+#ifndef BOLTZ_FUSED
+#define BOLTZ_FUSED 1  // single-kernel K1 / K3 when the N^3 cube fits in shared memory
+#endif
 
 namespace boltz_gpu {
 
@@ -280,6 +285,21 @@ struct Launch {
         const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
         const double par = ((N / 2) & 1) ? -1.0 : 1.0;  // ((-1)^{N/2})^3
         const double scale = sv * sv * sv * par;
+#if BOLTZ_FUSED
+        if constexpr (Fused<N>::FITS) {
+            using F = Fused<N>;
+            static bool configured = false;
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_fwd_fused<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+                configured = true;
+            }
+            Timed t_(c, KIND_FFT, s);
+            k_fwd_fused<N><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(f, c->dA, nc, scale,
+                                                                                          c->dFlag);
+            CK(cudaGetLastError());
+            return;
+        }
+#endif
         dim3 blk(32, 8);
         { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 2, -1, PASS_PACK_FWD><<<pass_grid(ng), blk, 0, s>>>(f, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0); }
         { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 1, -1, PASS_MID><<<pass_grid(ng), blk, 0, s>>>(nullptr, c->dA, nullptr, nullptr, c->dFlag, nc, 1.0); }
@@ -324,6 +344,31 @@ struct Launch {
         { Timed t_(c, KIND_FFT, s); k_fft_pass<N, 0, +1, PASS_INV_LAST><<<pass_grid(ng), blk, 0, s>>>(
             nullptr, c->dB, reinterpret_cast<double*>(c->dA), c->dMaxIm, c->dFlag, nc, scale * par); }
         CK(cudaGetLastError());
+    }
+    // group complex c->dB -> out = base + coef * P_N(Re iFFT) (user layout); max|Im| -> c->dMaxIm
+    static void inverse_project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef,
+                                cudaStream_t s) {
+#if BOLTZ_FUSED
+        if constexpr (Fused<N>::FITS) {
+            using F = Fused<N>;
+            const int64_t ng = (nc + 31) / 32;
+            const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
+            const double par = ((N / 2) & 1) ? -1.0 : 1.0;
+            static bool configured = false;
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_inv_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
+                configured = true;
+            }
+            Timed t_(c, KIND_PROJECT, s);
+            k_inv_project<N><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(
+                c->dB, base, out, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
+                c->dFlag);
+            CK(cudaGetLastError());
+            return;
+        }
+#endif
+        inverse(c, nc, s);
+        project(c, base, out, nc, coef, s);
     }
     // group real Qt in (double*)c->dA -> out = base + coef * P_N(Qt)  (user layout)
     static void project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef, cudaStream_t s) {
@@ -631,8 +676,7 @@ int boltz_collide_batch(boltz_ctx* c, const double* f, double* q, int64_t ncells
                                    using Lx = decltype(L);
                                    Lx::forward(c, in, nc, s);
                                    Lx::conv(c, nc, s);
-                                   Lx::inverse(c, nc, s);
-                                   Lx::project(c, nullptr, out, nc, inv_eps, s);
+                                   Lx::inverse_project(c, nullptr, out, nc, inv_eps, s);
                                });
                            });
     });
@@ -651,13 +695,11 @@ int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double i
                                    // stage 1: f* = f + dt/2 * collide(f)
                                    Lx::forward(c, out, nc, s);
                                    Lx::conv(c, nc, s);
-                                   Lx::inverse(c, nc, s);
-                                   Lx::project(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
+                                   Lx::inverse_project(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
                                    // stage 2: f <- f + dt * collide(f*)
                                    Lx::forward(c, c->dFs, nc, s);
                                    Lx::conv(c, nc, s);
-                                   Lx::inverse(c, nc, s);
-                                   Lx::project(c, out, out, nc, dt * inv_eps, s);
+                                   Lx::inverse_project(c, out, out, nc, dt * inv_eps, s);
                                });
                            });
     });

@@ -1,0 +1,206 @@
+// fused.cuh -- single-kernel K1 and K3 for grids whose N^3 cube fits in shared
+// memory (N <= 16): one CTA owns CPB whole cells, does all three FFT axes in
+// shared memory, and touches HBM exactly once per operand.
+//
+//   k_fwd_fused:     user f [cell][N^3]  -> group fhat (forward, fourier.hpp:11-12)
+//   k_inv_project:   group s_k*Qhat       -> out = base + coef * P_N(Re iFFT)  (+ max|Im|)
+//                    (inverse fourier.hpp:15-17, projection SPEC.md:204-212,
+//                     RK2 axpy SPEC.md:383-391)
+//
+// HBM traffic per cell (N=16): forward 32 KiB in + 64 KiB out; inverse+project
+// 64 KiB in + 32 KiB base + 32 KiB out -- versus 3 read+write sweeps each for
+// the multi-pass path (transforms.cuh), which remains for N = 24, 32.
+//
+// Shared layout per cell: [i1][i2][i3] complex with rows padded to N+1 so the
+// three axis passes are bank-conflict free for 16 B accesses.
+#pragma once
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace boltz_gpu {
+
+template <int N>
+struct Fused {
+    static constexpr int N3 = N * N * N;
+    static constexpr int ROW = N + 1;                 // padded row (complex elements)
+    static constexpr int CELL = N * N * ROW;          // complex elements per cell in smem
+    static constexpr int CELL_BYTES = CELL * 16;
+    // cells per block: largest power of two <= 32 whose cubes fit in ~200 KB
+    static constexpr int CPB = (CELL_BYTES * 32 <= 200 * 1024)   ? 32
+                               : (CELL_BYTES * 16 <= 200 * 1024) ? 16
+                               : (CELL_BYTES * 8 <= 200 * 1024)  ? 8
+                               : (CELL_BYTES * 4 <= 200 * 1024)  ? 4
+                               : (CELL_BYTES * 2 <= 200 * 1024)  ? 2
+                                                                 : 1;
+    static constexpr bool FITS = CELL_BYTES <= 200 * 1024;
+#ifndef BOLTZ_FUSED_THREADS
+#define BOLTZ_FUSED_THREADS 512
+#endif
+    static constexpr int THREADS = BOLTZ_FUSED_THREADS;
+    static constexpr int SMEM = CPB * CELL_BYTES + (THREADS / 32) * CPB * 6 * 8;  // cubes + reduction scratch
+    __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
+};
+
+// in-place FFT of every line along AXIS of the CPB cubes in shared memory
+template <int N, int AXIS, int SIGN>
+__device__ __forceinline__ void smem_axis_pass(double2* sm) {
+    using F = Fused<N>;
+    for (int r = threadIdx.x; r < F::CPB * N * N; r += F::THREADS) {
+        const int c = r / (N * N), q = r % (N * N), a = q / N, b = q % N;
+        double2* base = sm + c * F::CELL;
+        int off, stride;
+        if (AXIS == 2) { off = F::at(a, b, 0); stride = 1; }
+        else if (AXIS == 1) { off = F::at(a, 0, b); stride = F::ROW; }
+        else { off = F::at(0, a, b); stride = N * F::ROW; }
+        double2 x[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = base[off + j * stride];
+        RegFFT<N, SIGN, N>::run(x);
+#pragma unroll
+        for (int j = 0; j < N; ++j) base[off + j * stride] = x[j];
+    }
+}
+
+// grid = ngroups * 32 / CPB blocks; block b covers cells [b*CPB, b*CPB+CPB)
+template <int N>
+__global__ void __launch_bounds__(Fused<N>::THREADS)
+k_fwd_fused(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
+            int* __restrict__ flag) {
+    using F = Fused<N>;
+    constexpr int N3 = F::N3;
+    extern __shared__ __align__(16) double2 sm[];
+    const long long cell0 = (long long)blockIdx.x * F::CPB;
+    bool bad = false;
+    // load + pre-multiply by s_m c_m (coalesced per cell)
+#pragma unroll 4
+    for (int t = threadIdx.x; t < F::CPB * N3; t += F::THREADS) {
+        const int c = t / N3, idx = t % N3;
+        const long long cell = cell0 + c;
+        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+        double v = cell < ncells ? f[(size_t)cell * N3 + idx] : 0.0;
+        bad |= !isfinite(v);
+        double w = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3);
+        if ((i1 + i2 + i3) & 1) w = -w;
+        sm[c * F::CELL + F::at(i1, i2, i3)] = make_double2(v * w, 0.0);
+    }
+    if (bad) atomicOr(flag, 1);
+    __syncthreads();
+    smem_axis_pass<N, 2, -1>(sm);
+    __syncthreads();
+    smem_axis_pass<N, 1, -1>(sm);
+    __syncthreads();
+    smem_axis_pass<N, 0, -1>(sm);
+    __syncthreads();
+    // post-multiply scale*par*s_k and scatter into the group layout:
+    // CPB consecutive lanes of one group -> CPB*16 contiguous bytes per node
+    const long long g = cell0 / kLanes;
+    const int lane0 = (int)(cell0 % kLanes);
+#pragma unroll 4
+    for (int t = threadIdx.x; t < F::CPB * N3; t += F::THREADS) {
+        const int idx = t / F::CPB, c = t % F::CPB;
+        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+        const double s = ((i1 + i2 + i3) & 1) ? -scale : scale;
+        const double2 z = sm[c * F::CELL + F::at(i1, i2, i3)];
+        A[((size_t)g * N3 + idx) * kLanes + lane0 + c] = make_double2(z.x * s, z.y * s);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(Fused<N>::THREADS)
+k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
+              double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
+              int* __restrict__ flag) {
+    using F = Fused<N>;
+    constexpr int N3 = F::N3;
+    constexpr int CPB = F::CPB;
+    extern __shared__ __align__(16) double2 sm[];
+    double* red = reinterpret_cast<double*>(sm + CPB * F::CELL);  // [warps][CPB][6], after the cubes
+    __shared__ double lam[CPB][5];
+    const long long cell0 = (long long)blockIdx.x * CPB;
+    const long long g = cell0 / kLanes;
+    const int lane0 = (int)(cell0 % kLanes);
+#pragma unroll 4
+    for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
+        const int idx = t / CPB, c = t % CPB;
+        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+        sm[c * F::CELL + F::at(i1, i2, i3)] = B[((size_t)g * N3 + idx) * kLanes + lane0 + c];
+    }
+    __syncthreads();
+    smem_axis_pass<N, 2, +1>(sm);
+    __syncthreads();
+    smem_axis_pass<N, 1, +1>(sm);
+    __syncthreads();
+    smem_axis_pass<N, 0, +1>(sm);
+    __syncthreads();
+    // Qt = Re(scale*par*s_k*z) in place (.x); moments + max|Im| per cell with a
+    // deterministic reduction (fixed strided partials, shuffle tree, warps in order)
+    const double dv3 = pc.dv * pc.dv * pc.dv;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int c = 0; c < CPB; ++c) {
+        double part[6] = {0, 0, 0, 0, 0, 0};
+        for (int idx = threadIdx.x; idx < N3; idx += F::THREADS) {
+            const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+            double2* p = sm + c * F::CELL + F::at(i1, i2, i3);
+            const double2 z = *p;
+            const double s = ((i1 + i2 + i3) & 1) ? -scale : scale;
+            const double q = z.x * s;
+            p->x = q;
+            const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
+            const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3 * q;
+            part[0] += wq;
+            part[1] += v1 * wq;
+            part[2] += v2 * wq;
+            part[3] += v3 * wq;
+            part[4] += (v1 * v1 + v2 * v2 + v3 * v3) * wq;
+            part[5] = fmax(part[5], fabs(z.y * scale));
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+            double v = part[a];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double u = __shfl_xor_sync(0xffffffffu, v, o);
+                v = (a == 5) ? fmax(v, u) : v + u;
+            }
+            if (lane == 0) red[(wid * CPB + c) * 6 + a] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < CPB) {
+        const int c = threadIdx.x;
+        double m[6] = {0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < F::THREADS / 32; ++w)
+            for (int a = 0; a < 6; ++a) {
+                const double r = red[(w * CPB + c) * 6 + a];
+                m[a] = (a == 5) ? fmax(m[a], r) : m[a] + r;
+            }
+        for (int a = 0; a < 5; ++a) {
+            double t = 0.0;
+            for (int b = 0; b < 5; ++b) t = fma(pc.ginv[a * 5 + b], m[b], t);
+            lam[c][a] = t;
+        }
+        if (maximag && cell0 + c < ncells) maximag[cell0 + c] = m[5];
+    }
+    __syncthreads();
+    bool bad = false;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
+        const int c = t / N3, idx = t % N3;
+        const long long cell = cell0 + c;
+        if (cell >= ncells) continue;
+        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+        const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
+        const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3;
+        const double cl = lam[c][0] + v1 * lam[c][1] + v2 * lam[c][2] + v3 * lam[c][3] +
+                          (v1 * v1 + v2 * v2 + v3 * v3) * lam[c][4];
+        const double q = sm[c * F::CELL + F::at(i1, i2, i3)].x - wq * cl;
+        const size_t o = (size_t)cell * N3 + idx;
+        double v = coef * q;
+        if (base) v += base[o];
+        bad |= !isfinite(v);
+        out[o] = v;
+    }
+    if (bad) atomicOr(flag, 2);
+}
+
+}  // namespace boltz_gpu

@@ -4,9 +4,10 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
-    "base": ["BOLTZ_CONV_PIPE=0"],
-    "pipe": ["BOLTZ_CONV_PIPE=1"],
-    "pipe_w2": ["BOLTZ_CONV_PIPE=1", "BOLTZ_CONV_WARPS=2"],
+    "f256": ["BOLTZ_FUSED_THREADS=256"],
+    "f512": ["BOLTZ_FUSED_THREADS=512"],
+    "f1024": ["BOLTZ_FUSED_THREADS=1024"],
+    "nofuse": ["BOLTZ_FUSED=0"],
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)
