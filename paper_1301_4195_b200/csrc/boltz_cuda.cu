@@ -188,10 +188,14 @@ void build_table(boltz_ctx* c, const double* G_host) {
     std::vector<short2> term(c->slab, make_short2(-1, -1));
     for (int kc = 0; kc < nk; ++kc) {
         int pos = kc * slab_kc;
-        for (int sc = 0; sc < nk; ++sc)
-            for (int m3 = 0; m3 < n; ++m3)
+        for (int ti = 0; ti < nk; ++ti) {
+            const int sc = band_tile_sc(nk, kc, ti);
+            for (int i = 0; i < n; ++i) {
+                const int m3 = band_diag(n, nk, kc, ti, i);
                 for (int kk = 0; kk < t; ++kk)
                     if (band_term(n, t, kc, sc, m3, kk)) term[pos++] = make_short2((short)(kc * t + kk), (short)m3);
+            }
+        }
     }
     // entries: output row (k1,k2) x representative input row (m1,m2)
     std::vector<int2> ent;
@@ -312,8 +316,19 @@ struct Launch {
         const int64_t ng = (nc + 31) / 32;
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-#if BOLTZ_CONV_PIPE
-        if constexpr (NK == 1) {
+        if constexpr (conv_kernel_for(N) == 2 && NK == 2) {
+            using LY = T2Layout<N>;
+            const int smem = LY::W * LY::WARP_BYTES;
+            static bool configured = false;  // per process; attributes apply to every device
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_conv_t2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                CK(cudaFuncSetAttribute(k_conv_t2<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                configured = true;
+            }
+            dim3 g2(N * N * 2, (unsigned)((ng + LY::W - 1) / LY::W));
+            Timed t_(c, KIND_CONV, s);
+            k_conv_t2<N><<<g2, kLanes * LY::W, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+        } else if constexpr (conv_kernel_for(N) >= 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
             static bool configured = false;  // per process; attributes apply to every device
             if (!configured) {
@@ -325,7 +340,6 @@ struct Launch {
             k_conv_pipe<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
                                                                     (int)ng);
         } else
-#endif
         { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng); }
         CK(cudaGetLastError());
     }

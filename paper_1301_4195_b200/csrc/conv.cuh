@@ -3,7 +3,7 @@
 // ("the hot loop of the whole program",
 // SPEC.md:155), on FP64 CUDA cores.
 //
-// Structure (DESIGN.md §K2):
+// Structure (DESIGN.md §3):
 //  * Per axis the shifted index is s = k - m + N/2 (kept only in [0,N)), so for
 //    an output row (k1,k2) and an input row (m1,m2) the inner sum over
 //    (k3, m3) is a 1D band: out[k3] += H[k3][m3] * x[m3] * y[k3-m3+N/2] with
@@ -14,23 +14,43 @@
 //    fhat(m) fhat(sigma m), G' = G*omega.  Only representative input rows are
 //    visited (half of them); the self-paired row keeps its m3 <= s3 half.  The
 //    folded table H is built once per context from the caller's G.
-//  * lane == cell (group layout), so H is warp-uniform: one 16 B load feeds
-//    two terms for 32 cells.  Each thread keeps a T-wide k3 chunk of
-//    accumulators and a T-wide window of y in registers; x is loaded once per
+//  * lane == cell (group layout), so H is warp-uniform: one 16 B broadcast
+//    feeds two terms for 32 cells.  A thread keeps a T-wide chunk of k3
+//    accumulators and a T-wide chunk of y in registers; x is read once per
 //    diagonal.  Every (k3, m3) index is a compile-time constant after unroll.
 //  * Deterministic: each output is accumulated by one thread in a fixed order
 //    (SPEC.md:233); results are independent of batch composition.
+//
+// Kernels:
+//  k_conv_t2   T = N/2 (two k-chunks).  Per-warp shared memory holds ONE x row,
+//              ONE y chunk and a double-buffered H slab; x slots are refilled
+//              for the next row pair right after their last use, y chunks
+//              half a row ahead (cp.async), so ~25 KB per warp lets 8-16 warps
+//              share an SM.  The default for every N.
+//  k_conv_pipe x double-buffered, full y row staged (more smem per warp).
+//  k_conv      no staging, direct loads (reference implementation of the order).
 #pragma once
 #include "common.cuh"
 
 namespace boltz_gpu {
 
-// ---- band enumeration shared by the kernel (compile time) and the host table
+// ---------------------------------------------------------------------------
+// Band enumeration shared by the kernels (compile time) and the host table
 // builder (run time).  Tile (kc, sc): k3 in [kc*T, kc*T+T), s3 in [sc*T, sc*T+T),
-// m3 = k3 - s3 + N/2 must lie in [0, N).  Order: sc, then m3 ascending, then k3.
+// m3 = k3 - s3 + N/2 in [0, N).  Within a k-chunk, tiles are visited in order
+// t = 0..NK-1 and diagonals m3 in the order band_diag(); terms in k3 order.
+// For NK == 2 the triangle tile comes first and the square tile (sc == kc,
+// which covers every diagonal the row uses) last, walked so that the
+// diagonals the next row's first tile needs are finished first (k_conv_t2's
+// x-slot refill relies on it).
+// ---------------------------------------------------------------------------
 __host__ __device__ constexpr bool band_term(int n, int t, int kc, int sc, int m3, int kk) {
     int k3 = kc * t + kk, s3 = k3 - m3 + n / 2;
     return s3 >= sc * t && s3 < sc * t + t;
+}
+__host__ __device__ constexpr int band_tile_sc(int nk, int kc, int ti) { return nk == 2 ? (ti == 0 ? 1 - kc : kc) : ti; }
+__host__ __device__ constexpr int band_diag(int n, int nk, int kc, int ti, int i) {
+    return (nk == 2 && ti == 1 && kc == 1) ? n - 1 - i : i;
 }
 __host__ __device__ constexpr int band_kc_terms(int n, int t, int kc) {
     int c = 0;
@@ -44,89 +64,126 @@ __host__ __device__ constexpr int band_slab_kc(int n, int t) {
     for (int kc = 0; kc < n / t; ++kc) mx = band_kc_terms(n, t, kc) > mx ? band_kc_terms(n, t, kc) : mx;
     return (mx + 1) & ~1;  // even -> 16 B aligned double2 reads
 }
+// diagonal index i (in band_diag order) after which the x slot is refilled
+// for the next row pair in k_conv_t2: -1 = never used by this k-chunk.
+__host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m3) {
+    bool any = false;
+    for (int kk = 0; kk < t; ++kk) any = any || band_term(n, t, kc, sc, m3, kk);
+    return any;
+}
 
-// register tile width per N (accumulators + y window = 8T registers)
-__host__ __device__ constexpr int conv_tile(int n) { return n == 24 ? 12 : (n == 32 ? 16 : n); }
+// Register tile width and kernel per N, chosen by measurement on B200
+// (scripts/ab_conv.py; algorithmic TFLOP/s, round 1):
+//   N=16: T=16 k_conv_pipe 47.5 | T=8 k_conv_t2 42.4 | T=16 k_conv 41.1
+//   N=24: T=12 k_conv_t2 39.1   | T=24 k_conv_pipe 36.0 | T=12 k_conv 34.3
+//   N=32: T=16 k_conv 33.3      | T=16 k_conv_pipe 28.8 | T=16 k_conv_t2 26.7
+#ifndef BOLTZ_TILE16
+#define BOLTZ_TILE16 16
+#endif
+#ifndef BOLTZ_TILE24
+#define BOLTZ_TILE24 12
+#endif
+__host__ __device__ constexpr int conv_tile(int n) {
+    return n == 32 ? 16 : n == 24 ? BOLTZ_TILE24 : n == 16 ? BOLTZ_TILE16 : n;
+}
 #ifndef BOLTZ_CONV_WARPS
 #define BOLTZ_CONV_WARPS 4
 #endif
-#ifndef BOLTZ_CONV_MINB
-#define BOLTZ_CONV_MINB 1
+// 2 = k_conv_t2 (NK == 2 only), 1 = k_conv_pipe, 0 = k_conv; -1 = per-N default
+#ifndef BOLTZ_CONV_KERNEL
+#define BOLTZ_CONV_KERNEL -1
 #endif
-#ifndef BOLTZ_CONV_PREFETCH
-#define BOLTZ_CONV_PREFETCH 0
-#endif
-#ifndef BOLTZ_CONV_PIPE
-#define BOLTZ_CONV_PIPE 1  // cp.async-pipelined kernel for N <= 16
-#endif
-constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the H stream via L1)
+__host__ __device__ constexpr int conv_kernel_for(int n) {
+    return BOLTZ_CONV_KERNEL >= 0 ? BOLTZ_CONV_KERNEL : (n == 32 ? 0 : (n / conv_tile(n) == 2 ? 2 : 1));
+}
+constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the row stream / H via L1)
 
-template <int N, int T, int KC>
+// one tile of terms: acc[kk] += H * x[m3] * y[j]; the x source and the
+// per-diagonal hook (x refill) are policies
+template <int N, int T, int NK, int KC, int TI, typename XAt, typename AfterDiag>
+__device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[T], XAt x_at, const double2* hs,
+                                          int& p, double2& hb, AfterDiag after) {
+    constexpr int SC = band_tile_sc(NK, KC, TI);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const int m3 = band_diag(N, NK, KC, TI, i);
+        if (!diag_used(N, T, KC, SC, m3)) continue;
+        const double2 xm = x_at(m3);
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) {
+            if (!band_term(N, T, KC, SC, m3, kk)) continue;
+            const int j = KC * T + kk - m3 + N / 2 - SC * T;  // y chunk slot
+            double h;
+            if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
+            else h = hb.y;
+            ++p;
+            const double tr = fma(xm.x, y[j].x, -xm.y * y[j].y);
+            const double ti = fma(xm.x, y[j].y, xm.y * y[j].x);
+            acc[kk].x = fma(h, tr, acc[kk].x);
+            acc[kk].y = fma(h, ti, acc[kk].y);
+        }
+        after(i, m3);
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+template <int N, int T>
+__device__ __forceinline__ void write_row(double2* __restrict__ B, int g, int row, int kc, int lane,
+                                          const double2 (&acc)[T]) {
+    constexpr int N3 = N * N * N;
+    const int k1 = row / N, k2 = row % N;
+    double2* Bg = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
+#pragma unroll
+    for (int kk = 0; kk < T; ++kk) {
+        const int k3 = kc * T + kk;
+        const double s = ((k1 + k2 + k3) & 1) ? -1.0 : 1.0;  // inverse transform's input sign s_k
+        Bg[(size_t)k3 * kLanes] = make_double2(s * acc[kk].x, s * acc[kk].y);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// k_conv: direct loads, no staging (kept as the plain reference of the order)
+// ---------------------------------------------------------------------------
+template <int N, int KC>
 __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const double* __restrict__ H,
-                                          const int2* __restrict__ ent, int e0, int e1, double2 (&acc)[T]) {
-    constexpr int NK = N / T;
+                                          const int2* __restrict__ ent, int e0, int e1,
+                                          double2 (&acc)[conv_tile(N)]) {
+    constexpr int T = conv_tile(N), NK = N / T;
     constexpr int SLAB_KC = band_slab_kc(N, T);
-    constexpr int SLAB = NK * SLAB_KC;
     for (int e = e0; e < e1; ++e) {
         const int2 en = __ldg(ent + e);
-#if BOLTZ_CONV_PREFETCH
-        if (e + 1 < e1) {  // pull the next row pair into L1 while this one computes
-            const int2 nx = __ldg(ent + e + 1);
-            const double2* Xn = Ag + (size_t)nx.x * kLanes;
-            const double2* Yn = Ag + (size_t)nx.y * kLanes;
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(Xn + (size_t)j * kLanes));
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(Yn + (size_t)j * kLanes));
-            }
-        }
-#endif
         const double2* X = Ag + (size_t)en.x * kLanes;
         const double2* Y = Ag + (size_t)en.y * kLanes;
-        const double2* Hs = reinterpret_cast<const double2*>(H + (size_t)e * SLAB + KC * SLAB_KC);
+        const double2* Hs = reinterpret_cast<const double2*>(H + ((size_t)e * NK + KC) * SLAB_KC);
         int p = 0;
         double2 hb = make_double2(0.0, 0.0);
+        auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
+        auto none = [](int, int) {};
+        double2 y[T];
 #pragma unroll
-        for (int sc = 0; sc < NK; ++sc) {
-            double2 y[T];
+        for (int j = 0; j < T; ++j) y[j] = ldg2(Y + (size_t)(band_tile_sc(NK, KC, 0) * T + j) * kLanes);
+        band_tile<N, T, NK, KC, 0>(acc, y, xat, Hs, p, hb, none);
+        if constexpr (NK == 2) {
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ldg2(Y + (size_t)(sc * T + j) * kLanes);
-#pragma unroll
-            for (int m3 = 0; m3 < N; ++m3) {
-                bool any = false;
-#pragma unroll
-                for (int kk = 0; kk < T; ++kk) any |= band_term(N, T, KC, sc, m3, kk);
-                if (!any) continue;
-                const double2 xm = ldg2(X + (size_t)m3 * kLanes);
-#pragma unroll
-                for (int kk = 0; kk < T; ++kk) {
-                    if (!band_term(N, T, KC, sc, m3, kk)) continue;
-                    const int j = KC * T + kk - m3 + N / 2 - sc * T;  // y window slot
-                    double h;
-                    if ((p & 1) == 0) { hb = ldg2(Hs + (p >> 1)); h = hb.x; }
-                    else h = hb.y;
-                    ++p;
-                    const double tr = fma(xm.x, y[j].x, -xm.y * y[j].y);
-                    const double ti = fma(xm.x, y[j].y, xm.y * y[j].x);
-                    acc[kk].x = fma(h, tr, acc[kk].x);
-                    acc[kk].y = fma(h, ti, acc[kk].y);
-                }
-            }
+            for (int j = 0; j < T; ++j) y[j] = ldg2(Y + (size_t)(band_tile_sc(NK, KC, 1) * T + j) * kLanes);
+            band_tile<N, T, NK, KC, 1>(acc, y, xat, Hs, p, hb, none);
         }
     }
 }
 
-// grid = (N*N*NK, ceil(ngroups / W)); block = 32*W.  Output B carries the
-// inverse transform's input sign s_k (transforms.cuh).
 template <int N>
-__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_CONV_MINB)
+__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
        const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
-    constexpr int T = conv_tile(N);
-    constexpr int NK = N / T;
-    constexpr int N3 = N * N * N;
-    const int kc = blockIdx.x % NK;
-    const int row = blockIdx.x / NK;
+    constexpr int T = conv_tile(N), NK = N / T, N3 = N * N * N;
+    const int kc = blockIdx.x % NK, row = blockIdx.x / NK;
     const int lane = threadIdx.x & 31;
     const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
     if (g >= ngroups) return;
@@ -135,58 +192,204 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
 #pragma unroll
     for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
     const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
-    if (kc == 0) conv_rows<N, T, 0>(Ag, H, ent, e0, e1, acc);
-    else if constexpr (NK > 1) conv_rows<N, T, (NK > 1 ? 1 : 0)>(Ag, H, ent, e0, e1, acc);
-    const int k1 = row / N, k2 = row % N;
-    double2* Bg = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
-#pragma unroll
-    for (int kk = 0; kk < T; ++kk) {
-        const int k3 = kc * T + kk;
-        const double s = ((k1 + k2 + k3) & 1) ? -1.0 : 1.0;
-        Bg[(size_t)k3 * kLanes] = make_double2(s * acc[kk].x, s * acc[kk].y);
-    }
+    if (kc == 0) conv_rows<N, 0>(Ag, H, ent, e0, e1, acc);
+    else if constexpr (NK > 1) conv_rows<N, (NK > 1 ? 1 : 0)>(Ag, H, ent, e0, e1, acc);
+    write_row<N, T>(B, g, row, kc, lane, acc);
 }
 
 // ---------------------------------------------------------------------------
-// K2, pipelined variant for a single register tile (T == N, i.e. N <= 16).
-// Each warp owns a private shared-memory ring: while row pair e is computed
-// from registers (y, accumulators) and shared memory (x, H), cp.async streams
-// row pair e+1's x row, y row and H slab in behind it, so no global-memory
-// latency is exposed at row boundaries (the stall that bounded k_conv).
-//   per warp: x[2][N][32] + y[N][32] double2, H[2][SLAB] double
+// k_conv_t2: T = N/2, streaming x refill (see header)
+//   per warp: x[N][32] double2 | y[T][32] double2 | H[2][SLAB_KC] double
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
 template <int N>
-struct PipeLayout {
-    static constexpr int SLAB = band_slab_kc(N, N);                   // doubles, even
-    static constexpr int X_BYTES = N * kLanes * 16;                   // one row of 32 cells
-    static constexpr int H_BYTES = SLAB * 8;
-    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES;      // x[2], y, H[2]
+struct T2Layout {
+    static constexpr int W = N == 32 ? 3 : kConvWarps;                 // warps (cell groups) per CTA
+    static constexpr int MINB = N == 16 ? 4 : 2;                       // CTAs per SM the regs must allow
+    static constexpr int T = N / 2;
+    static constexpr int SLAB_KC = band_slab_kc(N, T);
+    static constexpr int X_BYTES = N * kLanes * 16;
+    static constexpr int Y_BYTES = T * kLanes * 16;
+    static constexpr int H_BYTES = SLAB_KC * 8;
+    static constexpr int WARP_BYTES = X_BYTES + Y_BYTES + 2 * H_BYTES;
 };
 
-template <int N>
-__device__ __forceinline__ void pipe_issue(char* wsm, int buf, const double2* __restrict__ Ag, const double* H,
-                                           int2 en, int e, int lane) {
-    using PL = PipeLayout<N>;
-    double2* xs = reinterpret_cast<double2*>(wsm + buf * PL::X_BYTES);
-    double2* ys = reinterpret_cast<double2*>(wsm + 2 * PL::X_BYTES);
-    char* hs = wsm + 3 * PL::X_BYTES + buf * PL::H_BYTES;
-    const double2* X = Ag + (size_t)en.x * kLanes;
-    const double2* Y = Ag + (size_t)en.y * kLanes;
+template <int N, int KC>
+__device__ __forceinline__ void t2_rows(char* wsm, const double2* __restrict__ Ag, const double* __restrict__ H,
+                                        const int2* __restrict__ ent, int e0, int e1, int lane,
+                                        double2 (&acc)[N / 2]) {
+    using LY = T2Layout<N>;
+    constexpr int T = LY::T, NK = 2;
+    constexpr int SC0 = band_tile_sc(NK, KC, 0), SC1 = band_tile_sc(NK, KC, 1);
+    double2* xs = reinterpret_cast<double2*>(wsm);
+    double2* ys = reinterpret_cast<double2*>(wsm + LY::X_BYTES);
+    char* hbase = wsm + LY::X_BYTES + LY::Y_BYTES;
+    const double* Hk = H + (size_t)KC * LY::SLAB_KC;  // + e * 2 * SLAB_KC
+    auto issue_h = [&](int buf, int e) {
+        const char* hg = reinterpret_cast<const char*>(Hk + (size_t)e * 2 * LY::SLAB_KC);
+        for (int o = lane * 16; o < LY::H_BYTES; o += kLanes * 16) cp_async16(hbase + buf * LY::H_BYTES + o, hg + o);
+    };
+    auto issue_y = [&](int2 en, int sc) {
+        const double2* Y = Ag + ((size_t)en.y + sc * T) * kLanes;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-        cp_async16(xs + j * kLanes + lane, X + (size_t)j * kLanes);
-        cp_async16(ys + j * kLanes + lane, Y + (size_t)j * kLanes);
+        for (int j = 0; j < T; ++j) cp_async16(ys + j * kLanes + lane, Y + (size_t)j * kLanes);
+    };
+    if (e0 >= e1) return;
+    int2 en = __ldg(ent + e0);
+    {   // prologue: x row, H slab, first y chunk of row e0
+        const double2* X = Ag + (size_t)en.x * kLanes;
+#pragma unroll
+        for (int j = 0; j < N; ++j) cp_async16(xs + j * kLanes + lane, X + (size_t)j * kLanes);
+        issue_h(0, e0);
+        issue_y(en, SC0);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
     }
-    const char* hg = reinterpret_cast<const char*>(H + (size_t)e * PL::SLAB);
-    for (int o = lane * 16; o < PL::H_BYTES; o += kLanes * 16) cp_async16(hs + o, hg + o);
+    double2 y[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+    issue_y(en, SC1);
     cp_async_commit();
+    for (int e = e0; e < e1; ++e) {
+        const int cur = (e - e0) & 1;
+        const bool more = e + 1 < e1;
+        const int2 nx = more ? __ldg(ent + e + 1) : en;
+        const double2* Xn = Ag + (size_t)nx.x * kLanes;
+        __syncwarp();  // every lane finished reading H[cur^1] (row e-1)
+        if (more) issue_h(cur ^ 1, e + 1);
+        cp_async_commit();
+        const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
+        int p = 0;
+        double2 hb = make_double2(0.0, 0.0);
+        auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
+        // tile 0 (triangle): slots it uses are needed again by tile 1, except
+        // slot 0 of k-chunk 0, which is refilled right away
+        band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, [&](int, int m3) {
+            if (KC == 0 && m3 == 0 && more) cp_async16(xs + lane, Xn);
+        });
+        cp_async_commit();
+        cp_async_wait_all();  // y chunk SC1 of row e (and H of row e+1)
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+        if (more) issue_y(nx, SC0);  // own-lane slots, read just above
+        cp_async_commit();
+        // tile 1 (square, all diagonals the row uses): refill each x slot after
+        // its last use; the first half holds the slots the next row's tile 0 needs
+        band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, [&](int i, int m3) {
+            if (more && m3 != 0) cp_async16(xs + m3 * kLanes + lane, Xn + (size_t)m3 * kLanes);
+            if (i == (KC == 0 ? T - 1 : T - 2)) cp_async_commit();  // R1: slots of the next tile 0
+        });
+        cp_async_commit();  // R2
+        if (more) {
+            cp_async_wait_1();  // all but R2: y chunk SC0 of row e+1 and the R1 slots
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+            issue_y(nx, SC1);
+            cp_async_commit();
+        }
+        en = nx;
+    }
+    cp_async_wait_all();
+}
+
+template <int N>
+__global__ void __launch_bounds__(kLanes* T2Layout<N>::W, T2Layout<N>::MINB)
+k_conv_t2(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+    using LY = T2Layout<N>;
+    constexpr int T = LY::T, N3 = N * N * N;
+    extern __shared__ __align__(16) char smem[];
+    const int kc = blockIdx.x & 1, row = blockIdx.x >> 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * LY::W + wid;
+    if (g >= ngroups) return;  // whole warp exits; warps never sync with each other
+    char* wsm = smem + wid * LY::WARP_BYTES;
+    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
+    double2 acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    if (kc == 0) t2_rows<N, 0>(wsm, Ag, H, ent, e0, e1, lane, acc);
+    else t2_rows<N, 1>(wsm, Ag, H, ent, e0, e1, lane, acc);
+    write_row<N, T>(B, g, row, kc, lane, acc);
+}
+
+// ---------------------------------------------------------------------------
+// k_conv_pipe: x double-buffered, full y row staged, H double-buffered
+//   per warp: x[2][N][32] + y[N][32] double2, H[2][SLAB_KC] double
+// ---------------------------------------------------------------------------
+template <int N>
+struct PipeLayout {
+    static constexpr int T = conv_tile(N);
+    static constexpr int NK = N / T;
+    static constexpr int SLAB_KC = band_slab_kc(N, T);
+    static constexpr int X_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = SLAB_KC * 8;
+    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES;
+};
+
+template <int N, int KC>
+__device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__ Ag, const double* __restrict__ H,
+                                          const int2* __restrict__ ent, int e0, int e1, int lane,
+                                          double2 (&acc)[conv_tile(N)]) {
+    using PL = PipeLayout<N>;
+    constexpr int T = PL::T, NK = PL::NK;
+    const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
+    auto issue_xh = [&](int buf, int2 en, int e) {
+        double2* xs = reinterpret_cast<double2*>(wsm + buf * PL::X_BYTES);
+        const double2* X = Ag + (size_t)en.x * kLanes;
+#pragma unroll
+        for (int j = 0; j < N; ++j) cp_async16(xs + j * kLanes + lane, X + (size_t)j * kLanes);
+        char* hs = wsm + 3 * PL::X_BYTES + buf * PL::H_BYTES;
+        const char* hg = reinterpret_cast<const char*>(H + ((size_t)e * NK + KC) * PL::SLAB_KC);
+        for (int o = lane * 16; o < PL::H_BYTES; o += kLanes * 16) cp_async16(hs + o, hg + o);
+        cp_async_commit();
+    };
+    auto issue_y = [&](int2 en) {
+        double2* yw = reinterpret_cast<double2*>(wsm + 2 * PL::X_BYTES);
+        const double2* Y = Ag + (size_t)en.y * kLanes;
+#pragma unroll
+        for (int j = 0; j < N; ++j) cp_async16(yw + j * kLanes + lane, Y + (size_t)j * kLanes);
+        cp_async_commit();
+    };
+    if (e0 >= e1) return;
+    int2 en_next = __ldg(ent + e0);
+    issue_xh(0, en_next, e0);
+    issue_y(en_next);
+    cp_async_wait_all();
+    __syncwarp();
+    double2 y[T];
+#pragma unroll
+    for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+    for (int e = e0; e < e1; ++e) {
+        const int cur = (e - e0) & 1;
+        const bool more = e + 1 < e1;
+        if (more) en_next = __ldg(ent + e + 1);
+        __syncwarp();
+        if (more) issue_xh(cur ^ 1, en_next, e + 1);
+        if (NK == 1 && more) issue_y(en_next);
+        const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
+        const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
+        int p = 0;
+        double2 hb = make_double2(0.0, 0.0);
+        auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
+        auto none = [](int, int) {};
+        band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+        if constexpr (NK == 2) {
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+            if (more) issue_y(en_next);
+            band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
+        }
+        if (more) {
+            cp_async_wait_all();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+        }
+    }
 }
 
 template <int N>
@@ -194,67 +397,21 @@ __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
     using PL = PipeLayout<N>;
-    constexpr int N3 = N * N * N;
+    constexpr int T = PL::T, NK = PL::NK, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int row = blockIdx.x;
-    const int lane = threadIdx.x & 31;
-    const int wid = threadIdx.x >> 5;
+    const int kc = blockIdx.x % NK, row = blockIdx.x / NK;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * kConvWarps + wid;
-    if (g >= ngroups) return;  // whole warp exits together; warps never sync across each other
+    if (g >= ngroups) return;
     char* wsm = smem + wid * PL::WARP_BYTES;
     const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
-    const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
-    double2 acc[N];
+    double2 acc[T];
 #pragma unroll
-    for (int i = 0; i < N; ++i) acc[i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
     const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
-    double2 y[N];
-    if (e0 < e1) {
-        pipe_issue<N>(wsm, 0, Ag, H, __ldg(ent + e0), e0, lane);
-        cp_async_wait_all();
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < N; ++j) y[j] = ys[j * kLanes + lane];
-    }
-    for (int e = e0; e < e1; ++e) {
-        const int cur = (e - e0) & 1;
-        __syncwarp();  // every lane is done reading the buffers the next issue overwrites
-        if (e + 1 < e1) pipe_issue<N>(wsm, cur ^ 1, Ag, H, __ldg(ent + e + 1), e + 1, lane);
-        const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
-        const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
-        int p = 0;
-        double2 hb = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int m3 = 0; m3 < N; ++m3) {
-            const double2 xm = xs[m3 * kLanes + lane];
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) {
-                if (!band_term(N, N, 0, 0, m3, kk)) continue;
-                const int j = kk - m3 + N / 2;
-                double h;
-                if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
-                else h = hb.y;
-                ++p;
-                const double tr = fma(xm.x, y[j].x, -xm.y * y[j].y);
-                const double ti = fma(xm.x, y[j].y, xm.y * y[j].x);
-                acc[kk].x = fma(h, tr, acc[kk].x);
-                acc[kk].y = fma(h, ti, acc[kk].y);
-            }
-        }
-        if (e + 1 < e1) {
-            cp_async_wait_all();
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j < N; ++j) y[j] = ys[j * kLanes + lane];
-        }
-    }
-    const int k1 = row / N, k2 = row % N;
-    double2* Bg = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
-#pragma unroll
-    for (int kk = 0; kk < N; ++kk) {
-        const double s = ((k1 + k2 + kk) & 1) ? -1.0 : 1.0;
-        Bg[(size_t)kk * kLanes] = make_double2(s * acc[kk].x, s * acc[kk].y);
-    }
+    if (kc == 0) pipe_rows<N, 0>(wsm, Ag, H, ent, e0, e1, lane, acc);
+    else if constexpr (NK > 1) pipe_rows<N, (NK > 1 ? 1 : 0)>(wsm, Ag, H, ent, e0, e1, lane, acc);
+    write_row<N, T>(B, g, row, kc, lane, acc);
 }
 
 // ---- H table builder: H[e][slab pos] from one k1-plane of the caller's dense

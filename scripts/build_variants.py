@@ -4,10 +4,10 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
-    "f256": ["BOLTZ_FUSED_THREADS=256"],
-    "f512": ["BOLTZ_FUSED_THREADS=512"],
-    "f1024": ["BOLTZ_FUSED_THREADS=1024"],
-    "nofuse": ["BOLTZ_FUSED=0"],
+    "t2": [],
+    "wide": ["BOLTZ_TILE16=16", "BOLTZ_TILE24=24"],
+    "k0": ["BOLTZ_CONV_KERNEL=0"],
+    "k1": ["BOLTZ_CONV_KERNEL=1"],
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)

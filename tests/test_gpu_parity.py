@@ -117,3 +117,25 @@ def test_empty_and_ragged_batches(gpu, O):
         for c in (0, 31, 32):
             assert rel_max(q[c], O.collide(n, L, G, f[c])[0]) < TOL_Q
         assert np.abs(op.collide(np.zeros((2, n ** 3)))).max() == 0.0
+
+
+@pytest.mark.parametrize("n,L,cells", [(24, 8.0, 2), (32, 8.0, 1)])
+def test_large_grids_vs_oracle(gpu, O, n, L, cells):
+    """The configs' large velocity grids (cfg4 N=24, cfg5 N=32): qhat and the
+    full collide vs the oracle on cfg2-style mixture cells (batch padded to a
+    full 32-cell group on the GPU)."""
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=13)
+    G = table(n, L)
+    with _op(n, L) as op:
+        fh = op.forward(f)
+        qh = op.evaluate_qhat(fh)
+        q = op.collide(f)
+    for c in range(cells):
+        assert rel_max(fh[c], O.forward(n, L, f[c])) < 1e-12
+        ref_qh = O.evaluate_qhat(n, L, G, fh[c], nthreads=8)
+        assert rel_max(qh[c], ref_qh) < TOL_Q
+        ref_q, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q[c], ref_q) < TOL_Q
+        m = O.moments(n, L, q[c])
+        assert np.abs(m[:5]).max() < TOL_CONS * O.moments(n, L, f[c])[0]
