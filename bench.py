@@ -36,6 +36,20 @@ N_VEL, L_VEL, LAM, CELLS, DT = 16, 6.0, 1.0, 4096, 0.01
 FLOP_PER_TERM = 10  # 2 DMUL + 4 DFMA per (k, m) term, SURVEY.md §8d
 
 
+def ncu_traffic(kernel, cells):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json), when it was taken on this workload."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)[kernel]
+    except (OSError, KeyError, ValueError):
+        return None
+    if d.get("cells") != cells:
+        return None
+    return {"bytes": d["dram_bytes_read"] + d["dram_bytes_write"], "unit": "B/launch",
+            "algorithmic_bytes": cells * 16 ** 3 * 32 + 28360704, "source": d["source"]}
+
+
 def terms_per_eval(n):
     return 27 * n ** 6 // 64
 
@@ -287,7 +301,7 @@ def main():
             "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
             "kernel_launches": klaunch,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_conv_pipe<16>", cells),
                          "kernel": "k_conv<16> (K2)",
                          "note": "achieved = 10 flop x 27/64 N^6 valid terms x cells per launch / mean launch time "
                                  "(algorithmic, SURVEY.md §8d); the kernel executes half of those terms "
