@@ -20,6 +20,9 @@
 #include "probe.cuh"
 #include "fused.cuh"
 
+#ifndef BOLTZ_K0_SPLIT
+#define BOLTZ_K0_SPLIT 0  // N=32: one kernel per k-chunk instead of one kernel for both
+#endif
 #ifndef BOLTZ_FUSED
 #define BOLTZ_FUSED 1  // single-kernel K1 / K3 when the N^3 cube fits in shared memory
 #endif
@@ -328,7 +331,7 @@ struct Launch {
             dim3 g2(N * N * 2, (unsigned)((ng + LY::W - 1) / LY::W));
             Timed t_(c, KIND_CONV, s);
             k_conv_t2<N><<<g2, kLanes * LY::W, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
-        } else if constexpr (conv_kernel_for(N) >= 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
+        } else if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
             static bool configured = false;  // per process; attributes apply to every device
             if (!configured) {
@@ -339,6 +342,29 @@ struct Launch {
             Timed t_(c, KIND_CONV, s);
             k_conv_pipe<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
                                                                     (int)ng);
+        } else if constexpr (conv_kernel_for(N) == 3) {
+            using LY = KcsLayout<N>;
+            const int smem = kConvWarps * LY::WARP_BYTES;
+            constexpr int KC1 = NK > 1 ? 1 : 0;
+            static bool configured = false;
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_conv_kcs<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                CK(cudaFuncSetAttribute(k_conv_kcs<N, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                CK(cudaFuncSetAttribute(k_conv_kcs<N, KC1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                CK(cudaFuncSetAttribute(k_conv_kcs<N, KC1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                configured = true;
+            }
+            dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+            Timed t_(c, KIND_CONV, s);
+            k_conv_kcs<N, 0><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+            if constexpr (NK > 1)
+                k_conv_kcs<N, KC1><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
+                                                                         (int)ng);
+        } else if constexpr (NK == 2 && BOLTZ_K0_SPLIT) {
+            dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+            Timed t_(c, KIND_CONV, s);
+            k_conv_kc<N, 0><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+            k_conv_kc<N, 1><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
         } else
         { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng); }
         CK(cudaGetLastError());

@@ -73,15 +73,15 @@ __host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m
 }
 
 // Register tile width and kernel per N, chosen by measurement on B200
-// (scripts/ab_conv.py; algorithmic TFLOP/s, round 1):
-//   N=16: T=16 k_conv_pipe 47.5 | T=8 k_conv_t2 42.4 | T=16 k_conv 41.1
-//   N=24: T=12 k_conv_t2 39.1   | T=24 k_conv_pipe 36.0 | T=12 k_conv 34.3
-//   N=32: T=16 k_conv 33.3      | T=16 k_conv_pipe 28.8 | T=16 k_conv_t2 26.7
+// (scripts/ab_conv.py, scripts/ab_n32.sh; algorithmic TFLOP/s, round 1):
+//   N=16: T=16 k_conv_pipe 47.5 | T=16 kcs 46.4 | T=8 t2 42.4 | T=8 kcs 39.7 | T=16 k_conv 41.1
+//   N=24: T=24 kcs 45.5         | T=12 kcs 43.5 | T=12 t2 39.1 | T=24 pipe 36.0 | T=12 k_conv 34.3
+//   N=32: T=16 kcs 45.3         | T=16 k_conv split per k-chunk 35.2 | k_conv 33.3 | pipe 28.8 | t2 26.7
 #ifndef BOLTZ_TILE16
 #define BOLTZ_TILE16 16
 #endif
 #ifndef BOLTZ_TILE24
-#define BOLTZ_TILE24 12
+#define BOLTZ_TILE24 24
 #endif
 __host__ __device__ constexpr int conv_tile(int n) {
     return n == 32 ? 16 : n == 24 ? BOLTZ_TILE24 : n == 16 ? BOLTZ_TILE16 : n;
@@ -89,12 +89,16 @@ __host__ __device__ constexpr int conv_tile(int n) {
 #ifndef BOLTZ_CONV_WARPS
 #define BOLTZ_CONV_WARPS 4
 #endif
-// 2 = k_conv_t2 (NK == 2 only), 1 = k_conv_pipe, 0 = k_conv; -1 = per-N default
+// 3 = k_conv_kcs (one kernel per k-chunk, y/H staged), 2 = k_conv_t2 (NK == 2
+// only), 1 = k_conv_pipe, 0 = k_conv; -1 = per-N default
 #ifndef BOLTZ_CONV_KERNEL
 #define BOLTZ_CONV_KERNEL -1
 #endif
+#ifndef BOLTZ_KERNEL24
+#define BOLTZ_KERNEL24 3
+#endif
 __host__ __device__ constexpr int conv_kernel_for(int n) {
-    return BOLTZ_CONV_KERNEL >= 0 ? BOLTZ_CONV_KERNEL : (n == 32 ? 0 : (n / conv_tile(n) == 2 ? 2 : 1));
+    return BOLTZ_CONV_KERNEL >= 0 ? BOLTZ_CONV_KERNEL : (n == 32 ? 3 : n == 24 ? BOLTZ_KERNEL24 : 1);
 }
 constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the row stream / H via L1)
 
@@ -195,6 +199,118 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
     if (kc == 0) conv_rows<N, 0>(Ag, H, ent, e0, e1, acc);
     else if constexpr (NK > 1) conv_rows<N, (NK > 1 ? 1 : 0)>(Ag, H, ent, e0, e1, acc);
     write_row<N, T>(B, g, row, kc, lane, acc);
+}
+
+// the same, one k-chunk per kernel (halves the instruction footprint an SM
+// streams at N=32, whose fully unrolled band is ~60 KB of SASS per chunk)
+#ifndef BOLTZ_K0_MINB
+#define BOLTZ_K0_MINB 1
+#endif
+template <int N, int KC>
+__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
+k_conv_kc(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+    constexpr int T = conv_tile(N), N3 = N * N * N;
+    const int row = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
+    if (g >= ngroups) return;
+    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
+    double2 acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    conv_rows<N, KC>(Ag, H, ent, e0, e1, acc);
+    write_row<N, T>(B, g, row, KC, lane, acc);
+}
+
+// ---------------------------------------------------------------------------
+// k_conv_kcs: one k-chunk per kernel; the y row and the H slab of the next row
+// pair are staged in shared memory by cp.async while the current one computes
+// (H is DRAM-resident at N=32: 1.85 GB), x is read per diagonal from L2.
+//   per warp: y[N][32] double2 | H[2][SLAB_KC] double   (N=32: 22.3 KB)
+// ---------------------------------------------------------------------------
+template <int N>
+struct KcsLayout {
+    static constexpr int T = conv_tile(N);
+    static constexpr int NK = N / T;
+    static constexpr int SLAB_KC = band_slab_kc(N, T);
+    static constexpr int Y_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = SLAB_KC * 8;
+    static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES;
+};
+
+template <int N, int KC>
+__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
+k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+    using LY = KcsLayout<N>;
+    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
+    extern __shared__ __align__(16) char smem[];
+    const int row = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * kConvWarps + wid;
+    if (g >= ngroups) return;
+    char* wsm = smem + wid * LY::WARP_BYTES;
+    double2* ys = reinterpret_cast<double2*>(wsm);
+    char* hbase = wsm + LY::Y_BYTES;
+    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
+    auto issue_h = [&](int buf, int e) {
+        const char* hg = reinterpret_cast<const char*>(H + ((size_t)e * NK + KC) * LY::SLAB_KC);
+        for (int o = lane * 16; o < LY::H_BYTES; o += kLanes * 16) cp_async16(hbase + buf * LY::H_BYTES + o, hg + o);
+    };
+    auto issue_y = [&](int2 en) {
+        const double2* Y = Ag + (size_t)en.y * kLanes;
+#pragma unroll
+        for (int j = 0; j < N; ++j) cp_async16(ys + j * kLanes + lane, Y + (size_t)j * kLanes);
+    };
+    double2 acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    if (e0 < e1) {
+        int2 en = __ldg(ent + e0);
+        issue_y(en);
+        issue_h(0, e0);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncwarp();
+        for (int e = e0; e < e1; ++e) {
+            const int cur = (e - e0) & 1;
+            const bool more = e + 1 < e1;
+            const int2 nx = more ? __ldg(ent + e + 1) : en;
+            __syncwarp();  // every lane finished reading H[cur^1]
+            if (more) issue_h(cur ^ 1, e + 1);
+            cp_async_commit();
+            const double2* X = Ag + (size_t)en.x * kLanes;
+            const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
+            int p = 0;
+            double2 hb = make_double2(0.0, 0.0);
+            auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
+            auto none = [](int, int) {};
+            double2 y[T];
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            if constexpr (NK == 1) {
+                if (more) issue_y(nx);  // own-lane slots, just read
+                cp_async_commit();
+                band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+            } else {
+                band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+#pragma unroll
+                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                if (more) issue_y(nx);
+                cp_async_commit();
+                band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
+            }
+            if (more) {
+                cp_async_wait_all();
+                __syncwarp();
+            }
+            en = nx;
+        }
+    }
+    write_row<N, T>(B, g, row, KC, lane, acc);
 }
 
 // ---------------------------------------------------------------------------

@@ -4,10 +4,8 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
-    "t2": [],
-    "wide": ["BOLTZ_TILE16=16", "BOLTZ_TILE24=24"],
-    "k0": ["BOLTZ_CONV_KERNEL=0"],
-    "k1": ["BOLTZ_CONV_KERNEL=1"],
+    "default": ["BOLTZ_KERNEL24=3"],
+    "kcs_full": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_TILE24=24"],   # N<=24 single tile, y/H staged, x from L2
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)
