@@ -74,6 +74,15 @@ int boltz_create(int n, double L, double lambda, double beta, double r0, const d
                  boltz_ctx** out);
 int boltz_destroy(boltz_ctx* ctx);
 
+/*
+ * As boltz_create, but the weight table is evaluated on the device (same
+ * closed forms / Gauss-Legendre quadrature with `panels` panels as
+ * boltz_generate_table) straight into the folded layout -- no host N^6 table
+ * (the reference generates on the host).
+ */
+int boltz_create_generated(int n, double L, double lambda, double beta, double r0, int panels, int device,
+                           boltz_ctx** out);
+
 /* Device bytes held by the context (folded table + workspace). */
 int boltz_memory_bytes(const boltz_ctx* ctx, int64_t* table_bytes, int64_t* workspace_bytes);
 

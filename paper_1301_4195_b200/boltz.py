@@ -80,6 +80,7 @@ def lib():
             "boltz_last_error": (C.c_char_p, []),
             "boltz_build_info": (C.c_char_p, []),
             "boltz_create": (i, [i, d, d, d, d, vp, i, C.POINTER(vp)]),
+            "boltz_create_generated": (i, [i, d, d, d, d, i, i, C.POINTER(vp)]),
             "boltz_destroy": (i, [vp]),
             "boltz_memory_bytes": (i, [vp, C.POINTER(i64), C.POINTER(i64)]),
             "boltz_forward_batch": (i, [vp, vp, vp, i64, i, vp]),
@@ -229,15 +230,26 @@ class CollisionOperator:
     Not thread-safe (like SpectralTransform, fourier.hpp:24-25).
     """
 
-    def __init__(self, grid: VelocityGrid, kernel: KernelSpec, table: np.ndarray, device: int = 0):
+    def __init__(self, grid: VelocityGrid, kernel: KernelSpec, table: Optional[np.ndarray], device: int = 0):
+        """table: the dense zeta-major N^6 host table (generate_table/load_table),
+        or None to evaluate it on the device (boltz_create_generated)."""
         self.grid, self.kernel, self.device = grid, kernel, device
-        table = np.ascontiguousarray(table, dtype=np.float64)
-        if table.size != grid.n ** 6:
-            raise ConfigError(f"weight table has {table.size} entries, expected N^6 = {grid.n ** 6}")
         h = C.c_void_p()
-        _check(lib().boltz_create(grid.n, grid.half_width, kernel.lam, kernel.beta, kernel.radius(grid),
-                                  table.ctypes.data, device, C.byref(h)))
+        if table is None:
+            _check(lib().boltz_create_generated(grid.n, grid.half_width, kernel.lam, kernel.beta,
+                                                kernel.radius(grid), kernel.panels, device, C.byref(h)))
+        else:
+            table = np.ascontiguousarray(table, dtype=np.float64)
+            if table.size != grid.n ** 6:
+                raise ConfigError(f"weight table has {table.size} entries, expected N^6 = {grid.n ** 6}")
+            _check(lib().boltz_create(grid.n, grid.half_width, kernel.lam, kernel.beta, kernel.radius(grid),
+                                      table.ctypes.data, device, C.byref(h)))
         self._h = h
+
+    @classmethod
+    def generated(cls, grid: VelocityGrid, kernel: KernelSpec, device: int = 0) -> "CollisionOperator":
+        """Context whose weight table is generated on the GPU (no host N^6 table)."""
+        return cls(grid, kernel, None, device)
 
     def close(self):
         if getattr(self, "_h", None):

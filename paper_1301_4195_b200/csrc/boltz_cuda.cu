@@ -19,6 +19,7 @@
 #include "transport.cuh"
 #include "probe.cuh"
 #include "fused.cuh"
+#include "gen.cuh"
 
 #ifndef BOLTZ_K0_SPLIT
 #define BOLTZ_K0_SPLIT 0  // N=32: one kernel per k-chunk instead of one kernel for both
@@ -81,6 +82,7 @@ struct boltz_ctx {
     int* hFlag = nullptr;    // pinned
     ProjConst pc{};
     int64_t table_bytes = 0, ws_bytes = 0;
+    int panels = 64;  // Gauss-Legendre panels of the on-device generator (0 < lambda < 1)
     // per-kernel-class CUDA-event timing (bench.py roofline) and launch counts
     bool timing = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -233,11 +235,19 @@ void build_table(boltz_ctx* c, const double* G_host) {
     try {
         CK(cudaMalloc(&dEntK, entk.size() * sizeof(int4)));
         CK(cudaMalloc(&dTerm, term.size() * sizeof(short2)));
-        CK(cudaMalloc(&dPlane, plane * sizeof(double)));
         CK(cudaMemcpy(dEntK, entk.data(), entk.size() * sizeof(int4), cudaMemcpyHostToDevice));
         CK(cudaMemcpy(dTerm, term.data(), term.size() * sizeof(short2), cudaMemcpyHostToDevice));
         const double dz = kPi / c->L, w3 = dz * dz * dz;
-        for (int k1 = 0; k1 < n; ++k1) {
+        if (!G_host) {  // on-device generation (gen.cuh)
+            GenParams gp{};
+            gp.lambda = c->lambda; gp.beta = c->beta; gp.r0 = c->r0; gp.dz2 = dz * dz; gp.w3 = w3;
+            gp.panels = c->panels; gp.n = n; gp.gl = boltz_w::gauss16();
+            const long long total = (long long)c->nent * c->slab;
+            k_gen_H<<<(unsigned)((total + 255) / 256), 256>>>(c->dH, dEntK, dTerm, c->nent, c->slab, gp);
+            CK(cudaGetLastError());
+        }
+        if (G_host) CK(cudaMalloc(&dPlane, plane * sizeof(double)));
+        for (int k1 = 0; G_host && k1 < n; ++k1) {
             CK(cudaMemcpy(dPlane, G_host + (size_t)k1 * plane, plane * sizeof(double), cudaMemcpyHostToDevice));
             const int e0 = row_start[k1 * n], e1 = row_start[k1 * n + n];
             const long long total = (long long)(e1 - e0) * c->slab;
@@ -573,6 +583,11 @@ int api(boltz_ctx* c, Body&& body) {
 
 }  // namespace
 
+namespace {
+int create_context(int n, double L, double lambda, double beta, double r0, int panels, const double* G_host,
+                   int device, boltz_ctx** out);
+}
+
 extern "C" {
 
 const char* boltz_last_error(void) { return g_err.c_str(); }
@@ -608,8 +623,38 @@ int boltz_create(int n, double L, double lambda, double beta, double r0, const d
         set_error("boltz_create: weight table is null");
         return BOLTZ_ERR_CONFIG;
     }
+    return create_context(n, L, lambda, beta, r0, 64, G_host, device, out);
+}
+
+int boltz_create_generated(int n, double L, double lambda, double beta, double r0, int panels, int device,
+                           boltz_ctx** out) {
+    if (!out) {
+        set_error("boltz_create_generated: out is null");
+        return BOLTZ_ERR_CONFIG;
+    }
+    *out = nullptr;
+    if (n < 4 || n % 2 != 0 || !(L > 0.0)) {
+        set_error("velocity grid: N must be even and >= 4 and L > 0");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!supported_n(n)) {
+        set_error("boltz_create_generated: N=" + std::to_string(n) + " has no compiled kernel");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!(lambda >= 0.0 && lambda <= 1.0) || !(beta > 0.0 && beta <= 1.0) || !(r0 > 0.0) || panels < 1) {
+        set_error("kernel spec: need 0<=lambda<=1, 0<beta<=1, r0>0, panels>=1");
+        return BOLTZ_ERR_CONFIG;
+    }
+    return create_context(n, L, lambda, beta, r0, panels, nullptr, device, out);
+}
+
+}  // extern "C"
+
+namespace {
+int create_context(int n, double L, double lambda, double beta, double r0, int panels, const double* G_host,
+                   int device, boltz_ctx** out) {
     boltz_ctx* c = new boltz_ctx();
-    c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device;
+    c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device; c->panels = panels;
     try {
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
@@ -626,6 +671,9 @@ int boltz_create(int n, double L, double lambda, double beta, double r0, const d
     *out = c;
     return BOLTZ_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int boltz_destroy(boltz_ctx* c) {
     if (!c) return BOLTZ_OK;

@@ -139,3 +139,25 @@ def test_large_grids_vs_oracle(gpu, O, n, L, cells):
         assert rel_max(q[c], ref_q) < TOL_Q
         m = O.moments(n, L, q[c])
         assert np.abs(m[:5]).max() < TOL_CONS * O.moments(n, L, f[c])[0]
+
+
+@pytest.mark.parametrize("n,L,lam", [(8, 5.0, 1.0), (8, 5.0, 0.0), (8, 5.0, 0.5), (16, 6.0, 1.0), (32, 8.0, 1.0)])
+def test_device_generated_table_matches_host_table(gpu, O, n, L, lam):
+    """the on-device table equals the host table (same closed
+    forms / quadrature), so Qhat agrees with the oracle driven by the HOST G."""
+    grid = VelocityGrid.create(n, L)
+    k = KernelSpec(lam, panels=32)
+    f = scenarios.mixture_cells(grid, 2, seed=17)
+    with CollisionOperator.generated(grid, k) as opg:
+        fh = opg.forward(f)
+        qg = opg.evaluate_qhat(fh)
+    if n <= 16:
+        from paper_1301_4195_b200 import generate_table
+        G = generate_table(grid, k)
+        with CollisionOperator(grid, k, G) as oph:
+            qh = oph.evaluate_qhat(fh)
+        assert rel_max(qg, qh) < 1e-12
+        assert rel_max(qg[0], O.evaluate_qhat(n, L, G, fh[0])) < TOL_Q
+    else:
+        G = table(n, L, lam)
+        assert rel_max(qg[0], O.evaluate_qhat(n, L, G, fh[0], nthreads=8)) < TOL_Q
