@@ -30,7 +30,7 @@
  * and is synchronous) or BOLTZ_MEM_DEVICE (pointers are device memory on the
  * context's device; the call is ordered on `stream` and synchronises it
  * before returning so that numeric errors can be reported).  `stream` may be
- * NULL (the context's own stream).
+ * NULL (the CUDA default stream), as in any CUDA API.
  *
  * Threading mirrors SpectralTransform (fourier.hpp:24-25): a context is not
  * thread-safe; distinct contexts may be used concurrently.
@@ -135,6 +135,17 @@ int boltz_transport_step(boltz_ctx* ctx, const double* field, const double* base
  */
 int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double* x_ext, int side, int kind,
                         double Tw, const double* Vw_host3, double* sigma_w, void* stream);
+
+/*
+ * Asynchronous mode (no reference counterpart): with
+ * enable != 0, device-pointer calls return as soon as their work is queued on
+ * the stream (no synchronisation, so a whole Strang step can be captured in a
+ * CUDA graph); non-finite detections accumulate and are reported -- and the
+ * stream synchronised -- by boltz_sync.  fill_boundary does not report
+ * sigma_w in this mode.  Host-pointer calls stay synchronous.
+ */
+int boltz_set_async(boltz_ctx* ctx, int enable);
+int boltz_sync(boltz_ctx* ctx, void* stream);
 
 /* ---- measurement hooks (bench.py; no reference counterpart) ---- */
 

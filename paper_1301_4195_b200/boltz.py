@@ -91,6 +91,8 @@ def lib():
             "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
             "boltz_transport_step": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
+            "boltz_set_async": (i, [vp, i]),
+            "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
             "boltz_get_timing": (i, [vp, vp, vp, i, i]),
             "boltz_fp64_peak": (i, [i, d, dp]),
@@ -272,6 +274,21 @@ class CollisionOperator:
         a, b = C.c_int64(), C.c_int64()
         _check(lib().boltz_memory_bytes(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    # -- asynchronous mode (CUDA-graph capturable device calls)
+    def set_async(self, enable: bool = True):
+        """Device-pointer calls stop synchronising; errors surface at sync()."""
+        _check(lib().boltz_set_async(self._h, int(enable)))
+
+    def sync(self, stream=None):
+        """Synchronise and raise NumericError for any non-finite value seen since the last sync."""
+        if stream is None:
+            try:
+                import torch
+                stream = torch.cuda.current_stream(self.device).cuda_stream
+            except Exception:
+                stream = None
+        _check(lib().boltz_sync(self._h, stream))
 
     # -- measurement hooks (bench.py)
     KINDS = ("conv", "fft", "project", "layout", "transport")

@@ -64,7 +64,6 @@ struct boltz_ctx {
     int n = 0;
     double L = 0, lambda = 0, beta = 0, r0 = 0;
     int device = 0;
-    cudaStream_t own_stream = nullptr;
     // folded convolution table (conv.cuh)
     double* dH = nullptr;
     int2* dEnt = nullptr;
@@ -85,6 +84,7 @@ struct boltz_ctx {
     int panels = 64;  // Gauss-Legendre panels of the on-device generator (0 < lambda < 1)
     // per-kernel-class CUDA-event timing (bench.py roofline) and launch counts
     bool timing = false;
+    bool async_mode = false;  // device-pointer calls return without a sync (boltz_set_async)
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<int> ev_kind;
@@ -513,6 +513,8 @@ int guard_ctx(boltz_ctx* c) {
 // Runs fn(chunk_in, chunk_out, cells, stream) over chunks of the batch, staging
 // host memory through the context buffers when mem == HOST.  in_elems /
 // out_elems: doubles per cell of the user-layout input / output.
+int check_flag(boltz_ctx* c, cudaStream_t s);
+
 template <typename Fn>
 int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems, int mem,
                 void* stream, double* max_imag, Fn&& fn) {
@@ -525,9 +527,10 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
         return BOLTZ_ERR_CONFIG;
     }
     if (ncells == 0) return BOLTZ_OK;
-    cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+    cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
     ensure_workspace(c, ncells);
-    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
+    const bool deferred = c->async_mode && mem == BOLTZ_MEM_DEVICE;  // flag checked at boltz_sync
+    if (!deferred) CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     for (int64_t c0 = 0; c0 < ncells; c0 += c->cap) {
         const int64_t nc = std::min<int64_t>(c->cap, ncells - c0);
         const double* din = in + c0 * in_elems;
@@ -542,19 +545,26 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
             CK(cudaMemcpyAsync(out + c0 * out_elems, c->dOut, (size_t)nc * out_elems * 8, cudaMemcpyDeviceToHost, s));
         }
         if (max_imag) {
-            std::vector<unsigned long long> tmp(nc);
-            CK(cudaMemcpyAsync(tmp.data(), c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
             if (mem == BOLTZ_MEM_HOST) {
+                std::vector<unsigned long long> tmp(nc);
+                CK(cudaMemcpyAsync(tmp.data(), c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
                 std::memcpy(max_imag + c0, tmp.data(), (size_t)nc * 8);
             } else {
                 CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToDevice, s));
             }
         }
     }
+    if (deferred) return BOLTZ_OK;
+    return check_flag(c, s);
+}
+
+// synchronise `s`, fold timing, report (and clear) the non-finite flag
+int check_flag(boltz_ctx* c, cudaStream_t s) {
     CK(cudaMemcpyAsync(c->hFlag, c->dFlag, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (c->timing) collect_timing(c);
+    if (*c->hFlag) CK(cudaMemset(c->dFlag, 0, sizeof(int)));
     if (*c->hFlag & 1) {
         set_error("NumericError: non-finite value in the input distribution");
         return BOLTZ_ERR_NUMERIC;
@@ -657,7 +667,6 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
     c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device; c->panels = panels;
     try {
         CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         CK(cudaMalloc(&c->dFlag, sizeof(int)));
         CK(cudaMallocHost(&c->hFlag, sizeof(int)));
         fill_twiddles();
@@ -682,7 +691,6 @@ int boltz_destroy(boltz_ctx* c) {
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     if (c->hFlag) cudaFreeHost(c->hFlag);
-    if (c->own_stream) cudaStreamDestroy(c->own_stream);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return BOLTZ_OK;
@@ -801,13 +809,14 @@ int boltz_transport_step(boltz_ctx* c, const double* field, const double* base, 
             set_error("transport_step: invalid arguments (out must not alias field/base)");
             return BOLTZ_ERR_CONFIG;
         }
-        cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+        cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
         {
             Timed t_(c, KIND_TRANSPORT, s);
             launch_transport(c->n, field, base, base ? alpha : 0.0, out, ncl, x_ext, dx_ext, dt, wall_left,
                              wall_right, c->pc.dv, s);
         }
         CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;
         CK(cudaStreamSynchronize(s));
         if (c->timing) collect_timing(c);
         return BOLTZ_OK;
@@ -825,7 +834,7 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
             set_error("fill_boundary: wall temperature must be positive");
             return BOLTZ_ERR_CONFIG;
         }
-        cudaStream_t s = stream ? (cudaStream_t)stream : c->own_stream;
+        cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
         double vw[3] = {0, 0, 0};
         if (Vw_host3) std::memcpy(vw, Vw_host3, sizeof vw);
         double* dsig = reinterpret_cast<double*>(c->dMaxIm);
@@ -838,6 +847,7 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
             launch_fill_boundary(c->n, field, ncl, x_ext, side, kind, Tw, vw[0], vw[1], vw[2], c->pc.dv, dsig, s);
         }
         CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;  // sigma_w stays on the device (not reported)
         double hs = 0.0;
         CK(cudaMemcpyAsync(&hs, dsig, sizeof(double), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -845,6 +855,16 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
         if (sigma_w) *sigma_w = hs;
         return BOLTZ_OK;
     });
+}
+
+int boltz_set_async(boltz_ctx* c, int enable) {
+    if (!c) return BOLTZ_ERR_CONFIG;
+    c->async_mode = enable != 0;
+    return BOLTZ_OK;
+}
+
+int boltz_sync(boltz_ctx* c, void* stream) {
+    return api(c, [&] { return check_flag(c, (cudaStream_t)stream); });
 }
 
 int boltz_set_timing(boltz_ctx* c, int enable) {

@@ -136,3 +136,37 @@ def test_uniform_equilibrium_is_quiescent(gpu):
             s.strang_step(dt)
         got = s.interior.cpu().numpy()
     assert np.abs(got - f0).max() < 5e-2 * f0.max()
+
+
+def test_async_graph_run_matches_eager(gpu):
+    """Solver1D.run (async library + CUDA graph of 3 Strang steps) is bitwise
+    the eager strang_step trajectory."""
+    n, L, nx, Tw = 8, 5.0, 12, 2.0
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    grid = VelocityGrid.create(n, L)
+    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (nx, 1))
+    with _op(n, L) as op:
+        a = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw))
+        b = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw))
+        dt = a.cfl_dt()
+        for _ in range(8):
+            a.strang_step(dt)
+        b.run(dt, 8)
+        assert b.graph_replays == 2
+        assert np.array_equal(a.interior.cpu().numpy(), b.interior.cpu().numpy())
+        assert abs(a.t - b.t) < 1e-15
+
+
+def test_async_mode_defers_numeric_error(gpu):
+    from paper_1301_4195_b200 import NumericError
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = torch.from_numpy(scenarios.mixture_cells(grid, 3, seed=2)).to(gpu)
+    f[1, 5] = float("nan")
+    with _op(n, L) as op:
+        op.set_async(True)
+        op.collision_rk2(f, 0.01)  # returns without raising
+        with pytest.raises(NumericError):
+            op.sync()
+        op.sync()  # flag cleared
+        op.set_async(False)
