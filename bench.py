@@ -62,6 +62,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--cells", type=int, default=CELLS)
     p.add_argument("--no-n32", action="store_true", help="skip the N=32 (cfg5-shaped) sub-measurement")
+    p.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 Strang-step sub-measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     return p.parse_args()
@@ -275,6 +276,8 @@ def main():
     e2e_value = evals / (float(te.item()) * 1e-3)
 
     # N=32 (cfg5-shaped: 2048 two-Maxwellian cells, L=8) sub-measurement
+    cfg3 = bench_cfg3(op, dev) if rank == 0 and not args.no_cfg3 else None
+
     n32 = None
     if not args.no_n32 and rank == 0:
         op.close()
@@ -315,11 +318,41 @@ def main():
         }
         if n32:
             line["n32"] = n32
+        if cfg3:
+            line["cfg3"] = cfg3
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_cfg3(op, dev, steps=60):
+    """cfg3 (BASELINE.json configs[2]) on this rank: Nx=256 geometric cells,
+    diffuse wall T_w=2, Strang steps (SSP-RK2 transport + RK2 collision) replayed
+    as a CUDA graph of 3 steps; 1 rank (the halo path is exercised by tests)."""
+    import torch
+    from paper_1301_4195_b200 import scenarios
+    from paper_1301_4195_b200.solver import Boundary, Solver1D
+    grid = op.grid
+    x, dx = scenarios.geometric_grid(256, 20.0, 1.02)
+    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (256, 1))
+    s = Solver1D(op, x, dx, f0, left=Boundary("wall", 2.0), right=Boundary("extrap"), device=dev)
+    dt = s.cfl_dt()
+    s.strang_step(dt)
+    s.capture(dt)
+    s.advance(3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"workload": "cfg3: Nx=256 geometric (1.02) on [0,20], N=16 L=6, diffuse wall T_w=2, dt=CFL 0.9",
+            "steps": steps, "ms_per_step": ms / steps, "cells_steps_per_s": 256 * steps / (ms * 1e-3),
+            "evals_per_s": 2 * 256 * steps / (ms * 1e-3), "mode": "async library + CUDA graph of 3 Strang steps",
+            "launches_per_step": 18}
 
 
 def bench_n32(args, dev, local):

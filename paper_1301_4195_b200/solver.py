@@ -190,37 +190,54 @@ class Solver1D:
         captured once in a CUDA graph and replayed (three steps return the
         field / scratch buffer rotation to its start).  Numeric errors are
         reported once, at the end (boltz_sync)."""
-        import torch
-        self.op.set_async(True)
-        try:
-            if not graph or self.world > 1 or steps < 3:
+        if not graph or self.world > 1 or steps < 4:
+            self.op.set_async(True)
+            try:
                 for _ in range(steps):
                     self.strang_step(dt)
                 self.op.sync()
-                return
-            self.strang_step(dt)  # warm-up outside capture: workspace + kernel attributes
-            self.op.sync()
-            steps -= 1
-            stream = torch.cuda.Stream(self.device)
-            stream.wait_stream(torch.cuda.current_stream(self.device))
-            g = torch.cuda.CUDAGraph()
-            ptrs = [t.data_ptr() for t in (self.field, self._tmp, self._tmp2)]
+            finally:
+                self.op.set_async(False)
+            return
+        self.strang_step(dt)  # warm-up outside capture: workspace + kernel attributes
+        self.capture(dt)
+        self.advance(steps - 1)
+
+    def capture(self, dt: float) -> None:
+        """Capture three Strang steps of size dt into a CUDA graph (not executed)."""
+        import torch
+        self.op.set_async(True)
+        stream = torch.cuda.Stream(self.device)
+        stream.wait_stream(torch.cuda.current_stream(self.device))
+        g = torch.cuda.CUDAGraph()
+        ptrs = [t.data_ptr() for t in (self.field, self._tmp, self._tmp2)]
+        t0 = self.t
+        try:
             with torch.cuda.stream(stream):
                 with torch.cuda.graph(g, stream=stream):
                     for _ in range(3):
                         self.strang_step(dt)
-            assert [t.data_ptr() for t in (self.field, self._tmp, self._tmp2)] == ptrs, "buffer rotation"
-            self.t -= 3 * dt  # capture does not execute
-            torch.cuda.current_stream(self.device).wait_stream(stream)
+        finally:
+            self.op.set_async(False)
+        assert [t.data_ptr() for t in (self.field, self._tmp, self._tmp2)] == ptrs, "buffer rotation"
+        torch.cuda.current_stream(self.device).wait_stream(stream)
+        self.t = t0
+        self._graph, self._graph_dt = g, dt
+
+    def advance(self, steps: int) -> None:
+        """`steps` Strang steps of the captured dt: graph replays + eager remainder."""
+        g, dt = self._graph, self._graph_dt
+        self.op.set_async(True)
+        try:
             for _ in range(steps // 3):
                 g.replay()
                 self.t += 3 * dt
             for _ in range(steps % 3):
                 self.strang_step(dt)
             self.op.sync()
-            self.graph_replays = steps // 3
         finally:
             self.op.set_async(False)
+        self.graph_replays = getattr(self, "graph_replays", 0) + steps // 3
 
 
 def strang_step_loopback(solvers: Sequence[Solver1D], dt: float) -> None:

@@ -80,15 +80,21 @@ def spatial(args, rank, world, dev):
     dt = s.cfl_dt()
     # warm-up step (not timed), then the run
     s.strang_step(dt)
+    graph = args.mode == "graph" and world == 1
+    if graph:
+        s.capture(dt)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     op.timing(reset=True)
-    op.set_timing(True)
+    op.set_timing(not graph)  # per-kernel events are not capturable
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(steps):
-        s.strang_step(dt)
+    if graph:
+        s.advance(steps)
+    else:
+        for _ in range(steps):
+            s.strang_step(dt)
     e1.record()
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -154,6 +160,7 @@ def main():
     p.add_argument("--config", type=int, required=True, choices=[1, 2, 3, 4, 5])
     p.add_argument("--steps", type=int, default=0)
     p.add_argument("--lam", type=float, default=1.0)
+    p.add_argument("--mode", default="graph", choices=["graph", "eager"])
     args = p.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
