@@ -74,8 +74,12 @@ struct boltz_ctx {
     double2* dA = nullptr;
     double2* dB = nullptr;
     double* dFs = nullptr;   // RK2 stage (user layout)
-    double* dIn = nullptr;   // host-call staging (user layout, complex-sized)
-    double* dOut = nullptr;
+    // host-call pipeline: double-buffered staging (user layout, complex-sized) + copy streams
+    int64_t stage_cap = 0;
+    double* dStageIn[2] = {nullptr, nullptr};
+    double* dStageOut[2] = {nullptr, nullptr};
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
     unsigned long long* dMaxIm = nullptr;
     int* dFlag = nullptr;
     int* hFlag = nullptr;    // pinned
@@ -220,6 +224,15 @@ void build_table(boltz_ctx* c, const double* G_host) {
         }
     row_start[n * n] = (int)ent.size();
     c->nent = (int)ent.size();
+    {   // processing order appended after the CSR offsets (conv.cuh conv_row): longest rows first
+        std::vector<int> order(n * n);
+        for (int r = 0; r < n * n; ++r) order[r] = r;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+            return row_start[a + 1] - row_start[a] > row_start[b + 1] - row_start[b];
+        });
+        row_start.insert(row_start.end(), order.begin(), order.end());
+        for (int r = 0; r < n * n; ++r) row_start.push_back(r);  // natural order
+    }
     const size_t hbytes = (size_t)c->nent * c->slab * sizeof(double);
     CK(cudaMalloc(&c->dH, hbytes));
     CK(cudaMalloc(&c->dEnt, ent.size() * sizeof(int2)));
@@ -272,22 +285,38 @@ void ensure_workspace(boltz_ctx* c, int64_t cells) {
     int64_t want = (cells + kLanes - 1) / kLanes * kLanes;
     // capacity: up to BOLTZ_WORKSPACE_GB (default 8) GiB of workspace per context
     const int64_t n3 = n3_of(c);
-    const int64_t per_cell = n3 * (16 + 16 + 8 + 16 + 16) + 8;
+    const int64_t per_cell = n3 * (16 + 16 + 8) + 8;
     double gb = 8.0;
     if (const char* e = std::getenv("BOLTZ_WORKSPACE_GB")) gb = std::max(0.01, std::atof(e));
     int64_t lim = std::max<int64_t>(kLanes, (int64_t)(gb * (1 << 30)) / per_cell / kLanes * kLanes);
     want = std::min(want, lim);
     if (want <= c->cap) return;
-    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut); cudaFree(c->dMaxIm);
-    c->dA = c->dB = nullptr; c->dFs = c->dIn = c->dOut = nullptr; c->dMaxIm = nullptr; c->cap = 0;
+    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dMaxIm);
+    c->dA = c->dB = nullptr; c->dFs = nullptr; c->dMaxIm = nullptr; c->cap = 0;
     CK(cudaMalloc(&c->dA, (size_t)want * n3 * 16));
     CK(cudaMalloc(&c->dB, (size_t)want * n3 * 16));
     CK(cudaMalloc(&c->dFs, (size_t)want * n3 * 8));
-    CK(cudaMalloc(&c->dIn, (size_t)want * n3 * 16));
-    CK(cudaMalloc(&c->dOut, (size_t)want * n3 * 16));
     CK(cudaMalloc(&c->dMaxIm, (size_t)want * 8));
     c->cap = want;
-    c->ws_bytes = want * per_cell;
+    c->ws_bytes = want * per_cell + c->stage_cap * n3 * 64;
+}
+
+// double-buffered device staging for host-memory calls (run_host_pipelined)
+void ensure_staging(boltz_ctx* c, int64_t cells) {
+    if (cells <= c->stage_cap) return;
+    const int64_t n3 = n3_of(c);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->dStageIn[b]);
+        cudaFree(c->dStageOut[b]);
+        c->dStageIn[b] = c->dStageOut[b] = nullptr;
+    }
+    c->stage_cap = 0;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&c->dStageIn[b], (size_t)cells * n3 * 16));
+        CK(cudaMalloc(&c->dStageOut[b], (size_t)cells * n3 * 16));
+    }
+    c->stage_cap = cells;
+    c->ws_bytes = c->cap * (n3 * 40 + 8) + c->stage_cap * n3 * 64;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -329,6 +358,8 @@ struct Launch {
         const int64_t ng = (nc + 31) / 32;
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+        // longest-rows-first only when the grid is a few waves deep (~2 CTAs per SM resident)
+        const int lpt = (int64_t)grid.x * grid.y < 8 * 2 * 148 ? 1 : 0;
         if constexpr (conv_kernel_for(N) == 2 && NK == 2) {
             using LY = T2Layout<N>;
             const int smem = LY::W * LY::WARP_BYTES;
@@ -340,7 +371,7 @@ struct Launch {
             }
             dim3 g2(N * N * 2, (unsigned)((ng + LY::W - 1) / LY::W));
             Timed t_(c, KIND_CONV, s);
-            k_conv_t2<N><<<g2, kLanes * LY::W, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+            k_conv_t2<N><<<g2, kLanes * LY::W, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
         } else if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
             static bool configured = false;  // per process; attributes apply to every device
@@ -351,7 +382,7 @@ struct Launch {
             }
             Timed t_(c, KIND_CONV, s);
             k_conv_pipe<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
-                                                                    (int)ng);
+                                                                    (int)ng, lpt);
         } else if constexpr (conv_kernel_for(N) == 3) {
             using LY = KcsLayout<N>;
             const int smem = kConvWarps * LY::WARP_BYTES;
@@ -366,17 +397,17 @@ struct Launch {
             }
             dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
             Timed t_(c, KIND_CONV, s);
-            k_conv_kcs<N, 0><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+            k_conv_kcs<N, 0><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
             if constexpr (NK > 1)
                 k_conv_kcs<N, KC1><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
-                                                                         (int)ng);
+                                                                         (int)ng, lpt);
         } else if constexpr (NK == 2 && BOLTZ_K0_SPLIT) {
             dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
             Timed t_(c, KIND_CONV, s);
-            k_conv_kc<N, 0><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
-            k_conv_kc<N, 1><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng);
+            k_conv_kc<N, 0><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
+            k_conv_kc<N, 1><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
         } else
-        { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng); }
+        { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt); }
         CK(cudaGetLastError());
     }
     // group complex c->dB (already * s_m) -> group real Qt in (double*)c->dA; max|Im| per cell
@@ -514,6 +545,9 @@ int guard_ctx(boltz_ctx* c) {
 // host memory through the context buffers when mem == HOST.  in_elems /
 // out_elems: doubles per cell of the user-layout input / output.
 int check_flag(boltz_ctx* c, cudaStream_t s);
+template <typename Fn>
+int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
+                       cudaStream_t s, double* max_imag, Fn&& fn);
 
 template <typename Fn>
 int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems, int mem,
@@ -528,34 +562,59 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
     }
     if (ncells == 0) return BOLTZ_OK;
     cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
+    if (mem == BOLTZ_MEM_HOST) return run_host_pipelined(c, in, out, ncells, in_elems, out_elems, s, max_imag, fn);
     ensure_workspace(c, ncells);
-    const bool deferred = c->async_mode && mem == BOLTZ_MEM_DEVICE;  // flag checked at boltz_sync
+    const bool deferred = c->async_mode;  // flag checked at boltz_sync
     if (!deferred) CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     for (int64_t c0 = 0; c0 < ncells; c0 += c->cap) {
         const int64_t nc = std::min<int64_t>(c->cap, ncells - c0);
-        const double* din = in + c0 * in_elems;
-        double* dout = out + c0 * out_elems;
-        if (mem == BOLTZ_MEM_HOST) {
-            CK(cudaMemcpyAsync(c->dIn, din, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice, s));
-            din = c->dIn;
-            dout = c->dOut;
-        }
-        fn(din, dout, nc, s);
-        if (mem == BOLTZ_MEM_HOST) {
-            CK(cudaMemcpyAsync(out + c0 * out_elems, c->dOut, (size_t)nc * out_elems * 8, cudaMemcpyDeviceToHost, s));
-        }
-        if (max_imag) {
-            if (mem == BOLTZ_MEM_HOST) {
-                std::vector<unsigned long long> tmp(nc);
-                CK(cudaMemcpyAsync(tmp.data(), c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
-                std::memcpy(max_imag + c0, tmp.data(), (size_t)nc * 8);
-            } else {
-                CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToDevice, s));
-            }
-        }
+        fn(in + c0 * in_elems, out + c0 * out_elems, nc, s);
+        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToDevice, s));
     }
     if (deferred) return BOLTZ_OK;
+    return check_flag(c, s);
+}
+
+// Host-memory calls: the batch is cut into chunks and pipelined over three
+// streams -- H2D of chunk i+1 (copy engine), compute of chunk i (`s`), D2H of
+// chunk i-1 (the other copy engine) -- through double-buffered staging, so
+// with pinned host memory the PCIe traffic hides behind the kernels.
+template <typename Fn>
+int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
+                       cudaStream_t s, double* max_imag, Fn&& fn) {
+    int64_t pieces = 4;  // pipeline depth; BOLTZ_HOST_CHUNKS overrides (tuning)
+    if (const char* e = std::getenv("BOLTZ_HOST_CHUNKS")) pieces = std::max(1, std::atoi(e));
+    int64_t chunk = ncells <= 512 ? ncells : std::max<int64_t>(256, (ncells + pieces - 1) / pieces);
+    chunk = (chunk + kLanes - 1) / kLanes * kLanes;
+    ensure_workspace(c, chunk);
+    chunk = std::min<int64_t>(chunk, c->cap);
+    ensure_staging(c, chunk);
+    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
+    const int64_t nchunks = (ncells + chunk - 1) / chunk;
+    auto h2d = [&](int64_t i) {
+        const int slot = (int)(i & 1);
+        const int64_t c0 = i * chunk, nc = std::min<int64_t>(chunk, ncells - c0);
+        if (i >= 2) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-2 done reading
+        CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice,
+                           c->h2d_stream));
+        CK(cudaEventRecord(c->ev_h2d[slot], c->h2d_stream));
+    };
+    h2d(0);
+    for (int64_t i = 0; i < nchunks; ++i) {
+        const int slot = (int)(i & 1);
+        const int64_t c0 = i * chunk, nc = std::min<int64_t>(chunk, ncells - c0);
+        CK(cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
+        if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
+        fn(c->dStageIn[slot], c->dStageOut[slot], nc, s);
+        CK(cudaEventRecord(c->ev_comp[slot], s));
+        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
+        if (i + 1 < nchunks) h2d(i + 1);
+        CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
+        CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
+                           cudaMemcpyDeviceToHost, c->d2h_stream));
+        CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
+    }
+    CK(cudaStreamSynchronize(c->d2h_stream));
     return check_flag(c, s);
 }
 
@@ -668,6 +727,14 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
     try {
         CK(cudaSetDevice(device));
         CK(cudaMalloc(&c->dFlag, sizeof(int)));
+        CK(cudaMemset(c->dFlag, 0, sizeof(int)));
+        CK(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming));
+        }
         CK(cudaMallocHost(&c->hFlag, sizeof(int)));
         fill_twiddles();
         build_projection(c);
@@ -688,8 +755,17 @@ int boltz_destroy(boltz_ctx* c) {
     if (!c) return BOLTZ_OK;
     cudaSetDevice(c->device);
     cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
-    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dIn); cudaFree(c->dOut);
+    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->dStageIn[b]);
+        cudaFree(c->dStageOut[b]);
+        if (c->ev_h2d[b]) cudaEventDestroy(c->ev_h2d[b]);
+        if (c->ev_comp[b]) cudaEventDestroy(c->ev_comp[b]);
+        if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
+    }
+    if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->hFlag) cudaFreeHost(c->hFlag);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;

@@ -138,6 +138,15 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// row_start holds the CSR offsets of the N*N output rows (N*N+1 ints), then two
+// processing orders of the rows: longest row list first (lpt != 0: for grids
+// of a few waves, so the last wave is made of short rows) and the natural order
+// (many waves: neighbouring rows share f-hat rows in L2).
+template <int N>
+__device__ __forceinline__ int conv_row(const int* __restrict__ row_start, int b, int lpt) {
+    return __ldg(row_start + N * N + 1 + (lpt ? 0 : N * N) + b);
+}
+
 template <int N, int T>
 __device__ __forceinline__ void write_row(double2* __restrict__ B, int g, int row, int kc, int lane,
                                           const double2 (&acc)[T]) {
@@ -185,9 +194,9 @@ __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const 
 template <int N>
 __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-       const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+       const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
     constexpr int T = conv_tile(N), NK = N / T, N3 = N * N * N;
-    const int kc = blockIdx.x % NK, row = blockIdx.x / NK;
+    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, lpt);
     const int lane = threadIdx.x & 31;
     const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
     if (g >= ngroups) return;
@@ -209,9 +218,9 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
 template <int N, int KC>
 __global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
 k_conv_kc(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
     constexpr int T = conv_tile(N), N3 = N * N * N;
-    const int row = blockIdx.x;
+    const int row = conv_row<N>(row_start, blockIdx.x, lpt);
     const int lane = threadIdx.x & 31;
     const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
     if (g >= ngroups) return;
@@ -243,11 +252,11 @@ struct KcsLayout {
 template <int N, int KC>
 __global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
 k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
     using LY = KcsLayout<N>;
     constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int row = blockIdx.x;
+    const int row = conv_row<N>(row_start, blockIdx.x, lpt);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * kConvWarps + wid;
     if (g >= ngroups) return;
@@ -413,11 +422,11 @@ __device__ __forceinline__ void t2_rows(char* wsm, const double2* __restrict__ A
 template <int N>
 __global__ void __launch_bounds__(kLanes* T2Layout<N>::W, T2Layout<N>::MINB)
 k_conv_t2(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
     using LY = T2Layout<N>;
     constexpr int T = LY::T, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int kc = blockIdx.x & 1, row = blockIdx.x >> 1;
+    const int kc = blockIdx.x & 1, row = conv_row<N>(row_start, blockIdx.x >> 1, lpt);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * LY::W + wid;
     if (g >= ngroups) return;  // whole warp exits; warps never sync with each other
@@ -511,11 +520,11 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
 template <int N>
 __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-            const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups) {
+            const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
     using PL = PipeLayout<N>;
     constexpr int T = PL::T, NK = PL::NK, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int kc = blockIdx.x % NK, row = blockIdx.x / NK;
+    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, lpt);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * kConvWarps + wid;
     if (g >= ngroups) return;

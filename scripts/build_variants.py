@@ -4,9 +4,9 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
-    "kcs16_m3": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3"],
-    "kcs16_m3_w8": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=1", "BOLTZ_CONV_WARPS=12"],
-    "kcs_m2_w8": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_CONV_WARPS=8"],
+    "w4": [],
+    "w1": ["BOLTZ_CONV_WARPS=1"],
+    "w2": ["BOLTZ_CONV_WARPS=2"],
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)
