@@ -89,6 +89,9 @@ __host__ __device__ constexpr int conv_tile(int n) {
 #ifndef BOLTZ_CONV_WARPS
 #define BOLTZ_CONV_WARPS 4
 #endif
+#ifndef BOLTZ_TERM_HX
+#define BOLTZ_TERM_HX 0  // term arithmetic: 0 = (x*y) then h*, 1 = (h*x) then *y
+#endif
 // 3 = k_conv_kcs (one kernel per k-chunk, y/H staged), 2 = k_conv_t2 (NK == 2
 // only), 1 = k_conv_pipe, 0 = k_conv; -1 = per-N default
 #ifndef BOLTZ_CONV_KERNEL
@@ -121,10 +124,19 @@ __device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[
             if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
             else h = hb.y;
             ++p;
+#if BOLTZ_TERM_HX
+            // b = h*x (independent of y and acc), then acc += b*y: 2 DMUL + 4 DFMA
+            const double bx = h * xm.x, by = h * xm.y;
+            acc[kk].x = fma(bx, y[j].x, acc[kk].x);
+            acc[kk].x = fma(-by, y[j].y, acc[kk].x);
+            acc[kk].y = fma(bx, y[j].y, acc[kk].y);
+            acc[kk].y = fma(by, y[j].x, acc[kk].y);
+#else
             const double tr = fma(xm.x, y[j].x, -xm.y * y[j].y);
             const double ti = fma(xm.x, y[j].y, xm.y * y[j].x);
             acc[kk].x = fma(h, tr, acc[kk].x);
             acc[kk].y = fma(h, ti, acc[kk].y);
+#endif
         }
         after(i, m3);
     }
@@ -144,7 +156,7 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 // (many waves: neighbouring rows share f-hat rows in L2).
 template <int N>
 __device__ __forceinline__ int conv_row(const int* __restrict__ row_start, int b, int lpt) {
-    return __ldg(row_start + N * N + 1 + (lpt ? 0 : N * N) + b);
+    return lpt ? __ldg(row_start + N * N + 1 + b) : b;
 }
 
 template <int N, int T>

@@ -26,12 +26,16 @@ struct Fused {
     static constexpr int CELL = N * N * ROW;          // complex elements per cell in smem
     static constexpr int CELL_BYTES = CELL * 16;
     // cells per block: largest power of two <= 32 whose cubes fit in ~200 KB
-    static constexpr int CPB = (CELL_BYTES * 32 <= 200 * 1024)   ? 32
-                               : (CELL_BYTES * 16 <= 200 * 1024) ? 16
-                               : (CELL_BYTES * 8 <= 200 * 1024)  ? 8
-                               : (CELL_BYTES * 4 <= 200 * 1024)  ? 4
-                               : (CELL_BYTES * 2 <= 200 * 1024)  ? 2
-                                                                 : 1;
+#ifndef BOLTZ_FUSED_BUDGET_KB
+#define BOLTZ_FUSED_BUDGET_KB 200
+#endif
+    static constexpr int BUDGET = BOLTZ_FUSED_BUDGET_KB * 1024;
+    static constexpr int CPB = (CELL_BYTES * 32 <= BUDGET)   ? 32
+                               : (CELL_BYTES * 16 <= BUDGET) ? 16
+                               : (CELL_BYTES * 8 <= BUDGET)  ? 8
+                               : (CELL_BYTES * 4 <= BUDGET)  ? 4
+                               : (CELL_BYTES * 2 <= BUDGET)  ? 2
+                                                             : 1;
     static constexpr bool FITS = CELL_BYTES <= 200 * 1024;
 #ifndef BOLTZ_FUSED_THREADS
 #define BOLTZ_FUSED_THREADS 512
