@@ -291,6 +291,7 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
     const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
     if (e0 < e1) {
         int2 en = __ldg(ent + e0);
+        int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;  // next entry, loaded a row early
         issue_y(en);
         issue_h(0, e0);
         cp_async_commit();
@@ -299,7 +300,8 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
         for (int e = e0; e < e1; ++e) {
             const int cur = (e - e0) & 1;
             const bool more = e + 1 < e1;
-            const int2 nx = more ? __ldg(ent + e + 1) : en;
+            const int2 nx = en_ahead;
+            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
             __syncwarp();  // every lane finished reading H[cur^1]
             if (more) issue_h(cur ^ 1, e + 1);
             cp_async_commit();
@@ -493,6 +495,9 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
     };
     if (e0 >= e1) return;
     int2 en_next = __ldg(ent + e0);
+    // the entry two row pairs ahead is loaded one row early, so the cp.async
+    // addresses at a row start never wait on a dependent global load
+    int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en_next;
     issue_xh(0, en_next, e0);
     issue_y(en_next);
     cp_async_wait_all();
@@ -503,7 +508,8 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
     for (int e = e0; e < e1; ++e) {
         const int cur = (e - e0) & 1;
         const bool more = e + 1 < e1;
-        if (more) en_next = __ldg(ent + e + 1);
+        en_next = en_ahead;
+        if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
         __syncwarp();
         if (more) issue_xh(cur ^ 1, en_next, e + 1);
         if (NK == 1 && more) issue_y(en_next);

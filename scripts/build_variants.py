@@ -4,10 +4,9 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
-    "base": [],
-    "hx": ["BOLTZ_TERM_HX=1"],
-    "cpb1": ["BOLTZ_FUSED_BUDGET_KB=100"],
-    "cpb1_256": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=256"],
+    "kcs16_m3": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3"],
+    "kcs16_m2": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=2"],
+    "kcs16_m3w2": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3", "BOLTZ_CONV_WARPS=2"],
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)
