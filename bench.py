@@ -305,7 +305,7 @@ def main():
             "kernel_launches": klaunch,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic("k_conv_pipe<16>", cells),
-                         "kernel": "k_conv<16> (K2)",
+                         "kernel": "k_conv_pipe<16> (K2)",
                          "note": "achieved = 10 flop x 27/64 N^6 valid terms x cells per launch / mean launch time "
                                  "(algorithmic, SURVEY.md §8d); the kernel executes half of those terms "
                                  "(pair symmetry, DESIGN.md), so executed-flop fraction = frac/2. peak = DFMA "

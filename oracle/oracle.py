@@ -22,7 +22,8 @@ _lib = None
 
 
 def build() -> None:
-    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    # stdout silenced: bench.py's contract is ONE JSON line on stdout
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True, stdout=subprocess.DEVNULL)
 
 
 def lib():
