@@ -21,9 +21,6 @@
 #include "fused.cuh"
 #include "gen.cuh"
 
-#ifndef BOLTZ_K0_SPLIT
-#define BOLTZ_K0_SPLIT 0  // N=32: one kernel per k-chunk instead of one kernel for both
-#endif
 #ifndef BOLTZ_FUSED
 #define BOLTZ_FUSED 1  // single-kernel K1 / K3 when the N^3 cube fits in shared memory
 #endif
@@ -360,19 +357,7 @@ struct Launch {
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
         // longest-rows-first only when the grid is a few waves deep (~2 CTAs per SM resident)
         const int lpt = (int64_t)grid.x * grid.y < 8 * 2 * 148 ? 1 : 0;
-        if constexpr (conv_kernel_for(N) == 2 && NK == 2) {
-            using LY = T2Layout<N>;
-            const int smem = LY::W * LY::WARP_BYTES;
-            static bool configured = false;  // per process; attributes apply to every device
-            if (!configured) {
-                CK(cudaFuncSetAttribute(k_conv_t2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                CK(cudaFuncSetAttribute(k_conv_t2<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                configured = true;
-            }
-            dim3 g2(N * N * 2, (unsigned)((ng + LY::W - 1) / LY::W));
-            Timed t_(c, KIND_CONV, s);
-            k_conv_t2<N><<<g2, kLanes * LY::W, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
-        } else if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
+        if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
             static bool configured = false;  // per process; attributes apply to every device
             if (!configured) {
@@ -401,11 +386,6 @@ struct Launch {
             if constexpr (NK > 1)
                 k_conv_kcs<N, KC1><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
                                                                          (int)ng, lpt);
-        } else if constexpr (NK == 2 && BOLTZ_K0_SPLIT) {
-            dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-            Timed t_(c, KIND_CONV, s);
-            k_conv_kc<N, 0><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
-            k_conv_kc<N, 1><<<g1, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
         } else
         { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt); }
         CK(cudaGetLastError());

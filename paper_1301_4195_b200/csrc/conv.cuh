@@ -21,14 +21,14 @@
 //  * Deterministic: each output is accumulated by one thread in a fixed order
 //    (SPEC.md:233); results are independent of batch composition.
 //
-// Kernels:
-//  k_conv_t2   T = N/2 (two k-chunks).  Per-warp shared memory holds ONE x row,
-//              ONE y chunk and a double-buffered H slab; x slots are refilled
-//              for the next row pair right after their last use, y chunks
-//              half a row ahead (cp.async), so ~25 KB per warp lets 8-16 warps
-//              share an SM.  The default for every N.
-//  k_conv_pipe x double-buffered, full y row staged (more smem per warp).
-//  k_conv      no staging, direct loads (reference implementation of the order).
+// Kernels (per-N choice by measurement, see conv_kernel_for):
+//  k_conv_pipe  N <= 16: per-warp cp.async ring -- the next row pair's x row,
+//               y row and H slab stream into shared memory while the current
+//               one computes.
+//  k_conv_kcs   N = 24, 32: one kernel per k-chunk (halves the unrolled code);
+//               y row and H slab staged one row ahead (H is DRAM-resident at
+//               N=32), x read from L2.
+//  k_conv       no staging, direct loads: the plain statement of the order.
 #pragma once
 #include "common.cuh"
 
@@ -41,8 +41,8 @@ namespace boltz_gpu {
 // t = 0..NK-1 and diagonals m3 in the order band_diag(); terms in k3 order.
 // For NK == 2 the triangle tile comes first and the square tile (sc == kc,
 // which covers every diagonal the row uses) last, walked so that the
-// diagonals the next row's first tile needs are finished first (k_conv_t2's
-// x-slot refill relies on it).
+// diagonals the next row's first tile needs are finished first (an x-slot
+// refill schedule; measured in round 1, the order is kept for all kernels).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr bool band_term(int n, int t, int kc, int sc, int m3, int kk) {
     int k3 = kc * t + kk, s3 = k3 - m3 + n / 2;
@@ -64,8 +64,7 @@ __host__ __device__ constexpr int band_slab_kc(int n, int t) {
     for (int kc = 0; kc < n / t; ++kc) mx = band_kc_terms(n, t, kc) > mx ? band_kc_terms(n, t, kc) : mx;
     return (mx + 1) & ~1;  // even -> 16 B aligned double2 reads
 }
-// diagonal index i (in band_diag order) after which the x slot is refilled
-// for the next row pair in k_conv_t2: -1 = never used by this k-chunk.
+// does diagonal m3 carry any term of tile (kc, sc)?
 __host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m3) {
     bool any = false;
     for (int kk = 0; kk < t; ++kk) any = any || band_term(n, t, kc, sc, m3, kk);
@@ -74,9 +73,11 @@ __host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m
 
 // Register tile width and kernel per N, chosen by measurement on B200
 // (scripts/ab_conv.py, scripts/ab_n32.sh; algorithmic TFLOP/s, round 1):
-//   N=16: T=16 k_conv_pipe 47.5 | T=16 kcs 46.4 | T=8 t2 42.4 | T=8 kcs 39.7 | T=16 k_conv 41.1
-//   N=24: T=24 kcs 45.5         | T=12 kcs 43.5 | T=12 t2 39.1 | T=24 pipe 36.0 | T=12 k_conv 34.3
-//   N=32: T=16 kcs 45.3         | T=16 k_conv split per k-chunk 35.2 | k_conv 33.3 | pipe 28.8 | t2 26.7
+//   N=16: T=16 k_conv_pipe 47.5 | T=16 kcs 46.4 | T=8 kcs 39.7 | T=16 k_conv 41.1
+//   N=24: T=24 kcs 45.5         | T=12 kcs 43.5 | T=24 pipe 36.0 | T=12 k_conv 34.3
+//   N=32: T=16 kcs 45.3         | T=16 k_conv 33.3 | pipe 28.8
+// (two removed variants also lost: a single-x-buffer streaming kernel with
+//  T = N/2, 42.4 / 39.1 / 26.7, and k_conv split per k-chunk, 35.2 at N=32)
 #ifndef BOLTZ_TILE16
 #define BOLTZ_TILE16 16
 #endif
@@ -92,8 +93,8 @@ __host__ __device__ constexpr int conv_tile(int n) {
 #ifndef BOLTZ_TERM_HX
 #define BOLTZ_TERM_HX 0  // term arithmetic: 0 = (x*y) then h*, 1 = (h*x) then *y
 #endif
-// 3 = k_conv_kcs (one kernel per k-chunk, y/H staged), 2 = k_conv_t2 (NK == 2
-// only), 1 = k_conv_pipe, 0 = k_conv; -1 = per-N default
+// 3 = k_conv_kcs (one kernel per k-chunk, y/H staged), 1 = k_conv_pipe,
+// 0 = k_conv; -1 = per-N default
 #ifndef BOLTZ_CONV_KERNEL
 #define BOLTZ_CONV_KERNEL -1
 #endif
@@ -222,29 +223,9 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
     write_row<N, T>(B, g, row, kc, lane, acc);
 }
 
-// the same, one k-chunk per kernel (halves the instruction footprint an SM
-// streams at N=32, whose fully unrolled band is ~60 KB of SASS per chunk)
 #ifndef BOLTZ_K0_MINB
 #define BOLTZ_K0_MINB 1
 #endif
-template <int N, int KC>
-__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
-k_conv_kc(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
-    constexpr int T = conv_tile(N), N3 = N * N * N;
-    const int row = conv_row<N>(row_start, blockIdx.x, lpt);
-    const int lane = threadIdx.x & 31;
-    const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
-    if (g >= ngroups) return;
-    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
-    double2 acc[T];
-#pragma unroll
-    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
-    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
-    conv_rows<N, KC>(Ag, H, ent, e0, e1, acc);
-    write_row<N, T>(B, g, row, KC, lane, acc);
-}
-
 // ---------------------------------------------------------------------------
 // k_conv_kcs: one k-chunk per kernel; the y row and the H slab of the next row
 // pair are staged in shared memory by cp.async while the current one computes
@@ -334,125 +315,6 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
         }
     }
     write_row<N, T>(B, g, row, KC, lane, acc);
-}
-
-// ---------------------------------------------------------------------------
-// k_conv_t2: T = N/2, streaming x refill (see header)
-//   per warp: x[N][32] double2 | y[T][32] double2 | H[2][SLAB_KC] double
-// ---------------------------------------------------------------------------
-template <int N>
-struct T2Layout {
-    static constexpr int W = N == 32 ? 3 : kConvWarps;                 // warps (cell groups) per CTA
-    static constexpr int MINB = N == 16 ? 4 : 2;                       // CTAs per SM the regs must allow
-    static constexpr int T = N / 2;
-    static constexpr int SLAB_KC = band_slab_kc(N, T);
-    static constexpr int X_BYTES = N * kLanes * 16;
-    static constexpr int Y_BYTES = T * kLanes * 16;
-    static constexpr int H_BYTES = SLAB_KC * 8;
-    static constexpr int WARP_BYTES = X_BYTES + Y_BYTES + 2 * H_BYTES;
-};
-
-template <int N, int KC>
-__device__ __forceinline__ void t2_rows(char* wsm, const double2* __restrict__ Ag, const double* __restrict__ H,
-                                        const int2* __restrict__ ent, int e0, int e1, int lane,
-                                        double2 (&acc)[N / 2]) {
-    using LY = T2Layout<N>;
-    constexpr int T = LY::T, NK = 2;
-    constexpr int SC0 = band_tile_sc(NK, KC, 0), SC1 = band_tile_sc(NK, KC, 1);
-    double2* xs = reinterpret_cast<double2*>(wsm);
-    double2* ys = reinterpret_cast<double2*>(wsm + LY::X_BYTES);
-    char* hbase = wsm + LY::X_BYTES + LY::Y_BYTES;
-    const double* Hk = H + (size_t)KC * LY::SLAB_KC;  // + e * 2 * SLAB_KC
-    auto issue_h = [&](int buf, int e) {
-        const char* hg = reinterpret_cast<const char*>(Hk + (size_t)e * 2 * LY::SLAB_KC);
-        for (int o = lane * 16; o < LY::H_BYTES; o += kLanes * 16) cp_async16(hbase + buf * LY::H_BYTES + o, hg + o);
-    };
-    auto issue_y = [&](int2 en, int sc) {
-        const double2* Y = Ag + ((size_t)en.y + sc * T) * kLanes;
-#pragma unroll
-        for (int j = 0; j < T; ++j) cp_async16(ys + j * kLanes + lane, Y + (size_t)j * kLanes);
-    };
-    if (e0 >= e1) return;
-    int2 en = __ldg(ent + e0);
-    {   // prologue: x row, H slab, first y chunk of row e0
-        const double2* X = Ag + (size_t)en.x * kLanes;
-#pragma unroll
-        for (int j = 0; j < N; ++j) cp_async16(xs + j * kLanes + lane, X + (size_t)j * kLanes);
-        issue_h(0, e0);
-        issue_y(en, SC0);
-        cp_async_commit();
-        cp_async_wait_all();
-        __syncwarp();
-    }
-    double2 y[T];
-#pragma unroll
-    for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
-    issue_y(en, SC1);
-    cp_async_commit();
-    for (int e = e0; e < e1; ++e) {
-        const int cur = (e - e0) & 1;
-        const bool more = e + 1 < e1;
-        const int2 nx = more ? __ldg(ent + e + 1) : en;
-        const double2* Xn = Ag + (size_t)nx.x * kLanes;
-        __syncwarp();  // every lane finished reading H[cur^1] (row e-1)
-        if (more) issue_h(cur ^ 1, e + 1);
-        cp_async_commit();
-        const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
-        int p = 0;
-        double2 hb = make_double2(0.0, 0.0);
-        auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
-        // tile 0 (triangle): slots it uses are needed again by tile 1, except
-        // slot 0 of k-chunk 0, which is refilled right away
-        band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, [&](int, int m3) {
-            if (KC == 0 && m3 == 0 && more) cp_async16(xs + lane, Xn);
-        });
-        cp_async_commit();
-        cp_async_wait_all();  // y chunk SC1 of row e (and H of row e+1)
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
-        if (more) issue_y(nx, SC0);  // own-lane slots, read just above
-        cp_async_commit();
-        // tile 1 (square, all diagonals the row uses): refill each x slot after
-        // its last use; the first half holds the slots the next row's tile 0 needs
-        band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, [&](int i, int m3) {
-            if (more && m3 != 0) cp_async16(xs + m3 * kLanes + lane, Xn + (size_t)m3 * kLanes);
-            if (i == (KC == 0 ? T - 1 : T - 2)) cp_async_commit();  // R1: slots of the next tile 0
-        });
-        cp_async_commit();  // R2
-        if (more) {
-            cp_async_wait_1();  // all but R2: y chunk SC0 of row e+1 and the R1 slots
-            __syncwarp();
-#pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
-            issue_y(nx, SC1);
-            cp_async_commit();
-        }
-        en = nx;
-    }
-    cp_async_wait_all();
-}
-
-template <int N>
-__global__ void __launch_bounds__(kLanes* T2Layout<N>::W, T2Layout<N>::MINB)
-k_conv_t2(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-          const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
-    using LY = T2Layout<N>;
-    constexpr int T = LY::T, N3 = N * N * N;
-    extern __shared__ __align__(16) char smem[];
-    const int kc = blockIdx.x & 1, row = conv_row<N>(row_start, blockIdx.x >> 1, lpt);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.y * LY::W + wid;
-    if (g >= ngroups) return;  // whole warp exits; warps never sync with each other
-    char* wsm = smem + wid * LY::WARP_BYTES;
-    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
-    double2 acc[T];
-#pragma unroll
-    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
-    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
-    if (kc == 0) t2_rows<N, 0>(wsm, Ag, H, ent, e0, e1, lane, acc);
-    else t2_rows<N, 1>(wsm, Ag, H, ent, e0, e1, lane, acc);
-    write_row<N, T>(B, g, row, kc, lane, acc);
 }
 
 // ---------------------------------------------------------------------------
