@@ -137,6 +137,12 @@ int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double
                         double Tw, const double* Vw_host3, double* sigma_w, void* stream);
 
 /*
+ * compute_moments per cell: out[c*7 + {0..6}] = rho,
+ * rho V1, rho V2, rho V3, rho e, T, H (H = sum_{f>0} f log f w; R = 1).
+ */
+int boltz_moments_batch(boltz_ctx* ctx, const double* f, double* out, int64_t ncells, int mem, void* stream);
+
+/*
  * Asynchronous mode (no reference counterpart): with
  * enable != 0, device-pointer calls return as soon as their work is queued on
  * the stream (no synchronisation, so a whole Strang step can be captured in a

@@ -91,6 +91,7 @@ def lib():
             "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
             "boltz_transport_step": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
+            "boltz_moments_batch": (i, [vp, vp, vp, i64, i, vp]),
             "boltz_set_async": (i, [vp, i]),
             "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
@@ -274,6 +275,16 @@ class CollisionOperator:
         a, b = C.c_int64(), C.c_int64()
         _check(lib().boltz_memory_bytes(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def moments(self, f):
+        """compute_moments per cell: (ncells, 7) =
+        rho, rho*V (3), rho*e, T, H."""
+        f = self._prep(f)
+        nc = self._ncells(f, self.grid.size())
+        out = self._alloc_like(f, (nc, 7))
+        (pf, po), mem, s = self._args(f, out)
+        _check(lib().boltz_moments_batch(self._h, pf, po, nc, mem, s))
+        return out
 
     # -- asynchronous mode (CUDA-graph capturable device calls)
     def set_async(self, enable: bool = True):

@@ -913,6 +913,18 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
     });
 }
 
+int boltz_moments_batch(boltz_ctx* c, const double* f, double* out, int64_t ncells, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, f, out, ncells, (int)n3, 7, mem, stream, nullptr,
+                           [&](const double* in, double* o, int64_t nc, cudaStream_t s) {
+                               Timed t_(c, KIND_LAYOUT, s);
+                               launch_moments(c->n, in, o, nc, c->pc.dv, s);
+                               CK(cudaGetLastError());
+                           });
+    });
+}
+
 int boltz_set_async(boltz_ctx* c, int enable) {
     if (!c) return BOLTZ_ERR_CONFIG;
     c->async_mode = enable != 0;

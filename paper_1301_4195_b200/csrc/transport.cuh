@@ -133,3 +133,68 @@ inline void launch_fill_boundary(int n, double* f, long long ncl, const double* 
 }
 
 }  // namespace boltz_gpu
+
+namespace boltz_gpu {
+
+// compute_moments for a batch of cells in the user layout:
+// out[c] = {rho, rho V1, rho V2, rho V3, rho e, T, H} with rho e = 1/2 sum |v|^2 f w,
+// T = (2 rho e / rho - |V|^2) / 3, H = sum_{f>0} f log f w.  One block per
+// cell, fixed-order tree reduction (deterministic).
+template <int N>
+__global__ void __launch_bounds__(256) k_moments(const double* __restrict__ f, double* __restrict__ out, double dv) {
+    constexpr int N3 = N * N * N;
+    const long long cell = blockIdx.x;
+    const double* fc = f + (size_t)cell * N3;
+    double m[6] = {0, 0, 0, 0, 0, 0};
+    const double dv3 = dv * dv * dv;
+    for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+        const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
+        const double v1 = dv * (a1 - N / 2), v2 = dv * (a2 - N / 2), v3 = dv * (a3 - N / 2);
+        const double w = axis_coeff(N, a1) * axis_coeff(N, a2) * axis_coeff(N, a3) * dv3;
+        const double x = fc[j], q = x * w;
+        m[0] += q;
+        m[1] += v1 * q;
+        m[2] += v2 * q;
+        m[3] += v3 * q;
+        m[4] += (v1 * v1 + v2 * v2 + v3 * v3) * q;
+        if (x > 0) m[5] += x * log(x) * w;
+    }
+    __shared__ double red[6][256];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) red[a][threadIdx.x] = m[a];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+#pragma unroll
+            for (int a = 0; a < 6; ++a) red[a][threadIdx.x] += red[a][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double rho = red[0][0];
+        double* o = out + cell * 7;
+        o[0] = rho;
+        o[1] = red[1][0];
+        o[2] = red[2][0];
+        o[3] = red[3][0];
+        o[4] = 0.5 * red[4][0];
+        double T = 0.0;
+        if (rho > 0) {
+            const double V2 = (o[1] * o[1] + o[2] * o[2] + o[3] * o[3]) / (rho * rho);
+            T = (2.0 * o[4] / rho - V2) / 3.0;
+        }
+        o[5] = T;
+        o[6] = red[5][0];
+    }
+}
+
+inline void launch_moments(int n, const double* f, double* out, long long ncells, double dv, cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_MO(N) \
+    case N: k_moments<N><<<(unsigned)ncells, 256, 0, s>>>(f, out, dv); break;
+        BOLTZ_FOR_EACH_N(BOLTZ_MO)
+#undef BOLTZ_MO
+        default: break;
+    }
+}
+
+}  // namespace boltz_gpu

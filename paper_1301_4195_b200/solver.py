@@ -134,6 +134,23 @@ class Solver1D:
     def interior(self):
         return self.field[2:self.ncl + 2]
 
+    def moments(self):
+        """(n_local, 7) device tensor: rho, rho V (3), rho e, T, H per interior cell (GPU)."""
+        return self.op.moments(self.interior)
+
+    def ledger(self):
+        """Global (mass, x-momentum, energy) = sum_j dx_j (rho, rho V1, rho e)_j over all
+        ranks -- the conservation ledger of SPEC.md:403 (collision conserves it to
+        round-off; transport changes it only by boundary fluxes)."""
+        import torch
+        m = self.moments()
+        dx = self.dx_ext[2:self.ncl + 2]
+        tot = torch.stack([(m[:, 0] * dx).sum(), (m[:, 1] * dx).sum(), (m[:, 4] * dx).sum()])
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(tot)
+        return tot.cpu().numpy()
+
     def cfl_dt(self, cfl: float = 0.9) -> float:
         """dt <= cfl * min dx / L; global min."""
         return cfl * float(self.dx_glob.min()) / self.op.grid.half_width

@@ -180,3 +180,19 @@ def test_host_pipeline_matches_device_path(gpu):
         op.collision_rk2(g, 0.01)
         op.collision_rk2(fd, 0.01)
         assert np.array_equal(g, fd.cpu().numpy())
+
+
+def test_moments_vs_oracle(gpu, O):
+    """GPU compute_moments vs the oracle, host and device paths."""
+    import torch
+    n, L = 16, 6.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 37, seed=23)
+    f[3] *= -1.0  # a negative cell: H skips f <= 0
+    with _op(n, L) as op:
+        mh = op.moments(f)
+        md = op.moments(torch.from_numpy(f).to(gpu)).cpu().numpy()
+    for c in range(37):
+        ref = O.moments(n, L, f[c])
+        assert np.allclose(mh[c], ref, rtol=1e-13, atol=1e-15 * np.abs(ref).max())
+    assert np.array_equal(mh, md)

@@ -170,3 +170,22 @@ def test_async_mode_defers_numeric_error(gpu):
             op.sync()
         op.sync()  # flag cleared
         op.set_async(False)
+
+
+def test_ledger_collision_conserves_and_wall_flux(gpu):
+    """SPEC.md:403 bookkeeping: the collision step leaves the global (mass,
+    momentum, energy) ledger unchanged to round-off; a transport step between
+    two extrapolating ends of a field at rest changes mass only through the
+    end fluxes (which vanish for a symmetric field at rest)."""
+    n, L, nx = 8, 5.0, 10
+    x, dx = scenarios.uniform_grid(nx, 0.0, 2.0)
+    grid = VelocityGrid.create(n, L)
+    f0 = scenarios.mixture_cells(grid, nx, seed=31)
+    with _op(n, L) as op:
+        s = Solver1D(op, x, dx, f0, left=Boundary("extrap"), right=Boundary("extrap"))
+        a = s.ledger()
+        s.collide(0.01)
+        b = s.ledger()
+        assert np.abs(b - a).max() < 1e-13 * np.abs(a).max()
+        m = s.moments().cpu().numpy()
+        assert np.all(m[:, 0] > 0) and np.all(m[:, 5] > 0)
