@@ -648,3 +648,90 @@ int bo_plan_decomposition(int64_t ncells, int nranks, int64_t *start, int64_t *c
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ */
+/* direct_collision_oracle: quadrature of the strong  */
+/* form Q(f,f)(v) = sum_{v*} w* |u|^lambda b sum_sigma w_sigma          */
+/*   [f(v') f(v*') - f(v) f(v*)],  b = 1/(4 pi),                        */
+/* v', v*' = (v+v*)/2 +- |u| sigma / 2 (elastic collision rule),        */
+/* sigma on S^2: Gauss-Legendre in cos(theta) x uniform azimuth,        */
+/* f at off-lattice v', v*' by trilinear interpolation (0 off the       */
+/* lattice).  Physics cross-check of the spectral operator; N <= 12.    */
+/* ------------------------------------------------------------------ */
+static double bo_trilinear(int n, double dv, const double *f, const double p[3]) {
+    double g[3];
+    int i0[3];
+    double t[3];
+    for (int a = 0; a < 3; ++a) {
+        g[a] = p[a] / dv + n / 2;
+        if (g[a] < 0.0 || g[a] > n - 1) return 0.0;
+        i0[a] = (int)floor(g[a]);
+        if (i0[a] >= n - 1) i0[a] = n - 2;
+        t[a] = g[a] - i0[a];
+    }
+    double s = 0.0;
+    for (int d = 0; d < 8; ++d) {
+        int b1 = d >> 2 & 1, b2 = d >> 1 & 1, b3 = d & 1;
+        double w = (b1 ? t[0] : 1 - t[0]) * (b2 ? t[1] : 1 - t[1]) * (b3 ? t[2] : 1 - t[2]);
+        if (w == 0.0) continue;
+        s += w * f[((int64_t)(i0[0] + b1) * n + (i0[1] + b2)) * n + (i0[2] + b3)];
+    }
+    return s;
+}
+
+/* returns 0, or 2 if n > 12 */
+int bo_direct_collision(int n, double L, double lambda, const double *f, int n_theta, int n_phi, double *q,
+                        int nthreads) {
+    if (n > 12 || n_theta < 1 || n_phi < 1) return 2;
+    const int64_t M = (int64_t)n * n * n;
+    const double dv = 2.0 * L / n;
+    double *gx = malloc(sizeof(double) * n_theta), *gw = malloc(sizeof(double) * n_theta);
+    bo_gauss_legendre(n_theta, gx, gw);
+    const int ns = n_theta * n_phi;
+    double *sig = malloc(sizeof(double) * 3 * ns), *sw = malloc(sizeof(double) * ns);
+    for (int k = 0; k < n_theta; ++k)
+        for (int j = 0; j < n_phi; ++j) {
+            double ct = gx[k], st = sqrt(fmax(0.0, 1.0 - ct * ct)), ph = 2.0 * BO_PI * j / n_phi;
+            int s = k * n_phi + j;
+            sig[3 * s] = st * cos(ph);
+            sig[3 * s + 1] = st * sin(ph);
+            sig[3 * s + 2] = ct;
+            sw[s] = gw[k] * 2.0 * BO_PI / n_phi / (4.0 * BO_PI); /* b = 1/(4 pi) folded in */
+        }
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 4)
+#endif
+    for (int64_t i = 0; i < M; ++i) {
+        int i1 = (int)(i / (n * n)), i2 = (int)((i / n) % n), i3 = (int)(i % n);
+        double v[3] = {dv * (i1 - n / 2), dv * (i2 - n / 2), dv * (i3 - n / 2)};
+        double acc = 0.0;
+        for (int64_t j = 0; j < M; ++j) {
+            int j1 = (int)(j / (n * n)), j2 = (int)((j / n) % n), j3 = (int)(j % n);
+            double vs[3] = {dv * (j1 - n / 2), dv * (j2 - n / 2), dv * (j3 - n / 2)};
+            double u[3] = {v[0] - vs[0], v[1] - vs[1], v[2] - vs[2]};
+            double um = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+            if (um == 0.0) continue;
+            double ws = axc(n, j1) * axc(n, j2) * axc(n, j3) * dv * dv * dv * pow(um, lambda);
+            double c[3] = {0.5 * (v[0] + vs[0]), 0.5 * (v[1] + vs[1]), 0.5 * (v[2] + vs[2])};
+            double gain = 0.0;
+            for (int s = 0; s < ns; ++s) {
+                double vp[3], vq[3];
+                for (int a = 0; a < 3; ++a) {
+                    vp[a] = c[a] + 0.5 * um * sig[3 * s + a];
+                    vq[a] = c[a] - 0.5 * um * sig[3 * s + a];
+                }
+                double fp = bo_trilinear(n, dv, f, vp);
+                if (fp == 0.0) continue;
+                gain += sw[s] * fp * bo_trilinear(n, dv, f, vq);
+            }
+            acc += ws * (gain - f[i] * f[j]); /* sum_sigma sw = 1 */
+        }
+        q[i] = acc;
+    }
+    free(gx);
+    free(gw);
+    free(sig);
+    free(sw);
+    return 0;
+}

@@ -51,6 +51,7 @@ def lib():
             "bo_fill_boundary": (None, [i, d, _dp, i64, _dp, i, i, d, _dp, C.POINTER(d)]),
             "bo_transport_step": (None, [i, d, _dp, _dp, i64, _dp, _dp, d, i, i]),
             "bo_plan_decomposition": (i, [i64, i, _ip, _ip]),
+            "bo_direct_collision": (i, [i, d, d, _dp, i, i, _dp, i]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -176,3 +177,17 @@ def plan_decomposition(ncells, nranks):
     if rc:
         raise ValueError(f"ConfigError({rc}): {nranks} ranks > {ncells} cells")
     return s, c
+
+
+def direct_collision(n, L, lam, f, n_theta=12, n_phi=24, nthreads=0):
+    """Strong-form quadrature oracle, N <= 12."""
+    out = np.empty(n ** 3)
+    rc = lib().bo_direct_collision(n, L, lam, _c(f).ravel(), n_theta, n_phi, out, nthreads)
+    if rc:
+        raise ValueError("direct_collision_oracle: N must be <= 12")
+    return out
+
+
+def q_tilde(n, L, G, f):
+    """Unprojected spectral operator: inverse(evaluate_qhat(forward(f)))."""
+    return inverse(n, L, evaluate_qhat(n, L, G, forward(n, L, f)))[0]
