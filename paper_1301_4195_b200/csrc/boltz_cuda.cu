@@ -562,18 +562,36 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
 template <typename Fn>
 int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
                        cudaStream_t s, double* max_imag, Fn&& fn) {
-    int64_t pieces = 4;  // pipeline depth; BOLTZ_HOST_CHUNKS overrides (tuning)
-    if (const char* e = std::getenv("BOLTZ_HOST_CHUNKS")) pieces = std::max(1, std::atoi(e));
-    int64_t chunk = ncells <= 512 ? ncells : std::max<int64_t>(256, (ncells + pieces - 1) / pieces);
-    chunk = (chunk + kLanes - 1) / kLanes * kLanes;
+    // Chunk schedule: the first H2D and the last D2H cannot overlap compute, so
+    // those two chunks are small (1/16 of the batch) and the middle two 7/16.
+    std::vector<int64_t> bounds{0};
+    auto up32 = [](int64_t x) { return (x + kLanes - 1) / kLanes * kLanes; };
+    if (ncells <= 1024) {
+        bounds.push_back(ncells);
+    } else {
+        int64_t edge = 16, nmid = 2;  // measured best of {8,16,32} x {2,3}; BOLTZ_HOST_EDGE / BOLTZ_HOST_MID override (tuning)
+        if (const char* e = std::getenv("BOLTZ_HOST_EDGE")) edge = std::max(2, std::atoi(e));
+        if (const char* e = std::getenv("BOLTZ_HOST_MID")) nmid = std::max(1, std::atoi(e));
+        const int64_t small = up32(ncells / edge), mid = up32((ncells - 2 * small + nmid - 1) / nmid);
+        for (int64_t b = small; b < ncells - small; b += mid) bounds.push_back(b);
+        bounds.push_back(ncells - small);
+        bounds.push_back(ncells);
+    }
+    int64_t chunk = 0;
+    for (size_t i = 1; i < bounds.size(); ++i) chunk = std::max(chunk, bounds[i] - bounds[i - 1]);
     ensure_workspace(c, chunk);
-    chunk = std::min<int64_t>(chunk, c->cap);
+    if (chunk > c->cap) {  // workspace limit: fall back to uniform chunks of the capacity
+        bounds.assign(1, 0);
+        for (int64_t b = c->cap; b < ncells; b += c->cap) bounds.push_back(b);
+        bounds.push_back(ncells);
+        chunk = c->cap;
+    }
     ensure_staging(c, chunk);
     CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
-    const int64_t nchunks = (ncells + chunk - 1) / chunk;
+    const int64_t nchunks = (int64_t)bounds.size() - 1;
     auto h2d = [&](int64_t i) {
         const int slot = (int)(i & 1);
-        const int64_t c0 = i * chunk, nc = std::min<int64_t>(chunk, ncells - c0);
+        const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
         if (i >= 2) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-2 done reading
         CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice,
                            c->h2d_stream));
@@ -582,7 +600,7 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     h2d(0);
     for (int64_t i = 0; i < nchunks; ++i) {
         const int slot = (int)(i & 1);
-        const int64_t c0 = i * chunk, nc = std::min<int64_t>(chunk, ncells - c0);
+        const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
         CK(cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
         if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
         fn(c->dStageIn[slot], c->dStageOut[slot], nc, s);
