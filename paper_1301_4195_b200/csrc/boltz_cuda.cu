@@ -431,6 +431,35 @@ struct Launch {
         inverse(c, nc, s);
         project(c, base, out, nc, coef, s);
     }
+    // RK2 stage hand-off: f* = base + coef * P_N(Re iFFT(c->dB)) and straight on to
+    // fhat(f*) in c->dA (fused when the cube fits in smem: f* never touches HBM);
+    // otherwise through the user-layout scratch `fs`.
+    static void inverse_project_forward(boltz_ctx* c, const double* base, double* fs, int64_t nc, double coef,
+                                        cudaStream_t s) {
+#if BOLTZ_FUSED
+        if constexpr (Fused<N>::FITS) {
+            using F = Fused<N>;
+            const int64_t ng = (nc + 31) / 32;
+            const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
+            const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
+            const double par = ((N / 2) & 1) ? -1.0 : 1.0;
+            static bool configured = false;
+            if (!configured) {
+                CK(cudaFuncSetAttribute(k_inv_project<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        F::SMEM));
+                configured = true;
+            }
+            Timed t_(c, KIND_PROJECT, s);
+            k_inv_project<N, true><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(
+                c->dB, base, nullptr, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
+                c->dFlag, c->dA, sv * sv * sv * par);
+            CK(cudaGetLastError());
+            return;
+        }
+#endif
+        inverse_project(c, base, fs, nc, coef, s);
+        forward(c, fs, nc, s);
+    }
     // group real Qt in (double*)c->dA -> out = base + coef * P_N(Qt)  (user layout)
     static void project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
@@ -865,9 +894,8 @@ int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double i
                                    // stage 1: f* = f + dt/2 * collide(f)
                                    Lx::forward(c, out, nc, s);
                                    Lx::conv(c, nc, s);
-                                   Lx::inverse_project(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
-                                   // stage 2: f <- f + dt * collide(f*)
-                                   Lx::forward(c, c->dFs, nc, s);
+                                   // stage 2: f <- f + dt * collide(f*), f* handed over as fhat(f*)
+                                   Lx::inverse_project_forward(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
                                    Lx::conv(c, nc, s);
                                    Lx::inverse_project(c, out, out, nc, dt * inv_eps, s);
                                });

@@ -109,11 +109,14 @@ k_fwd_fused(const double* __restrict__ f, double2* __restrict__ A, long long nce
     }
 }
 
-template <int N>
+// FWD = true fuses the next RK2 stage's forward transform: instead of writing
+// out = base + coef*Q, the kernel transforms that value in shared memory and
+// writes its fhat (times fwd_scale) into the group layout A_next.
+template <int N, bool FWD = false>
 __global__ void __launch_bounds__(Fused<N>::THREADS)
 k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
               double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
-              int* __restrict__ flag) {
+              int* __restrict__ flag, double2* __restrict__ A_next = nullptr, double fwd_scale = 0.0) {
     using F = Fused<N>;
     constexpr int N3 = F::N3;
     constexpr int CPB = F::CPB;
@@ -191,20 +194,52 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
     for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
         const int c = t / N3, idx = t % N3;
         const long long cell = cell0 + c;
-        if (cell >= ncells) continue;
+        if (!FWD && cell >= ncells) continue;
         const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
         const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
         const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3;
         const double cl = lam[c][0] + v1 * lam[c][1] + v2 * lam[c][2] + v3 * lam[c][3] +
                           (v1 * v1 + v2 * v2 + v3 * v3) * lam[c][4];
-        const double q = sm[c * F::CELL + F::at(i1, i2, i3)].x - wq * cl;
+        double2* p = sm + c * F::CELL + F::at(i1, i2, i3);
+        const double q = p->x - wq * cl;
         const size_t o = (size_t)cell * N3 + idx;
-        double v = coef * q;
-        if (base) v += base[o];
-        bad |= !isfinite(v);
-        out[o] = v;
+        if constexpr (FWD) {
+            // the RK2 stage value f* = base + coef*Q never leaves the SM: it is
+            // pre-multiplied by s_m c_m for the forward transform in place
+            double v = 0.0;
+            if (cell < ncells) {
+                v = coef * q;
+                if (base) v += base[o];
+                bad |= !isfinite(v);
+            }
+            double w = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3);
+            if ((i1 + i2 + i3) & 1) w = -w;
+            *p = make_double2(v * w, 0.0);
+        } else {
+            double v = coef * q;
+            if (base) v += base[o];
+            bad |= !isfinite(v);
+            out[o] = v;
+        }
     }
     if (bad) atomicOr(flag, 2);
+    if constexpr (FWD) {
+        __syncthreads();
+        smem_axis_pass<N, 2, -1>(sm);
+        __syncthreads();
+        smem_axis_pass<N, 1, -1>(sm);
+        __syncthreads();
+        smem_axis_pass<N, 0, -1>(sm);
+        __syncthreads();
+#pragma unroll 4
+        for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
+            const int idx = t / CPB, c = t % CPB;
+            const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+            const double s = ((i1 + i2 + i3) & 1) ? -fwd_scale : fwd_scale;
+            const double2 z = sm[c * F::CELL + F::at(i1, i2, i3)];
+            A_next[((size_t)g * N3 + idx) * kLanes + lane0 + c] = make_double2(z.x * s, z.y * s);
+        }
+    }
 }
 
 }  // namespace boltz_gpu
