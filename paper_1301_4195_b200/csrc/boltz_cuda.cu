@@ -463,8 +463,16 @@ struct Launch {
     // group real Qt in (double*)c->dA -> out = base + coef * P_N(Qt)  (user layout)
     static void project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
-        { Timed t_(c, KIND_PROJECT, s); k_project<N><<<(unsigned)ng, 256, 0, s>>>(reinterpret_cast<const double*>(c->dA), base, out, nc, coef, c->pc,
-                                                  c->dFlag); }
+        // partial moments go to c->dB: the convolution output is consumed by then
+        // (conserve() never uses it), and 40 B x 8 slices per cell fit many times over
+        double* part = reinterpret_cast<double*>(c->dB);
+        const double* R = reinterpret_cast<const double*>(c->dA);
+        dim3 grid((unsigned)(ng * 4), kProjSlices);
+        {
+            Timed t_(c, KIND_PROJECT, s);
+            k_project_moments<N><<<grid, 256, 0, s>>>(R, part, nc, c->pc);
+            k_project_apply<N><<<grid, 256, 0, s>>>(R, part, base, out, nc, coef, c->pc, c->dFlag);
+        }
         CK(cudaGetLastError());
     }
     static void pack_complex(boltz_ctx* c, const double* in, double2* dst, int64_t nc, int sign, cudaStream_t s) {

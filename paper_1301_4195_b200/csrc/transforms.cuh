@@ -104,84 +104,94 @@ k_fft_pass(const double* __restrict__ fuser, double2* __restrict__ A, double* __
 // K3 epilogue: conservation projection + RK2 axpy.
 //   Q   = Qt - C^T (C C^T)^{-1} C Qt        (C rows: w, v1 w, v2 w, v3 w, |v|^2 w)
 //   out = base + coef * Q    (base == nullptr -> out = coef * Q)
-// Qt comes in the group layout (real), out/base are in the user layout
-// [cell][N^3]; a 32x32 shared-memory tile transposes so both sides coalesce.
-// One block (8 warps) per group; deterministic fixed-order reductions.
+// Qt comes in the group layout (real), out/base are in the user layout [cell][N^3].
+// ---- K3 epilogue for grids whose cube does not fit in shared memory (N = 24, 32):
+// two launches over (cell octet) x (node slice) blocks so that every SM works
+// (one block per 32-cell group left most of the GPU idle: 10% of an N=24 step).
+//   k_project_moments: partial moments of each slice   -> part[cell][slice][5]
+//   k_project_apply:   fixed-order sum of the slices, lambda = (CC^T)^{-1} m,
+//                      out = base + coef * (Qt - C^T lambda) on its slice
+// Deterministic: fixed thread -> node assignment, fixed reduction order.
+constexpr int kProjSlices = 8;
+
+template <int N>
+__device__ __forceinline__ void proj_row(int idx, const ProjConst& pc, double& w, double& v1, double& v2, double& v3) {
+    const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+    v1 = pc.dv * (i1 - N / 2);
+    v2 = pc.dv * (i2 - N / 2);
+    v3 = pc.dv * (i3 - N / 2);
+    w = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * pc.dv * pc.dv * pc.dv;
+}
+
+// grid = (ngroups * 4, kProjSlices); block = 256 = 8 cells x 32 node strides
 template <int N>
 __global__ void __launch_bounds__(256)
-k_project(const double* __restrict__ R, const double* __restrict__ base, double* __restrict__ out,
-          long long ncells, double coef, ProjConst pc, int* __restrict__ flag) {
+k_project_moments(const double* __restrict__ R, double* __restrict__ part, long long ncells, ProjConst pc) {
     constexpr int N3 = N * N * N;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const long long g = blockIdx.x;
-    const double* Rg = R + (size_t)g * N3 * kLanes + lane;
-    __shared__ double part[8][5][kLanes];
-    __shared__ double lam[5][kLanes];
-    __shared__ double tile[32][33];
-
+    constexpr int SL = (N3 + kProjSlices - 1) / kProjSlices;
+    const long long g = blockIdx.x / 4;
+    const int c = threadIdx.x & 7, j = threadIdx.x >> 3;
+    const int lane = (blockIdx.x % 4) * 8 + c;
+    const int idx0 = blockIdx.y * SL, idx1 = min(N3, idx0 + SL);
     double m[5] = {0, 0, 0, 0, 0};
-    for (int idx = w; idx < N3; idx += 8) {
-        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-        const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
-        const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * pc.dv * pc.dv * pc.dv;
-        const double q = Rg[(size_t)idx * kLanes] * wq;
+    for (int idx = idx0 + j; idx < idx1; idx += 32) {
+        double w, v1, v2, v3;
+        proj_row<N>(idx, pc, w, v1, v2, v3);
+        const double q = R[((size_t)g * N3 + idx) * kLanes + lane] * w;
         m[0] += q;
         m[1] += v1 * q;
         m[2] += v2 * q;
         m[3] += v3 * q;
         m[4] += (v1 * v1 + v2 * v2 + v3 * v3) * q;
     }
+    __shared__ double red[5][32][8];
 #pragma unroll
-    for (int a = 0; a < 5; ++a) part[w][a][lane] = m[a];
+    for (int a = 0; a < 5; ++a) red[a][j][c] = m[a];
     __syncthreads();
-    if (w == 0) {
-        double s[5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-            s[a] = 0.0;
-            for (int ww = 0; ww < 8; ++ww) s[a] += part[ww][a][lane];
-        }
-#pragma unroll
+    if (j < 5) {  // thread (c, a=j) sums the 32 strides of moment a in order
+        double s = 0.0;
+        for (int r = 0; r < 32; ++r) s += red[j][r][c];
+        const long long cell = g * kLanes + lane;
+        if (cell < ncells) part[((size_t)cell * kProjSlices + blockIdx.y) * 5 + j] = s;
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256)
+k_project_apply(const double* __restrict__ R, const double* __restrict__ part, const double* __restrict__ base,
+                double* __restrict__ out, long long ncells, double coef, ProjConst pc, int* __restrict__ flag) {
+    constexpr int N3 = N * N * N;
+    constexpr int SL = (N3 + kProjSlices - 1) / kProjSlices;
+    const long long g = blockIdx.x / 4;
+    const int c = threadIdx.x & 7, j = threadIdx.x >> 3;
+    const int lane = (blockIdx.x % 4) * 8 + c;
+    const long long cell = g * kLanes + lane;
+    __shared__ double lam[8][5];
+    if (j == 0) {
+        double s[5] = {0, 0, 0, 0, 0};
+        if (cell < ncells)
+            for (int sl = 0; sl < kProjSlices; ++sl)
+                for (int a = 0; a < 5; ++a) s[a] += part[((size_t)cell * kProjSlices + sl) * 5 + a];
         for (int a = 0; a < 5; ++a) {
             double t = 0.0;
-#pragma unroll
             for (int b = 0; b < 5; ++b) t = fma(pc.ginv[a * 5 + b], s[b], t);
-            lam[a][lane] = t;
+            lam[c][a] = t;
         }
     }
     __syncthreads();
-
+    if (cell >= ncells) return;
+    const int idx0 = blockIdx.y * SL, idx1 = min(N3, idx0 + SL);
     bool bad = false;
-    for (int idx0 = 0; idx0 < N3; idx0 += 32) {
-        // phase A: warp w computes Q for nodes idx0 + w + 8t of its 32 cells
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int il = w + 8 * t, idx = idx0 + il;
-            if (idx < N3) {
-                const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-                const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
-                const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * pc.dv * pc.dv * pc.dv;
-                double c = lam[0][lane] + v1 * lam[1][lane] + v2 * lam[2][lane] + v3 * lam[3][lane] +
-                           (v1 * v1 + v2 * v2 + v3 * v3) * lam[4][lane];
-                tile[il][lane] = Rg[(size_t)idx * kLanes] - wq * c;
-            }
-        }
-        __syncthreads();
-        // phase B: warp w writes cells w + 8t, lane = node offset (coalesced)
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int cl = w + 8 * t;
-            const long long cell = g * kLanes + cl;
-            const int idx = idx0 + lane;
-            if (cell < ncells && idx < N3) {
-                const size_t o = (size_t)cell * N3 + idx;
-                double v = coef * tile[lane][cl];
-                if (base) v += base[o];
-                bad |= !isfinite(v);
-                out[o] = v;
-            }
-        }
-        __syncthreads();
+    for (int idx = idx0 + j; idx < idx1; idx += 32) {
+        double w, v1, v2, v3;
+        proj_row<N>(idx, pc, w, v1, v2, v3);
+        const double cl = lam[c][0] + v1 * lam[c][1] + v2 * lam[c][2] + v3 * lam[c][3] +
+                          (v1 * v1 + v2 * v2 + v3 * v3) * lam[c][4];
+        const size_t o = (size_t)cell * N3 + idx;
+        double v = coef * (R[((size_t)g * N3 + idx) * kLanes + lane] - w * cl);
+        if (base) v += base[o];
+        bad |= !isfinite(v);
+        out[o] = v;
     }
     if (bad) atomicOr(flag, 2);
 }
