@@ -48,3 +48,21 @@ def gpu():
 def rel_max(a, b):
     a, b = np.asarray(a), np.asarray(b)
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def bkw(n, L, K):
+    """Bobylev-Krook-Wu exact solution of the space-homogeneous Boltzmann
+    equation for Maxwell molecules (lambda = 0, isotropic b = 1/(4 pi), rho = 1):
+        f(v, K) = (2 pi K)^{-3/2} exp(-v^2 / 2K) [(5K - 3)/(2K) + (1 - K) v^2 / (2K^2)],
+        K(t) = 1 - exp(-t/6),  so  Q(f) = df/dt = df/dK (1 - K)/6  exactly.
+    Returns (f, Q) on the lattice of VelocityGrid(n, L) (flat index, last axis
+    fastest).  A pointwise analytic answer for the collision operator, valid for
+    3/5 <= K <= 1 (f >= 0)."""
+    dv = 2.0 * L / n
+    x = dv * (np.arange(n) - n // 2)
+    v2 = (x[:, None, None] ** 2 + x[None, :, None] ** 2 + x[None, None, :] ** 2).ravel()
+    E = (2 * np.pi * K) ** -1.5 * np.exp(-v2 / (2 * K))
+    a, b = (5 * K - 3) / (2 * K), (1 - K) / (2 * K * K)
+    f = E * (a + b * v2)
+    dfdK = E * ((-1.5 / K + v2 / (2 * K * K)) * (a + b * v2) + 1.5 / (K * K) + (K - 2) / (2 * K ** 3) * v2)
+    return f, dfdK * (1 - K) / 6

@@ -216,3 +216,20 @@ def test_gpu_collide_maxwell_molecule_stress_relaxation(gpu):
     pi11 = (f * w * (cvel[:, 0] ** 2 - cc / 3)).sum()
     rate = (q * w * (v[:, 0] ** 2 - (v * v).sum(1) / 3)).sum()
     assert abs(rate + 0.5 * rho * pi11) < 2e-4 * abs(0.5 * rho * pi11)
+
+
+@pytest.mark.parametrize("n,L,tol", [(16, 6.0, 1.15e-2), (24, 8.0, 1.7e-3), (32, 8.0, 2.5e-5)])
+def test_gpu_collide_bkw_exact_solution(gpu, n, L, tol):
+    """Pointwise analytic pin of the whole GPU path (tests/conftest.py bkw):
+    the projected GPU collide of the BKW state against its exact Q(f), with
+    the on-device generated lambda=0 table (no oracle, no host table).
+    Measured rel. L2 error on B200: 1.037e-2 (N=16), 1.536e-3 (N=24; the
+    oracle gives the same digits, test_oracle.py), 1.876e-5 (N=32): spectral
+    convergence of the method itself, not of the parity bar."""
+    from conftest import bkw
+    f, qe = bkw(n, L, 0.7)
+    with CollisionOperator.generated(VelocityGrid.create(n, L), KernelSpec(0.0)) as op:
+        q = op.collide(f.reshape(1, -1))[0]
+    err = np.linalg.norm(q - qe) / np.linalg.norm(qe)
+    print(f"BKW N={n} L={L}: rel L2 error {err:.3e}")
+    assert err < tol
