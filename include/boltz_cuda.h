@@ -128,10 +128,27 @@ int boltz_transport_step(boltz_ctx* ctx, const double* field, const double* base
                          int wall_right, void* stream);
 
 /*
+ * Boundary-flux ledger (reference SPEC.md:403 "conservation ledger ... vs
+ * wall-flux integral"; RunRecord): acc5[a] += coef * (F_a(right face) -
+ * F_a(left face)) for the 5 collision invariants (mass, momentum 1-3, energy
+ * |v|^2/2), through the faces of the first and last interior cells of this
+ * rank's field -- the exact face values boltz_transport_step uses.  acc5 is a
+ * DEVICE array of 5 doubles.  For one SSP-RK2 transport sub-step of size h,
+ * calling it with coef = h/2 before each of the two FV stages makes
+ * sum_ranks ledger(t) + acc constant to round-off.
+ */
+int boltz_end_flux(boltz_ctx* ctx, const double* field, int64_t ncl, const double* x_ext, const double* dx_ext,
+                   int wall_left, int wall_right, double coef, double* acc5, void* stream);
+
+/*
  * Ghost fill at a physical end (side 0 = left, 1 = right) of a device field:
  * kind 0 = linear extrapolation, kind 1 = diffuse wall with
- * T_w, V_w.  x_ext is a DEVICE array.  sigma_w (host
- * double, nullable) receives the wall's re-emission factor.
+ * T_w, V_w (sigma_w from the continuum half-range integral,
+ * so the lattice mass flux through the wall is only balanced to O(dv^2)),
+ * kind 2 = extension: the same wall with sigma_w from the discrete flux
+ * balance (lattice influx == outflux; zero net wall mass flux to round-off).
+ * x_ext is a DEVICE array.  sigma_w (host double, nullable) receives the
+ * wall's re-emission factor.
  */
 int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double* x_ext, int side, int kind,
                         double Tw, const double* Vw_host3, double* sigma_w, void* stream);
@@ -141,6 +158,13 @@ int boltz_fill_boundary(boltz_ctx* ctx, double* field, int64_t ncl, const double
  * rho V1, rho V2, rho V3, rho e, T, H (H = sum_{f>0} f log f w; R = 1).
  */
 int boltz_moments_batch(boltz_ctx* ctx, const double* f, double* out, int64_t ncells, int mem, void* stream);
+
+/*
+ * marginal_distribution (reference SPEC.md cli_io module, "[OP]
+ * marginal_distribution"; the Figure-4 output): g[c*N + i] = sum over v2, v3
+ * of f w2 w3 at v1 = dv (i - N/2), w = trapezoid coefficient x dv.
+ */
+int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t ncells, int mem, void* stream);
 
 /*
  * Asynchronous mode (no reference counterpart): with

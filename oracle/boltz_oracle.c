@@ -520,6 +520,18 @@ void bo_moments(int n, double L, const double *f, double out[7]) {
     out[6] = H;
 }
 
+/* marginal_distribution (SPEC.md "[OP] marginal_distribution", cli/scenario
+ * module): g(v1_i) = sum_{i2,i3} f(i,i2,i3) c(i2) c(i3) dv^2. */
+void bo_marginal(int n, double L, const double *f, double *g) {
+    const double dv = 2.0 * L / n;
+    for (int i1 = 0; i1 < n; ++i1) {
+        double s = 0.0;
+        for (int i2 = 0; i2 < n; ++i2)
+            for (int i3 = 0; i3 < n; ++i3) s += f[((int64_t)i1 * n + i2) * n + i3] * axc(n, i2) * axc(n, i3);
+        g[i1] = s * dv * dv;
+    }
+}
+
 void bo_maxwellian(int n, double L, double rho, const double V[3], double T,
                    double *f) {
     double dv = 2.0 * L / n;
@@ -582,8 +594,25 @@ void bo_fill_boundary(int n, double L, double *field, int64_t ncl,
             sw += un * I0[j] * w;
         }
     }
-    sw = -sqrt(2.0 * BO_PI / Tw) * sw;
-    double norm = sw / pow(2.0 * BO_PI * Tw, 1.5);
+    double norm;
+    if (kind == 2) {
+        /* extension (not in the reference): discrete flux balance -- scale the
+         * wall Maxwellian so that its lattice influx equals the lattice outflux
+         * (v1 here is the FV flux velocity; zero net mass flux up to round-off) */
+        double in = 0.0;
+        for (int64_t j = 0; j < M; ++j) {
+            int a1 = (int)(j / (n * n)), a2 = (int)((j / n) % n), a3 = (int)(j % n);
+            double c1 = dv * (a1 - n / 2) - Vw[0], c2 = dv * (a2 - n / 2) - Vw[1], c3 = dv * (a3 - n / 2) - Vw[2];
+            if (c1 * nrm > 0.0)
+                in += dv * (a1 - n / 2) * nrm * exp(-(c1 * c1 + c2 * c2 + c3 * c3) / (2.0 * Tw)) *
+                      (axc(n, a1) * axc(n, a2) * axc(n, a3) * dv * dv * dv);
+        }
+        norm = in > 0.0 ? -sw / in : 0.0;
+        sw = norm * pow(2.0 * BO_PI * Tw, 1.5);
+    } else {
+        sw = -sqrt(2.0 * BO_PI / Tw) * sw;
+        norm = sw / pow(2.0 * BO_PI * Tw, 1.5);
+    }
     for (int64_t j = 0; j < M; ++j) {
         int a1 = (int)(j / (n * n)), a2 = (int)((j / n) % n), a3 = (int)(j % n);
         double c1 = dv * (a1 - n / 2) - Vw[0], c2 = dv * (a2 - n / 2) - Vw[1],

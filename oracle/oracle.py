@@ -47,6 +47,7 @@ def lib():
             "bo_collision_rk2": (i, [i, d, _dp, _dp, i64, d, d, i]),
             "bo_moments": (None, [i, d, _dp, _dp]),
             "bo_maxwellian": (None, [i, d, d, _dp, d, _dp]),
+            "bo_marginal": (None, [i, d, _dp, _dp]),
             "bo_minmod3": (d, [d, d, d]),
             "bo_fill_boundary": (None, [i, d, _dp, i64, _dp, i, i, d, _dp, C.POINTER(d)]),
             "bo_transport_step": (None, [i, d, _dp, _dp, i64, _dp, _dp, d, i, i]),
@@ -141,6 +142,13 @@ def collision_rk2(n, L, G, f, dt, eps=1.0, nthreads=0):
 def moments(n, L, f):
     out = np.empty(7)
     lib().bo_moments(n, L, _c(f).ravel(), out)
+    return out
+
+
+def marginal(n, L, f):
+    """marginal_distribution: g(v1) over the N v1 nodes."""
+    out = np.empty(n)
+    lib().bo_marginal(n, L, _c(f).ravel(), out)
     return out
 
 

@@ -92,6 +92,8 @@ def lib():
             "boltz_transport_step": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
             "boltz_moments_batch": (i, [vp, vp, vp, i64, i, vp]),
+            "boltz_marginal_batch": (i, [vp, vp, vp, i64, i, vp]),
+            "boltz_end_flux": (i, [vp, vp, i64, vp, vp, i, i, d, vp, vp]),
             "boltz_set_async": (i, [vp, i]),
             "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
@@ -286,6 +288,15 @@ class CollisionOperator:
         _check(lib().boltz_moments_batch(self._h, pf, po, nc, mem, s))
         return out
 
+    def marginal(self, f):
+        """marginal_distribution per cell: (ncells, N) = g(v1) = sum_{v2,v3} f w2 w3."""
+        f = self._prep(f)
+        nc = self._ncells(f, self.grid.size())
+        out = self._alloc_like(f, (nc, self.grid.n))
+        (pf, po), mem, s = self._args(f, out)
+        _check(lib().boltz_marginal_batch(self._h, pf, po, nc, mem, s))
+        return out
+
     # -- asynchronous mode (CUDA-graph capturable device calls)
     def set_async(self, enable: bool = True):
         """Device-pointer calls stop synchronising; errors surface at sync()."""
@@ -433,6 +444,17 @@ class CollisionOperator:
         _check(lib().boltz_transport_step(self._h, ptrs[0], pb, alpha, ptrs[1], ncl, ptrs[2], ptrs[3], dt,
                                           int(wall_left), int(wall_right), s))
         return out
+
+    def end_flux(self, field, x_ext, dx_ext, acc, coef, wall_left=False, wall_right=False):
+        """Boundary-flux ledger: acc (5-double CUDA tensor) += coef * (F(right end
+        face) - F(left end face)) of (mass, momentum 1-3, energy)."""
+        ncl = field.shape[0] - 4
+        ptrs, mem, s = self._args(field, x_ext, dx_ext, acc)
+        if mem != MEM_DEVICE:
+            raise ConfigError("end_flux takes CUDA tensors")
+        _check(lib().boltz_end_flux(self._h, ptrs[0], ncl, ptrs[1], ptrs[2], int(wall_left), int(wall_right), coef,
+                                    ptrs[3], s))
+        return acc
 
     def fill_boundary(self, field, x_ext, side, kind, Tw=1.0, Vw=(0.0, 0.0, 0.0)):
         """Ghost fill at a physical end: kind 0 extrapolation, 1 diffuse wall. Returns sigma_w."""

@@ -933,14 +933,33 @@ int boltz_transport_step(boltz_ctx* c, const double* field, const double* base, 
     });
 }
 
+int boltz_end_flux(boltz_ctx* c, const double* field, int64_t ncl, const double* x_ext, const double* dx_ext,
+                   int wall_left, int wall_right, double coef, double* acc5, void* stream) {
+    return api(c, [&] {
+        if (ncl < 1 || !field || !x_ext || !dx_ext || !acc5) {
+            set_error("end_flux: invalid arguments");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_end_flux(c->n, field, ncl, x_ext, dx_ext, wall_left, wall_right, c->pc.dv, coef, acc5, s);
+        }
+        CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;
+        CK(cudaStreamSynchronize(s));
+        return BOLTZ_OK;
+    });
+}
+
 int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* x_ext, int side, int kind, double Tw,
                         const double* Vw_host3, double* sigma_w, void* stream) {
     return api(c, [&] {
-        if (ncl < 2 || !field || !x_ext || (side != 0 && side != 1) || (kind != 0 && kind != 1)) {
+        if (ncl < 2 || !field || !x_ext || (side != 0 && side != 1) || kind < 0 || kind > 2) {
             set_error("fill_boundary: invalid arguments (need >= 2 interior cells)");
             return BOLTZ_ERR_CONFIG;
         }
-        if (kind == 1 && !(Tw > 0.0)) {
+        if (kind != 0 && !(Tw > 0.0)) {
             set_error("fill_boundary: wall temperature must be positive");
             return BOLTZ_ERR_CONFIG;
         }
@@ -974,6 +993,18 @@ int boltz_moments_batch(boltz_ctx* c, const double* f, double* out, int64_t ncel
                            [&](const double* in, double* o, int64_t nc, cudaStream_t s) {
                                Timed t_(c, KIND_LAYOUT, s);
                                launch_moments(c->n, in, o, nc, c->pc.dv, s);
+                               CK(cudaGetLastError());
+                           });
+    });
+}
+
+int boltz_marginal_batch(boltz_ctx* c, const double* f, double* g, int64_t ncells, int mem, void* stream) {
+    return api(c, [&] {
+        const int64_t n3 = n3_of(c);
+        return run_chunked(c, f, g, ncells, (int)n3, c->n, mem, stream, nullptr,
+                           [&](const double* in, double* o, int64_t nc, cudaStream_t s) {
+                               Timed t_(c, KIND_LAYOUT, s);
+                               launch_marginal(c->n, in, o, nc, c->pc.dv, s);
                                CK(cudaGetLastError());
                            });
     });

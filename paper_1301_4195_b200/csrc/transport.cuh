@@ -15,6 +15,40 @@ __device__ __forceinline__ double minmod3(double a, double b, double c) {
     return 0.0;
 }
 
+// Upwind fluxes through the left and right faces of interior cell ce at
+// velocity node j: minmod slopes from the 5-cell stencil,
+// each cell's own half-width, zero slope in the wall ghost / wall cell.
+// Shared by the FV step and the boundary-flux ledger (bitwise the same faces).
+template <int N>
+__device__ __forceinline__ void face_fluxes(const double* __restrict__ f, long long ce, int j, long long ncl,
+                                            const double* __restrict__ x, const double* __restrict__ dx, int wl,
+                                            int wr, double dv, double& fc, double& Fl, double& Fr) {
+    constexpr int N3 = N * N * N;
+    const double v1 = dv * (j / (N * N) - N / 2);
+    double fv[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) fv[d] = f[(ce - 2 + d) * N3 + j];
+    double sg[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const long long c = ce - 1 + d;
+        const double fm = fv[d], f0 = fv[d + 1], fp = fv[d + 2];
+        double s = minmod3((fp - f0) / (x[c + 1] - x[c]), (f0 - fm) / (x[c] - x[c - 1]),
+                           (fp - fm) / (x[c + 1] - x[c - 1]));
+        if (wl && (c == 1 || c == 2)) s = 0.0;
+        if (wr && (c == ncl + 2 || c == ncl + 1)) s = 0.0;
+        sg[d] = s;
+    }
+    if (v1 >= 0.0) {
+        Fl = v1 * (fv[1] + 0.5 * dx[ce - 1] * sg[0]);
+        Fr = v1 * (fv[2] + 0.5 * dx[ce] * sg[1]);
+    } else {
+        Fl = v1 * (fv[2] - 0.5 * dx[ce] * sg[1]);
+        Fr = v1 * (fv[3] - 0.5 * dx[ce + 1] * sg[2]);
+    }
+    fc = fv[2];
+}
+
 // grid = (ceil(N^3/256), ncl + 4); ghosts are copied through.
 // out = alpha*base + (1-alpha)*(f - dt/dx (F_{j+1/2} - F_{j-1/2}))   (base may be null)
 // -- the second stage of the SSP-RK2 transport sub-step fused in.
@@ -31,31 +65,60 @@ k_transport(const double* __restrict__ f, const double* __restrict__ base, doubl
         out[ce * N3 + j] = f[ce * N3 + j];
         return;
     }
-    const double v1 = dv * (j / (N * N) - N / 2);
-    double fv[5];
-#pragma unroll
-    for (int d = 0; d < 5; ++d) fv[d] = f[(ce - 2 + d) * N3 + j];
-    double sg[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const long long c = ce - 1 + d;
-        const double fm = fv[d], f0 = fv[d + 1], fp = fv[d + 2];
-        double s = minmod3((fp - f0) / (x[c + 1] - x[c]), (f0 - fm) / (x[c] - x[c - 1]),
-                           (fp - fm) / (x[c + 1] - x[c - 1]));
-        if (wl && (c == 1 || c == 2)) s = 0.0;
-        if (wr && (c == ncl + 2 || c == ncl + 1)) s = 0.0;
-        sg[d] = s;
-    }
-    double Fl, Fr;
-    if (v1 >= 0.0) {
-        Fl = v1 * (fv[1] + 0.5 * dx[ce - 1] * sg[0]);
-        Fr = v1 * (fv[2] + 0.5 * dx[ce] * sg[1]);
-    } else {
-        Fl = v1 * (fv[2] - 0.5 * dx[ce] * sg[1]);
-        Fr = v1 * (fv[3] - 0.5 * dx[ce + 1] * sg[2]);
-    }
-    const double upd = fv[2] - dt / dx[ce] * (Fr - Fl);
+    double fc, Fl, Fr;
+    face_fluxes<N>(f, ce, j, ncl, x, dx, wl, wr, dv, fc, Fl, Fr);
+    const double upd = fc - dt / dx[ce] * (Fr - Fl);
     out[ce * N3 + j] = base ? alpha * base[ce * N3 + j] + (1.0 - alpha) * upd : upd;
+}
+
+// Boundary-flux ledger: acc[a] += coef * (F_a(right end face) - F_a(left end face))
+// for the 5 collision invariants a (w, v1 w, v2 w, v3 w, |v|^2/2 w) -- the
+// faces of the rank's first and last interior cells, the same values the FV
+// step uses.  Summed over ranks, interior faces cancel exactly, so
+//   ledger(t) - ledger(0) + acc == 0   up to round-off.
+// One block of 256 threads, fixed-order tree reduction.
+template <int N>
+__global__ void __launch_bounds__(256)
+k_end_flux(const double* __restrict__ f, long long ncl, const double* __restrict__ x, const double* __restrict__ dx,
+           int wl, int wr, double dv, double coef, double* __restrict__ acc) {
+    constexpr int N3 = N * N * N;
+    double m[5] = {0, 0, 0, 0, 0};
+    for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+        const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
+        const double v1 = dv * (a1 - N / 2), v2 = dv * (a2 - N / 2), v3 = dv * (a3 - N / 2);
+        const double w = axis_coeff(N, a1) * axis_coeff(N, a2) * axis_coeff(N, a3) * dv * dv * dv;
+        double fc, Fl, Fr, Gl, Gr;
+        face_fluxes<N>(f, 2, j, ncl, x, dx, wl, wr, dv, fc, Fl, Gr);
+        face_fluxes<N>(f, ncl + 1, j, ncl, x, dx, wl, wr, dv, fc, Gl, Fr);
+        const double q = (Fr - Fl) * w;
+        m[0] += q;
+        m[1] += v1 * q;
+        m[2] += v2 * q;
+        m[3] += v3 * q;
+        m[4] += 0.5 * (v1 * v1 + v2 * v2 + v3 * v3) * q;
+    }
+    __shared__ double red[5][256];
+#pragma unroll
+    for (int a = 0; a < 5; ++a) red[a][threadIdx.x] = m[a];
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s)
+#pragma unroll
+            for (int a = 0; a < 5; ++a) red[a][threadIdx.x] += red[a][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) acc[threadIdx.x] += coef * red[threadIdx.x][0];
+}
+
+inline void launch_end_flux(int n, const double* f, long long ncl, const double* x, const double* dx, int wl, int wr,
+                            double dv, double coef, double* acc, cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_EF(N) \
+    case N: k_end_flux<N><<<1, 256, 0, s>>>(f, ncl, x, dx, wl, wr, dv, coef, acc); break;
+        BOLTZ_FOR_EACH_N(BOLTZ_EF)
+#undef BOLTZ_EF
+        default: break;
+    }
 }
 
 // one block of 256 threads; sigma_w written to sig[0]
@@ -94,8 +157,30 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
         if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    const double sw = -sqrt(2.0 * kPi / Tw) * red[0];
-    const double norm = sw / pow(2.0 * kPi * Tw, 1.5);
+    const double out = red[0];
+    double sw = -sqrt(2.0 * kPi / Tw) * out;
+    double norm = sw / pow(2.0 * kPi * Tw, 1.5);
+    if (kind == 2) {
+        // extension (not in the reference): discrete flux balance -- the wall
+        // Maxwellian's lattice influx equals the lattice outflux (FV flux velocity v1)
+        __syncthreads();
+        double in = 0.0;
+        for (int j = threadIdx.x; j < N3; j += blockDim.x) {
+            const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
+            const double c1 = dv * (a1 - N / 2) - vw0, c2 = dv * (a2 - N / 2) - vw1, c3 = dv * (a3 - N / 2) - vw2;
+            if (c1 * nrm > 0.0)
+                in += dv * (a1 - N / 2) * nrm * exp(-(c1 * c1 + c2 * c2 + c3 * c3) / (2.0 * Tw)) *
+                      (axis_coeff(N, a1) * axis_coeff(N, a2) * axis_coeff(N, a3) * dv * dv * dv);
+        }
+        red[threadIdx.x] = in;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+            __syncthreads();
+        }
+        norm = red[0] > 0.0 ? -out / red[0] : 0.0;
+        sw = norm * pow(2.0 * kPi * Tw, 1.5);
+    }
     for (int j = threadIdx.x; j < N3; j += blockDim.x) {
         const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
         const double c1 = dv * (a1 - N / 2) - vw0, c2 = dv * (a2 - N / 2) - vw1, c3 = dv * (a3 - N / 2) - vw2;
@@ -184,6 +269,34 @@ __global__ void __launch_bounds__(256) k_moments(const double* __restrict__ f, d
         }
         o[5] = T;
         o[6] = red[5][0];
+    }
+}
+
+// marginal_distribution (SPEC.md cli_io/scenario module): g(v1_i) =
+// sum_{i2,i3} f c(i2) c(i3) dv^2, N values per cell.  One block per cell, one
+// warp per v1 plane; fixed lane-stride + xor-tree order (deterministic).
+template <int N>
+__global__ void __launch_bounds__(256) k_marginal(const double* __restrict__ f, double* __restrict__ g, double dv) {
+    constexpr int N2 = N * N;
+    const long long cell = blockIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i1 = w; i1 < N; i1 += 8) {
+        const double* p = f + ((size_t)cell * N + i1) * N2;
+        double s = 0.0;
+        for (int j = lane; j < N2; j += 32) s += p[j] * axis_coeff(N, j / N) * axis_coeff(N, j % N);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) g[(size_t)cell * N + i1] = s * dv * dv;
+    }
+}
+
+inline void launch_marginal(int n, const double* f, double* g, long long ncells, double dv, cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_MA(N) \
+    case N: k_marginal<N><<<(unsigned)ncells, 256, 0, s>>>(f, g, dv); break;
+        BOLTZ_FOR_EACH_N(BOLTZ_MA)
+#undef BOLTZ_MA
+        default: break;
     }
 }
 

@@ -6,6 +6,8 @@ Seeds are fixed and recorded in DESIGN.md.  Maxwellians follow SPEC.md:494-502.
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 from .boltz import VelocityGrid
@@ -88,6 +90,29 @@ def geometric_grid(ncells: int, length: float, ratio: float):
     dx *= length / dx.sum()
     edges = np.concatenate([[0.0], np.cumsum(dx)])
     return 0.5 * (edges[:-1] + edges[1:]), dx
+
+
+def zoned_grid(zones):
+    """Piecewise-uniform cells: zones = [(length, dx), ...] from x = 0 outwards.
+    Returns centres, widths."""
+    dx = np.concatenate([np.full(int(round(length / h)), h) for length, h in zones])
+    edges = np.concatenate([[0.0], np.cumsum(dx)])
+    return 0.5 * (edges[:-1] + edges[1:]), dx
+
+
+def sudden_heating(ratio: float = 2.0, T_before: float = 1.0, near: float = 2.0, far: float = 10.0,
+                   mfp: float = 1.0):
+    """The reference's sudden-heating / cooling scenario (SPEC.md scenario
+    module; PAPER.md Figures 1-4): wall at x = 0 jumps to T_w = ratio *
+    T_before at t = 0, uniform equilibrium M(1, 0, T_before) initially,
+    8 cells per mean free path near the wall (x < near), 2 per mfp beyond,
+    mfp = 1 (SPEC DESIGN DECISIONS), velocity half-width from the SPEC
+    heuristic L = 2 sqrt(2 T_max) * 1.25.  Returns (x, dx, L, T_wall)."""
+    if not ratio > 0:
+        raise ValueError("sudden_heating: ratio must be > 0")
+    x, dx = zoned_grid([(near, mfp / 8), (far - near, mfp / 2)])
+    T_max = max(ratio * T_before, T_before)
+    return x, dx, 2.0 * math.sqrt(2.0 * T_max) * 1.25, ratio * T_before
 
 
 def uniform_grid(ncells: int, a: float, b: float):

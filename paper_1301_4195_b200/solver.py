@@ -47,15 +47,23 @@ def plan_decomposition(ncells: int, nranks: int) -> List[Tuple[int, int]]:
 @dataclass
 class Boundary:
     """Physical end condition: kind 'extrap' (linear extrapolation,
-    SPEC.md:318) or 'wall' (diffuse Maxwell wall)."""
+    SPEC.md:318), 'wall' (diffuse Maxwell wall, continuum
+    sigma_w as in the reference) or 'wall_balanced' (extension: the same wall
+    with sigma_w from the discrete flux balance -- zero net wall mass flux)."""
     kind: str = "extrap"
     Tw: float = 1.0
     Vw: Tuple[float, float, float] = (0.0, 0.0, 0.0)
 
+    _CODES = {"extrap": 0, "wall": 1, "wall_balanced": 2}
+
     def code(self) -> int:
-        if self.kind not in ("extrap", "wall"):
+        if self.kind not in self._CODES:
             raise ConfigError(f"unknown boundary kind {self.kind!r}")
-        return 1 if self.kind == "wall" else 0
+        return self._CODES[self.kind]
+
+    @property
+    def is_wall(self) -> bool:
+        return self.code() != 0
 
 
 class TorchHalo:
@@ -138,6 +146,12 @@ class Solver1D:
         """(n_local, 7) device tensor: rho, rho V (3), rho e, T, H per interior cell (GPU)."""
         return self.op.moments(self.interior)
 
+    def marginals(self, cells: Optional[Sequence[int]] = None):
+        """(len(cells), N) device tensor of marginal_distribution g(v1) for the
+        given LOCAL interior cell indices (all interior cells by default; GPU)."""
+        rows = self.interior if cells is None else self.interior[list(cells)]
+        return self.op.marginal(rows)
+
     def ledger(self):
         """Global (mass, x-momentum, energy) = sum_j dx_j (rho, rho V1, rho e)_j over all
         ranks -- the conservation ledger of SPEC.md:403 (collision conserves it to
@@ -166,7 +180,7 @@ class Solver1D:
                                                     self.right.Vw)
 
     def _walls(self):
-        return (self.is_left_end and self.left.kind == "wall", self.is_right_end and self.right.kind == "wall")
+        return (self.is_left_end and self.left.is_wall, self.is_right_end and self.right.is_wall)
 
     def transport_stage(self, stage: int, dt: float, exchange: bool = True) -> None:
         """SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
@@ -175,14 +189,38 @@ class Solver1D:
         wl, wr = self._walls()
         if stage == 0:
             self.fill_ghosts(exchange)
+            self._track_flux(dt, wl, wr)
             self.op.transport_step(self.field, self._tmp, self.x_ext, self.dx_ext, dt, wl, wr)
         else:
             self.field, self._tmp = self._tmp, self.field  # field = t1, _tmp = f^n
             self.fill_ghosts(exchange)
+            self._track_flux(dt, wl, wr)
             out = self._tmp2
             self.op.transport_step(self.field, out, self.x_ext, self.dx_ext, dt, wl, wr, base=self._tmp, alpha=0.5)
             self._tmp2 = self.field
             self.field = out
+
+    def track_boundary_flux(self, enable: bool = True) -> None:
+        """Accumulate the end-face fluxes of every FV stage (boltz_end_flux) so
+        that ledger() + boundary_flux() is conserved to round-off: the
+        "ledger vs wall-flux integral" of the reference RunRecord."""
+        import torch
+        self._flux = torch.zeros(5, dtype=torch.float64, device=self.device) if enable else None
+
+    def boundary_flux(self):
+        """Integrated outflow (mass, momentum 1, energy) through the physical ends
+        since track_boundary_flux(), summed over ranks (collective)."""
+        import torch
+        f = self._flux[[0, 1, 4]].clone()
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(f)
+        return f.cpu().numpy()
+
+    def _track_flux(self, dt: float, wl: bool, wr: bool) -> None:
+        # SSP-RK2: f^{n+1} = f^n - dt/2 (D(f^n) + D(t1)), so each stage's face fluxes weigh dt/2
+        if getattr(self, "_flux", None) is not None:
+            self.op.end_flux(self.field, self.x_ext, self.dx_ext, self._flux, 0.5 * dt, wl, wr)
 
     def transport(self, dt: float, exchange: bool = True) -> None:
         """Transport sub-step T(dt): SSP-RK2 of the FV step."""

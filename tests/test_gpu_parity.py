@@ -233,3 +233,15 @@ def test_gpu_collide_bkw_exact_solution(gpu, n, L, tol):
     err = np.linalg.norm(q - qe) / np.linalg.norm(qe)
     print(f"BKW N={n} L={L}: rel L2 error {err:.3e}")
     assert err < tol
+
+
+def test_marginal_vs_oracle(gpu, O):
+    """marginal_distribution on the GPU vs the oracle (fixed-order sums: 1e-14)."""
+    for n, L in [(8, 5.0), (16, 6.0), (24, 8.0)]:
+        grid = VelocityGrid.create(n, L)
+        f = scenarios.mixture_cells(grid, 5, seed=7)
+        with _op(n, L) as op:
+            g = op.marginal(f)
+        for c in range(5):
+            ref = O.marginal(n, L, f[c])
+            assert rel_max(g[c], ref) < 1e-14

@@ -36,7 +36,7 @@ def test_transport_step_vs_oracle(gpu, O, wl, wr):
         assert rel_max(out2.cpu().numpy(), exp) < 1e-13
 
 
-@pytest.mark.parametrize("side,kind", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("side,kind", [(0, 0), (1, 0), (0, 1), (1, 1), (0, 2), (1, 2)])
 def test_fill_boundary_vs_oracle(gpu, O, side, kind):
     n, L, nx = 8, 5.0, 6
     x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)

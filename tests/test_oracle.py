@@ -540,3 +540,43 @@ def test_bkw_closed_form_derivative():
         f0, _ = bkw(8, 5.0, K - 1e-6)
         _, q = bkw(8, 5.0, K)
         assert np.abs((f1 - f0) / 2e-6 * (1 - K) / 6 - q).max() < 1e-8 * np.abs(q).max()
+
+
+def test_marginal_spec_examples(O):
+    """SPEC marginal_distribution examples: Maxwellian(1,0,1) -> (2 pi)^{-1/2}
+    exp(-v1^2/2) within 1e-6; sum g dv c = rho; f = 0 -> 0."""
+    n, L = 24, 6.0
+    f = O.maxwellian(n, L, 1.0, np.zeros(3), 1.0)
+    g = O.marginal(n, L, f)
+    v = 2 * L / n * (np.arange(n) - n // 2)
+    assert np.abs(g - np.exp(-v * v / 2) / np.sqrt(2 * np.pi)).max() < 1e-6
+    c = np.where((np.arange(n) == 0) | (np.arange(n) == n - 1), 0.5, 1.0)
+    assert abs((g * c).sum() * 2 * L / n - O.moments(n, L, f)[0]) < 1e-13
+    assert np.all(O.marginal(n, L, np.zeros(n ** 3)) == 0)
+
+
+@pytest.mark.parametrize("side", [0, 1])
+def test_balanced_wall_has_zero_net_mass_flux(O, side):
+    """Wall kind 2 (extension): the re-emitted lattice influx equals the lattice
+    outflux to round-off; kind 1 (the reference's continuum sigma_w) does not
+    (2-3% at dv = 0.625, O(dv^2))."""
+    n, L, nx = 16, 5.0, 6
+    x = np.arange(nx + 4) - 1.5
+    rng = np.random.default_rng(5)
+    base = np.tile(O.maxwellian(n, L, 1.0, np.array([0.3, 0.1, 0.0]), 1.0), (nx + 4, 1))
+    base *= 1 + 0.1 * rng.random(base.shape)
+    v1 = np.repeat(2 * L / n * (np.arange(n) - n // 2), n * n)
+    k = np.arange(n)
+    c = np.where((k == 0) | (k == n - 1), 0.5, 1.0)
+    w = (c[:, None, None] * c[None, :, None] * c[None, None, :]).ravel() * (2 * L / n) ** 3
+    nrm = 1.0 if side == 0 else -1.0
+    gi, ii = (1, 2) if side == 0 else (nx + 2, nx + 1)
+    imb = {}
+    for kind in (1, 2):
+        f = base.copy()
+        O.fill_boundary(n, L, f, x, side, kind, Tw=1.7)
+        un = v1 * nrm
+        out = -(un * f[ii] * w)[un <= 0].sum()
+        inn = (un * f[gi] * w)[un > 0].sum()
+        imb[kind] = abs(inn - out) / out
+    assert imb[2] < 1e-14 and imb[1] > 1e-3
