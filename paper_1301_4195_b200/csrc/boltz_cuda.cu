@@ -603,7 +603,25 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     // those two chunks are small (1/16 of the batch) and the middle two 7/16.
     std::vector<int64_t> bounds{0};
     auto up32 = [](int64_t x) { return (x + kLanes - 1) / kLanes * kLanes; };
-    if (ncells <= 1024) {
+    const char* sched = std::getenv("BOLTZ_HOST_CHUNKS");  // tuning: "a,b,c" relative chunk weights
+    if (sched && ncells > 1024) {
+        std::vector<double> w;
+        for (const char* p = sched; *p;) {
+            char* end = nullptr;
+            const double v = std::strtod(p, &end);
+            if (end == p) break;
+            if (v > 0) w.push_back(v);
+            p = (*end == ',') ? end + 1 : end;
+        }
+        double tot = 0, acc = 0;
+        for (double v : w) tot += v;
+        for (size_t i = 0; i + 1 < w.size(); ++i) {
+            acc += w[i];
+            const int64_t b = std::min<int64_t>(ncells, up32((int64_t)(ncells * acc / tot)));
+            if (b > bounds.back() && b < ncells) bounds.push_back(b);
+        }
+        bounds.push_back(ncells);
+    } else if (ncells <= 1024) {
         bounds.push_back(ncells);
     } else {
         int64_t edge = 16, nmid = 2;  // measured best of {8,16,32} x {2,3}; BOLTZ_HOST_EDGE / BOLTZ_HOST_MID override (tuning)

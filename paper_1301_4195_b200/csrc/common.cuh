@@ -40,4 +40,13 @@ __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
 __host__ __device__ __forceinline__ double axis_coeff(int n, int k) { return (k == 0 || k == n - 1) ? 0.5 : 1.0; }
 
+// cp.async (LDGSTS) 16-byte global -> shared copies and their group fences
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 }  // namespace boltz_gpu

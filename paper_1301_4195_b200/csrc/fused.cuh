@@ -41,7 +41,11 @@ struct Fused {
 #define BOLTZ_FUSED_THREADS 512
 #endif
     static constexpr int THREADS = BOLTZ_FUSED_THREADS;
-    static constexpr int SMEM = CPB * CELL_BYTES + (THREADS / 32) * CPB * 6 * 8;  // cubes + reduction scratch
+    // real staging (CPB x N^3 doubles): the forward's f, the inverse's RK2 base,
+    // both fetched by cp.async so every load of the tile is in flight at once
+    static constexpr int STAGE_BYTES = CPB * N3 * 8;
+    static constexpr int RED_BYTES = (THREADS / 32) * CPB * 6 * 8;
+    static constexpr int SMEM = CPB * CELL_BYTES + RED_BYTES + STAGE_BYTES;  // cubes + reduction scratch + staging
     __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
 };
 
@@ -65,6 +69,36 @@ __device__ __forceinline__ void smem_axis_pass(double2* sm) {
     }
 }
 
+// CPB consecutive user-layout cells [cell0, cell0 + CPB) of src -> stage
+// (CPB x N^3 doubles) with 16-byte cp.async (one commit group); cells past
+// ncells are zero.  src must be 16-byte aligned (the callers check).
+template <int N>
+__device__ __forceinline__ void stage_cells(double* stage, const double* __restrict__ src, long long cell0,
+                                            long long ncells) {
+    using F = Fused<N>;
+    constexpr int N3 = F::N3, CH = N3 / 2;  // 16-byte chunks per cell
+    for (int t = threadIdx.x; t < F::CPB * CH; t += F::THREADS) {
+        const int c = t / CH, j = t % CH;
+        double* d = stage + (size_t)c * N3 + 2 * j;
+        if (cell0 + c < ncells) cp_async16(d, src + (size_t)(cell0 + c) * N3 + 2 * j);
+        else d[0] = d[1] = 0.0;
+    }
+    cp_async_commit();
+}
+
+// group-layout complex cube of CPB cells -> padded smem cubes (one commit group)
+template <int N>
+__device__ __forceinline__ void stage_group(double2* sm, const double2* __restrict__ B, long long g, int lane0) {
+    using F = Fused<N>;
+    constexpr int N3 = F::N3;
+    for (int t = threadIdx.x; t < F::CPB * N3; t += F::THREADS) {
+        const int idx = t / F::CPB, c = t % F::CPB;
+        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+        cp_async16(sm + c * F::CELL + F::at(i1, i2, i3), B + ((size_t)g * N3 + idx) * kLanes + lane0 + c);
+    }
+    cp_async_commit();
+}
+
 // grid = ngroups * 32 / CPB blocks; block b covers cells [b*CPB, b*CPB+CPB)
 template <int N>
 __global__ void __launch_bounds__(Fused<N>::THREADS)
@@ -73,15 +107,22 @@ k_fwd_fused(const double* __restrict__ f, double2* __restrict__ A, long long nce
     using F = Fused<N>;
     constexpr int N3 = F::N3;
     extern __shared__ __align__(16) double2 sm[];
+    double* stage = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + F::CPB * F::CELL_BYTES + F::RED_BYTES);
     const long long cell0 = (long long)blockIdx.x * F::CPB;
+    const bool staged = (reinterpret_cast<uintptr_t>(f) & 15) == 0;
+    if (staged) {
+        stage_cells<N>(stage, f, cell0, ncells);
+        cp_async_wait_all();
+        __syncthreads();
+    }
     bool bad = false;
-    // load + pre-multiply by s_m c_m (coalesced per cell)
+    // pre-multiply by s_m c_m (coalesced per cell)
 #pragma unroll 4
     for (int t = threadIdx.x; t < F::CPB * N3; t += F::THREADS) {
         const int c = t / N3, idx = t % N3;
         const long long cell = cell0 + c;
         const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-        double v = cell < ncells ? f[(size_t)cell * N3 + idx] : 0.0;
+        double v = staged ? stage[t] : (cell < ncells ? f[(size_t)cell * N3 + idx] : 0.0);
         bad |= !isfinite(v);
         double w = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3);
         if ((i1 + i2 + i3) & 1) w = -w;
@@ -122,15 +163,20 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
     constexpr int CPB = F::CPB;
     extern __shared__ __align__(16) double2 sm[];
     double* red = reinterpret_cast<double*>(sm + CPB * F::CELL);  // [warps][CPB][6], after the cubes
+    double* stage = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + CPB * F::CELL_BYTES + F::RED_BYTES);
     __shared__ double lam[CPB][5];
     const long long cell0 = (long long)blockIdx.x * CPB;
     const long long g = cell0 / kLanes;
     const int lane0 = (int)(cell0 % kLanes);
-#pragma unroll 4
-    for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
-        const int idx = t / CPB, c = t % CPB;
-        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-        sm[c * F::CELL + F::at(i1, i2, i3)] = B[((size_t)g * N3 + idx) * kLanes + lane0 + c];
+    // every load of the tile in flight at once: the cube, then the RK2 base
+    // (which is only needed after the transform and the projection)
+    stage_group<N>(sm, B, g, lane0);
+    const bool staged = base && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+    if (staged) {
+        stage_cells<N>(stage, base, cell0, ncells);
+        cp_async_wait_1();
+    } else {
+        cp_async_wait_all();
     }
     __syncthreads();
     smem_axis_pass<N, 2, +1>(sm);
@@ -189,12 +235,17 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
         if (maximag && cell0 + c < ncells) maximag[cell0 + c] = m[5];
     }
     __syncthreads();
+    if (staged) {
+        cp_async_wait_all();
+        __syncthreads();
+    }
     bool bad = false;
 #pragma unroll 4
     for (int t = threadIdx.x; t < CPB * N3; t += F::THREADS) {
         const int c = t / N3, idx = t % N3;
         const long long cell = cell0 + c;
         if (!FWD && cell >= ncells) continue;
+        const double bv = staged ? stage[t] : (base && cell < ncells ? base[(size_t)cell * N3 + idx] : 0.0);
         const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
         const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
         const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3;
@@ -209,7 +260,7 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
             double v = 0.0;
             if (cell < ncells) {
                 v = coef * q;
-                if (base) v += base[o];
+                if (base) v += bv;
                 bad |= !isfinite(v);
             }
             double w = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3);
@@ -217,7 +268,7 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
             *p = make_double2(v * w, 0.0);
         } else {
             double v = coef * q;
-            if (base) v += base[o];
+            if (base) v += bv;
             bad |= !isfinite(v);
             out[o] = v;
         }

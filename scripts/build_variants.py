@@ -4,6 +4,11 @@ from concurrent.futures import ThreadPoolExecutor
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
+    "base": [],
+    "f1t256": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=256"],
+    "f1t512": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=512"],
+    "f1t128": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=128"],
+    "f2t256": ["BOLTZ_FUSED_THREADS=256"],
     "kcs16_m3": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3"],
     "kcs16_m2": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=2"],
     "kcs16_m3w2": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3", "BOLTZ_CONV_WARPS=2"],

@@ -1,0 +1,20 @@
+"""Pinned host<->device copy bandwidth, one direction and both at once (dev aid)."""
+import torch
+n = 128 << 20
+h1, h2 = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
+d1, d2 = torch.empty(n, dtype=torch.uint8, device="cuda"), torch.empty(n, dtype=torch.uint8, device="cuda")
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+for _ in range(3):
+    d1.copy_(h1, non_blocking=True); h2.copy_(d2, non_blocking=True)
+torch.cuda.synchronize()
+def t(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); e0.record(); fn(); e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+print("H2D GB/s", n / t(lambda: d1.copy_(h1, non_blocking=True)) / 1e6)
+print("D2H GB/s", n / t(lambda: h2.copy_(d2, non_blocking=True)) / 1e6)
+def both():
+    with torch.cuda.stream(s1): d1.copy_(h1, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+print("both GB/s each", n / t(both) / 1e6)
