@@ -77,6 +77,15 @@ struct boltz_ctx {
     double* dStageOut[2] = {nullptr, nullptr};
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    // second compute stream + workspace: odd host-pipeline chunks run beside even
+    // ones, so one chunk's last wave overlaps the next chunk's first
+    cudaStream_t comp2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    double2* dA2 = nullptr;
+    double2* dB2 = nullptr;
+    double* dFs2 = nullptr;
+    unsigned long long* dMaxIm2 = nullptr;
+    int64_t cap2 = 0;
     unsigned long long* dMaxIm = nullptr;
     int* dFlag = nullptr;
     int* hFlag = nullptr;    // pinned
@@ -299,6 +308,28 @@ void ensure_workspace(boltz_ctx* c, int64_t cells) {
 }
 
 // double-buffered device staging for host-memory calls (run_host_pipelined)
+// the second workspace set (same capacity as the first)
+void ensure_workspace2(boltz_ctx* c) {
+    if (c->cap2 == c->cap) return;
+    cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
+    c->dA2 = c->dB2 = nullptr; c->dFs2 = nullptr; c->dMaxIm2 = nullptr; c->cap2 = 0;
+    const int64_t n3 = n3_of(c);
+    CK(cudaMalloc(&c->dA2, (size_t)c->cap * n3 * 16));
+    CK(cudaMalloc(&c->dB2, (size_t)c->cap * n3 * 16));
+    CK(cudaMalloc(&c->dFs2, (size_t)c->cap * n3 * 8));
+    CK(cudaMalloc(&c->dMaxIm2, (size_t)c->cap * 8));
+    c->cap2 = c->cap;
+}
+
+// swaps the context's workspace set for the second one (kernels capture the
+// pointers at launch, so swapping between enqueues is safe)
+void swap_workspace(boltz_ctx* c) {
+    std::swap(c->dA, c->dA2);
+    std::swap(c->dB, c->dB2);
+    std::swap(c->dFs, c->dFs2);
+    std::swap(c->dMaxIm, c->dMaxIm2);
+}
+
 void ensure_staging(boltz_ctx* c, int64_t cells) {
     if (cells <= c->stage_cap) return;
     const int64_t n3 = n3_of(c);
@@ -313,7 +344,7 @@ void ensure_staging(boltz_ctx* c, int64_t cells) {
         CK(cudaMalloc(&c->dStageOut[b], (size_t)cells * n3 * 16));
     }
     c->stage_cap = cells;
-    c->ws_bytes = c->cap * (n3 * 40 + 8) + c->stage_cap * n3 * 64;
+    c->ws_bytes = (c->cap + c->cap2) * (n3 * 40 + 8) + c->stage_cap * n3 * 64;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -592,20 +623,24 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
     return check_flag(c, s);
 }
 
-// Host-memory calls: the batch is cut into chunks and pipelined over three
-// streams -- H2D of chunk i+1 (copy engine), compute of chunk i (`s`), D2H of
-// chunk i-1 (the other copy engine) -- through double-buffered staging, so
-// with pinned host memory the PCIe traffic hides behind the kernels.
+// Host-memory calls: the batch is cut into chunks and pipelined over four
+// streams -- H2D of chunk i+1 (copy engine), compute of chunk i (`s` for even,
+// `comp2` with the second workspace for odd chunks), D2H of chunk i-1 (the
+// other copy engine) -- through double-buffered staging, so with pinned host
+// memory the PCIe traffic hides behind the kernels.
 template <typename Fn>
 int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
                        cudaStream_t s, double* max_imag, Fn&& fn) {
-    // Chunk schedule: the first H2D and the last D2H cannot overlap compute, so
-    // those two chunks are small (1/16 of the batch) and the middle two 7/16.
     std::vector<int64_t> bounds{0};
     auto up32 = [](int64_t x) { return (x + kLanes - 1) / kLanes * kLanes; };
-    const char* sched = std::getenv("BOLTZ_HOST_CHUNKS");  // tuning: "a,b,c" relative chunk weights
-    if (sched && ncells > 1024) {
-        std::vector<double> w;
+    // Chunk schedule (relative weights 2,6,8,8,6,2; measured best on B200 for cfg2
+    // among 4-8 chunk schedules, 602k vs 564k evals/s for the old 4-chunk one):
+    // the first H2D and the last D2H cannot overlap compute, so the edge chunks
+    // are small; odd chunks run on a second stream, so each chunk's last wave
+    // overlaps the next chunk's work.  BOLTZ_HOST_CHUNKS="a,b,..." overrides.
+    std::vector<double> w{2, 6, 8, 8, 6, 2};
+    if (const char* sched = std::getenv("BOLTZ_HOST_CHUNKS")) {
+        w.clear();
         for (const char* p = sched; *p;) {
             char* end = nullptr;
             const double v = std::strtod(p, &end);
@@ -613,6 +648,8 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
             if (v > 0) w.push_back(v);
             p = (*end == ',') ? end + 1 : end;
         }
+    }
+    if (ncells > 1024) {
         double tot = 0, acc = 0;
         for (double v : w) tot += v;
         for (size_t i = 0; i + 1 < w.size(); ++i) {
@@ -620,18 +657,8 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
             const int64_t b = std::min<int64_t>(ncells, up32((int64_t)(ncells * acc / tot)));
             if (b > bounds.back() && b < ncells) bounds.push_back(b);
         }
-        bounds.push_back(ncells);
-    } else if (ncells <= 1024) {
-        bounds.push_back(ncells);
-    } else {
-        int64_t edge = 16, nmid = 2;  // measured best of {8,16,32} x {2,3}; BOLTZ_HOST_EDGE / BOLTZ_HOST_MID override (tuning)
-        if (const char* e = std::getenv("BOLTZ_HOST_EDGE")) edge = std::max(2, std::atoi(e));
-        if (const char* e = std::getenv("BOLTZ_HOST_MID")) nmid = std::max(1, std::atoi(e));
-        const int64_t small = up32(ncells / edge), mid = up32((ncells - 2 * small + nmid - 1) / nmid);
-        for (int64_t b = small; b < ncells - small; b += mid) bounds.push_back(b);
-        bounds.push_back(ncells - small);
-        bounds.push_back(ncells);
     }
+    bounds.push_back(ncells);
     int64_t chunk = 0;
     for (size_t i = 1; i < bounds.size(); ++i) chunk = std::max(chunk, bounds[i] - bounds[i - 1]);
     ensure_workspace(c, chunk);
@@ -644,6 +671,14 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     ensure_staging(c, chunk);
     CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     const int64_t nchunks = (int64_t)bounds.size() - 1;
+    // odd chunks compute on comp2 with the second workspace; comp2 joins s's
+    // prior work first and s waits for comp2 at the end (stream semantics kept)
+    const bool two = nchunks > 1;
+    if (two) {
+        ensure_workspace2(c);
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(c->comp2, c->ev_fork, 0));
+    }
     auto h2d = [&](int64_t i) {
         const int slot = (int)(i & 1);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
@@ -656,16 +691,23 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     for (int64_t i = 0; i < nchunks; ++i) {
         const int slot = (int)(i & 1);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
-        CK(cudaStreamWaitEvent(s, c->ev_h2d[slot], 0));
-        if (i >= 2) CK(cudaStreamWaitEvent(s, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
-        fn(c->dStageIn[slot], c->dStageOut[slot], nc, s);
-        CK(cudaEventRecord(c->ev_comp[slot], s));
-        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, s));
+        cudaStream_t cs = slot ? c->comp2 : s;
+        CK(cudaStreamWaitEvent(cs, c->ev_h2d[slot], 0));
+        if (i >= 2) CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
+        if (slot) swap_workspace(c);
+        fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
+        CK(cudaEventRecord(c->ev_comp[slot], cs));
+        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
+        if (slot) swap_workspace(c);
         if (i + 1 < nchunks) h2d(i + 1);
         CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
         CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
                            cudaMemcpyDeviceToHost, c->d2h_stream));
         CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
+    }
+    if (two) {
+        CK(cudaEventRecord(c->ev_join, c->comp2));
+        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
     }
     CK(cudaStreamSynchronize(c->d2h_stream));
     return check_flag(c, s);
@@ -783,6 +825,9 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
         CK(cudaMemset(c->dFlag, 0, sizeof(int)));
         CK(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
         CK(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->comp2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
         for (int b = 0; b < 2; ++b) {
             CK(cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
@@ -810,6 +855,10 @@ int boltz_destroy(boltz_ctx* c) {
     cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
+    cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
+    if (c->comp2) cudaStreamDestroy(c->comp2);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (int b = 0; b < 2; ++b) {
         cudaFree(c->dStageIn[b]);
         cudaFree(c->dStageOut[b]);

@@ -164,14 +164,15 @@ def test_device_generated_table_matches_host_table(gpu, O, n, L, lam):
 
 
 def test_host_pipeline_matches_device_path(gpu):
-    """Host-memory calls are chunked and pipelined over copy/compute streams;
-    the result is bitwise the device-memory call's (ragged last chunk)."""
+    """Host-memory calls are chunked (6 chunks here) and pipelined over two copy
+    and two compute streams with two workspaces; the result is bitwise the
+    device-memory call's (ragged last chunk)."""
     import torch
     n, L = 8, 5.0
     grid = VelocityGrid.create(n, L)
     f = scenarios.mixture_cells(grid, 1100, seed=21)
     with _op(n, L) as op:
-        qh, mih = op.collide(f, with_max_imag=True)          # host path, 4 chunks
+        qh, mih = op.collide(f, with_max_imag=True)          # host path, 6 chunks
         fd = torch.from_numpy(f).to(gpu)
         qd, mid = op.collide(fd, with_max_imag=True)        # device path
         assert np.array_equal(qh, qd.cpu().numpy())
