@@ -189,23 +189,54 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
     // deterministic reduction (fixed strided partials, shuffle tree, warps in order)
     const double dv3 = pc.dv * pc.dv * pc.dv;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // THREADS a multiple of N^2: every node a thread visits has the same (i2, i3),
+    // so the per-node weights and moments factor into per-thread constants and
+    // three FMAs per node (sums over i1 only; the result is reassembled below)
+    constexpr bool kFixed23 = F::THREADS % (N * N) == 0;
+    const int f2 = (threadIdx.x / N) % N, f3 = threadIdx.x % N;
+    const double fv2 = pc.dv * (f2 - N / 2), fv3 = pc.dv * (f3 - N / 2);
+    const double fw23 = axis_coeff(N, f2) * axis_coeff(N, f3) * dv3;
     for (int c = 0; c < CPB; ++c) {
         double part[6] = {0, 0, 0, 0, 0, 0};
-        for (int idx = threadIdx.x; idx < N3; idx += F::THREADS) {
-            const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-            double2* p = sm + c * F::CELL + F::at(i1, i2, i3);
-            const double2 z = *p;
-            const double s = ((i1 + i2 + i3) & 1) ? -scale : scale;
-            const double q = z.x * s;
-            p->x = q;
-            const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
-            const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3 * q;
-            part[0] += wq;
-            part[1] += v1 * wq;
-            part[2] += v2 * wq;
-            part[3] += v3 * wq;
-            part[4] += (v1 * v1 + v2 * v2 + v3 * v3) * wq;
-            part[5] = fmax(part[5], fabs(z.y * scale));
+        if constexpr (kFixed23) {
+            double s0 = 0.0, s1 = 0.0, s4 = 0.0, mi = 0.0;
+            const double sg23 = ((f2 + f3) & 1) ? -scale : scale;
+            for (int idx = threadIdx.x; idx < N3; idx += F::THREADS) {
+                const int i1 = idx / (N * N);
+                double2* p = sm + c * F::CELL + F::at(i1, f2, f3);
+                const double2 z = *p;
+                const double q = z.x * ((i1 & 1) ? -sg23 : sg23);
+                p->x = q;
+                const double v1 = pc.dv * (i1 - N / 2);
+                const double cq = axis_coeff(N, i1) * q;
+                s0 += cq;
+                s1 = fma(v1, cq, s1);
+                s4 = fma(v1 * v1, cq, s4);
+                mi = fmax(mi, fabs(z.y));
+            }
+            part[0] = fw23 * s0;
+            part[1] = fw23 * s1;
+            part[2] = fv2 * part[0];
+            part[3] = fv3 * part[0];
+            part[4] = fw23 * fma(fv2 * fv2 + fv3 * fv3, s0, s4);
+            part[5] = mi * fabs(scale);
+        } else {
+            for (int idx = threadIdx.x; idx < N3; idx += F::THREADS) {
+                const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
+                double2* p = sm + c * F::CELL + F::at(i1, i2, i3);
+                const double2 z = *p;
+                const double s = ((i1 + i2 + i3) & 1) ? -scale : scale;
+                const double q = z.x * s;
+                p->x = q;
+                const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
+                const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3 * q;
+                part[0] += wq;
+                part[1] += v1 * wq;
+                part[2] += v2 * wq;
+                part[3] += v3 * wq;
+                part[4] += (v1 * v1 + v2 * v2 + v3 * v3) * wq;
+                part[5] = fmax(part[5], fabs(z.y * scale));
+            }
         }
 #pragma unroll
         for (int a = 0; a < 6; ++a) {
@@ -246,11 +277,18 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
         const long long cell = cell0 + c;
         if (!FWD && cell >= ncells) continue;
         const double bv = staged ? stage[t] : (base && cell < ncells ? base[(size_t)cell * N3 + idx] : 0.0);
-        const int i1 = idx / (N * N), i2 = (idx / N) % N, i3 = idx % N;
-        const double v1 = pc.dv * (i1 - N / 2), v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
-        const double wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3;
-        const double cl = lam[c][0] + v1 * lam[c][1] + v2 * lam[c][2] + v3 * lam[c][3] +
-                          (v1 * v1 + v2 * v2 + v3 * v3) * lam[c][4];
+        const int i1 = idx / (N * N), i2 = kFixed23 ? f2 : (idx / N) % N, i3 = kFixed23 ? f3 : idx % N;
+        const double v1 = pc.dv * (i1 - N / 2);
+        double wq, cl;
+        if constexpr (kFixed23) {
+            wq = axis_coeff(N, i1) * fw23;
+            cl = fma(v1, fma(v1, lam[c][4], lam[c][1]),
+                     lam[c][0] + fv2 * lam[c][2] + fv3 * lam[c][3] + (fv2 * fv2 + fv3 * fv3) * lam[c][4]);
+        } else {
+            const double v2 = pc.dv * (i2 - N / 2), v3 = pc.dv * (i3 - N / 2);
+            wq = axis_coeff(N, i1) * axis_coeff(N, i2) * axis_coeff(N, i3) * dv3;
+            cl = lam[c][0] + v1 * lam[c][1] + v2 * lam[c][2] + v3 * lam[c][3] + (v1 * v1 + v2 * v2 + v3 * v3) * lam[c][4];
+        }
         double2* p = sm + c * F::CELL + F::at(i1, i2, i3);
         const double q = p->x - wq * cl;
         const size_t o = (size_t)cell * N3 + idx;
