@@ -203,6 +203,34 @@ int boltz_save_table(const char* path, int n, double L, double lambda, double be
 int boltz_load_table(const char* path, int n, double L, double lambda, double beta, double r0, int panels,
                      double* G);
 
+/* ---- halo exchange of the sharded spatial domain (SURVEY §8b
+ * "halo_exchange(...)", §8e), NCCL over NVLink / NVSwitch ---- */
+#define BOLTZ_HALO_ID_BYTES 128
+typedef struct boltz_halo boltz_halo;
+
+/* rank 0 makes the communicator id and shares it out of band (one process per GPU) */
+int boltz_halo_unique_id(unsigned char id[BOLTZ_HALO_ID_BYTES]);
+/* ncclCommInitRank on `device` (collective over the `world` ranks) */
+int boltz_halo_create(int rank, int world, const unsigned char id[BOLTZ_HALO_ID_BYTES], int device,
+                      boltz_halo** out);
+/* one process driving `world` GPUs (ncclCommInitAll): out[r] for devices[r] */
+int boltz_halo_create_all(int world, const int* devices, boltz_halo** out);
+int boltz_halo_destroy(boltz_halo* halo);
+/*
+ * Replaces halo_exchange: field is the
+ * rank's DEVICE (ncl + 4) x n3 array; sends cells 2,3 left and ncl, ncl+1
+ * right, receives into ghosts 0,1 and ncl+2, ncl+3 -- one grouped NCCL call,
+ * one contiguous 2*n3 message per direction, ordered on `stream`.  The end
+ * ranks leave their physical-end ghosts to boltz_fill_boundary.  Collective:
+ * every rank calls it.
+ */
+int boltz_halo_exchange(boltz_halo* halo, double* field, int64_t ncl, int64_t n3, void* stream);
+/* in-place sum over ranks of `count` device doubles (the conservation ledger) */
+int boltz_halo_allreduce_sum(boltz_halo* halo, double* buf, int64_t count, void* stream);
+/* in-process loopback backend: fields[r] are device arrays of
+ * (ncl[r] + 4) x n3 on one device; copies every rank pair's ghosts */
+int boltz_halo_exchange_loopback(double* const* fields, const int64_t* ncl, int nranks, int64_t n3, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

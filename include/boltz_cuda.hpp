@@ -55,6 +55,13 @@ public:
             throw Error(BOLTZ_ERR_CONFIG, "weight table size is not N^6");
         check(boltz_create(n, L, k.lambda, k.beta, k.r0 > 0 ? k.r0 : L, table.data(), device, &ctx_));
     }
+    // the weights generated on the device (no N^6 host table)
+    struct Generated {
+        int panels = 64;
+    };
+    CollisionOperator(int n, double L, const Kernel& k, Generated g, int device = 0) : n_(n) {
+        check(boltz_create_generated(n, L, k.lambda, k.beta, k.r0 > 0 ? k.r0 : L, g.panels, device, &ctx_));
+    }
     ~CollisionOperator() { boltz_destroy(ctx_); }
     CollisionOperator(const CollisionOperator&) = delete;
     CollisionOperator& operator=(const CollisionOperator&) = delete;
@@ -89,6 +96,18 @@ public:
     // device-pointer variants (ordered on `stream`)
     void collision_rk2_device(double* field, int64_t ncells, double dt, double epsilon, void* stream = nullptr) {
         check(boltz_rk2_batch(ctx_, field, ncells, dt, 1.0 / epsilon, BOLTZ_MEM_DEVICE, stream));
+    }
+    // compute_moments: 7 values per cell (rho, rho V, rho e, T, H)
+    std::vector<double> moments(std::span<const double> f) {
+        std::vector<double> out(7 * static_cast<size_t>(cells(f.size())));
+        check(boltz_moments_batch(ctx_, f.data(), out.data(), cells(f.size()), BOLTZ_MEM_HOST, nullptr));
+        return out;
+    }
+    // marginal_distribution g(v1): N values per cell
+    std::vector<double> marginal(std::span<const double> f) {
+        std::vector<double> out(static_cast<size_t>(n_) * cells(f.size()));
+        check(boltz_marginal_batch(ctx_, f.data(), out.data(), cells(f.size()), BOLTZ_MEM_HOST, nullptr));
+        return out;
     }
     boltz_ctx* handle() { return ctx_; }
 

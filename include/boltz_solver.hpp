@@ -1,0 +1,265 @@
+// boltz_solver.hpp -- header-only C++ host driver of the space-inhomogeneous
+// problem over the C ABI (boltz_cuda.h): the reference's grid / time-stepping
+// drivers in the reference's language, with every kernel on
+// the GPU.  Mirrors paper_1301_4195_b200/solver.py (same call order, so the two
+// produce bitwise-identical fields; tests/test_cpp_solver.py checks that).
+//
+//   strang_step(dt) = T(dt/2) o C_RK2(dt) o T(dt/2)
+//   T(h):  SSP-RK2 of the FV step, ghost refresh before each
+//          stage: halo exchange (NCCL / loopback) + physical ends
+//   C_RK2: boltz_rk2_batch over the rank's interior cells (cell-local)
+//
+// Field: (ncl + 4) x N^3 doubles on the device, ghosts at 0,1 and ncl+2,ncl+3
+// (SPEC.md:296).  Decomposition: contiguous ranges balanced to +-1
+// (SPEC.md:426-444).  Build with nvcc, or g++ -I<cuda>/include -lcudart.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <span>
+#include <utility>
+#include <vector>
+
+#include "boltz_cuda.h"
+#include "boltz_cuda.hpp"
+
+namespace boltz::cuda {
+
+inline void cuda_check(cudaError_t e) {
+    if (e != cudaSuccess) throw Error(BOLTZ_ERR_CUDA, cudaGetErrorString(e));
+}
+
+// plan_decomposition: (start, count) per rank, contiguous,
+// |count_r - count_s| <= 1, larger ranges first.
+inline std::vector<std::pair<int64_t, int64_t>> plan_decomposition(int64_t ncells, int nranks) {
+    if (nranks < 1 || ncells < nranks) throw Error(BOLTZ_ERR_CONFIG, "plan_decomposition: more ranks than cells");
+    std::vector<std::pair<int64_t, int64_t>> out;
+    const int64_t base = ncells / nranks, rem = ncells % nranks;
+    int64_t s = 0;
+    for (int r = 0; r < nranks; ++r) {
+        const int64_t c = base + (r < rem ? 1 : 0);
+        out.emplace_back(s, c);
+        s += c;
+    }
+    return out;
+}
+
+// centres / widths of the global field with 2 mirrored ghost cells per end
+// (ghost widths mirror the adjacent interior cells; scenarios.extend_ghosts)
+inline void extend_ghosts(std::span<const double> x, std::span<const double> dx, std::vector<double>& xe,
+                          std::vector<double>& dxe) {
+    const size_t n = x.size();
+    if (n < 2 || dx.size() != n) throw Error(BOLTZ_ERR_CONFIG, "extend_ghosts: need >= 2 cells");
+    dxe.assign(n + 4, 0.0);
+    dxe[0] = dx[1];
+    dxe[1] = dx[0];
+    for (size_t i = 0; i < n; ++i) dxe[i + 2] = dx[i];
+    dxe[n + 2] = dx[n - 1];
+    dxe[n + 3] = dx[n - 2];
+    xe.assign(n + 4, 0.0);
+    for (size_t i = 0; i < n; ++i) xe[i + 2] = x[i];
+    xe[1] = x[0] - 0.5 * (dx[0] + dxe[1]);
+    xe[0] = xe[1] - 0.5 * (dxe[1] + dxe[0]);
+    xe[n + 2] = x[n - 1] + 0.5 * (dx[n - 1] + dxe[n + 2]);
+    xe[n + 3] = xe[n + 2] + 0.5 * (dxe[n + 2] + dxe[n + 3]);
+}
+
+// physical end condition; WallBalanced is the
+// flux-balanced wall extension (boltz_fill_boundary kind 2)
+struct Boundary {
+    enum Kind { Extrap = 0, Wall = 1, WallBalanced = 2 };
+    Kind kind = Extrap;
+    double Tw = 1.0;
+    std::array<double, 3> Vw{0.0, 0.0, 0.0};
+    bool is_wall() const { return kind != Extrap; }
+};
+
+// Device buffer (RAII)
+template <typename T>
+class DeviceArray {
+public:
+    DeviceArray() = default;
+    explicit DeviceArray(size_t n) : n_(n) { cuda_check(cudaMalloc(&p_, n * sizeof(T))); }
+    ~DeviceArray() { cudaFree(p_); }
+    DeviceArray(const DeviceArray&) = delete;
+    DeviceArray& operator=(const DeviceArray&) = delete;
+    DeviceArray(DeviceArray&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+    DeviceArray& operator=(DeviceArray&& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        return *this;
+    }
+    T* data() { return p_; }
+    const T* data() const { return p_; }
+    size_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+class Solver1D {
+public:
+    // x, dx: GLOBAL cell centres / widths; f0: this rank's interior cells,
+    // ncl x N^3 host doubles (ncl from plan_decomposition(x.size(), world)).
+    // halo: NCCL communicator for world > 1 (nullptr with the loopback driver).
+    Solver1D(CollisionOperator& op, int n, double half_width, std::span<const double> x, std::span<const double> dx,
+             std::span<const double> f0, int rank = 0, int world = 1, Boundary left = {}, Boundary right = {},
+             double epsilon = 1.0, boltz_halo* halo = nullptr, cudaStream_t stream = nullptr)
+        : op_(op), n3_((int64_t)n * n * n), L_(half_width), rank_(rank), world_(world), left_(left), right_(right),
+          eps_(epsilon), halo_(halo), s_(stream) {
+        const auto plan = plan_decomposition((int64_t)x.size(), world);
+        start_ = plan[rank].first;
+        ncl_ = plan[rank].second;
+        if (ncl_ < 2) throw Error(BOLTZ_ERR_CONFIG, "each rank needs at least 2 cells (2-cell halo, SPEC.md:438)");
+        if ((int64_t)f0.size() != ncl_ * n3_) throw Error(BOLTZ_ERR_CONFIG, "f0 must hold this rank's ncl x N^3 values");
+        std::vector<double> xe, dxe;
+        extend_ghosts(x, dx, xe, dxe);
+        dx_min_ = dx[0];
+        for (double v : dx) dx_min_ = std::fmin(dx_min_, v);
+        dx_host_.assign(dx.begin() + start_, dx.begin() + start_ + ncl_);
+        x_ext_ = DeviceArray<double>(ncl_ + 4);
+        dx_ext_ = DeviceArray<double>(ncl_ + 4);
+        cuda_check(cudaMemcpy(x_ext_.data(), xe.data() + start_, (ncl_ + 4) * sizeof(double), cudaMemcpyHostToDevice));
+        cuda_check(cudaMemcpy(dx_ext_.data(), dxe.data() + start_, (ncl_ + 4) * sizeof(double), cudaMemcpyHostToDevice));
+        for (auto* b : {&field_, &tmp_, &tmp2_}) *b = DeviceArray<double>((ncl_ + 4) * n3_);
+        cuda_check(cudaMemset(field_.data(), 0, (ncl_ + 4) * n3_ * sizeof(double)));
+        cuda_check(cudaMemcpy(field_.data() + 2 * n3_, f0.data(), ncl_ * n3_ * sizeof(double), cudaMemcpyHostToDevice));
+        red_ = DeviceArray<double>(8);
+    }
+
+    int64_t ncl() const { return ncl_; }
+    int64_t cell_values() const { return n3_; }
+    int64_t start() const { return start_; }
+    double time() const { return t_; }
+    double* field() { return field_.data(); }
+    double* interior() { return field_.data() + 2 * n3_; }
+    double cfl_dt(double cfl = 0.9) const { return cfl * dx_min_ / L_; }  // SPEC.md:379,408 (global min dx)
+
+    // ghost refresh: halo exchange (unless exchange = false: the loopback driver
+    // exchanged already) and the physical ends of the end ranks
+    void fill_ghosts(bool exchange = true) {
+        if (exchange && halo_) check(boltz_halo_exchange(halo_, field_.data(), ncl_, n3_, s_));
+        if (rank_ == 0)
+            check(boltz_fill_boundary(op_.handle(), field_.data(), ncl_, x_ext_.data(), 0, left_.kind, left_.Tw,
+                                      left_.Vw.data(), &sigma_w_[0], s_));
+        if (rank_ == world_ - 1)
+            check(boltz_fill_boundary(op_.handle(), field_.data(), ncl_, x_ext_.data(), 1, right_.kind, right_.Tw,
+                                      right_.Vw.data(), &sigma_w_[1], s_));
+    }
+
+    // SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
+    // stage 1: f <- f/2 + S(t1)/2, S = one FV step after a ghost refresh
+    void transport_stage(int stage, double h, bool exchange = true) {
+        const int wl = rank_ == 0 && left_.is_wall(), wr = rank_ == world_ - 1 && right_.is_wall();
+        if (stage == 0) {
+            fill_ghosts(exchange);
+            check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
+                                       dx_ext_.data(), h, wl, wr, s_));
+        } else {
+            std::swap(field_, tmp_);  // field = t1, tmp = f^n
+            fill_ghosts(exchange);
+            check(boltz_transport_step(op_.handle(), field_.data(), tmp_.data(), 0.5, tmp2_.data(), ncl_,
+                                       x_ext_.data(), dx_ext_.data(), h, wl, wr, s_));
+            std::swap(tmp2_, field_);  // field = out, tmp2 = t1
+        }
+    }
+
+    // field of the loopback driver's stage-1 exchange (t1 lives in tmp until the stage swaps it in)
+    double* stage_input(int stage) { return stage == 0 ? field_.data() : tmp_.data(); }
+
+    void transport(double h) {
+        if (h * L_ > dx_min_ * (1 + 1e-12)) throw Error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
+        transport_stage(0, h);
+        transport_stage(1, h);
+    }
+
+    void collide(double dt) { check(boltz_rk2_batch(op_.handle(), interior(), ncl_, dt, 1.0 / eps_, BOLTZ_MEM_DEVICE, s_)); }
+
+    void strang_step(double dt) {
+        transport(0.5 * dt);
+        collide(dt);
+        transport(0.5 * dt);
+        t_ += dt;
+    }
+    void advance_time(double dt) { t_ += dt; }
+
+    // compute_moments of the interior: ncl x 7 host doubles
+    std::vector<double> moments() {
+        DeviceArray<double> m(ncl_ * 7);
+        check(boltz_moments_batch(op_.handle(), interior(), m.data(), ncl_, BOLTZ_MEM_DEVICE, s_));
+        std::vector<double> h(ncl_ * 7);
+        cuda_check(cudaMemcpyAsync(h.data(), m.data(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        cuda_check(cudaStreamSynchronize(s_));
+        return h;
+    }
+
+    // global (mass, x-momentum, energy) = sum_j dx_j (rho, rho V1, rho e)_j over all ranks
+    std::array<double, 3> ledger() {
+        const auto m = moments();
+        double tot[3] = {0, 0, 0};
+        for (int64_t j = 0; j < ncl_; ++j) {
+            tot[0] += m[j * 7 + 0] * dx_host_[j];
+            tot[1] += m[j * 7 + 1] * dx_host_[j];
+            tot[2] += m[j * 7 + 4] * dx_host_[j];
+        }
+        if (halo_ && world_ > 1) {
+            cuda_check(cudaMemcpyAsync(red_.data(), tot, sizeof tot, cudaMemcpyHostToDevice, s_));
+            check(boltz_halo_allreduce_sum(halo_, red_.data(), 3, s_));
+            cuda_check(cudaMemcpyAsync(tot, red_.data(), sizeof tot, cudaMemcpyDeviceToHost, s_));
+            cuda_check(cudaStreamSynchronize(s_));
+        }
+        return {tot[0], tot[1], tot[2]};
+    }
+
+    // interior cells -> host (ncl x N^3)
+    void download(std::span<double> out) {
+        if ((int64_t)out.size() != ncl_ * n3_) throw Error(BOLTZ_ERR_CONFIG, "download: size must be ncl x N^3");
+        cuda_check(cudaMemcpyAsync(out.data(), interior(), out.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        cuda_check(cudaStreamSynchronize(s_));
+    }
+
+    double sigma_w(int side) const { return sigma_w_[side]; }
+
+private:
+    CollisionOperator& op_;
+    int64_t n3_;
+    double L_;
+    int rank_, world_;
+    Boundary left_, right_;
+    double eps_;
+    boltz_halo* halo_;
+    cudaStream_t s_;
+    int64_t start_ = 0, ncl_ = 0;
+    double dx_min_ = 0, t_ = 0;
+    double sigma_w_[2] = {0, 0};
+    std::vector<double> dx_host_;
+    DeviceArray<double> x_ext_, dx_ext_, field_, tmp_, tmp2_, red_;
+};
+
+// One Strang step of n virtual ranks of one device (loopback backend,
+// SPEC.md:470): the ghost exchange runs between per-rank fields before every
+// transport stage; bitwise equal to one rank (tests/test_cpp_solver.py).
+inline void strang_step_loopback(std::vector<Solver1D*>& ranks, double dt, cudaStream_t s = nullptr) {
+    std::vector<double*> fields(ranks.size());
+    std::vector<int64_t> ncl(ranks.size());
+    for (size_t r = 0; r < ranks.size(); ++r) ncl[r] = ranks[r]->ncl();
+    auto exchange = [&](int stage, int64_t cells) {
+        for (size_t r = 0; r < ranks.size(); ++r) fields[r] = ranks[r]->stage_input(stage);
+        check(boltz_halo_exchange_loopback(fields.data(), ncl.data(), (int)ranks.size(), cells, s));
+    };
+    for (int half = 0; half < 2; ++half) {
+        for (int stage = 0; stage < 2; ++stage) {
+            exchange(stage, ranks[0]->cell_values());
+            for (auto* r : ranks) r->transport_stage(stage, 0.5 * dt, false);
+        }
+        if (half == 0)
+            for (auto* r : ranks) r->collide(dt);
+    }
+    for (auto* r : ranks) r->advance_time(dt);
+}
+
+}  // namespace boltz::cuda

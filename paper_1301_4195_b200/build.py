@@ -15,7 +15,7 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libboltz_cuda.so"
-SOURCES = [CSRC / "boltz_cuda.cu", CSRC / "host_weights.cpp"]
+SOURCES = [CSRC / "boltz_cuda.cu", CSRC / "host_weights.cpp", CSRC / "halo.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -25,7 +25,7 @@ def _nvcc() -> str:
 
 
 def _inputs():
-    return SOURCES + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "boltz_cuda.h"]
+    return SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "boltz_cuda.h"]
 
 
 def up_to_date() -> bool:
@@ -42,7 +42,7 @@ def build(verbose: bool = False, force: bool = False, out: pathlib.Path = LIB, d
     out.parent.mkdir(parents=True, exist_ok=True)
     cmd = [
         _nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--shared", "-Xcompiler", "-fPIC,-fopenmp",
-        "-ccbin", "/usr/bin/g++", *[f"-D{d}" for d in defines], "-o", str(out), *map(str, SOURCES), "-lgomp",
+        "-ccbin", "/usr/bin/g++", *[f"-D{d}" for d in defines], "-o", str(out), *map(str, SOURCES), "-lgomp", "-ldl",
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

@@ -1,0 +1,95 @@
+// The C++ host driver (include/boltz_solver.hpp) on the GPU: the reference's
+// time-stepping loop in the reference's language over the C ABI.  Built and
+// checked by tests/test_cpp_solver.py against the Python driver (solver.py).
+//
+//   solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE
+//     DIR/x.bin, DIR/dx.bin: Nx doubles; DIR/f0.bin: Nx x N^3 doubles
+//     MODE nccl:     one rank, an NCCL communicator of world 1 (exchange is
+//                    then a no-op; allreduce of the ledger is exercised)
+//     MODE loopback: NRANKS virtual ranks of one device
+//   writes DIR/out_<MODE>_<NRANKS>.bin (Nx x N^3) and prints the ledger.
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "boltz_solver.hpp"
+
+using namespace boltz::cuda;
+
+static std::vector<double> read_bin(const std::string& path) {
+    std::ifstream f(path, std::ios::binary | std::ios::ate);
+    if (!f) throw Error(BOLTZ_ERR_IO, "cannot read " + path);
+    const std::streamsize n = f.tellg();
+    std::vector<double> v(n / sizeof(double));
+    f.seekg(0);
+    f.read(reinterpret_cast<char*>(v.data()), n);
+    return v;
+}
+
+int main(int argc, char** argv) {
+    if (argc != 10) {
+        std::fprintf(stderr, "usage: solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE\n");
+        return 2;
+    }
+    const std::string dir = argv[1], mode = argv[9];
+    const int n = std::atoi(argv[2]), steps = std::atoi(argv[7]), nranks = std::atoi(argv[8]);
+    const double L = std::atof(argv[3]), lam = std::atof(argv[4]), Tw = std::atof(argv[5]), dt = std::atof(argv[6]);
+    try {
+        const auto x = read_bin(dir + "/x.bin"), dx = read_bin(dir + "/dx.bin"), f0 = read_bin(dir + "/f0.bin");
+        const size_t nx = x.size(), n3 = (size_t)n * n * n;
+        Kernel k;
+        k.lambda = lam;
+        CollisionOperator op(n, L, k, CollisionOperator::Generated{});
+        Boundary left{Boundary::Wall, Tw}, right{Boundary::Extrap, 1.0};
+        std::vector<double> out(nx * n3);
+        std::array<double, 3> led0{}, led1{};
+        if (mode == "nccl") {
+            unsigned char id[BOLTZ_HALO_ID_BYTES];
+            check(boltz_halo_unique_id(id));
+            boltz_halo* halo = nullptr;
+            check(boltz_halo_create(0, 1, id, 0, &halo));
+            {
+                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, halo);
+                led0 = s.ledger();
+                for (int i = 0; i < steps; ++i) s.strang_step(dt);
+                led1 = s.ledger();
+                s.download(out);
+                // the ledger all-reduce of a world-1 communicator is the identity
+                DeviceArray<double> buf(3);
+                cuda_check(cudaMemset(buf.data(), 0, 3 * sizeof(double)));
+                check(boltz_halo_allreduce_sum(halo, buf.data(), 3, nullptr));
+                cuda_check(cudaDeviceSynchronize());
+            }
+            check(boltz_halo_destroy(halo));
+        } else {
+            const auto plan = plan_decomposition((int64_t)nx, nranks);
+            std::vector<std::unique_ptr<Solver1D>> ranks;
+            std::vector<Solver1D*> ptrs;
+            for (int r = 0; r < nranks; ++r) {
+                std::span<const double> f0r(f0.data() + plan[r].first * n3, plan[r].second * n3);
+                ranks.push_back(std::make_unique<Solver1D>(op, n, L, x, dx, f0r, r, nranks, left, right));
+                ptrs.push_back(ranks.back().get());
+            }
+            for (auto* r : ptrs) {
+                const auto l = r->ledger();
+                for (int a = 0; a < 3; ++a) led0[a] += l[a];
+            }
+            for (int i = 0; i < steps; ++i) strang_step_loopback(ptrs, dt);
+            for (int r = 0; r < nranks; ++r) {
+                const auto l = ptrs[r]->ledger();
+                for (int a = 0; a < 3; ++a) led1[a] += l[a];
+                ptrs[r]->download(std::span<double>(out.data() + plan[r].first * n3, plan[r].second * n3));
+            }
+        }
+        const std::string path = dir + "/out_" + mode + "_" + std::to_string(nranks) + ".bin";
+        std::ofstream(path, std::ios::binary).write(reinterpret_cast<const char*>(out.data()), out.size() * 8);
+        std::printf("ledger mass %.17g -> %.17g\n", led0[0], led1[0]);
+        return 0;
+    } catch (const Error& e) {
+        std::fprintf(stderr, "error category %d: %s\n", e.category(), e.what());
+        return e.category();
+    }
+}
