@@ -195,12 +195,21 @@ def main():
 
     if rank == 0:
         build()
+    # one rank per GPU over NCCL; BOLTZ_BENCH_DIST=gloo (CPU collectives, ranks
+    # folded onto the visible GPUs) only checks the multi-rank plumbing on a
+    # box with fewer GPUs than ranks -- its timings are not bench values
+    backend = os.environ.get("BOLTZ_BENCH_DIST", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend == "gloo" else local
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
         dist.barrier()
         build()  # no-op unless stale
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where the timing collectives run
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
     grid = VelocityGrid.create(N_VEL, L_VEL)
@@ -243,7 +252,7 @@ def main():
     op.set_timing(False)
     kms, klaunch = op.timing(reset=True)
     total_ms = sum(step_ms)
-    tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    tmax = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     total_ms = float(tmax.item())
@@ -272,7 +281,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
-    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = evals / (float(te.item()) * 1e-3)
