@@ -22,7 +22,12 @@ namespace boltz_gpu {
 template <int N>
 struct Fused {
     static constexpr int N3 = N * N * N;
-    static constexpr int ROW = N + 1;                 // padded row (complex elements)
+    // Shared layout per cell: [i1][i2][i3] complex.  Rows are padded to N+1 when
+    // that fits (N <= 16), which makes the three axis passes conflict-free for
+    // 16 B accesses; otherwise (N = 24: 221 KB unpadded) i3 is XOR-swizzled with
+    // the low 3 bits of i2 -- the same effect without the padding.
+    static constexpr bool PAD = N * N * (N + 1) * 16 <= 200 * 1024;
+    static constexpr int ROW = PAD ? N + 1 : N;       // row length (complex elements)
     static constexpr int CELL = N * N * ROW;          // complex elements per cell in smem
     static constexpr int CELL_BYTES = CELL * 16;
     // cells per block: largest power of two <= 32 whose cubes fit in ~200 KB
@@ -36,17 +41,23 @@ struct Fused {
                                : (CELL_BYTES * 4 <= BUDGET)  ? 4
                                : (CELL_BYTES * 2 <= BUDGET)  ? 2
                                                              : 1;
-    static constexpr bool FITS = CELL_BYTES <= 200 * 1024;
 #ifndef BOLTZ_FUSED_THREADS
 #define BOLTZ_FUSED_THREADS 512
 #endif
-    static constexpr int THREADS = BOLTZ_FUSED_THREADS;
+    // the N=24 register FFT needs ~130 registers: 256 threads
+    static constexpr int THREADS = N > 16 ? 256 : BOLTZ_FUSED_THREADS;
+    static constexpr int RED_BYTES = (THREADS / 32) * CPB * 6 * 8;
+    static constexpr int SMEM_MAX = 232448;  // 227 KB opt-in dynamic shared memory per block
     // real staging (CPB x N^3 doubles): the forward's f, the inverse's RK2 base,
     // both fetched by cp.async so every load of the tile is in flight at once
-    static constexpr int STAGE_BYTES = CPB * N3 * 8;
-    static constexpr int RED_BYTES = (THREADS / 32) * CPB * 6 * 8;
+    // (only where it fits beside the cubes: not at N = 24)
+    static constexpr int STAGE_BYTES =
+        CPB * CELL_BYTES + RED_BYTES + CPB * N3 * 8 <= SMEM_MAX ? CPB * N3 * 8 : 0;
     static constexpr int SMEM = CPB * CELL_BYTES + RED_BYTES + STAGE_BYTES;  // cubes + reduction scratch + staging
-    __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
+    static constexpr bool FITS = CPB * CELL_BYTES + RED_BYTES <= SMEM_MAX;
+    __device__ static int at(int i1, int i2, int i3) {
+        return PAD ? (i1 * N + i2) * ROW + i3 : (i1 * N + i2) * N + (i3 ^ (i2 & 7));
+    }
 };
 
 // in-place FFT of every line along AXIS of the CPB cubes in shared memory
@@ -56,16 +67,15 @@ __device__ __forceinline__ void smem_axis_pass(double2* sm) {
     for (int r = threadIdx.x; r < F::CPB * N * N; r += F::THREADS) {
         const int c = r / (N * N), q = r % (N * N), a = q / N, b = q % N;
         double2* base = sm + c * F::CELL;
-        int off, stride;
-        if (AXIS == 2) { off = F::at(a, b, 0); stride = 1; }
-        else if (AXIS == 1) { off = F::at(a, 0, b); stride = F::ROW; }
-        else { off = F::at(0, a, b); stride = N * F::ROW; }
+        auto pos = [&](int j) {
+            return AXIS == 2 ? F::at(a, b, j) : AXIS == 1 ? F::at(a, j, b) : F::at(j, a, b);
+        };
         double2 x[N];
 #pragma unroll
-        for (int j = 0; j < N; ++j) x[j] = base[off + j * stride];
+        for (int j = 0; j < N; ++j) x[j] = base[pos(j)];
         RegFFT<N, SIGN, N>::run(x);
 #pragma unroll
-        for (int j = 0; j < N; ++j) base[off + j * stride] = x[j];
+        for (int j = 0; j < N; ++j) base[pos(j)] = x[j];
     }
 }
 
@@ -109,7 +119,7 @@ k_fwd_fused(const double* __restrict__ f, double2* __restrict__ A, long long nce
     extern __shared__ __align__(16) double2 sm[];
     double* stage = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + F::CPB * F::CELL_BYTES + F::RED_BYTES);
     const long long cell0 = (long long)blockIdx.x * F::CPB;
-    const bool staged = (reinterpret_cast<uintptr_t>(f) & 15) == 0;
+    const bool staged = F::STAGE_BYTES > 0 && (reinterpret_cast<uintptr_t>(f) & 15) == 0;
     if (staged) {
         stage_cells<N>(stage, f, cell0, ncells);
         cp_async_wait_all();
@@ -171,7 +181,7 @@ k_inv_project(const double2* __restrict__ B, const double* __restrict__ base, do
     // every load of the tile in flight at once: the cube, then the RK2 base
     // (which is only needed after the transform and the projection)
     stage_group<N>(sm, B, g, lane0);
-    const bool staged = base && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
+    const bool staged = F::STAGE_BYTES > 0 && base && (reinterpret_cast<uintptr_t>(base) & 15) == 0;
     if (staged) {
         stage_cells<N>(stage, base, cell0, ncells);
         cp_async_wait_1();
