@@ -1,5 +1,5 @@
 // fused.cuh -- single-kernel K1 and K3 for grids whose N^3 cube fits in shared
-// memory (N <= 16): one CTA owns CPB whole cells, does all three FFT axes in
+// memory (N <= 24): one CTA owns CPB whole cells, does all three FFT axes in
 // shared memory, and touches HBM exactly once per operand.
 //
 //   k_fwd_fused:     user f [cell][N^3]  -> group fhat (forward, fourier.hpp:11-12)
@@ -9,7 +9,7 @@
 //
 // HBM traffic per cell (N=16): forward 32 KiB in + 64 KiB out; inverse+project
 // 64 KiB in + 32 KiB base + 32 KiB out -- versus 3 read+write sweeps each for
-// the multi-pass path (transforms.cuh), which remains for N = 24, 32.
+// the multi-pass path (transforms.cuh), which remains for N = 32.
 //
 // Shared layout per cell: [i1][i2][i3] complex with rows padded to N+1 so the
 // three axis passes are bank-conflict free for 16 B accesses.

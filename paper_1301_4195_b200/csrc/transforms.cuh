@@ -105,7 +105,7 @@ k_fft_pass(const double* __restrict__ fuser, double2* __restrict__ A, double* __
 //   Q   = Qt - C^T (C C^T)^{-1} C Qt        (C rows: w, v1 w, v2 w, v3 w, |v|^2 w)
 //   out = base + coef * Q    (base == nullptr -> out = coef * Q)
 // Qt comes in the group layout (real), out/base are in the user layout [cell][N^3].
-// ---- K3 epilogue for grids whose cube does not fit in shared memory (N = 24, 32):
+// ---- K3 epilogue for grids whose cube does not fit in shared memory (N = 32; also conserve()):
 // two launches over (cell octet) x (node slice) blocks so that every SM works
 // (one block per 32-cell group left most of the GPU idle: 10% of an N=24 step).
 //   k_project_moments: partial moments of each slice   -> part[cell][slice][5]
