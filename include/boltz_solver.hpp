@@ -83,7 +83,9 @@ class DeviceArray {
 public:
     DeviceArray() = default;
     explicit DeviceArray(size_t n) : n_(n) { cuda_check(cudaMalloc(&p_, n * sizeof(T))); }
-    ~DeviceArray() { cudaFree(p_); }
+    ~DeviceArray() {
+        if (p_) cudaFree(p_);  // cudaFree(nullptr) is still illegal while a stream is capturing
+    }
     DeviceArray(const DeviceArray&) = delete;
     DeviceArray& operator=(const DeviceArray&) = delete;
     DeviceArray(DeviceArray&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
@@ -91,6 +93,10 @@ public:
         std::swap(p_, o.p_);
         std::swap(n_, o.n_);
         return *this;
+    }
+    void swap(DeviceArray& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
     }
     T* data() { return p_; }
     const T* data() const { return p_; }
@@ -160,11 +166,11 @@ public:
             check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
                                        dx_ext_.data(), h, wl, wr, s_));
         } else {
-            std::swap(field_, tmp_);  // field = t1, tmp = f^n
+            field_.swap(tmp_);  // field = t1, tmp = f^n
             fill_ghosts(exchange);
             check(boltz_transport_step(op_.handle(), field_.data(), tmp_.data(), 0.5, tmp2_.data(), ncl_,
                                        x_ext_.data(), dx_ext_.data(), h, wl, wr, s_));
-            std::swap(tmp2_, field_);  // field = out, tmp2 = t1
+            tmp2_.swap(field_);  // field = out, tmp2 = t1
         }
     }
 
@@ -224,6 +230,81 @@ public:
 
     double sigma_w(int side) const { return sigma_w_[side]; }
 
+    // `steps` Strang steps with the device queue kept full: one eager step (the
+    // library allocates its workspace and sets kernel attributes lazily, which
+    // cannot happen under capture), then capture() + advance(steps - 1).
+    void run(double dt, int steps) {
+        if (steps < 4 || !s_) {
+            for (int i = 0; i < steps; ++i) strang_step(dt);
+            return;
+        }
+        strang_step(dt);
+        capture(dt);
+        advance(steps - 1);
+    }
+
+    // CUDA-graph replay: capture three Strang steps of size
+    // dt on the solver's stream (three steps bring the field / scratch rotation
+    // back to its start), with the library in asynchronous mode.  Needs a
+    // non-default stream and one eager step first (see run()).  The NCCL halo
+    // is captured too when world > 1.  Does not advance the state.
+    void capture(double dt) {
+        if (!s_) throw Error(BOLTZ_ERR_CONFIG, "capture: the solver needs a non-default stream");
+        const double* p0[3] = {field_.data(), tmp_.data(), tmp2_.data()};
+        check(boltz_set_async(op_.handle(), 1));
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(s_, cudaStreamCaptureModeThreadLocal));
+        try {
+            for (int i = 0; i < 3; ++i) {
+                transport(0.5 * dt);
+                collide(dt);
+                transport(0.5 * dt);
+            }
+        } catch (...) {
+            cudaStreamEndCapture(s_, &g);
+            if (g) cudaGraphDestroy(g);
+            boltz_set_async(op_.handle(), 0);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(s_, &g));
+        check(boltz_set_async(op_.handle(), 0));
+        if (field_.data() != p0[0] || tmp_.data() != p0[1] || tmp2_.data() != p0[2]) {
+            cudaGraphDestroy(g);
+            throw Error(BOLTZ_ERR_CONFIG, "capture: buffer rotation did not close after 3 steps");
+        }
+        if (exec_) cudaGraphExecDestroy(exec_);
+        exec_ = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec_, g, 0);
+        cudaGraphDestroy(g);
+        cuda_check(e);
+        graph_dt_ = dt;
+    }
+
+    // `steps` Strang steps of the captured dt: graph replays + eager remainder;
+    // numeric errors are reported once, at the end (boltz_sync)
+    void advance(int steps) {
+        if (!exec_) throw Error(BOLTZ_ERR_CONFIG, "advance: capture() first");
+        check(boltz_set_async(op_.handle(), 1));
+        try {
+            for (int i = 0; i < steps / 3; ++i) {
+                cuda_check(cudaGraphLaunch(exec_, s_));
+                t_ += 3 * graph_dt_;
+            }
+            for (int i = 0; i < steps % 3; ++i) strang_step(graph_dt_);
+            check(boltz_sync(op_.handle(), s_));
+        } catch (...) {
+            boltz_set_async(op_.handle(), 0);
+            throw;
+        }
+        check(boltz_set_async(op_.handle(), 0));
+    }
+
+    ~Solver1D() {
+        if (exec_) cudaGraphExecDestroy(exec_);
+    }
+    Solver1D(const Solver1D&) = delete;
+    Solver1D& operator=(const Solver1D&) = delete;
+
 private:
     CollisionOperator& op_;
     int64_t n3_;
@@ -238,6 +319,8 @@ private:
     double sigma_w_[2] = {0, 0};
     std::vector<double> dx_host_;
     DeviceArray<double> x_ext_, dx_ext_, field_, tmp_, tmp2_, red_;
+    cudaGraphExec_t exec_ = nullptr;
+    double graph_dt_ = 0;
 };
 
 // One Strang step of n virtual ranks of one device (loopback backend,

@@ -7,6 +7,8 @@
 //     MODE nccl:     one rank, an NCCL communicator of world 1 (exchange is
 //                    then a no-op; allreduce of the ledger is exercised)
 //     MODE loopback: NRANKS virtual ranks of one device
+//     MODE graph:    one rank on its own stream: one eager step, then 3 Strang
+//                    steps captured in a CUDA graph and replayed (Solver1D::run)
 //   writes DIR/out_<MODE>_<NRANKS>.bin (Nx x N^3) and prints the ledger.
 #include <cstdio>
 #include <cstdlib>
@@ -64,6 +66,17 @@ int main(int argc, char** argv) {
                 cuda_check(cudaDeviceSynchronize());
             }
             check(boltz_halo_destroy(halo));
+        } else if (mode == "graph") {
+            cudaStream_t st;
+            cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            {
+                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, nullptr, st);
+                led0 = s.ledger();
+                s.run(dt, steps);
+                led1 = s.ledger();
+                s.download(out);
+            }
+            cuda_check(cudaStreamDestroy(st));
         } else {
             const auto plan = plan_decomposition((int64_t)nx, nranks);
             std::vector<std::unique_ptr<Solver1D>> ranks;

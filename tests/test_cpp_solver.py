@@ -2,7 +2,8 @@
 loopback and NCCL halo, over the C ABI) compiles on CPU and, on a GPU,
 reproduces the Python driver (paper_1301_4195_b200/solver.py) bit for bit --
 the same kernels in the same order -- for 1 rank with an NCCL communicator and
-for 3 loopback ranks (decomposition transparency)."""
+for 3 loopback ranks (decomposition transparency), and with
+CUDA-graph replay of the Strang step (7 steps = 1 eager + 2 replays)."""
 import pathlib
 import subprocess
 
@@ -51,7 +52,7 @@ def test_cpp_solver_matches_python_driver(gpu, tmp_path):
     from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, scenarios
     from paper_1301_4195_b200.solver import Boundary, Solver1D
     _compile()
-    n, L, lam, Tw, nx, steps = 8, 5.0, 1.0, 2.0, 10, 3
+    n, L, lam, Tw, nx, steps = 8, 5.0, 1.0, 2.0, 10, 7
     grid = VelocityGrid.create(n, L)
     x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
     f0 = scenarios.mixture_cells(grid, nx, seed=17)
@@ -65,7 +66,7 @@ def test_cpp_solver_matches_python_driver(gpu, tmp_path):
             s.strang_step(dt)
         ref = s.interior.cpu().numpy()
     torch.cuda.synchronize()
-    for mode, nranks in [("nccl", 1), ("loopback", 3)]:
+    for mode, nranks in [("nccl", 1), ("loopback", 3), ("graph", 1)]:
         r = subprocess.run([str(EXE), str(tmp_path), str(n), repr(L), repr(lam), repr(Tw), repr(dt), str(steps),
                             str(nranks), mode], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
