@@ -138,9 +138,34 @@ def cpu_baseline(seconds, threads=None):
         el = time.perf_counter() - t0
         if el >= seconds or ev >= 100000:
             break
+    # the reference's bench_collision table (Tables 1-4):
+    # median wall time of one collide() per worker count, ratio to the previous
+    # row and total speed-up over 1 worker
+    def table(n, L, Gt, fs):
+        rows, t1, prev = [], None, None
+        w = 1
+        while w <= threads:
+            reps = []
+            for r in range(3):
+                t0 = time.perf_counter()
+                O.collide(n, L, Gt, fs[r], 1.0, nthreads=w)
+                reps.append(time.perf_counter() - t0)
+            t = sorted(reps)[1]
+            t1 = t1 or t
+            rows.append({"cores": w, "time": t, "ratio": (prev / t) if prev else 1.0, "total_speedup": t1 / t})
+            prev = t
+            w *= 2
+        return {"columns": "cores,time,ratio,total_speedup", "N": n, "L": L, "rows": rows}
+
+    tables = [table(N_VEL, L_VEL, G, cells)]
+    del G
+    g24 = VelocityGrid.create(24, 8.0)  # cfg4's grid (Tables 2/4 are N=24)
+    G24 = O.generate_table(24, 8.0, LAM, nthreads=threads)
+    tables.append(table(24, 8.0, G24, scenarios.mixture_cells(g24, 3, seed=4195)))
     return {"value": ev / el, "unit": "evals/s", "cores": threads, "kind": "port",
             "sample": f"{ev} single-cell collide() evals at N=16 (cfg2 cells 0..63, OpenMP over zeta_k, "
-                      f"{threads} threads, {el:.1f} s)"}
+                      f"{threads} threads, {el:.1f} s)",
+            "tables_1_4": tables}
 
 
 def run_reference(args, rank, world):
