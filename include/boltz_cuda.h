@@ -128,6 +128,26 @@ int boltz_transport_step(boltz_ctx* ctx, const double* field, const double* base
                          int wall_right, void* stream);
 
 /*
+ * The halo exchange fused into the transport step (B200 peer memory; no
+ * reference counterpart -- it replaces transport_step + halo_exchange,
+ * SPEC.md:342-350,446-453).  Same step as boltz_transport_step, plus: the
+ * updated cells 2,3 are also stored at left_dst (the left rank's output field
+ * + (ncl_left + 2) * N^3, i.e. its right ghosts) and cells ncl, ncl+1 at
+ * right_dst (the right rank's output field, i.e. its left ghosts 0,1); null =
+ * no neighbour.  This rank's own ghost rows of `out` are not written (its
+ * neighbours and boltz_fill_boundary own them).  Pointers are device or peer
+ * (cudaDeviceEnablePeerAccess / IPC) addresses.  The caller orders each step
+ * after the neighbours' previous step (events) -- see include/boltz_solver.hpp.
+ */
+int boltz_transport_step_peer(boltz_ctx* ctx, const double* field, const double* base, double alpha, double* out,
+                              int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                              int wall_right, double* left_dst, double* right_dst, void* stream);
+/* the collision step's half of the fused exchange: interior cells 0,1 ->
+ * left_dst, ncells-2, ncells-1 -> right_dst (addressing as above) */
+int boltz_store_edges(boltz_ctx* ctx, const double* interior, int64_t ncells, double* left_dst, double* right_dst,
+                      void* stream);
+
+/*
  * Boundary-flux ledger (reference SPEC.md:403 "conservation ledger ... vs
  * wall-flux integral"; RunRecord): acc5[a] += coef * (F_a(right face) -
  * F_a(left face)) for the 5 collision invariants (mass, momentum 1-3, energy

@@ -117,6 +117,7 @@ public:
              double epsilon = 1.0, boltz_halo* halo = nullptr, cudaStream_t stream = nullptr)
         : op_(op), n3_((int64_t)n * n * n), L_(half_width), rank_(rank), world_(world), left_(left), right_(right),
           eps_(epsilon), halo_(halo), s_(stream) {
+        cuda_check(cudaGetDevice(&device_));
         const auto plan = plan_decomposition((int64_t)x.size(), world);
         start_ = plan[rank].first;
         ncl_ = plan[rank].second;
@@ -149,12 +150,49 @@ public:
     // exchanged already) and the physical ends of the end ranks
     void fill_ghosts(bool exchange = true) {
         if (exchange && halo_) check(boltz_halo_exchange(halo_, field_.data(), ncl_, n3_, s_));
+        fill_physical(field_.data());
+    }
+
+    // ghosts of the physical ends (wall / extrapolation) of `buf`, on the end ranks
+    void fill_physical(double* buf) {
         if (rank_ == 0)
-            check(boltz_fill_boundary(op_.handle(), field_.data(), ncl_, x_ext_.data(), 0, left_.kind, left_.Tw,
+            check(boltz_fill_boundary(op_.handle(), buf, ncl_, x_ext_.data(), 0, left_.kind, left_.Tw,
                                       left_.Vw.data(), &sigma_w_[0], s_));
         if (rank_ == world_ - 1)
-            check(boltz_fill_boundary(op_.handle(), field_.data(), ncl_, x_ext_.data(), 1, right_.kind, right_.Tw,
+            check(boltz_fill_boundary(op_.handle(), buf, ncl_, x_ext_.data(), 1, right_.kind, right_.Tw,
                                       right_.Vw.data(), &sigma_w_[1], s_));
+    }
+
+    // ---- fused peer-memory halo (PeerGroup) ----
+    // stage inputs / outputs BEFORE the stage runs (stage 1 rotates afterwards)
+    double* stage_in(int stage) { return stage == 0 ? field_.data() : tmp_.data(); }
+    double* stage_out(int stage) { return stage == 0 ? tmp_.data() : tmp2_.data(); }
+    cudaStream_t stream() const { return s_; }
+    int device() const { return device_; }
+    boltz_ctx* op_handle() { return op_.handle(); }
+
+    // one transport stage with the exchange fused into the kernel: the updated
+    // edge cells go straight into the neighbours' stage outputs (left_dst /
+    // right_dst); this rank's ghosts were written by its neighbours' previous op
+    void transport_stage_peer(int stage, double h, double* left_dst, double* right_dst) {
+        if (h * L_ > dx_min_ * (1 + 1e-12)) throw Error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
+        const int wl = rank_ == 0 && left_.is_wall(), wr = rank_ == world_ - 1 && right_.is_wall();
+        double* in = stage_in(stage);
+        fill_physical(in);
+        check(boltz_transport_step_peer(op_.handle(), in, stage ? field_.data() : nullptr, stage ? 0.5 : 0.0,
+                                        stage_out(stage), ncl_, x_ext_.data(), dx_ext_.data(), h, wl, wr, left_dst,
+                                        right_dst, s_));
+        if (stage == 1) {
+            field_.swap(tmp_);
+            tmp2_.swap(field_);
+        }
+    }
+
+    // the collision step + its half of the exchange: the post-collision edge
+    // cells into the neighbours' fields' ghosts
+    void collide_peer(double dt, double* left_dst, double* right_dst) {
+        collide(dt);
+        check(boltz_store_edges(op_.handle(), interior(), ncl_, left_dst, right_dst, s_));
     }
 
     // SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
@@ -310,6 +348,7 @@ private:
     int64_t n3_;
     double L_;
     int rank_, world_;
+    int device_ = 0;
     Boundary left_, right_;
     double eps_;
     boltz_halo* halo_;
@@ -321,6 +360,94 @@ private:
     DeviceArray<double> x_ext_, dx_ext_, field_, tmp_, tmp2_, red_;
     cudaGraphExec_t exec_ = nullptr;
     double graph_dt_ = 0;
+};
+
+// One process driving the ranks of a sharded domain in lockstep -- several
+// GPUs of one box (peer access over NVLink / NVSwitch) or virtual ranks of one
+// device -- with the halo exchange fused into the transport kernel: every
+// transport stage stores its updated edge cells straight into the neighbours'
+// stage outputs, and the collision step stores its edge cells into the
+// neighbours' fields (boltz_transport_step_peer / boltz_store_edges), so no
+// separate exchange runs at all.  Ordering is by CUDA events only: before op t
+// a rank's stream waits for its neighbours' op t-1 (two events per rank, by
+// op parity), which covers both the ghosts it reads (RAW) and the ghosts it
+// writes next door (their readers finished, WAR).  Each rank needs its own
+// CollisionOperator (workspace) and its own stream.
+class PeerGroup {
+public:
+    explicit PeerGroup(std::vector<Solver1D*> ranks) : r_(std::move(ranks)) {
+        if (r_.empty()) throw Error(BOLTZ_ERR_CONFIG, "PeerGroup: no ranks");
+        ev_.resize(2 * r_.size());
+        for (size_t i = 0; i < r_.size(); ++i) {
+            if (!r_[i]->stream()) throw Error(BOLTZ_ERR_CONFIG, "PeerGroup: every rank needs its own stream");
+            cuda_check(cudaSetDevice(r_[i]->device()));
+            for (int p = 0; p < 2; ++p) cuda_check(cudaEventCreateWithFlags(&ev_[2 * i + p], cudaEventDisableTiming));
+            for (int d : {-1, 1}) {  // peer access to the neighbours' devices
+                const long j = (long)i + d;
+                if (j < 0 || j >= (long)r_.size() || r_[j]->device() == r_[i]->device()) continue;
+                const cudaError_t e = cudaDeviceEnablePeerAccess(r_[j]->device(), 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e);
+                cudaGetLastError();
+            }
+        }
+        // the first op's ghosts: every rank's edge cells into its neighbours' fields
+        op([](size_t, double*, double*) {}, Kind::Prime);
+    }
+    ~PeerGroup() {
+        for (cudaEvent_t e : ev_) cudaEventDestroy(e);
+    }
+    PeerGroup(const PeerGroup&) = delete;
+    PeerGroup& operator=(const PeerGroup&) = delete;
+
+    void strang_step(double dt) {
+        for (int half = 0; half < 2; ++half) {
+            for (int stage = 0; stage < 2; ++stage)
+                op([&](size_t i, double* l, double* r) { r_[i]->transport_stage_peer(stage, 0.5 * dt, l, r); },
+                   stage == 0 ? Kind::Stage0 : Kind::Stage1);
+            if (half == 0) op([&](size_t i, double* l, double* r) { r_[i]->collide_peer(dt, l, r); }, Kind::Collide);
+        }
+        for (auto* s : r_) s->advance_time(dt);
+    }
+
+private:
+    enum class Kind { Prime, Stage0, Stage1, Collide };
+
+    // destinations (from the neighbours' pointers before anyone rotates), then
+    // per rank: wait for the neighbours' previous op, run, record
+    template <typename F>
+    void op(F&& run, Kind k) {
+        const size_t R = r_.size();
+        std::vector<double*> L(R, nullptr), Rt(R, nullptr);
+        for (size_t i = 0; i < R; ++i) {
+            auto target = [&](size_t j) {
+                return (k == Kind::Stage0) ? r_[j]->stage_out(0) : (k == Kind::Stage1) ? r_[j]->stage_out(1)
+                                                                                       : r_[j]->field();
+            };
+            if (i > 0) L[i] = target(i - 1) + (r_[i - 1]->ncl() + 2) * r_[i - 1]->cell_values();
+            if (i + 1 < R) Rt[i] = target(i + 1);
+        }
+        const int prev = parity_ ^ 1;
+        for (size_t i = 0; i < R; ++i) {
+            cuda_check(cudaSetDevice(r_[i]->device()));
+            if (started_) {
+                if (i > 0) cuda_check(cudaStreamWaitEvent(r_[i]->stream(), ev_[2 * (i - 1) + prev], 0));
+                if (i + 1 < R) cuda_check(cudaStreamWaitEvent(r_[i]->stream(), ev_[2 * (i + 1) + prev], 0));
+            }
+            if (k == Kind::Prime)
+                check(boltz_store_edges(r_[i]->op_handle(), r_[i]->interior(), r_[i]->ncl(), L[i], Rt[i],
+                                        r_[i]->stream()));
+            else
+                run(i, L[i], Rt[i]);
+            cuda_check(cudaEventRecord(ev_[2 * i + parity_], r_[i]->stream()));
+        }
+        started_ = true;
+        parity_ ^= 1;
+    }
+
+    std::vector<Solver1D*> r_;
+    std::vector<cudaEvent_t> ev_;
+    int parity_ = 0;
+    bool started_ = false;
 };
 
 // One Strang step of n virtual ranks of one device (loopback backend,

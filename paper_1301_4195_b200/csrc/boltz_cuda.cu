@@ -1000,6 +1000,47 @@ int boltz_transport_step(boltz_ctx* c, const double* field, const double* base, 
     });
 }
 
+int boltz_transport_step_peer(boltz_ctx* c, const double* field, const double* base, double alpha, double* out,
+                              int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                              int wall_right, double* left_dst, double* right_dst, void* stream) {
+    return api(c, [&] {
+        if (ncl < 2 || !field || !out || !x_ext || !dx_ext || out == field || (base && out == base)) {
+            set_error("transport_step_peer: invalid arguments (out must not alias field/base, ncl >= 2)");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_transport(c->n, field, base, base ? alpha : 0.0, out, ncl, x_ext, dx_ext, dt, wall_left,
+                             wall_right, c->pc.dv, s, 1, left_dst, right_dst);
+        }
+        CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;
+        CK(cudaStreamSynchronize(s));
+        if (c->timing) collect_timing(c);
+        return BOLTZ_OK;
+    });
+}
+
+int boltz_store_edges(boltz_ctx* c, const double* interior, int64_t ncells, double* left_dst, double* right_dst,
+                      void* stream) {
+    return api(c, [&] {
+        if (ncells < 2 || !interior) {
+            set_error("store_edges: need >= 2 interior cells");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_store_edges(c->n, interior, ncells, left_dst, right_dst, s);
+        }
+        CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;
+        CK(cudaStreamSynchronize(s));
+        return BOLTZ_OK;
+    });
+}
+
 int boltz_end_flux(boltz_ctx* c, const double* field, int64_t ncl, const double* x_ext, const double* dx_ext,
                    int wall_left, int wall_right, double coef, double* acc5, void* stream) {
     return api(c, [&] {

@@ -52,23 +52,63 @@ __device__ __forceinline__ void face_fluxes(const double* __restrict__ f, long l
 // grid = (ceil(N^3/256), ncl + 4); ghosts are copied through.
 // out = alpha*base + (1-alpha)*(f - dt/dx (F_{j+1/2} - F_{j-1/2}))   (base may be null)
 // -- the second stage of the SSP-RK2 transport sub-step fused in.
+// Peer mode (peer != 0) fuses the halo exchange into the step: the two first
+// and two last updated interior cells are also stored straight into the
+// neighbours' output fields (left_dst: the left rank's ghosts ncl_L+2, ncl_L+3;
+// right_dst: the right rank's ghosts 0, 1 -- peer memory over NVLink, or
+// another field of the same device), and this rank's own ghost rows are NOT
+// written (its neighbours and boltz_fill_boundary own them).
 template <int N>
 __global__ void __launch_bounds__(256)
 k_transport(const double* __restrict__ f, const double* __restrict__ base, double alpha, double* __restrict__ out,
             long long ncl, const double* __restrict__ x, const double* __restrict__ dx, double dt, int wl, int wr,
-            double dv) {
+            double dv, int peer, double* __restrict__ left_dst, double* __restrict__ right_dst) {
     constexpr int N3 = N * N * N;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const long long ce = blockIdx.y;
     if (j >= N3) return;
     if (ce < 2 || ce > ncl + 1) {
-        out[ce * N3 + j] = f[ce * N3 + j];
+        if (!peer) out[ce * N3 + j] = f[ce * N3 + j];
         return;
     }
     double fc, Fl, Fr;
     face_fluxes<N>(f, ce, j, ncl, x, dx, wl, wr, dv, fc, Fl, Fr);
     const double upd = fc - dt / dx[ce] * (Fr - Fl);
-    out[ce * N3 + j] = base ? alpha * base[ce * N3 + j] + (1.0 - alpha) * upd : upd;
+    const double v = base ? alpha * base[ce * N3 + j] + (1.0 - alpha) * upd : upd;
+    out[ce * N3 + j] = v;
+    if (left_dst && ce < 4) left_dst[(ce - 2) * N3 + j] = v;
+    if (right_dst && ce >= ncl) right_dst[(ce - ncl) * N3 + j] = v;
+}
+
+// the collision step's half of the fused exchange: cells 0,1 and n-2,n-1 of a
+// rank's interior batch -> the neighbours' ghosts (same addressing as above)
+template <int N>
+__global__ void __launch_bounds__(256)
+k_store_edges(const double* __restrict__ interior, long long n, double* __restrict__ left_dst,
+              double* __restrict__ right_dst) {
+    constexpr int N3 = N * N * N;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int e = blockIdx.y;  // 0,1: left edge cells; 2,3: right edge cells
+    if (j >= N3) return;
+    if (e < 2) {
+        if (left_dst) left_dst[(size_t)e * N3 + j] = interior[(size_t)e * N3 + j];
+    } else if (right_dst) {
+        right_dst[(size_t)(e - 2) * N3 + j] = interior[(size_t)(n - 4 + e) * N3 + j];
+    }
+}
+
+inline void launch_store_edges(int n, const double* interior, long long ncells, double* left_dst, double* right_dst,
+                               cudaStream_t s) {
+    switch (n) {
+#define BOLTZ_SE(N)                                                                                  \
+    case N: {                                                                                        \
+        dim3 grid((N * N * N + 255) / 256, 4);                                                       \
+        k_store_edges<N><<<grid, 256, 0, s>>>(interior, ncells, left_dst, right_dst);                \
+    } break;
+        BOLTZ_FOR_EACH_N(BOLTZ_SE)
+#undef BOLTZ_SE
+        default: break;
+    }
 }
 
 // Boundary-flux ledger: acc[a] += coef * (F_a(right end face) - F_a(left end face))
@@ -193,12 +233,14 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
 
 inline void launch_transport(int n, const double* f, const double* base, double alpha, double* out, long long ncl,
                              const double* x, const double* dx, double dt, int wl, int wr, double dv,
-                             cudaStream_t s) {
+                             cudaStream_t s, int peer = 0, double* left_dst = nullptr,
+                             double* right_dst = nullptr) {
     switch (n) {
 #define BOLTZ_TR(N)                                                                                        \
     case N: {                                                                                              \
         dim3 grid((N * N * N + 255) / 256, (unsigned)(ncl + 4));                                          \
-        k_transport<N><<<grid, 256, 0, s>>>(f, base, alpha, out, ncl, x, dx, dt, wl, wr, dv);              \
+        k_transport<N><<<grid, 256, 0, s>>>(f, base, alpha, out, ncl, x, dx, dt, wl, wr, dv, peer, left_dst, \
+                                            right_dst);                                                    \
     } break;
         BOLTZ_FOR_EACH_N(BOLTZ_TR)
 #undef BOLTZ_TR

@@ -7,6 +7,8 @@
 //     MODE nccl:     one rank, an NCCL communicator of world 1 (exchange is
 //                    then a no-op; allreduce of the ledger is exercised)
 //     MODE loopback: NRANKS virtual ranks of one device
+//     MODE peer:     NRANKS ranks of one device, each with its own context and
+//                    stream, halo fused into the transport kernels (PeerGroup)
 //     MODE graph:    one rank on its own stream: one eager step, then 3 Strang
 //                    steps captured in a CUDA graph and replayed (Solver1D::run)
 //   writes DIR/out_<MODE>_<NRANKS>.bin (Nx x N^3) and prints the ledger.
@@ -66,6 +68,29 @@ int main(int argc, char** argv) {
                 cuda_check(cudaDeviceSynchronize());
             }
             check(boltz_halo_destroy(halo));
+        } else if (mode == "peer") {
+            const auto plan = plan_decomposition((int64_t)nx, nranks);
+            std::vector<std::unique_ptr<CollisionOperator>> ops;
+            std::vector<std::unique_ptr<Solver1D>> ranks;
+            std::vector<cudaStream_t> streams(nranks);
+            std::vector<Solver1D*> ptrs;
+            for (int r = 0; r < nranks; ++r) {
+                cuda_check(cudaStreamCreateWithFlags(&streams[r], cudaStreamNonBlocking));
+                ops.push_back(std::make_unique<CollisionOperator>(n, L, k, CollisionOperator::Generated{}));
+                std::span<const double> f0r(f0.data() + plan[r].first * n3, plan[r].second * n3);
+                ranks.push_back(std::make_unique<Solver1D>(*ops.back(), n, L, x, dx, f0r, r, nranks, left, right, 1.0,
+                                                           nullptr, streams[r]));
+                ptrs.push_back(ranks.back().get());
+            }
+            {
+                PeerGroup group(ptrs);
+                for (int i = 0; i < steps; ++i) group.strang_step(dt);
+            }
+            for (int r = 0; r < nranks; ++r)
+                ptrs[r]->download(std::span<double>(out.data() + plan[r].first * n3, plan[r].second * n3));
+            ranks.clear();
+            ops.clear();
+            for (auto st : streams) cuda_check(cudaStreamDestroy(st));
         } else if (mode == "graph") {
             cudaStream_t st;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

@@ -3,7 +3,9 @@ loopback and NCCL halo, over the C ABI) compiles on CPU and, on a GPU,
 reproduces the Python driver (paper_1301_4195_b200/solver.py) bit for bit --
 the same kernels in the same order -- for 1 rank with an NCCL communicator and
 for 3 loopback ranks (decomposition transparency), and with
-CUDA-graph replay of the Strang step (7 steps = 1 eager + 2 replays)."""
+CUDA-graph replay of the Strang step (7 steps = 1 eager + 2 replays), and with
+the halo fused into the transport kernels (PeerGroup, 3 and 5 ranks with their
+own contexts and streams on one device)."""
 import pathlib
 import subprocess
 
@@ -66,7 +68,7 @@ def test_cpp_solver_matches_python_driver(gpu, tmp_path):
             s.strang_step(dt)
         ref = s.interior.cpu().numpy()
     torch.cuda.synchronize()
-    for mode, nranks in [("nccl", 1), ("loopback", 3), ("graph", 1)]:
+    for mode, nranks in [("nccl", 1), ("loopback", 3), ("graph", 1), ("peer", 3), ("peer", 5)]:
         r = subprocess.run([str(EXE), str(tmp_path), str(n), repr(L), repr(lam), repr(Tw), repr(dt), str(steps),
                             str(nranks), mode], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
