@@ -7,6 +7,6 @@ reference API over that ABI (boltz.py), synthetic inputs for the configs
 (solver.py).
 """
 from .boltz import (  # noqa: F401
-    BoltzError, CollisionOperator, ConfigError, CudaError, IoError, KernelSpec, NumericError, VelocityGrid,
+    BoltzError, CollisionOperator, ConfigError, CudaError, IoError, KernelSpec, NcclHalo, NumericError, VelocityGrid,
     generate_table, lib, load_table, save_table, weight,
 )

@@ -103,6 +103,11 @@ def lib():
             "boltz_weight": (d, [d, d, d, vp, vp, i]),
             "boltz_save_table": (i, [C.c_char_p, i, d, d, d, d, i, vp]),
             "boltz_load_table": (i, [C.c_char_p, i, d, d, d, d, i, vp]),
+            "boltz_halo_unique_id": (i, [vp]),
+            "boltz_halo_create": (i, [i, i, vp, i, C.POINTER(vp)]),
+            "boltz_halo_destroy": (i, [vp]),
+            "boltz_halo_exchange": (i, [vp, vp, i64, i64, vp]),
+            "boltz_halo_allreduce_sum": (i, [vp, vp, i64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -216,6 +221,56 @@ def fp64_peak(device: int = 0, seconds: float = 0.5) -> float:
     t = C.c_double()
     _check(lib().boltz_fp64_peak(device, seconds, C.byref(t)))
     return t.value
+
+
+# --------------------------------------------------------------- halo
+class NcclHalo:
+    """The C ABI's NCCL halo (boltz_halo_*, csrc/halo.cpp): one grouped
+    send/recv of the two edge cells per neighbour on the caller's stream, plus
+    the ledger all-reduce.  Rank 0's communicator id is broadcast over
+    torch.distributed (any backend).  Unlike torch.distributed P2P it can be
+    captured in a CUDA graph, so Solver1D.run replays multi-rank steps too.
+    Import torch before creating one (the library then binds torch's NCCL)."""
+
+    def __init__(self, rank: int, world: int, device: int = 0):
+        import torch  # noqa: F401  (NCCL binding order, csrc/halo.cpp)
+        self.rank, self.world = rank, world
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib().boltz_halo_unique_id(uid))
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0)
+            uid = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().boltz_halo_create(rank, world, uid, device, C.byref(h)))
+        self._h = h
+
+    def exchange(self, field) -> int:
+        """Refresh the 2+2 halo ghosts of a (ncl+4, N^3) CUDA field (collective)."""
+        import torch
+        s = torch.cuda.current_stream(field.device).cuda_stream
+        _check(lib().boltz_halo_exchange(self._h, C.c_void_p(field.data_ptr()), field.shape[0] - 4, field.shape[1],
+                                         C.c_void_p(s)))
+        return (self.rank > 0) + (self.rank < self.world - 1)
+
+    def all_reduce(self, t) -> None:
+        """In-place sum over ranks of a float64 CUDA tensor (collective)."""
+        import torch
+        s = torch.cuda.current_stream(t.device).cuda_stream
+        _check(lib().boltz_halo_allreduce_sum(self._h, C.c_void_p(t.data_ptr()), t.numel(), C.c_void_p(s)))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _check(lib().boltz_halo_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------ operator

@@ -26,7 +26,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .boltz import CollisionOperator, ConfigError, NumericError
+from .boltz import CollisionOperator, ConfigError, NcclHalo, NumericError
 from .scenarios import extend_ghosts
 
 
@@ -161,8 +161,11 @@ class Solver1D:
         dx = self.dx_ext[2:self.ncl + 2]
         tot = torch.stack([(m[:, 0] * dx).sum(), (m[:, 1] * dx).sum(), (m[:, 4] * dx).sum()])
         if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(tot)
+            if hasattr(self.halo, "all_reduce"):
+                self.halo.all_reduce(tot)
+            else:
+                import torch.distributed as dist
+                dist.all_reduce(tot)
         return tot.cpu().numpy()
 
     def cfl_dt(self, cfl: float = 0.9) -> float:
@@ -241,11 +244,13 @@ class Solver1D:
 
     def run(self, dt: float, steps: int, graph: bool = True) -> None:
         """`steps` Strang steps with the device queue kept full: the library runs
-        asynchronously (boltz_set_async) and, on a single rank, three steps are
-        captured once in a CUDA graph and replayed (three steps return the
-        field / scratch buffer rotation to its start).  Numeric errors are
-        reported once, at the end (boltz_sync)."""
-        if not graph or self.world > 1 or steps < 4:
+        asynchronously (boltz_set_async) and, on a single rank or with the
+        NcclHalo (whose NCCL calls are captured), three steps are captured once
+        in a CUDA graph and replayed (three steps return the field / scratch
+        buffer rotation to its start).  Numeric errors are reported once, at
+        the end (boltz_sync)."""
+        capturable = self.world == 1 or isinstance(self.halo, NcclHalo)  # torch P2P is not captured
+        if not graph or not capturable or steps < 4:
             self.op.set_async(True)
             try:
                 for _ in range(steps):

@@ -76,7 +76,11 @@ def spatial(args, rank, world, dev):
         return scenarios.mixture_cells(grid, count, seed=4195, first=start)
 
     plan = plan_decomposition(nx, world)
-    s = Solver1D(op, x, dx, init, rank=rank, world=world, left=left, right=right, plan=plan, device=dev)
+    halo = None
+    if world > 1 and args.halo == "nccl":
+        from paper_1301_4195_b200 import NcclHalo
+        halo = NcclHalo(rank, world, dev.index)  # the C ABI's NCCL halo: capturable, so graphs across ranks
+    s = Solver1D(op, x, dx, init, rank=rank, world=world, left=left, right=right, plan=plan, device=dev, halo=halo)
     dt = s.cfl_dt()
     # warm-up step (not timed), then the run
     s.strang_step(dt)
@@ -161,6 +165,8 @@ def main():
     p.add_argument("--steps", type=int, default=0)
     p.add_argument("--lam", type=float, default=1.0)
     p.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    p.add_argument("--halo", default="nccl", choices=["nccl", "torch"],
+                   help="multi-rank halo: the library's NCCL halo (graph-capturable) or torch.distributed P2P")
     args = p.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -189,3 +189,27 @@ def test_ledger_collision_conserves_and_wall_flux(gpu):
         assert np.abs(b - a).max() < 1e-13 * np.abs(a).max()
         m = s.moments().cpu().numpy()
         assert np.all(m[:, 0] > 0) and np.all(m[:, 5] > 0)
+
+
+def test_nccl_halo_graph_run_matches_eager(gpu):
+    """Solver1D with the library's NCCL halo (world 1: the exchange is a no-op,
+    the communicator and the capture path are real): 7 graph-replayed Strang
+    steps are bitwise the eager steps without a halo."""
+    import torch  # noqa: F401
+    from paper_1301_4195_b200 import NcclHalo
+    n, L, nx = 8, 5.0, 12
+    grid = VelocityGrid.create(n, L)
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    f0 = scenarios.mixture_cells(grid, nx, seed=41)
+    with _op(n, L) as op:
+        a = Solver1D(op, x, dx, f0, left=Boundary("wall", 2.0), right=Boundary("extrap"))
+        dt = a.cfl_dt()
+        for _ in range(7):
+            a.strang_step(dt)
+        ref = a.interior.cpu().numpy()
+        halo = NcclHalo(0, 1, 0)
+        b = Solver1D(op, x, dx, f0, left=Boundary("wall", 2.0), right=Boundary("extrap"), halo=halo)
+        b.run(dt, 7)
+        assert getattr(b, "graph_replays", 0) == 2
+        assert np.array_equal(b.interior.cpu().numpy(), ref)
+        halo.close()
