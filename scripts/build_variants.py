@@ -5,6 +5,8 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
     "base": [],
+    "xpf1": ["BOLTZ_XPF=1"],
+    "xpf2": ["BOLTZ_XPF=2"],
     "f1t256": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=256"],
     "f1t512": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=512"],
     "f1t128": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=128"],
