@@ -194,6 +194,15 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * stream synchronised -- by boltz_sync.  fill_boundary does not report
  * sigma_w in this mode.  Host-pointer calls stay synchronous.
  */
+/*
+ * K2 schedule (no reference counterpart): 0 = throughput (default; one warp per
+ * output row and 32-cell group), s = 1..4 = latency (each row's entry list in
+ * 4s fixed segments on 4s warps + an ordered reduction; small batches, N <= 16;
+ * other N keep the throughput schedule).
+ * Results are bitwise reproducible and independent of batch composition
+ * within a schedule; the two schedules differ by round-off.
+ */
+int boltz_set_schedule(boltz_ctx* ctx, int schedule);
 int boltz_set_async(boltz_ctx* ctx, int enable);
 int boltz_sync(boltz_ctx* ctx, void* stream);
 

@@ -95,6 +95,7 @@ def lib():
             "boltz_marginal_batch": (i, [vp, vp, vp, i64, i, vp]),
             "boltz_end_flux": (i, [vp, vp, i64, vp, vp, i, i, d, vp, vp]),
             "boltz_set_async": (i, [vp, i]),
+            "boltz_set_schedule": (i, [vp, i]),
             "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
             "boltz_get_timing": (i, [vp, vp, vp, i, i]),
@@ -351,6 +352,14 @@ class CollisionOperator:
         (pf, po), mem, s = self._args(f, out)
         _check(lib().boltz_marginal_batch(self._h, pf, po, nc, mem, s))
         return out
+
+    def set_schedule(self, schedule="throughput"):
+        """K2 schedule: "throughput" (default), "latency" (each row's entries in 4
+        fixed segments on 4 warps: small batches, N <= 16), "latency8" (8
+        segments: a few cells), or the ABI's integer 0..4.  Bitwise
+        reproducible within a schedule; schedules differ by round-off."""
+        code = {"throughput": 0, "latency": 1, "latency8": 2}.get(schedule, schedule)
+        _check(lib().boltz_set_schedule(self._h, int(code)))
 
     # -- asynchronous mode (CUDA-graph capturable device calls)
     def set_async(self, enable: bool = True):

@@ -95,6 +95,11 @@ struct boltz_ctx {
     // per-kernel-class CUDA-event timing (bench.py roofline) and launch counts
     bool timing = false;
     bool async_mode = false;  // device-pointer calls return without a sync (boltz_set_async)
+    int schedule = 0;         // K2: 0 throughput, 1 latency (segmented rows, boltz_set_schedule)
+    double2* dSeg = nullptr;  // latency schedule's segment partials
+    int64_t seg_cap = 0;      // cells
+    double2* dSeg2 = nullptr; // ... of the second workspace set (swap_workspace)
+    int64_t seg_cap2 = 0;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<int> ev_kind;
@@ -308,10 +313,22 @@ void ensure_workspace(boltz_ctx* c, int64_t cells) {
 }
 
 // double-buffered device staging for host-memory calls (run_host_pipelined)
+// latency schedule scratch: S = kConvWarps x schedule segment partials per cell (complex N^3);
+// `cells` counts cells x schedule
+void ensure_seg(boltz_ctx* c, int64_t cells) {
+    if (cells <= c->seg_cap) return;
+    cudaFree(c->dSeg); cudaFree(c->dSeg2);
+    c->dSeg = nullptr;
+    c->seg_cap = 0;
+    CK(cudaMalloc(&c->dSeg, (size_t)kConvWarps * cells * n3_of(c) * 16));
+    c->seg_cap = cells;
+}
+
 // the second workspace set (same capacity as the first)
 void ensure_workspace2(boltz_ctx* c) {
     if (c->cap2 == c->cap) return;
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
+    cudaFree(c->dSeg);
     c->dA2 = c->dB2 = nullptr; c->dFs2 = nullptr; c->dMaxIm2 = nullptr; c->cap2 = 0;
     const int64_t n3 = n3_of(c);
     CK(cudaMalloc(&c->dA2, (size_t)c->cap * n3 * 16));
@@ -328,6 +345,8 @@ void swap_workspace(boltz_ctx* c) {
     std::swap(c->dB, c->dB2);
     std::swap(c->dFs, c->dFs2);
     std::swap(c->dMaxIm, c->dMaxIm2);
+    std::swap(c->dSeg, c->dSeg2);
+    std::swap(c->seg_cap, c->seg_cap2);
 }
 
 void ensure_staging(boltz_ctx* c, int64_t cells) {
@@ -384,6 +403,27 @@ struct Launch {
     // group complex c->dA -> group complex (s_k * Qhat) in c->dB
     static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
+        if constexpr (conv_kernel_for(N) == 1 && conv_tile(N) == N &&
+                      kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
+            if (c->schedule > 0) {
+                const int S = kConvWarps * c->schedule;  // segments per row
+                const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
+                static bool configured = false;
+                if (!configured) {
+                    CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    configured = true;
+                }
+                ensure_seg(c, ng * kLanes * c->schedule);
+                Timed t_(c, KIND_CONV, s);
+                k_conv_seg<N><<<dim3(N * N, (unsigned)ng, (unsigned)c->schedule), kLanes * kConvWarps, smem, s>>>(
+                    c->dA, c->dSeg, c->dH, c->dEnt, c->dRowStart, (int)ng, S);
+                const long long total = ng * N3 * kLanes;
+                k_conv_seg_reduce<N><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(c->dSeg, c->dB, ng, S);
+                CK(cudaGetLastError());
+                return;
+            }
+        }
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
         // longest-rows-first only when the grid is a few waves deep (~2 CTAs per SM resident)
@@ -1116,6 +1156,15 @@ int boltz_marginal_batch(boltz_ctx* c, const double* f, double* g, int64_t ncell
                                CK(cudaGetLastError());
                            });
     });
+}
+
+int boltz_set_schedule(boltz_ctx* c, int schedule) {
+    if (!c || schedule < 0 || schedule > 4) {
+        set_error("set_schedule: 0 (throughput) or 1..4 (latency: 4 x schedule segments per row)");
+        return BOLTZ_ERR_CONFIG;
+    }
+    c->schedule = schedule;
+    return BOLTZ_OK;
 }
 
 int boltz_set_async(boltz_ctx* c, int enable) {

@@ -412,6 +412,67 @@ k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double
     write_row<N, T>(B, g, row, kc, lane, acc);
 }
 
+// ---------------------------------------------------------------------------
+// Latency schedule (boltz_set_schedule(ctx, 1)) for small batches: a CTA owns
+// one (output row, group) and its kConvWarps warps take kConvWarps fixed,
+// contiguous segments of the row's entry list -- kConvWarps x the warps of the
+// throughput schedule when there are only a few groups, and each warp's list
+// is a quarter as long.  Segment partials go to scratch P[s][g][row][k3][lane]
+// and k_conv_seg_reduce adds them in segment order.  The per-cell arithmetic
+// depends only on the row lists, so results are bitwise independent of batch
+// size and composition in this schedule too (they differ from the throughput
+// schedule's by round-off: a different summation order).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int seg_begin(int e0, int e1, int s, int S) {
+    return e0 + (int)(((long long)(e1 - e0) * s) / S);
+}
+
+// grid = (N^2 rows, groups, S / kConvWarps); warp w of CTA z takes segment
+// z * kConvWarps + w of S
+template <int N>
+__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
+k_conv_seg(const double2* __restrict__ A, double2* __restrict__ P, const double* __restrict__ H,
+           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int S) {
+    using PL = PipeLayout<N>;
+    static_assert(PL::NK == 1, "latency schedule: single-tile rows");
+    constexpr int T = PL::T, N3 = N * N * N;
+    extern __shared__ __align__(16) char smem[];
+    const int row = conv_row<N>(row_start, blockIdx.x, 1);
+    const int g = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int sgm = blockIdx.z * kConvWarps + w;
+    char* wsm = smem + w * PL::WARP_BYTES;
+    const double2* Ag = A + (size_t)g * N3 * kLanes + lane;
+    double2 acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    pipe_rows<N, 0>(wsm, Ag, H, ent, seg_begin(e0, e1, sgm, S), seg_begin(e0, e1, sgm + 1, S), lane, acc);
+    double2* Pg = P + (((size_t)sgm * ngroups + g) * N3 + (size_t)row * N) * kLanes + lane;
+#pragma unroll
+    for (int kk = 0; kk < T; ++kk) Pg[(size_t)kk * kLanes] = acc[kk];
+}
+
+// B = s_k * (((0 + P_0) + P_1) + ...) over the S segments
+template <int N>
+__global__ void __launch_bounds__(256)
+k_conv_seg_reduce(const double2* __restrict__ P, double2* __restrict__ B, long long ngroups, int S) {
+    constexpr int N3 = N * N * N;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over ngroups * N3 * kLanes
+    const long long total = ngroups * N3 * kLanes;
+    if (i >= total) return;
+    double2 sum = make_double2(0.0, 0.0);
+    for (int sgm = 0; sgm < S; ++sgm) {
+        const double2 v = P[(size_t)sgm * total + i];
+        sum.x += v.x;
+        sum.y += v.y;
+    }
+    const int idx = (int)((i / kLanes) % N3);
+    const int k1 = idx / (N * N), k2 = (idx / N) % N, k3 = idx % N;
+    const double sg = ((k1 + k2 + k3) & 1) ? -1.0 : 1.0;  // inverse transform's input sign s_k
+    B[i] = make_double2(sg * sum.x, sg * sum.y);
+}
+
 // ---- H table builder: H[e][slab pos] from one k1-plane of the caller's dense
 // zeta-major G: Gk1[(k2*N + k3) * N^3 + m].  Entry e = output
 // row (k1,k2) x representative input row (m1,m2).  term[pos] = (k3, m3) or

@@ -63,6 +63,10 @@ def spatial(args, rank, world, dev):
     G = generate_table(grid, KernelSpec(lam))
     op = CollisionOperator(grid, KernelSpec(lam), G, device=dev.index or 0)
     del G
+    if args.schedule != "auto":
+        op.set_schedule(args.schedule)
+    elif n <= 16 and -(-nx // world) <= 256:  # small per-rank batches: rows split over warps
+        op.set_schedule("latency")
     t_setup = time.perf_counter() - t0
 
     def init(start, count):
@@ -136,6 +140,7 @@ def homogeneous(args, dev):
     grid = VelocityGrid.create(n, L)
     op = CollisionOperator(grid, KernelSpec(1.0), generate_table(grid, KernelSpec(1.0)), device=dev.index or 0)
     if cfg == 1:
+        op.set_schedule("latency8" if args.schedule == "auto" else args.schedule)  # one cell: latency-bound
         f0 = scenarios.config1_initial(grid)
         f = torch.from_numpy(f0.reshape(1, -1).copy()).to(dev)
         q = op.collide(f)
@@ -165,6 +170,8 @@ def main():
     p.add_argument("--steps", type=int, default=0)
     p.add_argument("--lam", type=float, default=1.0)
     p.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    p.add_argument("--schedule", default="auto", choices=["auto", "throughput", "latency", "latency8"],
+                   help="K2 schedule (auto: latency for <= 256 cells per rank at N <= 16)")
     p.add_argument("--halo", default="nccl", choices=["nccl", "torch"],
                    help="multi-rank halo: the library's NCCL halo (graph-capturable) or torch.distributed P2P")
     args = p.parse_args()

@@ -268,3 +268,35 @@ def test_workspace_limit_chunks_bitwise(gpu, monkeypatch):
         op.collision_rk2(g, 0.01)                      # host pipeline, uniform chunks of the capacity
         assert np.array_equal(g, ref_f)
         assert op.memory_bytes()[1] < 64 << 20  # (table, workspace) bytes
+
+
+@pytest.mark.parametrize("n,L", [(8, 5.0), (16, 6.0)])
+def test_latency_schedule_vs_oracle_and_batch_invariance(gpu, O, n, L):
+    """K2's latency schedule (rows split into 4 fixed segments on 4 warps,
+    ordered reduction): Q-hat within 1e-10 of the oracle; per-cell results
+    bitwise independent of the batch (1 cell, 37 cells, 37 cells permuted);
+    within round-off of the throughput schedule."""
+    import torch
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 37, seed=43)
+    G = table(n, L)
+    with _op(n, L) as op:
+        fh = op.forward(torch.from_numpy(f).to(gpu))
+        q_thr = op.evaluate_qhat(fh).cpu().numpy()
+        op.set_schedule("latency")
+        q_all = op.evaluate_qhat(fh).cpu().numpy()
+        q_one = op.evaluate_qhat(fh[5:6].contiguous()).cpu().numpy()
+        perm = torch.arange(36, -1, -1, device=gpu)
+        q_perm = op.evaluate_qhat(fh[perm].contiguous()).cpu().numpy()
+        assert np.array_equal(q_one[0], q_all[5])
+        assert np.array_equal(q_perm[::-1], q_all)
+        for c in (0, 5, 36):
+            ref = O.evaluate_qhat(n, L, G, fh[c].cpu().numpy())
+            assert rel_max(q_all[c], ref) < TOL_Q
+        assert rel_max(q_all, q_thr) < 1e-13
+        g = f.copy()
+        op.collision_rk2(g, 0.01)                      # host pipeline in the latency schedule
+        op.set_schedule("throughput")
+        h = f.copy()
+        op.collision_rk2(h, 0.01)
+        assert rel_max(g, h) < 1e-13
