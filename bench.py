@@ -431,7 +431,8 @@ def bench_n32(args, dev, local):
     return {"workload": f"cfg5-shaped: {cells} cells, N=32^3 on [-8,8]^3, lambda=1, RK2 steps",
             "value": 2 * cells * steps / (ms * 1e-3), "unit": "evals/s", "steps": steps, "warmup": 1,
             "ms_per_step": ms / steps, "conv_tflops_algorithmic": flop_total / (kms["conv"] * 1e-3) / 1e12,
-            "conv_ms_per_launch": conv_avg, "table_generate_s": round(t_gen, 2)}
+            "conv_ms_per_kernel": conv_avg, "conv_kernels_per_eval": kl["conv"] / (2 * steps),
+            "table_generate_s": round(t_gen, 2)}
 
 
 if __name__ == "__main__":

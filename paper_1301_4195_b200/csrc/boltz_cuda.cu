@@ -420,6 +420,7 @@ struct Launch {
                     c->dA, c->dSeg, c->dH, c->dEnt, c->dRowStart, (int)ng, S);
                 const long long total = ng * N3 * kLanes;
                 k_conv_seg_reduce<N><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(c->dSeg, c->dB, ng, S);
+                c->launches[KIND_CONV]++;  // two kernels under one timing bracket
                 CK(cudaGetLastError());
                 return;
             }
@@ -457,6 +458,7 @@ struct Launch {
             if constexpr (NK > 1)
                 k_conv_kcs<N, KC1><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
                                                                          (int)ng, lpt);
+            if constexpr (NK > 1) c->launches[KIND_CONV]++;  // one k-chunk kernel each
         } else
         { Timed t_(c, KIND_CONV, s); k_conv<N><<<grid, kLanes * kConvWarps, 0, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt); }
         CK(cudaGetLastError());
@@ -543,6 +545,7 @@ struct Launch {
             Timed t_(c, KIND_PROJECT, s);
             k_project_moments<N><<<grid, 256, 0, s>>>(R, part, nc, c->pc);
             k_project_apply<N><<<grid, 256, 0, s>>>(R, part, base, out, nc, coef, c->pc, c->dFlag);
+            c->launches[KIND_PROJECT]++;
         }
         CK(cudaGetLastError());
     }
