@@ -1,4 +1,6 @@
 """K4 transport / ghost fill and the Strang driver vs the CPU oracle (GPU)."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -213,3 +215,22 @@ def test_nccl_halo_graph_run_matches_eager(gpu):
         assert getattr(b, "graph_replays", 0) == 2
         assert np.array_equal(b.interior.cpu().numpy(), ref)
         halo.close()
+
+
+def test_new_abi_entries_reject_bad_arguments(gpu):
+    """ConfigError (category 2) for the peer transport, the edge store and the
+    schedule setter on invalid input (no CUDA call is made)."""
+    from paper_1301_4195_b200.boltz import lib
+    n, L = 8, 5.0
+    with _op(n, L) as op:
+        h = op._h
+        assert lib().boltz_set_schedule(h, 7) == 2
+        assert lib().boltz_set_schedule(h, 0) == 0
+        f = torch.zeros((6, n ** 3), dtype=torch.float64, device=gpu)
+        p = f.data_ptr()
+        L_ = lib()
+        L_.boltz_transport_step_peer.restype = ctypes.c_int
+        assert L_.boltz_transport_step_peer(ctypes.c_void_p(h.value), ctypes.c_void_p(p), None, ctypes.c_double(0.0),
+                                            ctypes.c_void_p(p), ctypes.c_int64(2), None, None, ctypes.c_double(0.1),
+                                            0, 0, None, None, None) == 2  # out aliases field, no grid
+        assert L_.boltz_store_edges(ctypes.c_void_p(h.value), None, ctypes.c_int64(4), None, None, None) == 2
