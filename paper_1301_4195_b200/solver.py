@@ -44,6 +44,19 @@ def plan_decomposition(ncells: int, nranks: int) -> List[Tuple[int, int]]:
     return out
 
 
+def predict_speedup(n: int, p: int, N: int, M: int, T_mem: float, T_flop: float, C: float) -> float:
+    """The paper's leading-order speed-up model of the decomposed solver
+    (§4.2; reference SPEC.md:454-462): n processes of p cores, N^3
+    velocity nodes, M cells, halo cost 4 n N^3 T_mem against C M N^6 T_flop of
+    collision work,
+        S = C M N^6 T_flop / (4 n N^3 T_mem + C M N^6 T_flop / (n p)).
+    T_mem = 0 gives exactly n p."""
+    if min(n, p, N, M, C, T_flop) <= 0 or T_mem < 0:
+        raise ConfigError("predict_speedup: all arguments must be positive (T_mem >= 0)")
+    work = C * M * float(N) ** 6 * T_flop
+    return work / (4.0 * n * float(N) ** 3 * T_mem + work / (n * p))
+
+
 @dataclass
 class Boundary:
     """Physical end condition: kind 'extrap' (linear extrapolation,

@@ -99,3 +99,18 @@ def test_plan_decomposition_contract():
     from paper_1301_4195_b200 import ConfigError
     with pytest.raises(ConfigError):
         plan_decomposition(2, 3)
+
+
+def test_predict_speedup_limits():
+    """SPEC acceptance 9: the speed-up model reproduces its analytic limits
+    exactly (n p when T_mem = 0; 1 when n p = 1 and T_mem = 0), and the
+    regression point of SPEC.md:462 is the formula's value."""
+    from paper_1301_4195_b200.solver import predict_speedup
+    assert predict_speedup(4, 16, 16, 256, 0.0, 1e-9, 10.0) == 64.0
+    assert predict_speedup(1, 1, 24, 64, 0.0, 1e-9, 10.0) == 1.0
+    v = predict_speedup(2, 16, 24, 64, 100.0, 1.0, 10.0)
+    w = 10 * 64 * 24 ** 6
+    assert v == w / (4 * 2 * 24 ** 3 * 100.0 + w / 32)
+    assert 31.9 < v < 32.0
+    with pytest.raises(Exception):
+        predict_speedup(0, 16, 24, 64, 1.0, 1.0, 10.0)
