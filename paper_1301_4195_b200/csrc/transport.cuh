@@ -3,7 +3,8 @@
 // (linear extrapolation SPEC.md:318; diffuse Maxwell wall SPEC.md:333-341).
 // Elementwise over (cell, velocity node); user layout field[cell][N^3] with
 // two ghost cells per side, so consecutive threads touch
-// consecutive nodes of one cell (coalesced).  HBM-bound.
+// consecutive nodes of one cell (coalesced).  HBM-bound: one load per f value
+// (sliding stencil), per-cell geometry hoisted out of the node loop.
 #pragma once
 #include "common.cuh"
 
@@ -15,14 +16,37 @@ __device__ __forceinline__ double minmod3(double a, double b, double c) {
     return 0.0;
 }
 
+// Per-cell geometry of the 5-cell stencil around interior cell ce: inverse
+// centre distances of the three minmod candidates of cells ce-1, ce, ce+1, their
+// half widths, and dt/dx[ce].  Scalars per cell, so a block (one cell) computes
+// them once instead of 9 FP64 divisions per velocity node.
+struct StencilCoef {
+    double r1[3], r2[3], r3[3];  // 1/(x[c+1]-x[c]), 1/(x[c]-x[c-1]), 1/(x[c+1]-x[c-1]), c = ce-1+d
+    double hdx[3];               // 0.5 * dx[c]
+};
+
+__device__ __forceinline__ StencilCoef stencil_coef(long long ce, const double* __restrict__ x,
+                                                    const double* __restrict__ dx) {
+    StencilCoef k;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const long long c = ce - 1 + d;
+        k.r1[d] = 1.0 / (x[c + 1] - x[c]);
+        k.r2[d] = 1.0 / (x[c] - x[c - 1]);
+        k.r3[d] = 1.0 / (x[c + 1] - x[c - 1]);
+        k.hdx[d] = 0.5 * dx[c];
+    }
+    return k;
+}
+
 // Upwind fluxes through the left and right faces of interior cell ce at
 // velocity node j: minmod slopes from the 5-cell stencil,
 // each cell's own half-width, zero slope in the wall ghost / wall cell.
 // Shared by the FV step and the boundary-flux ledger (bitwise the same faces).
 template <int N>
 __device__ __forceinline__ void face_fluxes(const double* __restrict__ f, long long ce, int j, long long ncl,
-                                            const double* __restrict__ x, const double* __restrict__ dx, int wl,
-                                            int wr, double dv, double& fc, double& Fl, double& Fr) {
+                                            const StencilCoef& k, int wl, int wr, double dv, double& fc, double& Fl,
+                                            double& Fr) {
     constexpr int N3 = N * N * N;
     const double v1 = dv * (j / (N * N) - N / 2);
     double fv[5];
@@ -33,23 +57,28 @@ __device__ __forceinline__ void face_fluxes(const double* __restrict__ f, long l
     for (int d = 0; d < 3; ++d) {
         const long long c = ce - 1 + d;
         const double fm = fv[d], f0 = fv[d + 1], fp = fv[d + 2];
-        double s = minmod3((fp - f0) / (x[c + 1] - x[c]), (f0 - fm) / (x[c] - x[c - 1]),
-                           (fp - fm) / (x[c + 1] - x[c - 1]));
+        double s = minmod3((fp - f0) * k.r1[d], (f0 - fm) * k.r2[d], (fp - fm) * k.r3[d]);
         if (wl && (c == 1 || c == 2)) s = 0.0;
         if (wr && (c == ncl + 2 || c == ncl + 1)) s = 0.0;
         sg[d] = s;
     }
     if (v1 >= 0.0) {
-        Fl = v1 * (fv[1] + 0.5 * dx[ce - 1] * sg[0]);
-        Fr = v1 * (fv[2] + 0.5 * dx[ce] * sg[1]);
+        Fl = v1 * (fv[1] + k.hdx[0] * sg[0]);
+        Fr = v1 * (fv[2] + k.hdx[1] * sg[1]);
     } else {
-        Fl = v1 * (fv[2] - 0.5 * dx[ce] * sg[1]);
-        Fr = v1 * (fv[3] - 0.5 * dx[ce + 1] * sg[2]);
+        Fl = v1 * (fv[2] - k.hdx[1] * sg[1]);
+        Fr = v1 * (fv[3] - k.hdx[2] * sg[2]);
     }
     fc = fv[2];
 }
 
-// grid = (ceil(N^3/256), ncl + 4); ghosts are copied through.
+// grid = (ceil(N^3/512), ceil(ncl/kTrCells)): a thread owns velocity nodes
+// 2p, 2p+1 (16-byte loads) of kTrCells consecutive interior cells and slides the 5-cell stencil along
+// them, so each f value is loaded once (not 5 times), each minmod slope and
+// each face flux is computed once and shared by its two cells -- the same
+// arithmetic, face for face, as face_fluxes (bitwise).  Per-cell geometry
+// (inverse distances, half widths, dt/dx) is computed once per block.
+// Ghosts are copied through by the first / last chunk.
 // out = alpha*base + (1-alpha)*(f - dt/dx (F_{j+1/2} - F_{j-1/2}))   (base may be null)
 // -- the second stage of the SSP-RK2 transport sub-step fused in.
 // Peer mode (peer != 0) fuses the halo exchange into the step: the two first
@@ -58,26 +87,85 @@ __device__ __forceinline__ void face_fluxes(const double* __restrict__ f, long l
 // right_dst: the right rank's ghosts 0, 1 -- peer memory over NVLink, or
 // another field of the same device), and this rank's own ghost rows are NOT
 // written (its neighbours and boltz_fill_boundary own them).
+constexpr int kTrCells = 8;
+
 template <int N>
 __global__ void __launch_bounds__(256)
 k_transport(const double* __restrict__ f, const double* __restrict__ base, double alpha, double* __restrict__ out,
             long long ncl, const double* __restrict__ x, const double* __restrict__ dx, double dt, int wl, int wr,
             double dv, int peer, double* __restrict__ left_dst, double* __restrict__ right_dst) {
     constexpr int N3 = N * N * N;
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    const long long ce = blockIdx.y;
-    if (j >= N3) return;
-    if (ce < 2 || ce > ncl + 1) {
-        if (!peer) out[ce * N3 + j] = f[ce * N3 + j];
-        return;
+    constexpr int P3 = N3 / 2;  // node pairs: a thread owns nodes 2p, 2p+1 (same v1: N is even)
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    const long long c0 = 2 + (long long)blockIdx.y * kTrCells;
+    const long long c1 = c0 + kTrCells < ncl + 2 ? c0 + kTrCells : ncl + 2;  // [c0, c1) interior
+    // per-cell geometry of cells c0-1 .. c1 (slopes) and c0 .. c1-1 (dt/dx)
+    __shared__ double s_r1[kTrCells + 2], s_r2[kTrCells + 2], s_r3[kTrCells + 2], s_h[kTrCells + 2];
+    __shared__ double s_lam[kTrCells];
+    for (int t = threadIdx.x; t < (int)(c1 - c0) + 2; t += blockDim.x) {
+        const long long c = c0 - 1 + t;
+        s_r1[t] = 1.0 / (x[c + 1] - x[c]);
+        s_r2[t] = 1.0 / (x[c] - x[c - 1]);
+        s_r3[t] = 1.0 / (x[c + 1] - x[c - 1]);
+        s_h[t] = 0.5 * dx[c];
+        if (t < (int)(c1 - c0)) s_lam[t] = dt / dx[c0 + t];
     }
-    double fc, Fl, Fr;
-    face_fluxes<N>(f, ce, j, ncl, x, dx, wl, wr, dv, fc, Fl, Fr);
-    const double upd = fc - dt / dx[ce] * (Fr - Fl);
-    const double v = base ? alpha * base[ce * N3 + j] + (1.0 - alpha) * upd : upd;
-    out[ce * N3 + j] = v;
-    if (left_dst && ce < 4) left_dst[(ce - 2) * N3 + j] = v;
-    if (right_dst && ce >= ncl) right_dst[(ce - ncl) * N3 + j] = v;
+    __syncthreads();
+    if (p >= P3) return;
+    const double2* F = reinterpret_cast<const double2*>(f);
+    const double2* Bs = reinterpret_cast<const double2*>(base);
+    double2* O = reinterpret_cast<double2*>(out);
+    if (!peer) {  // ghost rows copied through
+        if (blockIdx.y == 0) {
+            O[p] = F[p];
+            O[P3 + p] = F[P3 + p];
+        }
+        if (c1 == ncl + 2) {
+            O[(ncl + 2) * P3 + p] = F[(ncl + 2) * P3 + p];
+            O[(ncl + 3) * P3 + p] = F[(ncl + 3) * P3 + p];
+        }
+    }
+    const double v1 = dv * ((2 * p) / (N * N) - N / 2);
+    // slope of cell c (window index t = c - c0 + 1) from f[c-1], f[c], f[c+1]
+    auto slope = [&](long long c, double fm, double f0, double fp) {
+        const int t = (int)(c - c0 + 1);
+        double sl = minmod3((fp - f0) * s_r1[t], (f0 - fm) * s_r2[t], (fp - fm) * s_r3[t]);
+        if (wl && (c == 1 || c == 2)) sl = 0.0;
+        if (wr && (c == ncl + 2 || c == ncl + 1)) sl = 0.0;
+        return sl;
+    };
+    auto slope2 = [&](long long c, double2 fm, double2 f0, double2 fp) {
+        return make_double2(slope(c, fm.x, f0.x, fp.x), slope(c, fm.y, f0.y, fp.y));
+    };
+    // upwind flux through the face between cells c and c+1
+    auto face = [&](long long c, double fa, double sa, double fb, double sb) {
+        return v1 >= 0.0 ? v1 * (fa + s_h[c - c0 + 1] * sa) : v1 * (fb - s_h[c - c0 + 2] * sb);
+    };
+    auto face2 = [&](long long c, double2 fa, double2 sa, double2 fb, double2 sb) {
+        return make_double2(face(c, fa.x, sa.x, fb.x, sb.x), face(c, fa.y, sa.y, fb.y, sb.y));
+    };
+    double2 fm1 = F[(c0 - 1) * P3 + p], f0 = F[c0 * P3 + p], fp1 = F[(c0 + 1) * P3 + p];
+    double2 sm1 = slope2(c0 - 1, F[(c0 - 2) * P3 + p], fm1, f0);
+    double2 s0 = slope2(c0, fm1, f0, fp1);
+    double2 Fl = face2(c0 - 1, fm1, sm1, f0, s0);
+    for (long long ce = c0; ce < c1; ++ce) {
+        const double2 fp2 = F[(ce + 2) * P3 + p];
+        const double2 sp1 = slope2(ce + 1, f0, fp1, fp2);
+        const double2 Fr = face2(ce, f0, s0, fp1, sp1);
+        const double lam = s_lam[ce - c0];
+        double2 v = make_double2(f0.x - lam * (Fr.x - Fl.x), f0.y - lam * (Fr.y - Fl.y));
+        if (base) {
+            const double2 b = Bs[ce * P3 + p];
+            v = make_double2(alpha * b.x + (1.0 - alpha) * v.x, alpha * b.y + (1.0 - alpha) * v.y);
+        }
+        O[ce * P3 + p] = v;
+        if (left_dst && ce < 4) reinterpret_cast<double2*>(left_dst)[(ce - 2) * P3 + p] = v;
+        if (right_dst && ce >= ncl) reinterpret_cast<double2*>(right_dst)[(ce - ncl) * P3 + p] = v;
+        f0 = fp1;
+        fp1 = fp2;
+        s0 = sp1;
+        Fl = Fr;
+    }
 }
 
 // the collision step's half of the fused exchange: cells 0,1 and n-2,n-1 of a
@@ -122,14 +210,15 @@ __global__ void __launch_bounds__(256)
 k_end_flux(const double* __restrict__ f, long long ncl, const double* __restrict__ x, const double* __restrict__ dx,
            int wl, int wr, double dv, double coef, double* __restrict__ acc) {
     constexpr int N3 = N * N * N;
+    const StencilCoef kl = stencil_coef(2, x, dx), kr = stencil_coef(ncl + 1, x, dx);
     double m[5] = {0, 0, 0, 0, 0};
     for (int j = threadIdx.x; j < N3; j += blockDim.x) {
         const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
         const double v1 = dv * (a1 - N / 2), v2 = dv * (a2 - N / 2), v3 = dv * (a3 - N / 2);
         const double w = axis_coeff(N, a1) * axis_coeff(N, a2) * axis_coeff(N, a3) * dv * dv * dv;
         double fc, Fl, Fr, Gl, Gr;
-        face_fluxes<N>(f, 2, j, ncl, x, dx, wl, wr, dv, fc, Fl, Gr);
-        face_fluxes<N>(f, ncl + 1, j, ncl, x, dx, wl, wr, dv, fc, Gl, Fr);
+        face_fluxes<N>(f, 2, j, ncl, kl, wl, wr, dv, fc, Fl, Gr);
+        face_fluxes<N>(f, ncl + 1, j, ncl, kr, wl, wr, dv, fc, Gl, Fr);
         const double q = (Fr - Fl) * w;
         m[0] += q;
         m[1] += v1 * q;
@@ -238,7 +327,7 @@ inline void launch_transport(int n, const double* f, const double* base, double 
     switch (n) {
 #define BOLTZ_TR(N)                                                                                        \
     case N: {                                                                                              \
-        dim3 grid((N * N * N + 255) / 256, (unsigned)(ncl + 4));                                          \
+        dim3 grid((N * N * N / 2 + 255) / 256, (unsigned)((ncl + kTrCells - 1) / kTrCells));              \
         k_transport<N><<<grid, 256, 0, s>>>(f, base, alpha, out, ncl, x, dx, dt, wl, wr, dv, peer, left_dst, \
                                             right_dst);                                                    \
     } break;
