@@ -250,9 +250,11 @@ inline void launch_end_flux(int n, const double* f, long long ncl, const double*
     }
 }
 
-// one block of 256 threads; sigma_w written to sig[0]
+// one block of kFillThreads threads; sigma_w written to sig[0]
+constexpr int kFillThreads = 1024;  // one block: the wall's sigma_w is a whole-cell reduction
+
 template <int N>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kFillThreads)
 k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict__ x, int side, int kind, double Tw,
                 double vw0, double vw1, double vw2, double dv, double* __restrict__ sig) {
     constexpr int N3 = N * N * N;
@@ -273,7 +275,7 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
         return;
     }
     const double nrm = side == 0 ? 1.0 : -1.0;
-    __shared__ double red[256];
+    __shared__ double red[kFillThreads];
     double part = 0.0;
     for (int j = threadIdx.x; j < N3; j += blockDim.x) {
         const int a1 = j / (N * N), a2 = (j / N) % N, a3 = j % N;
@@ -282,7 +284,7 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
     }
     red[threadIdx.x] = part;
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
+    for (int w = kFillThreads / 2; w > 0; w >>= 1) {
         if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
@@ -303,7 +305,7 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
         }
         red[threadIdx.x] = in;
         __syncthreads();
-        for (int w = 128; w > 0; w >>= 1) {
+        for (int w = kFillThreads / 2; w > 0; w >>= 1) {
             if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
             __syncthreads();
         }
@@ -341,7 +343,7 @@ inline void launch_fill_boundary(int n, double* f, long long ncl, const double* 
                                  double vw0, double vw1, double vw2, double dv, double* sig, cudaStream_t s) {
     switch (n) {
 #define BOLTZ_FB(N) \
-    case N: k_fill_boundary<N><<<1, 256, 0, s>>>(f, ncl, x, side, kind, Tw, vw0, vw1, vw2, dv, sig); break;
+    case N: k_fill_boundary<N><<<1, kFillThreads, 0, s>>>(f, ncl, x, side, kind, Tw, vw0, vw1, vw2, dv, sig); break;
         BOLTZ_FOR_EACH_N(BOLTZ_FB)
 #undef BOLTZ_FB
         default: break;
