@@ -300,3 +300,27 @@ def test_latency_schedule_vs_oracle_and_batch_invariance(gpu, O, n, L):
         h = f.copy()
         op.collision_rk2(h, 0.01)
         assert rel_max(g, h) < 1e-13
+
+
+@pytest.mark.parametrize("n,L,cells", [(16, 6.0, 4096), (32, 8.0, 2048)])
+def test_full_size_batches_properties(gpu, n, L, cells):
+    """BASELINE's full batch sizes (cfg2: 4096 cells at N=16; cfg5: 2048 cells at
+    N=32), through size-independent properties: every cell's Q conserves mass,
+    momentum and energy to 1e-12 rho; an RK2 step changes no
+    cell's invariants beyond 1e-12; a 32-cell slice of the batch is bitwise
+    the same rows of the full-batch result (per-cell determinism)."""
+    import torch
+    grid = VelocityGrid.create(n, L)
+    f = torch.from_numpy(scenarios.mixture_cells(grid, cells, seed=4195)).to(gpu)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        q = op.collide(f)
+        assert bool(torch.isfinite(q).all())
+        mf, mq = op.moments(f), op.moments(q)
+        rho = mf[:, 0]
+        assert float((mq[:, :5].abs().max(dim=1).values / rho).max()) < TOL_CONS
+        part = op.collide(f[1000:1032].contiguous())
+        assert torch.equal(part, q[1000:1032])
+        g = f.clone()
+        op.collision_rk2(g, 0.01)
+        mg = op.moments(g)
+        assert float(((mg[:, :5] - mf[:, :5]).abs().max(dim=1).values / rho).max()) < 1e-12
