@@ -427,8 +427,10 @@ struct Launch {
         }
         constexpr int NK = N / conv_tile(N);
         dim3 grid(N * N * NK, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-        // longest-rows-first only when the grid is a few waves deep (~2 CTAs per SM resident)
-        const int lpt = (int64_t)grid.x * grid.y < 8 * 2 * 148 ? 1 : 0;
+        // longest-rows-first in every column when the grid is a few waves deep (~2
+        // CTAs per SM resident), else in the last column only (conv.cuh conv_row)
+        int lpt = (int64_t)grid.x * grid.y < 8 * 2 * 148 ? 0 : (int)grid.y - 1;
+        if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
         if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
             static bool configured = false;  // per process; attributes apply to every device

@@ -145,9 +145,12 @@ __device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[
 
 
 // row_start holds the CSR offsets of the N*N output rows (N*N+1 ints), then two
-// processing orders of the rows: longest row list first (lpt != 0: for grids
-// of a few waves, so the last wave is made of short rows) and the natural order
-// (many waves: neighbouring rows share f-hat rows in L2).
+// processing orders of the rows: longest row list first and the natural order.
+// A CTA of column blockIdx.y (a set of cell groups) uses the longest-first order
+// when blockIdx.y >= lpt_from: every column for grids of a few waves, the last
+// column only for many-wave grids -- so the final wave is made of short rows
+// while the earlier columns keep the L2-friendly natural order (neighbouring
+// rows share f-hat rows).  The row order does not change any result.
 template <int N>
 __device__ __forceinline__ int conv_row(const int* __restrict__ row_start, int b, int lpt) {
     return lpt ? __ldg(row_start + N * N + 1 + b) : b;
@@ -200,9 +203,9 @@ __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const 
 template <int N>
 __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-       const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
+       const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt_from) {
     constexpr int T = conv_tile(N), NK = N / T, N3 = N * N * N;
-    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, lpt);
+    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, (int)blockIdx.y >= lpt_from);
     const int lane = threadIdx.x & 31;
     const int g = blockIdx.y * kConvWarps + (threadIdx.x >> 5);
     if (g >= ngroups) return;
@@ -238,11 +241,11 @@ struct KcsLayout {
 template <int N, int KC>
 __global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
 k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
+           const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt_from) {
     using LY = KcsLayout<N>;
     constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int row = conv_row<N>(row_start, blockIdx.x, lpt);
+    const int row = conv_row<N>(row_start, blockIdx.x, (int)blockIdx.y >= lpt_from);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * kConvWarps + wid;
     if (g >= ngroups) return;
@@ -393,11 +396,11 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
 template <int N>
 __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-            const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt) {
+            const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt_from) {
     using PL = PipeLayout<N>;
     constexpr int T = PL::T, NK = PL::NK, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, lpt);
+    const int kc = blockIdx.x % NK, row = conv_row<N>(row_start, blockIdx.x / NK, (int)blockIdx.y >= lpt_from);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int g = blockIdx.y * kConvWarps + wid;
     if (g >= ngroups) return;
