@@ -393,8 +393,11 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
     }
 }
 
+#ifndef BOLTZ_PIPE_MINB
+#define BOLTZ_PIPE_MINB 1
+#endif
 template <int N>
-__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
+__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_PIPE_MINB)
 k_conv_pipe(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int2* __restrict__ ent, const int* __restrict__ row_start, int ngroups, int lpt_from) {
     using PL = PipeLayout<N>;

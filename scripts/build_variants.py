@@ -5,6 +5,9 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
     "base": [],
+    "pipe_m3": ["BOLTZ_PIPE_MINB=3"],
+    "pipe_m3_w2": ["BOLTZ_PIPE_MINB=3", "BOLTZ_CONV_WARPS=2"],
+    "pipe_m6_w2": ["BOLTZ_PIPE_MINB=6", "BOLTZ_CONV_WARPS=2"],
     "xpf1": ["BOLTZ_XPF=1"],
     "xpf2": ["BOLTZ_XPF=2"],
     "f1t256": ["BOLTZ_FUSED_BUDGET_KB=100", "BOLTZ_FUSED_THREADS=256"],
