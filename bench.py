@@ -32,6 +32,9 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+# the paper's best published N=16 collision-operator rate, one
+# eval in 0.00408 s on 16 Stampede cores = 245.1 evals/s
+PUBLISHED_EVALS_PER_S = 1.0 / 0.00408
 N_VEL, L_VEL, LAM, CELLS, DT = 16, 6.0, 1.0, 4096, 0.01
 FLOP_PER_TERM = 10  # 2 DMUL + 4 DFMA per (k, m) term, SURVEY.md §8d
 # executed / algorithmic terms at N=16: 18464 row pairs x 192-term slabs / (27/64 16^6)
@@ -192,7 +195,7 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": "collision-operator evals/s (N=16, cfg2 two-Maxwellian cells, RK2)",
         "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "vs_baseline": value / PUBLISHED_EVALS_PER_S, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"cfg2 sample: RK2 step of {sample} cells (of 4096), N=16, L=6, lambda=1",
                    "cells_per_step": sample},
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
@@ -329,7 +332,9 @@ def main():
             "metric": "collision-operator evals/s (N=16, cfg2; FP64)",
             "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": value / PUBLISHED_EVALS_PER_S, "dtype": "f64", "data": "synthetic",
+            "vs_baseline_ref": "BASELINE.md: 245.1 evals/s = 1 / 0.00408 s per N=16 eval on 16 Stampede cores "
+                               "(PAPER.md:358), other hardware",
             "config": {"workload": f"cfg2: {cells} independent cells per GPU, N=16^3 on [-6,6]^3, hard spheres, "
                                    "one collision RK2 step (2 collide evals) per cell per step",
                        "cells_per_gpu": cells, "N": N_VEL, "L": L_VEL, "lambda": LAM, "dt": DT,
