@@ -46,7 +46,7 @@ def build(verbose: bool = False, force: bool = False, out: pathlib.Path = LIB, d
     ]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
-    print("[build]", " ".join(cmd), flush=True)
+    print("[build]", " ".join(cmd), file=sys.stderr, flush=True)  # stdout belongs to callers (bench.py's JSON)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or r.returncode != 0:
         sys.stdout.write(r.stdout)
