@@ -317,6 +317,9 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
 // k_conv_pipe: x double-buffered, full y row staged, H double-buffered
 //   per warp: x[2][N][32] + y[N][32] double2, H[2][SLAB_KC] double
 // ---------------------------------------------------------------------------
+#ifndef BOLTZ_PIPE_TMA
+#define BOLTZ_PIPE_TMA 1  // row-pair staging by 1D TMA bulk copies + mbarriers (single-tile rows); 0: per-lane cp.async
+#endif
 template <int N>
 struct PipeLayout {
     static constexpr int T = conv_tile(N);
@@ -324,8 +327,27 @@ struct PipeLayout {
     static constexpr int SLAB_KC = band_slab_kc(N, T);
     static constexpr int X_BYTES = N * kLanes * 16;
     static constexpr int H_BYTES = SLAB_KC * 8;
-    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES;
+    static constexpr bool TMA = BOLTZ_PIPE_TMA && NK == 1;
+    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES + (TMA ? 16 : 0);  // + 2 mbarriers
 };
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1D TMA: bytes (multiple of 16) global -> this CTA's shared memory, completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
 
 template <int N, int KC>
 __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__ Ag, const double* __restrict__ H,
@@ -334,6 +356,58 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
     using PL = PipeLayout<N>;
     constexpr int T = PL::T, NK = PL::NK;
     const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
+    if constexpr (PL::TMA) {
+        // the next row pair's x row (8 KB at N=16, contiguous in the group layout),
+        // y row and H slab: three bulk copies issued by lane 0, completing on the
+        // slot's mbarrier (slot = entry parity); every lane waits on the parity
+        unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + 3 * PL::X_BYTES + 2 * PL::H_BYTES);
+        const double2* Abase = Ag - lane;
+        auto issue = [&](int slot, int2 en, int e) {
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot are done
+                mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + PL::H_BYTES);
+                bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
+                bulk_g2s(wsm + 2 * PL::X_BYTES, Abase + (size_t)en.y * kLanes, PL::X_BYTES, bar + slot);
+                bulk_g2s(wsm + 3 * PL::X_BYTES + slot * PL::H_BYTES, H + (size_t)e * PL::SLAB_KC, PL::H_BYTES,
+                         bar + slot);
+            }
+        };
+        if (e0 >= e1) return;
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int2 en_next = __ldg(ent + e0);
+        int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en_next;
+        issue(0, en_next, e0);
+        mbar_wait(bar, 0);
+        double2 y[T];
+#pragma unroll
+        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+        for (int e = e0; e < e1; ++e) {
+            const int i = e - e0, cur = i & 1;
+            const bool more = e + 1 < e1;
+            en_next = en_ahead;
+            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
+            __syncwarp();  // every lane read y (registers) and is done with slot cur^1
+            if (more) issue(cur ^ 1, en_next, e + 1);
+            const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
+            const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
+            int p = 0;
+            double2 hb = make_double2(0.0, 0.0);
+            auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
+            auto none = [](int, int) {};
+            band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+            if (more) {
+                mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+#pragma unroll
+                for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+            }
+        }
+        return;
+    }
     auto issue_xh = [&](int buf, int2 en, int e) {
         double2* xs = reinterpret_cast<double2*>(wsm + buf * PL::X_BYTES);
         const double2* X = Ag + (size_t)en.x * kLanes;

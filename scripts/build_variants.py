@@ -5,6 +5,7 @@ sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
 from paper_1301_4195_b200.build import build
 V = {
     "base": [],
+    "tma": ["BOLTZ_PIPE_TMA=1"],
     "pipe_m3": ["BOLTZ_PIPE_MINB=3"],
     "pipe_m3_w2": ["BOLTZ_PIPE_MINB=3", "BOLTZ_CONV_WARPS=2"],
     "pipe_m6_w2": ["BOLTZ_PIPE_MINB=6", "BOLTZ_CONV_WARPS=2"],
