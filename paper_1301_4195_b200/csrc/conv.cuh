@@ -222,6 +222,27 @@ k_conv(const double2* __restrict__ A, double2* __restrict__ B, const double* __r
 #ifndef BOLTZ_K0_MINB
 #define BOLTZ_K0_MINB 1
 #endif
+#ifndef BOLTZ_PIPE_TMA
+#define BOLTZ_PIPE_TMA 1  // row-pair staging by 1D TMA bulk copies + mbarriers (single-tile rows); 0: per-lane cp.async
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// 1D TMA: bytes (multiple of 16) global -> this CTA's shared memory, completing on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // k_conv_kcs: one k-chunk per kernel; the y row and the H slab of the next row
 // pair are staged in shared memory by cp.async while the current one computes
@@ -235,7 +256,7 @@ struct KcsLayout {
     static constexpr int SLAB_KC = band_slab_kc(N, T);
     static constexpr int Y_BYTES = N * kLanes * 16;
     static constexpr int H_BYTES = SLAB_KC * 8;
-    static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES;
+    static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + (BOLTZ_PIPE_TMA && NK == 2 ? 16 : 0);  // + 2 mbarriers
 };
 
 template <int N, int KC>
@@ -266,6 +287,73 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
 #pragma unroll
     for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
     const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    // 1D TMA staging (N=32; measured neutral-to-negative at N=24): the next
+    // entry's H slab (double-buffered) and y row (single buffer, refilled once
+    // its chunk is in registers) are two bulk copies by lane 0, each arriving
+    // (with its byte count) on the slot's 2-count mbarrier
+    constexpr bool KTMA = BOLTZ_PIPE_TMA && NK == 2;
+    if constexpr (KTMA) {
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + LY::Y_BYTES + 2 * LY::H_BYTES);
+    const double2* Abase = Ag - lane;
+    auto tma_h = [&](int slot, int e) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, LY::H_BYTES);
+            bulk_g2s(hbase + slot * LY::H_BYTES, H + ((size_t)e * NK + KC) * LY::SLAB_KC, LY::H_BYTES, bar + slot);
+        }
+    };
+    auto tma_y = [&](int slot, int2 en) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, LY::Y_BYTES);
+            bulk_g2s(ys, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+        }
+    };
+    if (e0 < e1) {
+        if (lane == 0) {
+            mbar_init(bar, 2);
+            mbar_init(bar + 1, 2);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int2 en = __ldg(ent + e0);
+        int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;
+        tma_y(0, en);
+        tma_h(0, e0);
+        mbar_wait(bar, 0);
+        for (int e = e0; e < e1; ++e) {
+            const int i = e - e0, cur = i & 1;
+            const bool more = e + 1 < e1;
+            const int2 nx = en_ahead;
+            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
+            __syncwarp();  // every lane finished reading H[cur^1]
+            if (more) tma_h(cur ^ 1, e + 1);
+            const double2* X = Ag + (size_t)en.x * kLanes;
+            const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
+            int p = 0;
+            double2 hb = make_double2(0.0, 0.0);
+            auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
+            auto none = [](int, int) {};
+            double2 y[T];
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            if constexpr (NK == 1) {
+                __syncwarp();  // every lane holds its y chunk: the buffer may be refilled
+                if (more) tma_y(cur ^ 1, nx);
+                band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+            } else {
+                band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
+#pragma unroll
+                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                __syncwarp();
+                if (more) tma_y(cur ^ 1, nx);
+                band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
+            }
+            if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+            en = nx;
+        }
+    }
+    } else {
     if (e0 < e1) {
         int2 en = __ldg(ent + e0);
         int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;  // next entry, loaded a row early
@@ -310,6 +398,7 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
             en = nx;
         }
     }
+    }
     write_row<N, T>(B, g, row, KC, lane, acc);
 }
 
@@ -317,9 +406,6 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
 // k_conv_pipe: x double-buffered, full y row staged, H double-buffered
 //   per warp: x[2][N][32] + y[N][32] double2, H[2][SLAB_KC] double
 // ---------------------------------------------------------------------------
-#ifndef BOLTZ_PIPE_TMA
-#define BOLTZ_PIPE_TMA 1  // row-pair staging by 1D TMA bulk copies + mbarriers (single-tile rows); 0: per-lane cp.async
-#endif
 template <int N>
 struct PipeLayout {
     static constexpr int T = conv_tile(N);
@@ -330,24 +416,6 @@ struct PipeLayout {
     static constexpr bool TMA = BOLTZ_PIPE_TMA && NK == 1;
     static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES + (TMA ? 16 : 0);  // + 2 mbarriers
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
-        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// 1D TMA: bytes (multiple of 16) global -> this CTA's shared memory, completing on bar
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
 
 template <int N, int KC>
 __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__ Ag, const double* __restrict__ H,
