@@ -718,7 +718,8 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     const int64_t nchunks = (int64_t)bounds.size() - 1;
     // odd chunks compute on comp2 with the second workspace; comp2 joins s's
     // prior work first and s waits for comp2 at the end (stream semantics kept)
-    const bool two = nchunks > 1;
+    bool two = nchunks > 1;
+    if (const char* e = std::getenv("BOLTZ_HOST_STREAMS")) two = two && std::atoi(e) > 1;  // tuning / A-B
     if (two) {
         ensure_workspace2(c);
         CK(cudaEventRecord(c->ev_fork, s));
@@ -736,14 +737,14 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     for (int64_t i = 0; i < nchunks; ++i) {
         const int slot = (int)(i & 1);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
-        cudaStream_t cs = slot ? c->comp2 : s;
+        cudaStream_t cs = (slot && two) ? c->comp2 : s;
         CK(cudaStreamWaitEvent(cs, c->ev_h2d[slot], 0));
         if (i >= 2) CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
-        if (slot) swap_workspace(c);
+        if (slot && two) swap_workspace(c);
         fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
         CK(cudaEventRecord(c->ev_comp[slot], cs));
         if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
-        if (slot) swap_workspace(c);
+        if (slot && two) swap_workspace(c);
         if (i + 1 < nchunks) h2d(i + 1);
         CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
         CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
