@@ -37,8 +37,6 @@ sys.path.insert(0, REPO)
 PUBLISHED_EVALS_PER_S = 1.0 / 0.00408
 N_VEL, L_VEL, LAM, CELLS, DT = 16, 6.0, 1.0, 4096, 0.01
 FLOP_PER_TERM = 10  # 2 DMUL + 4 DFMA per (k, m) term, SURVEY.md §8d
-# executed / algorithmic terms at N=16: 18464 row pairs x 192-term slabs / (27/64 16^6)
-EXECUTED_TERM_RATIO_16 = 18464 * 192 / (27 * 16 ** 6 / 64)
 
 
 def ncu_traffic(kernel, cells):
@@ -288,6 +286,9 @@ def main():
     value = evals / (total_ms * 1e-3)
 
     # roofline of the dominant kernel (K2 convolution)
+    terms_plain, terms_mirror = op.schedule_terms()
+    conv_kernel = "k_conv_mirror<16>" if terms_mirror else "k_conv_pipe<16>"
+    exec_ratio = (terms_mirror or terms_plain) / terms_per_eval(N_VEL)
     conv_launches = klaunch["conv"]
     conv_ms_avg = kms["conv"] / max(conv_launches, 1)
     flop_per_launch = FLOP_PER_TERM * terms_per_eval(N_VEL) * cells
@@ -345,14 +346,17 @@ def main():
             "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
             "kernel_launches": klaunch,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_conv_pipe<16>", cells),
-                         "kernel": "k_conv_pipe<16> (K2)",
-                         "executed_fp64_slot_fraction": achieved / peak * EXECUTED_TERM_RATIO_16 * 12 / 10,
+                         "frac": achieved / peak, "traffic": ncu_traffic(conv_kernel, cells),
+                         "kernel": f"{conv_kernel} (K2)",
+                         "executed_term_ratio": exec_ratio,
+                         "executed_fp64_slot_fraction": achieved / peak * exec_ratio * 12 / 10,
                          "note": "achieved = 10 flop x 27/64 N^6 valid terms x cells per launch / mean launch time "
-                                 "(algorithmic, SURVEY.md §8d). The kernel executes 0.5009 of those terms (pair "
-                                 "symmetry, DESIGN.md §2) at 6 FP64 pipe instructions (2 DMUL + 4 DFMA) each, so "
-                                 "the FP64 pipe-slot fraction is frac x 0.5009 x 12/10. peak = DFMA probe "
-                                 "measured in this run (MEASURED_PEAKS.json has no FP64 entry)"},
+                                 "(algorithmic, SURVEY.md §8d). The kernel executes executed_term_ratio of those "
+                                 "terms (pair symmetry, plus the Hermitian mirror of interior terms for collide / "
+                                 "RK2, DESIGN.md §2-3; the ratio is the library's folded-table size) at 6 FP64 "
+                                 "pipe instructions (2 DMUL + 4 DFMA) each, so the FP64 pipe-slot fraction is frac "
+                                 "x executed_term_ratio x 12/10. peak = DFMA probe measured in this run "
+                                 "(MEASURED_PEAKS.json has no FP64 entry)"},
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(cells * N_VEL ** 3 * 8),
                     "d2h_bytes_per_step": int(cells * N_VEL ** 3 * 8),
                     "path": "CollisionOperator.collision_rk2(pinned numpy) -> boltz_rk2_batch(mem=HOST)"},

@@ -96,6 +96,7 @@ def lib():
             "boltz_end_flux": (i, [vp, vp, i64, vp, vp, i, i, d, vp, vp]),
             "boltz_set_async": (i, [vp, i]),
             "boltz_set_schedule": (i, [vp, i]),
+            "boltz_schedule_terms": (i, [vp, C.POINTER(i64), C.POINTER(i64)]),
             "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
             "boltz_get_timing": (i, [vp, vp, vp, i, i]),
@@ -352,6 +353,13 @@ class CollisionOperator:
         (pf, po), mem, s = self._args(f, out)
         _check(lib().boltz_marginal_batch(self._h, pf, po, nc, mem, s))
         return out
+
+    def schedule_terms(self):
+        """(plain, mirror) executed K2 terms per cell eval (mirror 0 when the
+        Hermitian mirror schedule is not active)."""
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib().boltz_schedule_terms(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_schedule(self, schedule="throughput"):
         """K2 schedule: "throughput" (default), "latency" (each row's entries in 4

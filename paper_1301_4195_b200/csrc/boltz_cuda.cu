@@ -66,6 +66,13 @@ struct boltz_ctx {
     int2* dEnt = nullptr;
     int* dRowStart = nullptr;
     int nent = 0, slab = 0;
+    // Hermitian mirror schedule (conv.cuh k_conv_mirror) for collide / RK2
+    bool mirror = false;
+    int64_t terms_plain = 0, terms_mirror = 0;  // executed K2 terms per cell eval (H table sizes)
+    double* dMH = nullptr;
+    int4* dMEnt = nullptr;
+    int* dItems = nullptr;  // nitems x kItemInts, then the longest-first order
+    int nitems = 0;
     // workspace (group layout), capacity in cells (multiple of 32)
     int64_t cap = 0;
     double2* dA = nullptr;
@@ -197,15 +204,47 @@ void build_projection(boltz_ctx* c) {
     c->pc.half = n / 2;
 }
 
-// Build the folded, pair-symmetric table H (conv.cuh) from the host G, one
-// k1-plane (N^5 doubles) at a time so the dense N^6 table is never resident.
-void build_table(boltz_ctx* c, const double* G_host) {
-    const int n = c->n, h = n / 2;
+// Is the caller's G mirror-symmetric, G(N-k, N-m) == G(k, m) for all k, m with
+// every index >= 1, to 1e-14 of max|G|?  (True for the weights of SPEC.md:93-166,
+// which depend on |zeta|, |xi|, |xi - beta zeta/2|; a table that is not keeps
+// the plain schedule only.)
+bool g_mirror_symmetric(int n, const double* G) {
+    const int64_t n3 = (int64_t)n * n * n;
+    double gmax = 0.0, dmax = 0.0;
+#pragma omp parallel for reduction(max : gmax, dmax) schedule(static)
+    for (int64_t k = 0; k < n3; ++k) {
+        const int k1 = (int)(k / (n * n)), k2 = (int)((k / n) % n), k3 = (int)(k % n);
+        if (!k1 || !k2 || !k3) continue;
+        const int64_t km = ((int64_t)(n - k1) * n + (n - k2)) * n + (n - k3);
+        for (int m1 = 1; m1 < n; ++m1)
+            for (int m2 = 1; m2 < n; ++m2)
+                for (int m3 = 1; m3 < n; ++m3) {
+                    const int64_t m = ((int64_t)m1 * n + m2) * n + m3;
+                    const int64_t mm = ((int64_t)(n - m1) * n + (n - m2)) * n + (n - m3);
+                    const double a = G[k * n3 + m], b = G[km * n3 + mm];
+                    gmax = std::max(gmax, std::fabs(a));
+                    dmax = std::max(dmax, std::fabs(a - b));
+                }
+    }
+    return dmax <= 1e-14 * gmax;
+}
+
+// Entries, their H offsets / band types and the slab term orders of one
+// schedule (plain: every entry BT_FULL in the conv_rows / pipe_rows / kcs
+// order; mirror: k_conv_mirror's typed single-tile bands).
+struct TableLayout {
+    std::vector<short2> term;
+    TermSet ts{};
+    std::vector<int4> entk;  // k1, k2, m1, m2
+    std::vector<int2> meta;  // H offset, band type
+    size_t hsize = 0;        // doubles
+};
+
+void layout_terms_plain(int n, TableLayout& T, int& slab) {
     const int t = conv_tile(n), nk = n / t;
     const int slab_kc = band_slab_kc(n, t);
-    c->slab = nk * slab_kc;
-    // slab term order (must match conv_rows)
-    std::vector<short2> term(c->slab, make_short2(-1, -1));
+    slab = nk * slab_kc;
+    T.term.assign(slab, make_short2(-1, -1));  // slab term order (must match conv_rows)
     for (int kc = 0; kc < nk; ++kc) {
         int pos = kc * slab_kc;
         for (int ti = 0; ti < nk; ++ti) {
@@ -213,13 +252,93 @@ void build_table(boltz_ctx* c, const double* G_host) {
             for (int i = 0; i < n; ++i) {
                 const int m3 = band_diag(n, nk, kc, ti, i);
                 for (int kk = 0; kk < t; ++kk)
-                    if (band_term(n, t, kc, sc, m3, kk)) term[pos++] = make_short2((short)(kc * t + kk), (short)m3);
+                    if (band_term(n, t, kc, sc, m3, kk)) T.term[pos++] = make_short2((short)(kc * t + kk), (short)m3);
             }
         }
     }
-    // entries: output row (k1,k2) x representative input row (m1,m2)
+    T.ts.slab_max = slab;
+    T.ts.slab[0] = slab;
+}
+
+void layout_terms_mirror(int n, TableLayout& T) {
+    int off = 0;
+    for (int ty = 0; ty < kBandTypes; ++ty) {
+        const int sl = band_slab_type(n, ty);
+        T.ts.off[ty] = off;
+        T.ts.slab[ty] = sl;
+        T.ts.slab_max = std::max(T.ts.slab_max, sl);
+        T.term.resize(off + sl, make_short2(-1, -1));
+        int pos = 0;
+        for (int m3 = 0; m3 < n; ++m3)  // band_diag(n, 1, 0, 0, i) == i
+            for (int kk = 0; kk < n; ++kk)
+                if (band_term_t(n, n, 0, 0, m3, kk, ty)) T.term[off + pos++] = make_short2((short)kk, (short)m3);
+        off += sl;
+    }
+}
+
+// H values of every entry of a layout into dH, from the host G one k1-plane at
+// a time (the dense N^6 table is never resident) or generated on the device.
+void fill_table(boltz_ctx* c, const double* G_host, TableLayout& T, double* dH) {
+    const int n = c->n;
+    const int nent = (int)T.entk.size();
+    std::vector<int> list(nent);
+    for (int e = 0; e < nent; ++e) list[e] = e;
+    std::stable_sort(list.begin(), list.end(), [&](int a, int b) { return T.entk[a].x < T.entk[b].x; });
+    std::vector<int> kstart(n + 1, 0);
+    for (int e = 0; e < nent; ++e) kstart[T.entk[e].x + 1]++;
+    for (int k = 0; k < n; ++k) kstart[k + 1] += kstart[k];
+    int4* dEntK = nullptr;
+    int2* dMeta = nullptr;
+    int* dList = nullptr;
+    short2* dTerm = nullptr;
+    double* dPlane = nullptr;
+    const size_t n3 = (size_t)n * n * n, plane = (size_t)n * n * n3;
+    try {
+        CK(cudaMalloc(&dEntK, (size_t)nent * sizeof(int4)));
+        CK(cudaMalloc(&dMeta, (size_t)nent * sizeof(int2)));
+        CK(cudaMalloc(&dList, (size_t)nent * sizeof(int)));
+        CK(cudaMalloc(&dTerm, T.term.size() * sizeof(short2)));
+        CK(cudaMemcpy(dEntK, T.entk.data(), (size_t)nent * sizeof(int4), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dMeta, T.meta.data(), (size_t)nent * sizeof(int2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dList, list.data(), (size_t)nent * sizeof(int), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(dTerm, T.term.data(), T.term.size() * sizeof(short2), cudaMemcpyHostToDevice));
+        TermSet ts = T.ts;
+        ts.term = dTerm;
+        const double dz = kPi / c->L, w3 = dz * dz * dz;
+        if (!G_host) {  // on-device generation (gen.cuh)
+            GenParams gp{};
+            gp.lambda = c->lambda; gp.beta = c->beta; gp.r0 = c->r0; gp.dz2 = dz * dz; gp.w3 = w3;
+            gp.panels = c->panels; gp.n = n; gp.gl = boltz_w::gauss16();
+            const long long total = (long long)nent * ts.slab_max;
+            k_gen_H<<<(unsigned)((total + 255) / 256), 256>>>(dH, dEntK, dMeta, nent, ts, gp);
+            CK(cudaGetLastError());
+        } else {
+            CK(cudaMalloc(&dPlane, plane * sizeof(double)));
+            for (int k1 = 0; k1 < n; ++k1) {
+                const int e0 = kstart[k1], e1 = kstart[k1 + 1];
+                const long long total = (long long)(e1 - e0) * ts.slab_max;
+                if (total == 0) continue;
+                CK(cudaMemcpy(dPlane, G_host + (size_t)k1 * plane, plane * sizeof(double), cudaMemcpyHostToDevice));
+                k_build_H<<<(unsigned)((total + 255) / 256), 256>>>(dPlane, dH, dEntK, dMeta, dList, e0, e1, ts, n,
+                                                                    w3);
+                CK(cudaGetLastError());
+            }
+        }
+        CK(cudaDeviceSynchronize());
+    } catch (...) {
+        cudaFree(dEntK); cudaFree(dMeta); cudaFree(dList); cudaFree(dTerm); cudaFree(dPlane);
+        throw;
+    }
+    cudaFree(dEntK); cudaFree(dMeta); cudaFree(dList); cudaFree(dTerm); cudaFree(dPlane);
+}
+
+// Plain schedule: output row (k1,k2) x representative input row (m1,m2); CSR
+// row_start + the longest-first order (conv.cuh conv_row).
+void build_table_plain(boltz_ctx* c, const double* G_host) {
+    const int n = c->n, h = n / 2;
+    TableLayout T;
+    layout_terms_plain(n, T, c->slab);
     std::vector<int2> ent;
-    std::vector<int4> entk;
     std::vector<int> row_start(n * n + 1, 0);
     for (int k1 = 0; k1 < n; ++k1)
         for (int k2 = 0; k2 < n; ++k2) {
@@ -229,7 +348,9 @@ void build_table(boltz_ctx* c, const double* G_host) {
                     const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
                     if (m1 < s1 || (m1 == s1 && m2 <= s2)) {
                         ent.push_back(make_int2((m1 * n + m2) * n, (s1 * n + s2) * n));
-                        entk.push_back(make_int4(k1, k2, m1, m2));
+                        T.meta.push_back(make_int2((int)T.hsize, BT_FULL));
+                        T.hsize += c->slab;
+                        T.entk.push_back(make_int4(k1, k2, m1, m2));
                     }
                 }
         }
@@ -244,52 +365,110 @@ void build_table(boltz_ctx* c, const double* G_host) {
         row_start.insert(row_start.end(), order.begin(), order.end());
         for (int r = 0; r < n * n; ++r) row_start.push_back(r);  // natural order
     }
-    const size_t hbytes = (size_t)c->nent * c->slab * sizeof(double);
+    if (T.hsize >= (size_t)UINT32_MAX) throw CudaError{"weight table too large for 32-bit H offsets"};
+    const size_t hbytes = T.hsize * sizeof(double);
     CK(cudaMalloc(&c->dH, hbytes));
     CK(cudaMalloc(&c->dEnt, ent.size() * sizeof(int2)));
     CK(cudaMalloc(&c->dRowStart, row_start.size() * sizeof(int)));
     CK(cudaMemcpy(c->dEnt, ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(c->dRowStart, row_start.data(), row_start.size() * sizeof(int), cudaMemcpyHostToDevice));
-    c->table_bytes = (int64_t)hbytes + (int64_t)ent.size() * 8 + (int64_t)row_start.size() * 4;
+    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 8 + (int64_t)row_start.size() * 4;
+    c->terms_plain = (int64_t)T.hsize;
+    fill_table(c, G_host, T, c->dH);
+}
 
-    int4* dEntK = nullptr;
-    short2* dTerm = nullptr;
-    double* dPlane = nullptr;
-    const size_t n3 = (size_t)n * n * n, plane = (size_t)n * n * n3;
-    try {
-        CK(cudaMalloc(&dEntK, entk.size() * sizeof(int4)));
-        CK(cudaMalloc(&dTerm, term.size() * sizeof(short2)));
-        CK(cudaMemcpy(dEntK, entk.data(), entk.size() * sizeof(int4), cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(dTerm, term.data(), term.size() * sizeof(short2), cudaMemcpyHostToDevice));
-        const double dz = kPi / c->L, w3 = dz * dz * dz;
-        if (!G_host) {  // on-device generation (gen.cuh)
-            GenParams gp{};
-            gp.lambda = c->lambda; gp.beta = c->beta; gp.r0 = c->r0; gp.dz2 = dz * dz; gp.w3 = w3;
-            gp.panels = c->panels; gp.n = n; gp.gl = boltz_w::gauss16();
-            const long long total = (long long)c->nent * c->slab;
-            k_gen_H<<<(unsigned)((total + 255) / 256), 256>>>(c->dH, dEntK, dTerm, c->nent, c->slab, gp);
-            CK(cudaGetLastError());
+// Mirror schedule (conv.cuh k_conv_mirror): work items over rows / row pairs.
+void build_table_mirror(boltz_ctx* c, const double* G_host) {
+    const int n = c->n, h = n / 2;
+    TableLayout T;
+    layout_terms_mirror(n, T);
+    std::vector<int4> ent;
+    std::vector<int> items;
+    std::vector<long long> cost;
+    auto add = [&](int k1, int k2, int m1, int m2, int ty) {
+        const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+        ent.push_back(make_int4((m1 * n + m2) * n, (s1 * n + s2) * n, (int)T.hsize, ty));
+        T.meta.push_back(make_int2((int)T.hsize, ty));
+        T.hsize += T.ts.slab[ty];
+        T.entk.push_back(make_int4(k1, k2, m1, m2));
+    };
+    // representative input rows of output row (k1,k2) in the plain order, with
+    // "interior" = all of m1, m2, s1, s2 in [2, N-2]
+    auto reps = [&](int k1, int k2, auto&& fn) {
+        for (int m1 = std::max(0, k1 - h + 1); m1 <= std::min(n - 1, k1 + h); ++m1)
+            for (int m2 = std::max(0, k2 - h + 1); m2 <= std::min(n - 1, k2 + h); ++m2) {
+                const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+                if (m1 < s1 || (m1 == s1 && m2 <= s2))
+                    fn(m1, m2, mirror_interior(n, m1) && mirror_interior(n, m2) && mirror_interior(n, s1) &&
+                                   mirror_interior(n, s2));
+            }
+    };
+    for (int k1 = 0; k1 < n; ++k1)
+        for (int k2 = 0; k2 < n; ++k2) {
+            const int r = k1 * n + k2;
+            const bool has = k1 >= 1 && k2 >= 1;
+            const int rm = has ? (n - k1) * n + (n - k2) : -1;
+            if (has && rm < r) continue;  // handled with its partner
+            const bool pair = has && rm != r;
+            const size_t first = ent.size();
+            int it[kItemInts];
+            it[0] = r;
+            it[1] = pair ? rm : -1;
+            it[2] = (int)ent.size();
+            if (!pair) {
+                reps(k1, k2, [&](int m1, int m2, bool) { add(k1, k2, m1, m2, BT_FULL); });
+                it[3] = it[2];
+                it[4] = it[5] = (int)ent.size();
+            } else {
+                const int j1 = n - k1, j2 = n - k2;
+                reps(k1, k2, [&](int m1, int m2, bool in) { if (in) add(k1, k2, m1, m2, BT_A); });
+                it[3] = (int)ent.size();
+                reps(k1, k2, [&](int m1, int m2, bool in) { if (!in) add(k1, k2, m1, m2, BT_FULL); });
+                reps(k1, k2, [&](int m1, int m2, bool in) { if (in) add(k1, k2, m1, m2, BT_REST); });
+                it[4] = (int)ent.size();
+                reps(j1, j2, [&](int m1, int m2, bool in) { if (!in) add(j1, j2, m1, m2, BT_FULL); });
+                reps(j1, j2, [&](int m1, int m2, bool in) { if (in) add(j1, j2, m1, m2, BT_REST); });
+                it[5] = (int)ent.size();
+            }
+            long long w = 0;
+            for (size_t e = first; e < ent.size(); ++e) w += T.ts.slab[ent[e].w];
+            cost.push_back(w);
+            items.insert(items.end(), it, it + kItemInts);
         }
-        if (G_host) CK(cudaMalloc(&dPlane, plane * sizeof(double)));
-        for (int k1 = 0; G_host && k1 < n; ++k1) {
-            CK(cudaMemcpy(dPlane, G_host + (size_t)k1 * plane, plane * sizeof(double), cudaMemcpyHostToDevice));
-            const int e0 = row_start[k1 * n], e1 = row_start[k1 * n + n];
-            const long long total = (long long)(e1 - e0) * c->slab;
-            const int blk = 256;
-            k_build_H<<<(unsigned)((total + blk - 1) / blk), blk>>>(dPlane, c->dH, dEntK, dTerm, e0, e1, c->slab, n,
-                                                                     w3);
-            CK(cudaGetLastError());
-        }
-        CK(cudaDeviceSynchronize());
-    } catch (...) {
-        cudaFree(dEntK);
-        cudaFree(dTerm);
-        cudaFree(dPlane);
-        throw;
+    c->nitems = (int)cost.size();
+    {   // longest items first (the conv_row lpt order, per item)
+        std::vector<int> order(c->nitems);
+        for (int i = 0; i < c->nitems; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+        items.insert(items.end(), order.begin(), order.end());
     }
-    cudaFree(dEntK);
-    cudaFree(dTerm);
-    cudaFree(dPlane);
+    if (T.hsize >= (size_t)INT32_MAX) throw CudaError{"mirror table too large for 32-bit H offsets"};
+    const size_t hbytes = T.hsize * sizeof(double);
+    CK(cudaMalloc(&c->dMH, hbytes));
+    CK(cudaMalloc(&c->dMEnt, ent.size() * sizeof(int4)));
+    CK(cudaMalloc(&c->dItems, items.size() * sizeof(int)));
+    CK(cudaMemcpy(c->dMEnt, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dItems, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 16 + (int64_t)items.size() * 4;
+    c->terms_mirror = (int64_t)T.hsize;
+    fill_table(c, G_host, T, c->dMH);
+}
+
+// the mirror schedule runs where the convolution is the single-tile TMA pipe
+constexpr bool mirror_eligible_n(int n) {
+    return n >= 8 && conv_tile(n) == n && conv_kernel_for(n) == 1 && BOLTZ_PIPE_TMA;
+}
+
+// Build the folded, pair-symmetric table H (conv.cuh) -- and, where eligible,
+// the mirror schedule's table beside it -- from the host G or on the device.
+void build_table(boltz_ctx* c, const double* G_host) {
+    c->table_bytes = 0;
+    build_table_plain(c, G_host);
+    bool mirror = mirror_eligible_n(c->n);
+    if (const char* e = std::getenv("BOLTZ_MIRROR")) mirror = mirror && std::atoi(e) != 0;
+    if (mirror && G_host) mirror = g_mirror_symmetric(c->n, G_host);
+    if (mirror) build_table_mirror(c, G_host);
+    c->mirror = mirror;
 }
 
 void ensure_workspace(boltz_ctx* c, int64_t cells) {
@@ -401,8 +580,33 @@ struct Launch {
         CK(cudaGetLastError());
     }
     // group complex c->dA -> group complex (s_k * Qhat) in c->dB
-    static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s) {
+    // hermitian: the input is the transform of a real f (collide / RK2), so the
+    // mirror schedule may run; evaluate_qhat of a caller's fhat never does
+    static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s, bool hermitian = false) {
         const int64_t ng = (nc + 31) / 32;
+        if constexpr (mirror_eligible_n(N)) {
+            if (hermitian && c->mirror && c->schedule == 0) {
+                const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
+                static bool configured = false;
+                if (!configured) {
+                    CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    configured = true;
+                }
+                dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+                // longest items first in every column: items range from single rows to
+                // row pairs (~1.6x), and LPT everywhere measured best (11.17 ms against
+                // 11.26 in the last column only and 11.49 never)
+                int lpt = 0;
+                if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
+                Timed t_(c, KIND_CONV, s);
+                k_conv_mirror<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dItems,
+                                                                         c->dItems + kItemInts * c->nitems, (int)ng,
+                                                                         lpt);
+                CK(cudaGetLastError());
+                return;
+            }
+        }
         if constexpr (conv_kernel_for(N) == 1 && conv_tile(N) == N &&
                       kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             if (c->schedule > 0) {
@@ -678,12 +882,14 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
                        cudaStream_t s, double* max_imag, Fn&& fn) {
     std::vector<int64_t> bounds{0};
     auto up32 = [](int64_t x) { return (x + kLanes - 1) / kLanes * kLanes; };
-    // Chunk schedule (relative weights 2,6,8,8,6,2; measured best on B200 for cfg2
-    // among 4-8 chunk schedules, 602k vs 564k evals/s for the old 4-chunk one):
-    // the first H2D and the last D2H cannot overlap compute, so the edge chunks
-    // are small; odd chunks run on a second stream, so each chunk's last wave
-    // overlaps the next chunk's work.  BOLTZ_HOST_CHUNKS="a,b,..." overrides.
-    std::vector<double> w{2, 6, 8, 8, 6, 2};
+    // Chunk schedule (relative weights, measured best on B200 for cfg2): the first
+    // H2D and the last D2H cannot overlap compute, so the edge chunks are small;
+    // odd chunks run on a second stream, so each chunk's last wave overlaps the
+    // next chunk's work.  With the mirror schedule, whose work items are row
+    // pairs and which only pays from ~1.5k cells up, fewer larger chunks win:
+    // 1,3,3,1 (621k evals/s); the plain schedule prefers 2,6,8,8,6,2 (602k).
+    // BOLTZ_HOST_CHUNKS="a,b,..." overrides.
+    std::vector<double> w = c->mirror ? std::vector<double>{1, 3, 3, 1} : std::vector<double>{2, 6, 8, 8, 6, 2};
     if (const char* sched = std::getenv("BOLTZ_HOST_CHUNKS")) {
         w.clear();
         for (const char* p = sched; *p;) {
@@ -899,6 +1105,7 @@ int boltz_destroy(boltz_ctx* c) {
     if (!c) return BOLTZ_OK;
     cudaSetDevice(c->device);
     cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
+    cudaFree(c->dMH); cudaFree(c->dMEnt); cudaFree(c->dItems);
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
@@ -965,7 +1172,7 @@ int boltz_qhat_batch(boltz_ctx* c, const double* fhat, double* qhat, int64_t nce
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
                                    Lx::pack_complex(c, in, c->dA, nc, 0, s);
-                                   Lx::conv(c, nc, s);
+                                   Lx::conv(c, nc, s, std::getenv("BOLTZ_QHAT_MIRROR") != nullptr);  // debug
                                    Lx::unpack_complex(c, c->dB, out, nc, 1, s);
                                });
                            });
@@ -995,7 +1202,7 @@ int boltz_collide_batch(boltz_ctx* c, const double* f, double* q, int64_t ncells
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
                                    Lx::forward(c, in, nc, s);
-                                   Lx::conv(c, nc, s);
+                                   Lx::conv(c, nc, s, true);  // fhat of a real f: mirror schedule
                                    Lx::inverse_project(c, nullptr, out, nc, inv_eps, s);
                                });
                            });
@@ -1014,10 +1221,10 @@ int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double i
                                    using Lx = decltype(L);
                                    // stage 1: f* = f + dt/2 * collide(f)
                                    Lx::forward(c, out, nc, s);
-                                   Lx::conv(c, nc, s);
+                                   Lx::conv(c, nc, s, true);  // fhat of a real f: mirror schedule
                                    // stage 2: f <- f + dt * collide(f*), f* handed over as fhat(f*)
                                    Lx::inverse_project_forward(c, out, c->dFs, nc, 0.5 * dt * inv_eps, s);
-                                   Lx::conv(c, nc, s);
+                                   Lx::conv(c, nc, s, true);  // fhat of a real f: mirror schedule
                                    Lx::inverse_project(c, out, out, nc, dt * inv_eps, s);
                                });
                            });
@@ -1162,6 +1369,13 @@ int boltz_marginal_batch(boltz_ctx* c, const double* f, double* g, int64_t ncell
                                CK(cudaGetLastError());
                            });
     });
+}
+
+int boltz_schedule_terms(boltz_ctx* c, int64_t* plain, int64_t* mirror) {
+    if (!c) return BOLTZ_ERR_CONFIG;
+    if (plain) *plain = c->terms_plain;
+    if (mirror) *mirror = c->mirror ? c->terms_mirror : 0;
+    return BOLTZ_OK;
 }
 
 int boltz_set_schedule(boltz_ctx* c, int schedule) {

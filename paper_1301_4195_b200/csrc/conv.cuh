@@ -71,6 +71,44 @@ __host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m
     return any;
 }
 
+// ---------------------------------------------------------------------------
+// Band types of the Hermitian mirror schedule (k_conv_mirror).  For real f,
+// fhat(N-m) = conj fhat(m) (index mirror per axis) and G(N-k, N-m) = G(k, m)
+// (G depends on |zeta|, |xi|, |xi - beta zeta/2|).  A folded term (k, {m, s})
+// whose six indices m_a, s_a all lie in [2, N-2] -- where both trapezoid
+// weights are 1 -- is the complex conjugate of its mirror term (N-k, {N-m,
+// N-s}).  So the interior part of output row k is summed once and written,
+// conjugated and k3-reversed, into row N-k as well.
+//   BT_FULL every band term
+//   BT_A    interior terms (m3, s3 in [2, N-2]) with k3 >= 1: these are mirrored
+//   BT_REST the others: non-interior terms and the k3 = 0 column, whose mirror
+//           (k3 = N) does not exist -- summed directly, for r and for N - r
+// (two typed bands plus the full one keep the unrolled code small)
+// ---------------------------------------------------------------------------
+enum BandType { BT_FULL = 0, BT_A = 1, BT_REST = 2 };
+constexpr int kBandTypes = 3;
+__host__ __device__ constexpr bool mirror_interior(int n, int a) { return a >= 2 && a <= n - 2; }
+__host__ __device__ constexpr bool type_term(int n, int ty, int k3, int m3) {
+    const int s3 = k3 - m3 + n / 2;
+    const bool mirrored = mirror_interior(n, m3) && mirror_interior(n, s3) && k3 != 0;
+    return ty == BT_FULL ? true : ty == BT_A ? mirrored : !mirrored;
+}
+__host__ __device__ constexpr bool band_term_t(int n, int t, int kc, int sc, int m3, int kk, int ty) {
+    return band_term(n, t, kc, sc, m3, kk) && type_term(n, ty, kc * t + kk, m3);
+}
+__host__ __device__ constexpr bool diag_used_t(int n, int t, int kc, int sc, int m3, int ty) {
+    bool any = false;
+    for (int kk = 0; kk < t; ++kk) any = any || band_term_t(n, t, kc, sc, m3, kk, ty);
+    return any;
+}
+// H slab length (even) of one single-tile (T == N) entry of band type ty
+__host__ __device__ constexpr int band_slab_type(int n, int ty) {
+    int c = 0;
+    for (int m3 = 0; m3 < n; ++m3)
+        for (int kk = 0; kk < n; ++kk) c += band_term_t(n, n, 0, 0, m3, kk, ty) ? 1 : 0;
+    return (c + 1) & ~1;
+}
+
 // Register tile width and kernel per N, chosen by measurement on B200
 // (scripts/ab_conv.py, scripts/ab_n32.sh; algorithmic TFLOP/s, round 1):
 //   N=16: T=16 k_conv_pipe 47.5 | T=16 kcs 46.4 | T=8 kcs 39.7 | T=16 k_conv 41.1
@@ -108,18 +146,18 @@ constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the 
 
 // one tile of terms: acc[kk] += H * x[m3] * y[j]; the x source and the
 // per-diagonal hook (x refill) are policies
-template <int N, int T, int NK, int KC, int TI, typename XAt, typename AfterDiag>
+template <int N, int T, int NK, int KC, int TI, int TY = BT_FULL, typename XAt, typename AfterDiag>
 __device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[T], XAt x_at, const double2* hs,
                                           int& p, double2& hb, AfterDiag after) {
     constexpr int SC = band_tile_sc(NK, KC, TI);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const int m3 = band_diag(N, NK, KC, TI, i);
-        if (!diag_used(N, T, KC, SC, m3)) continue;
+        if (!diag_used_t(N, T, KC, SC, m3, TY)) continue;
         const double2 xm = x_at(m3);
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) {
-            if (!band_term(N, T, KC, SC, m3, kk)) continue;
+            if (!band_term_t(N, T, KC, SC, m3, kk, TY)) continue;
             const int j = KC * T + kk - m3 + N / 2 - SC * T;  // y chunk slot
             double h;
             if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
@@ -621,35 +659,164 @@ k_conv_seg_reduce(const double2* __restrict__ P, double2* __restrict__ B, long l
     B[i] = make_double2(sg * sum.x, sg * sum.y);
 }
 
-// ---- H table builder: H[e][slab pos] from one k1-plane of the caller's dense
-// zeta-major G: Gk1[(k2*N + k3) * N^3 + m].  Entry e = output
-// row (k1,k2) x representative input row (m1,m2).  term[pos] = (k3, m3) or
-// (-1,-1) for padding.  omega_m = c3(m) dzeta^3 (velocity_grid.hpp:43-46).
+// ---------------------------------------------------------------------------
+// k_conv_mirror (single-tile rows, TMA staging): the Hermitian mirror schedule.
+// A work item is an output row r with no mirror partner (k1 = 0, k2 = 0 or
+// r = N - r), or a pair (r, r' = N - r).  Its entries are one contiguous list
+//     [A(r) | FULL(r) | REST(r) | FULL(r') | REST(r')]
+// (int4 {x row, y row, H offset, band type}), staged by one continuous TMA
+// pipeline.  One warp (one 32-cell group) runs the item:
+//   after A(r):   acc holds the interior sums of r; conj(acc[N - k3']) goes to
+//                 row r' of B (k3' = 1..N-1, 0 at k3' = 0); r keeps summing
+//   after B(r):   row r is written; acc reloads row r' of B
+//   at the end:   row r' (or r for a single row) is written
+// The warp owns both rows, so the order is fixed and no other warp touches
+// them.  Only for collide / RK2, whose fhat is the transform of a real f.
+// item[] = {r, r' (-1: none), begin, end of A, begin of r', end}.
+// ---------------------------------------------------------------------------
+constexpr int kItemInts = 6;
+
+template <int N>
+__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
+k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+              const int4* __restrict__ ent, const int* __restrict__ items, const int* __restrict__ order, int ngroups,
+              int lpt_from) {
+    using PL = PipeLayout<N>;
+    static_assert(PL::TMA, "the mirror schedule runs on the TMA pipe (single-tile rows)");
+    constexpr int T = N, N3 = N * N * N;
+    extern __shared__ __align__(16) char smem[];
+    const int* it = items + kItemInts * ((int)blockIdx.y >= lpt_from ? __ldg(order + blockIdx.x) : (int)blockIdx.x);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * kConvWarps + wid;
+    if (g >= ngroups) return;
+    const int r = __ldg(it), rm = __ldg(it + 1);
+    const int e_begin = __ldg(it + 2), e_endA = __ldg(it + 3), e_rm = __ldg(it + 4), e_end = __ldg(it + 5);
+    char* wsm = smem + wid * PL::WARP_BYTES;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + 3 * PL::X_BYTES + 2 * PL::H_BYTES);
+    const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
+    const double2* Abase = A + (size_t)g * N3 * kLanes;
+    double2* Bm = B + ((size_t)g * N3 + (size_t)(rm < 0 ? 0 : rm) * N) * kLanes + lane;
+    constexpr int slab_bytes[kBandTypes] = {band_slab_type(N, BT_FULL) * 8, band_slab_type(N, BT_A) * 8,
+                                            band_slab_type(N, BT_REST) * 8};
+    auto issue = [&](int slot, int4 en) {
+        if (lane == 0) {
+            const unsigned hb = (unsigned)slab_bytes[en.w];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + hb);
+            bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
+            bulk_g2s(wsm + 2 * PL::X_BYTES, Abase + (size_t)en.y * kLanes, PL::X_BYTES, bar + slot);
+            bulk_g2s(wsm + 3 * PL::X_BYTES + slot * PL::H_BYTES, H + (size_t)(unsigned)en.z, hb, bar + slot);
+        }
+    };
+    double2 acc[T];
+#pragma unroll
+    for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+    // the item's segment boundaries (r' parts only for pairs)
+    auto boundary = [&](int e) {
+        if (rm < 0) return;
+        if (e == e_endA) {  // A(r) done: its conjugate, k3-reversed, seeds row r' (row r keeps summing)
+            Bm[0] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int k = 1; k < N; ++k) Bm[(size_t)k * kLanes] = make_double2(acc[N - k].x, -acc[N - k].y);
+        }
+        if (e == e_rm) {  // row r complete: write it, continue with row r'
+            write_row<N, T>(B, g, r, 0, lane, acc);
+#pragma unroll
+            for (int k = 0; k < N; ++k) acc[k] = Bm[(size_t)k * kLanes];
+        }
+    };
+    if (e_begin < e_end) {
+        if (lane == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int4 en = __ldg(ent + e_begin);
+        int4 en_ahead = e_begin + 1 < e_end ? __ldg(ent + e_begin + 1) : en;
+        issue(0, en);
+        mbar_wait(bar, 0);
+        double2 y[T];
+#pragma unroll
+        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+        for (int e = e_begin; e < e_end; ++e) {
+            const int i = e - e_begin, cur = i & 1;
+            const bool more = e + 1 < e_end;
+            const int4 nx = en_ahead;
+            if (e + 2 < e_end) en_ahead = __ldg(ent + e + 2);
+            boundary(e);
+            __syncwarp();  // every lane read y (registers) and is done with slot cur^1
+            if (more) issue(cur ^ 1, nx);
+            const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
+            const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
+            int p = 0;
+            double2 hb = make_double2(0.0, 0.0);
+            auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
+            auto none = [](int, int) {};
+            switch (en.w) {  // warp-uniform
+                case BT_A: band_tile<N, T, 1, 0, 0, BT_A>(acc, y, xat, hs, p, hb, none); break;
+                case BT_REST: band_tile<N, T, 1, 0, 0, BT_REST>(acc, y, xat, hs, p, hb, none); break;
+                default: band_tile<N, T, 1, 0, 0, BT_FULL>(acc, y, xat, hs, p, hb, none); break;
+            }
+            if (more) {
+                mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+#pragma unroll
+                for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+            }
+            en = nx;
+        }
+    }
+    boundary(e_end);  // boundaries that coincide with the end of the list
+    write_row<N, T>(B, g, rm >= 0 ? rm : r, 0, lane, acc);
+}
+
+// ---- H table builder.  Entry e = output row (k1,k2) x representative input
+// row (m1,m2) (entk = {k1,k2,m1,m2}) with meta[e] = {H offset, band type};
+// term[ts.off[type] + pos] = (k3, m3) of slab position pos, or (-1,-1) for
+// padding.  Folding: H = G'(k,m) + G'(k,sigma m), G' = G omega_m,
+// omega_m = c3(m) dzeta^3 (velocity_grid.hpp:43-46); the self-paired input
+// row keeps its m3 <= s3 half.
+struct TermSet {
+    const short2* term;
+    int off[kBandTypes];
+    int slab[kBandTypes];
+    int slab_max;
+};
+
+template <typename GF>
+__device__ __forceinline__ double folded_h(int n, double w3, int4 q, short2 km, GF&& G) {
+    const int h = n / 2;
+    const int k2 = q.y, m1 = q.z, m2 = q.w, k3 = km.x, m3 = km.y;
+    const int s1 = q.x - m1 + h, s2 = k2 - m2 + h, s3 = k3 - m3 + h;
+    const double wm = axis_coeff(n, m1) * axis_coeff(n, m2) * axis_coeff(n, m3) * w3;
+    const double ws = axis_coeff(n, s1) * axis_coeff(n, s2) * axis_coeff(n, s3) * w3;
+    const bool self_row = (m1 == s1) && (m2 == s2);
+    if (!self_row || m3 < s3) return G(k3, m1, m2, m3) * wm + G(k3, s1, s2, s3) * ws;
+    if (m3 == s3) return G(k3, m1, m2, m3) * wm;
+    return 0.0;
+}
+
+// from one k1-plane of the caller's dense zeta-major G:
+// Gk1[(k2*N + k3) * N^3 + m]; list[e_begin..e_end) = the entries of that plane
 __global__ void k_build_H(const double* __restrict__ Gk1, double* __restrict__ H, const int4* __restrict__ entk,
-                          const short2* __restrict__ term, int e_begin, int e_end, int slab, int n, double w3) {
+                          const int2* __restrict__ meta, const int* __restrict__ list, int e_begin, int e_end,
+                          TermSet ts, int n, double w3) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long total = (long long)(e_end - e_begin) * slab;
-    if (tid >= total) return;
-    const int e = e_begin + (int)(tid / slab);
-    const int pos = (int)(tid % slab);
-    const int4 q = entk[e];  // k1, k2, m1, m2
-    const short2 km = term[pos];
+    if (tid >= (long long)(e_end - e_begin) * ts.slab_max) return;
+    const int e = list[e_begin + (int)(tid / ts.slab_max)];
+    const int pos = (int)(tid % ts.slab_max);
+    const int2 mt = meta[e];
+    if (pos >= ts.slab[mt.y]) return;
+    const int4 q = entk[e];
+    const short2 km = ts.term[ts.off[mt.y] + pos];
     double out = 0.0;
     if (km.x >= 0) {
-        const int h = n / 2;
-        const int k2 = q.y, m1 = q.z, m2 = q.w, k3 = km.x, m3 = km.y;
-        const int s1 = q.x - m1 + h, s2 = k2 - m2 + h, s3 = k3 - m3 + h;
         const long long n3 = (long long)n * n * n;
-        const double* Gk = Gk1 + ((long long)k2 * n + k3) * n3;
-        const long long mf = ((long long)m1 * n + m2) * n + m3;
-        const long long sf = ((long long)s1 * n + s2) * n + s3;
-        const double wm = axis_coeff(n, m1) * axis_coeff(n, m2) * axis_coeff(n, m3) * w3;
-        const double ws = axis_coeff(n, s1) * axis_coeff(n, s2) * axis_coeff(n, s3) * w3;
-        const bool self_row = (m1 == s1) && (m2 == s2);
-        if (!self_row || m3 < s3) out = Gk[mf] * wm + Gk[sf] * ws;
-        else if (m3 == s3) out = Gk[mf] * wm;
+        out = folded_h(n, w3, q, km, [&](int k3, int a1, int a2, int a3) {
+            return Gk1[((long long)q.y * n + k3) * n3 + ((long long)a1 * n + a2) * n + a3];
+        });
     }
-    H[(size_t)e * slab + pos] = out;
+    H[(size_t)(unsigned)mt.x + pos] = out;
 }
 
 }  // namespace boltz_gpu

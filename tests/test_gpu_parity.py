@@ -164,15 +164,15 @@ def test_device_generated_table_matches_host_table(gpu, O, n, L, lam):
 
 
 def test_host_pipeline_matches_device_path(gpu):
-    """Host-memory calls are chunked (6 chunks here) and pipelined over two copy
-    and two compute streams with two workspaces; the result is bitwise the
-    device-memory call's (ragged last chunk)."""
+    """Host-memory calls are chunked and pipelined over two copy and two compute
+    streams with two workspaces; the result is bitwise the device-memory call's
+    (ragged last chunk)."""
     import torch
     n, L = 8, 5.0
     grid = VelocityGrid.create(n, L)
     f = scenarios.mixture_cells(grid, 1100, seed=21)
     with _op(n, L) as op:
-        qh, mih = op.collide(f, with_max_imag=True)          # host path, 6 chunks
+        qh, mih = op.collide(f, with_max_imag=True)          # host path, chunked
         fd = torch.from_numpy(f).to(gpu)
         qd, mid = op.collide(fd, with_max_imag=True)        # device path
         assert np.array_equal(qh, qd.cpu().numpy())
@@ -324,3 +324,24 @@ def test_full_size_batches_properties(gpu, n, L, cells):
         op.collision_rk2(g, 0.01)
         mg = op.moments(g)
         assert float(((mg[:, :5] - mf[:, :5]).abs().max(dim=1).values / rho).max()) < 1e-12
+
+
+@pytest.mark.parametrize("n,L", [(8, 5.0), (12, 6.0), (16, 6.0)])
+def test_mirror_schedule_active_and_consistent(gpu, O, n, L):
+    """collide / RK2 at N <= 16 run the Hermitian mirror schedule (fewer executed
+    terms than the plain fold); its Q matches the oracle to 1e-10 and
+    evaluate_qhat's plain-schedule composition to round-off."""
+    import torch
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 7, seed=53)
+    G = table(n, L)
+    with _op(n, L) as op:
+        plain, mirror = op.schedule_terms()
+        assert 0 < mirror < plain
+        q = op.collide(f)                              # mirror schedule
+        fh = op.forward(f)
+        q2 = op.conserve(op.inverse(op.evaluate_qhat(fh))[0])  # plain schedule, composed
+    for c in range(7):
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q[c], ref) < TOL_Q
+    assert rel_max(q, q2) < 1e-12
