@@ -1172,7 +1172,7 @@ int boltz_qhat_batch(boltz_ctx* c, const double* fhat, double* qhat, int64_t nce
                                dispatch(c->n, [&](auto L) {
                                    using Lx = decltype(L);
                                    Lx::pack_complex(c, in, c->dA, nc, 0, s);
-                                   Lx::conv(c, nc, s, std::getenv("BOLTZ_QHAT_MIRROR") != nullptr);  // debug
+                                   Lx::conv(c, nc, s);  // a caller's fhat: plain schedule
                                    Lx::unpack_complex(c, c->dB, out, nc, 1, s);
                                });
                            });
