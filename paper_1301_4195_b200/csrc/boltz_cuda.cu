@@ -261,17 +261,26 @@ void layout_terms_plain(int n, TableLayout& T, int& slab) {
 }
 
 void layout_terms_mirror(int n, TableLayout& T) {
+    // slab of one typed band in band_tile order (band_diag(n, 1, 0, 0, i) == i), padded to even
+    auto typed = [&](int ty) {
+        std::vector<short2> v(band_slab_type(n, ty), make_short2(-1, -1));
+        int pos = 0;
+        for (int m3 = 0; m3 < n; ++m3)
+            for (int kk = 0; kk < n; ++kk)
+                if (band_term_t(n, n, 0, 0, m3, kk, ty)) v[pos++] = make_short2((short)kk, (short)m3);
+        return v;
+    };
+    const auto a = typed(BT_A), rest = typed(BT_REST);
     int off = 0;
     for (int ty = 0; ty < kBandTypes; ++ty) {
-        const int sl = band_slab_type(n, ty);
+        std::vector<short2> v = ty == BT_A ? a : rest;
+        if (ty == BT_FULL) v.insert(v.begin(), a.begin(), a.end());  // k_conv_mirror: A half, then REST half
+        const int sl = mirror_slab(n, ty);
+        if ((int)v.size() != sl) throw CudaError{"mirror slab layout mismatch"};
         T.ts.off[ty] = off;
         T.ts.slab[ty] = sl;
         T.ts.slab_max = std::max(T.ts.slab_max, sl);
-        T.term.resize(off + sl, make_short2(-1, -1));
-        int pos = 0;
-        for (int m3 = 0; m3 < n; ++m3)  // band_diag(n, 1, 0, 0, i) == i
-            for (int kk = 0; kk < n; ++kk)
-                if (band_term_t(n, n, 0, 0, m3, kk, ty)) T.term[off + pos++] = make_short2((short)kk, (short)m3);
+        T.term.insert(T.term.end(), v.begin(), v.end());
         off += sl;
     }
 }
@@ -586,7 +595,7 @@ struct Launch {
         const int64_t ng = (nc + 31) / 32;
         if constexpr (mirror_eligible_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
-                const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
+                const int smem = kConvWarps * MirrorLayout<N>::WARP_BYTES;
                 static bool configured = false;
                 if (!configured) {
                     CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

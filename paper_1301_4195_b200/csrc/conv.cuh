@@ -79,11 +79,11 @@ __host__ __device__ constexpr bool diag_used(int n, int t, int kc, int sc, int m
 // weights are 1 -- is the complex conjugate of its mirror term (N-k, {N-m,
 // N-s}).  So the interior part of output row k is summed once and written,
 // conjugated and k3-reversed, into row N-k as well.
-//   BT_FULL every band term
+//   BT_FULL every band term (in the mirror table: the A terms, then the REST terms)
 //   BT_A    interior terms (m3, s3 in [2, N-2]) with k3 >= 1: these are mirrored
 //   BT_REST the others: non-interior terms and the k3 = 0 column, whose mirror
 //           (k3 = N) does not exist -- summed directly, for r and for N - r
-// (two typed bands plus the full one keep the unrolled code small)
+// (the kernel unrolls the two typed bands only: a FULL entry runs both)
 // ---------------------------------------------------------------------------
 enum BandType { BT_FULL = 0, BT_A = 1, BT_REST = 2 };
 constexpr int kBandTypes = 3;
@@ -107,6 +107,12 @@ __host__ __device__ constexpr int band_slab_type(int n, int ty) {
     for (int m3 = 0; m3 < n; ++m3)
         for (int kk = 0; kk < n; ++kk) c += band_term_t(n, n, 0, 0, m3, kk, ty) ? 1 : 0;
     return (c + 1) & ~1;
+}
+// H slab length of a mirror-table entry: a BT_FULL entry holds its A terms,
+// then its REST terms, and runs as the two typed bands back to back (one copy
+// of the unrolled term code instead of three)
+__host__ __device__ constexpr int mirror_slab(int n, int ty) {
+    return ty == BT_FULL ? band_slab_type(n, BT_A) + band_slab_type(n, BT_REST) : band_slab_type(n, ty);
 }
 
 // Register tile width and kernel per N, chosen by measurement on B200
@@ -677,12 +683,19 @@ k_conv_seg_reduce(const double2* __restrict__ P, double2* __restrict__ B, long l
 constexpr int kItemInts = 6;
 
 template <int N>
+struct MirrorLayout {
+    static constexpr int X_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = mirror_slab(N, BT_FULL) * 8;
+    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+};
+
+template <int N>
 __global__ void __launch_bounds__(kLanes* kConvWarps, 1)
 k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
               const int4* __restrict__ ent, const int* __restrict__ items, const int* __restrict__ order, int ngroups,
               int lpt_from) {
-    using PL = PipeLayout<N>;
-    static_assert(PL::TMA, "the mirror schedule runs on the TMA pipe (single-tile rows)");
+    using PL = MirrorLayout<N>;
+    static_assert(PipeLayout<N>::TMA, "the mirror schedule runs on the TMA pipe (single-tile rows)");
     constexpr int T = N, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
     const int* it = items + kItemInts * ((int)blockIdx.y >= lpt_from ? __ldg(order + blockIdx.x) : (int)blockIdx.x);
@@ -696,11 +709,10 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
     const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
     const double2* Abase = A + (size_t)g * N3 * kLanes;
     double2* Bm = B + ((size_t)g * N3 + (size_t)(rm < 0 ? 0 : rm) * N) * kLanes + lane;
-    constexpr int slab_bytes[kBandTypes] = {band_slab_type(N, BT_FULL) * 8, band_slab_type(N, BT_A) * 8,
-                                            band_slab_type(N, BT_REST) * 8};
     auto issue = [&](int slot, int4 en) {
         if (lane == 0) {
-            const unsigned hb = (unsigned)slab_bytes[en.w];
+            const unsigned hb = 8u * (en.w == BT_A ? mirror_slab(N, BT_A) : en.w == BT_REST ? mirror_slab(N, BT_REST)
+                                                                                         : mirror_slab(N, BT_FULL));
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + hb);
             bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
@@ -749,14 +761,17 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
             if (more) issue(cur ^ 1, nx);
             const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
             const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
-            int p = 0;
-            double2 hb = make_double2(0.0, 0.0);
             auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
             auto none = [](int, int) {};
-            switch (en.w) {  // warp-uniform
-                case BT_A: band_tile<N, T, 1, 0, 0, BT_A>(acc, y, xat, hs, p, hb, none); break;
-                case BT_REST: band_tile<N, T, 1, 0, 0, BT_REST>(acc, y, xat, hs, p, hb, none); break;
-                default: band_tile<N, T, 1, 0, 0, BT_FULL>(acc, y, xat, hs, p, hb, none); break;
+            double2 hb = make_double2(0.0, 0.0);
+            if (en.w != BT_REST) {  // warp-uniform: A, or the A half of a FULL entry
+                int p = 0;
+                band_tile<N, T, 1, 0, 0, BT_A>(acc, y, xat, hs, p, hb, none);
+            }
+            if (en.w != BT_A) {  // REST, or the REST half of a FULL entry
+                int p = 0;
+                band_tile<N, T, 1, 0, 0, BT_REST>(acc, y, xat, hs + (en.w == BT_FULL ? mirror_slab(N, BT_A) / 2 : 0),
+                                                  p, hb, none);
             }
             if (more) {
                 mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
