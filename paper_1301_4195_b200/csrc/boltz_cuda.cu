@@ -73,6 +73,9 @@ struct boltz_ctx {
     int4* dMEnt = nullptr;
     int* dItems = nullptr;  // nitems x kItemInts, then the longest-first order
     int nitems = 0;
+    int* dListP = nullptr;  // k_conv_kcsm (N = 24, 32): phase-0 / phase-1 row lists
+    int* dListQ = nullptr;
+    int nP = 0, nQ = 0;
     // workspace (group layout), capacity in cells (multiple of 32)
     int64_t cap = 0;
     double2* dA = nullptr;
@@ -463,10 +466,119 @@ void build_table_mirror(boltz_ctx* c, const double* G_host) {
     fill_table(c, G_host, T, c->dMH);
 }
 
+// Mirror schedule of the k-chunked kcs kernels (conv.cuh k_conv_kcsm): entries
+// as in build_table_mirror; phase-0 rows = pair leaders (A entries), phase-1
+// rows = every output row (FULL / REST entries).
+void layout_terms_kcsm(int n, TableLayout& T) {
+    const int t = conv_tile(n), nk = n / t;
+    int off = 0;
+    for (int ty = 0; ty < kBandTypes; ++ty) {
+        const int stride = kcsm_slab(n, ty);
+        std::vector<short2> v((size_t)nk * stride, make_short2(-1, -1));
+        for (int kc = 0; kc < nk; ++kc)
+            for (int ti = 0; ti < nk; ++ti) {
+                const int sc = band_tile_sc(nk, kc, ti);
+                for (int piece : {(int)BT_A, (int)BT_REST}) {
+                    if ((piece == BT_A && ty == BT_REST) || (piece == BT_REST && ty == BT_A)) continue;
+                    int pos = kc * stride + kcsm_piece_off(n, t, kc, ti, ty, piece);
+                    for (int i = 0; i < n; ++i) {  // band_tile's visiting order
+                        const int m3 = band_diag(n, nk, kc, ti, i);
+                        for (int kk = 0; kk < t; ++kk)
+                            if (band_term_t(n, t, kc, sc, m3, kk, piece))
+                                v[pos++] = make_short2((short)(kc * t + kk), (short)m3);
+                    }
+                }
+            }
+        T.ts.off[ty] = off;
+        T.ts.slab[ty] = nk * stride;
+        T.ts.slab_max = std::max(T.ts.slab_max, nk * stride);
+        T.term.insert(T.term.end(), v.begin(), v.end());
+        off += nk * stride;
+    }
+}
+
+void build_table_mirror_kcs(boltz_ctx* c, const double* G_host) {
+    const int n = c->n, h = n / 2;
+    TableLayout T;
+    layout_terms_kcsm(n, T);
+    std::vector<int4> ent;
+    auto add = [&](int k1, int k2, int m1, int m2, int ty) {
+        const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+        ent.push_back(make_int4((m1 * n + m2) * n, (s1 * n + s2) * n, (int)T.hsize, ty));
+        T.meta.push_back(make_int2((int)T.hsize, ty));
+        T.hsize += T.ts.slab[ty];
+        T.entk.push_back(make_int4(k1, k2, m1, m2));
+    };
+    auto reps = [&](int k1, int k2, auto&& fn) {
+        for (int m1 = std::max(0, k1 - h + 1); m1 <= std::min(n - 1, k1 + h); ++m1)
+            for (int m2 = std::max(0, k2 - h + 1); m2 <= std::min(n - 1, k2 + h); ++m2) {
+                const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+                if (m1 < s1 || (m1 == s1 && m2 <= s2))
+                    fn(m1, m2, mirror_interior(n, m1) && mirror_interior(n, m2) && mirror_interior(n, s1) &&
+                                   mirror_interior(n, s2));
+            }
+    };
+    struct Rows {
+        std::vector<int> start, row, aux;
+        std::vector<long long> cost;
+    } P, Q;
+    auto partner = [&](int k1, int k2) { return (k1 >= 1 && k2 >= 1) ? (n - k1) * n + (n - k2) : -1; };
+    for (int phase = 0; phase < 2; ++phase)
+        for (int k1 = 0; k1 < n; ++k1)
+            for (int k2 = 0; k2 < n; ++k2) {
+                const int r = k1 * n + k2, rm = partner(k1, k2);
+                const bool pair = rm >= 0 && rm != r;
+                Rows& R = phase == 0 ? P : Q;
+                if (phase == 0 && !(pair && r < rm)) continue;
+                const size_t first = ent.size();
+                R.start.push_back((int)first);
+                R.row.push_back(r);
+                R.aux.push_back(phase == 0 ? rm : (pair ? 1 : 0));
+                if (phase == 0)
+                    reps(k1, k2, [&](int m1, int m2, bool in) { if (in) add(k1, k2, m1, m2, BT_A); });
+                else
+                    reps(k1, k2, [&](int m1, int m2, bool in) { add(k1, k2, m1, m2, pair && in ? BT_REST : BT_FULL); });
+                long long w = 0;
+                for (size_t e = first; e < ent.size(); ++e) w += T.ts.slab[ent[e].w];
+                R.cost.push_back(w);
+            }
+    auto finish = [&](Rows& R, int end) {
+        const int nr = (int)R.row.size();
+        std::vector<int> list(R.start);
+        list.push_back(end);
+        list.insert(list.end(), R.row.begin(), R.row.end());
+        list.insert(list.end(), R.aux.begin(), R.aux.end());
+        std::vector<int> order(nr);
+        for (int i = 0; i < nr; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return R.cost[a] > R.cost[b]; });
+        list.insert(list.end(), order.begin(), order.end());
+        return list;
+    };
+    const auto lp = finish(P, Q.start.empty() ? (int)ent.size() : Q.start.front());
+    const auto lq = finish(Q, (int)ent.size());
+    c->nP = (int)P.row.size();
+    c->nQ = (int)Q.row.size();
+    if (T.hsize >= (size_t)INT32_MAX) throw CudaError{"mirror table too large for 32-bit H offsets"};
+    const size_t hbytes = T.hsize * sizeof(double);
+    CK(cudaMalloc(&c->dMH, hbytes));
+    CK(cudaMalloc(&c->dMEnt, ent.size() * sizeof(int4)));
+    CK(cudaMalloc(&c->dListP, lp.size() * sizeof(int)));
+    CK(cudaMalloc(&c->dListQ, lq.size() * sizeof(int)));
+    CK(cudaMemcpy(c->dMEnt, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dListP, lp.data(), lp.size() * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dListQ, lq.data(), lq.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 16 + (int64_t)(lp.size() + lq.size()) * 4;
+    c->terms_mirror = (int64_t)T.hsize;
+    fill_table(c, G_host, T, c->dMH);
+}
+
 // the mirror schedule runs where the convolution is the single-tile TMA pipe
-constexpr bool mirror_eligible_n(int n) {
+// (k_conv_mirror) or the k-chunked TMA kcs kernel (k_conv_kcsm)
+constexpr bool mirror_pipe_n(int n) {
     return n >= 8 && conv_tile(n) == n && conv_kernel_for(n) == 1 && BOLTZ_PIPE_TMA;
 }
+constexpr bool mirror_kcs_n(int n) { return n >= 8 && conv_kernel_for(n) == 3 && BOLTZ_PIPE_TMA; }
+constexpr bool mirror_eligible_n(int n) { return mirror_pipe_n(n) || mirror_kcs_n(n); }
 
 // Build the folded, pair-symmetric table H (conv.cuh) -- and, where eligible,
 // the mirror schedule's table beside it -- from the host G or on the device.
@@ -476,7 +588,10 @@ void build_table(boltz_ctx* c, const double* G_host) {
     bool mirror = mirror_eligible_n(c->n);
     if (const char* e = std::getenv("BOLTZ_MIRROR")) mirror = mirror && std::atoi(e) != 0;
     if (mirror && G_host) mirror = g_mirror_symmetric(c->n, G_host);
-    if (mirror) build_table_mirror(c, G_host);
+    if (mirror) {
+        if (mirror_pipe_n(c->n)) build_table_mirror(c, G_host);
+        else build_table_mirror_kcs(c, G_host);
+    }
     c->mirror = mirror;
 }
 
@@ -593,7 +708,43 @@ struct Launch {
     // mirror schedule may run; evaluate_qhat of a caller's fhat never does
     static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s, bool hermitian = false) {
         const int64_t ng = (nc + 31) / 32;
-        if constexpr (mirror_eligible_n(N)) {
+        if constexpr (mirror_kcs_n(N)) {
+            if (hermitian && c->mirror && c->schedule == 0) {
+                constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
+                const int smem = kConvWarps * KcsmLayout<N>::WARP_BYTES;
+                static bool configured = false;
+                if (!configured) {
+                    auto cfg = [&](auto fn) {
+                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    };
+                    cfg(k_conv_kcsm<N, 0, 0>);
+                    cfg(k_conv_kcsm<N, KC1, 0>);
+                    cfg(k_conv_kcsm<N, 0, 1>);
+                    cfg(k_conv_kcsm<N, KC1, 1>);
+                    configured = true;
+                }
+                const unsigned gy = (unsigned)((ng + kConvWarps - 1) / kConvWarps);
+                // longest rows first in the last column of many-wave grids (conv_row)
+                auto lpt = [&](int nrows) { return (int64_t)nrows * gy < 8 * 2 * 148 ? 0 : (int)gy - 1; };
+                Timed t_(c, KIND_CONV, s);
+                // phase 0 (pair leaders' A sums + mirror seeds), then phase 1, per k-chunk
+                k_conv_kcsm<N, 0, 0><<<dim3(c->nP, gy), kLanes * kConvWarps, smem, s>>>(
+                    c->dA, c->dB, c->dMH, c->dMEnt, c->dListP, c->nP, (int)ng, lpt(c->nP));
+                if constexpr (NK > 1)
+                    k_conv_kcsm<N, KC1, 0><<<dim3(c->nP, gy), kLanes * kConvWarps, smem, s>>>(
+                        c->dA, c->dB, c->dMH, c->dMEnt, c->dListP, c->nP, (int)ng, lpt(c->nP));
+                k_conv_kcsm<N, 0, 1><<<dim3(c->nQ, gy), kLanes * kConvWarps, smem, s>>>(
+                    c->dA, c->dB, c->dMH, c->dMEnt, c->dListQ, c->nQ, (int)ng, lpt(c->nQ));
+                if constexpr (NK > 1)
+                    k_conv_kcsm<N, KC1, 1><<<dim3(c->nQ, gy), kLanes * kConvWarps, smem, s>>>(
+                        c->dA, c->dB, c->dMH, c->dMEnt, c->dListQ, c->nQ, (int)ng, lpt(c->nQ));
+                c->launches[KIND_CONV] += 2 * NK - 1;  // 2 NK kernels under one timing bracket
+                CK(cudaGetLastError());
+                return;
+            }
+        }
+        if constexpr (mirror_pipe_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 const int smem = kConvWarps * MirrorLayout<N>::WARP_BYTES;
                 static bool configured = false;
@@ -1114,7 +1265,7 @@ int boltz_destroy(boltz_ctx* c) {
     if (!c) return BOLTZ_OK;
     cudaSetDevice(c->device);
     cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
-    cudaFree(c->dMH); cudaFree(c->dMEnt); cudaFree(c->dItems);
+    cudaFree(c->dMH); cudaFree(c->dMEnt); cudaFree(c->dItems); cudaFree(c->dListP); cudaFree(c->dListQ);
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);

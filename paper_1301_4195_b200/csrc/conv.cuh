@@ -785,6 +785,192 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
     write_row<N, T>(B, g, rm >= 0 ? rm : r, 0, lane, acc);
 }
 
+// ---------------------------------------------------------------------------
+// k_conv_kcsm (N = 24, 32: the k-chunked kcs kernels, TMA staging): the
+// Hermitian mirror schedule in two phases, so that each kernel still unrolls
+// one k-chunk's code.  The k3 reversal maps chunk KC of row r onto chunk
+// NK-1-KC of r' = N - r, which a kernel of chunk KC cannot sum, so:
+//   phase 0 (one launch per KC, rows = pair leaders r < r'): sums A(r) over the
+//     interior input rows and writes it, raw, to chunk KC of row r of B, and
+//     its conjugate, k3-reversed, to row r' (B[r'][N - k3] = conj A[r][k3]);
+//   phase 1 (one launch per KC, rows = every output row): starts from B (pair
+//     rows) or 0, adds the FULL / REST entries and writes the chunk with s_k.
+// Launch order P(0..NK-1), Q(0..NK-1).  Slab of an entry of type ty for chunk
+// KC at H + en.z + KC * kcsm_slab(N, ty), made of even-padded pieces in tile
+// order: A [A t0 | A t1], REST [R t0 | R t1], FULL [A t0 | R t0 | A t1 | R t1];
+// a FULL entry runs the A band and the REST band of each tile on the same
+// staged y window (one copy of the unrolled term code per band type).
+// list = [CSR offsets (nrows + 1) | output row (nrows) | aux (nrows) |
+//         longest-first order (nrows)], aux = partner r' (phase 0) or
+//         1 if the row is seeded from B (phase 1).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int even_up(int c) { return (c + 1) & ~1; }
+__host__ __device__ constexpr int tile_terms_t(int n, int t, int kc, int ti, int ty) {
+    const int nk = n / t, sc = band_tile_sc(nk, kc, ti);
+    int c = 0;
+    for (int m3 = 0; m3 < n; ++m3)
+        for (int kk = 0; kk < t; ++kk) c += band_term_t(n, t, kc, sc, m3, kk, ty) ? 1 : 0;
+    return c;
+}
+// offset (doubles) of the A / REST piece of tile ti within a chunk slab of type ty
+__host__ __device__ constexpr int kcsm_piece_off(int n, int t, int kc, int ti, int ty, int piece) {
+    int o = 0;
+    for (int u = 0; u < ti; ++u) {
+        if (ty != BT_REST) o += even_up(tile_terms_t(n, t, kc, u, BT_A));
+        if (ty != BT_A) o += even_up(tile_terms_t(n, t, kc, u, BT_REST));
+    }
+    if (piece == BT_REST && ty == BT_FULL) o += even_up(tile_terms_t(n, t, kc, ti, BT_A));
+    return o;
+}
+__host__ __device__ constexpr int kcsm_slab_kc(int n, int t, int kc, int ty) {
+    return kcsm_piece_off(n, t, kc, n / t, ty, BT_A);
+}
+// per-chunk stride of an entry's slab (max over chunks)
+__host__ __device__ constexpr int kcsm_slab(int n, int ty) {
+    const int t = conv_tile(n);
+    int mx = 0;
+    for (int kc = 0; kc < n / t; ++kc) mx = kcsm_slab_kc(n, t, kc, ty) > mx ? kcsm_slab_kc(n, t, kc, ty) : mx;
+    return mx;
+}
+
+template <int N>
+struct KcsmLayout {
+    static constexpr int T = conv_tile(N);
+    static constexpr int NK = N / T;
+    static constexpr int Y_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = kcsm_slab(N, BT_FULL) * 8;
+    static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+};
+
+// one tile of a k_conv_kcsm entry: its A piece and / or its REST piece on the
+// y window in registers (x per diagonal from L2)
+template <int N, int KC, int TI, int PHASE>
+__device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const double2 (&y)[conv_tile(N)],
+                                          const double2* X, const double2* hs, int ty) {
+    constexpr int T = conv_tile(N), NK = N / T;
+    constexpr int oA_A = kcsm_piece_off(N, T, KC, TI, BT_A, BT_A), oA_F = kcsm_piece_off(N, T, KC, TI, BT_FULL, BT_A);
+    constexpr int oR_R = kcsm_piece_off(N, T, KC, TI, BT_REST, BT_REST);
+    constexpr int oR_F = kcsm_piece_off(N, T, KC, TI, BT_FULL, BT_REST);
+    auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
+    auto none = [](int, int) {};
+    double2 hb = make_double2(0.0, 0.0);
+    if (ty != BT_REST) {
+        int p = 0;
+        band_tile<N, T, NK, KC, TI, BT_A>(acc, y, xat, hs + (ty == BT_A ? oA_A : oA_F) / 2, p, hb, none);
+    }
+    if constexpr (PHASE == 1) {
+        if (ty != BT_A) {
+            int p = 0;
+            band_tile<N, T, NK, KC, TI, BT_REST>(acc, y, xat, hs + (ty == BT_REST ? oR_R : oR_F) / 2, p, hb, none);
+        }
+    }
+}
+
+template <int N, int KC, int PHASE>
+__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
+k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
+    using LY = KcsmLayout<N>;
+    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
+    constexpr int SA = kcsm_slab(N, BT_A), SR = kcsm_slab(N, BT_REST), SF = kcsm_slab(N, BT_FULL);
+    constexpr unsigned BA = 8u * kcsm_slab_kc(N, T, KC, BT_A), BR = 8u * kcsm_slab_kc(N, T, KC, BT_REST),
+                       BF = 8u * kcsm_slab_kc(N, T, KC, BT_FULL);
+    extern __shared__ __align__(16) char smem[];
+    const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * kConvWarps + wid;
+    if (g >= ngroups) return;
+    const int row = __ldg(list + nrows + 1 + wi), aux = __ldg(list + 2 * nrows + 1 + wi);
+    const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
+    char* wsm = smem + wid * LY::WARP_BYTES;
+    double2* ys = reinterpret_cast<double2*>(wsm);
+    char* hbase = wsm + LY::Y_BYTES;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + LY::Y_BYTES + 2 * LY::H_BYTES);
+    const double2* Abase = A + (size_t)g * N3 * kLanes;
+    const double2* Ag = Abase + lane;
+    double2* Brow = B + ((size_t)g * N3 + (size_t)row * N + KC * T) * kLanes + lane;
+    double2 acc[T];
+    if (PHASE == 1 && aux) {
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) acc[kk] = Brow[(size_t)kk * kLanes];
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) acc[kk] = make_double2(0.0, 0.0);
+    }
+    auto tma_h = [&](int slot, int4 en) {
+        if (lane == 0) {
+            const int w = en.w;
+            const size_t off = (size_t)(unsigned)en.z + (size_t)KC * (w == BT_A ? SA : w == BT_REST ? SR : SF);
+            const unsigned bytes = w == BT_A ? BA : w == BT_REST ? BR : BF;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, bytes);
+            bulk_g2s(hbase + slot * LY::H_BYTES, H + off, bytes, bar + slot);
+        }
+    };
+    auto tma_y = [&](int slot, int4 en) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, LY::Y_BYTES);
+            bulk_g2s(ys, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+        }
+    };
+    if (e0 < e1) {
+        if (lane == 0) {
+            mbar_init(bar, 2);
+            mbar_init(bar + 1, 2);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int4 en = __ldg(ent + e0);
+        int4 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;
+        tma_y(0, en);
+        tma_h(0, en);
+        mbar_wait(bar, 0);
+        for (int e = e0; e < e1; ++e) {
+            const int i = e - e0, cur = i & 1;
+            const bool more = e + 1 < e1;
+            const int4 nx = en_ahead;
+            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
+            __syncwarp();  // every lane finished reading H[cur^1]
+            if (more) tma_h(cur ^ 1, nx);
+            const double2* X = Ag + (size_t)en.x * kLanes;
+            const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
+            const int ty = PHASE == 0 ? (int)BT_A : en.w;
+            double2 y[T];
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            if constexpr (NK == 1) {
+                __syncwarp();  // every lane holds its y window: the buffer may be refilled
+                if (more) tma_y(cur ^ 1, nx);
+                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, ty);
+            } else {
+                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, ty);
+#pragma unroll
+                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                __syncwarp();
+                if (more) tma_y(cur ^ 1, nx);
+                kcsm_tile<N, KC, (NK > 1 ? 1 : 0), PHASE>(acc, y, X, hs, ty);
+            }
+            if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+            en = nx;
+        }
+    }
+    if constexpr (PHASE == 0) {
+        // raw A(r) of chunk KC; conj seeds k3' = N - k3 of the partner (k3' = 0: none)
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) Brow[(size_t)kk * kLanes] = acc[kk];
+        double2* Bm = B + ((size_t)g * N3 + (size_t)aux * N) * kLanes + lane;
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) {
+            const int k3 = KC * T + kk;
+            if (k3 != 0) Bm[(size_t)(N - k3) * kLanes] = make_double2(acc[kk].x, -acc[kk].y);
+        }
+        if (KC == NK - 1) Bm[0] = make_double2(0.0, 0.0);
+    } else {
+        write_row<N, T>(B, g, row, KC, lane, acc);
+    }
+}
+
 // ---- H table builder.  Entry e = output row (k1,k2) x representative input
 // row (m1,m2) (entk = {k1,k2,m1,m2}) with meta[e] = {H offset, band type};
 // term[ts.off[type] + pos] = (k3, m3) of slab position pos, or (-1,-1) for

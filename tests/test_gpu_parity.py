@@ -345,3 +345,31 @@ def test_mirror_schedule_active_and_consistent(gpu, O, n, L):
         ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
         assert rel_max(q[c], ref) < TOL_Q
     assert rel_max(q, q2) < 1e-12
+
+
+@pytest.mark.parametrize("n,L,cells", [(24, 8.0, 40), (32, 8.0, 40)])
+def test_mirror_schedule_kcs_consistent(gpu, O, n, L, cells):
+    """N = 24, 32 (the k-chunked kcs kernels) run the two-phase mirror schedule
+    (conv.cuh k_conv_kcsm): fewer executed terms than the plain fold, Q equal
+    to evaluate_qhat's plain-schedule composition to round-off, conserved to
+    1e-12 rho, bitwise independent of the batch; at N=24 two
+    cells also against the oracle with the host table (1e-10)."""
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=61)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        plain, mirror = op.schedule_terms()
+        assert 0 < mirror < 0.8 * plain
+        q = op.collide(f)                              # mirror schedule
+        q2 = op.conserve(op.inverse(op.evaluate_qhat(op.forward(f)))[0])  # plain schedule, composed
+        assert rel_max(q, q2) < 1e-12
+        assert np.array_equal(op.collide(f[7:9]), q[7:9])
+        for c in range(0, cells, 13):
+            m = O.moments(n, L, q[c])
+            assert np.abs(m[:5]).max() < TOL_CONS * O.moments(n, L, f[c])[0]
+    if n == 24:
+        G = table(n, L)
+        with _op(n, L) as op:
+            qh = op.collide(f[:2])
+        for c in range(2):
+            ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+            assert rel_max(qh[c], ref) < TOL_Q
