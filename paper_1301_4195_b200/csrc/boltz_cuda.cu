@@ -478,15 +478,11 @@ void layout_terms_kcsm(int n, TableLayout& T) {
         for (int kc = 0; kc < nk; ++kc)
             for (int ti = 0; ti < nk; ++ti) {
                 const int sc = band_tile_sc(nk, kc, ti);
-                for (int piece : {(int)BT_A, (int)BT_REST}) {
-                    if ((piece == BT_A && ty == BT_REST) || (piece == BT_REST && ty == BT_A)) continue;
-                    int pos = kc * stride + kcsm_piece_off(n, t, kc, ti, ty, piece);
-                    for (int i = 0; i < n; ++i) {  // band_tile's visiting order
-                        const int m3 = band_diag(n, nk, kc, ti, i);
-                        for (int kk = 0; kk < t; ++kk)
-                            if (band_term_t(n, t, kc, sc, m3, kk, piece))
-                                v[pos++] = make_short2((short)(kc * t + kk), (short)m3);
-                    }
+                int pos = kc * stride + kcsm_piece_off(n, t, kc, ti, ty);
+                for (int i = 0; i < n; ++i) {  // band_tile's visiting order
+                    const int m3 = band_diag(n, nk, kc, ti, i);
+                    for (int kk = 0; kk < t; ++kk)
+                        if (band_term_t(n, t, kc, sc, m3, kk, ty)) v[pos++] = make_short2((short)(kc * t + kk), (short)m3);
                 }
             }
         T.ts.off[ty] = off;

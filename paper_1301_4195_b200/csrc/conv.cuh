@@ -796,10 +796,10 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
 //   phase 1 (one launch per KC, rows = every output row): starts from B (pair
 //     rows) or 0, adds the FULL / REST entries and writes the chunk with s_k.
 // Launch order P(0..NK-1), Q(0..NK-1).  Slab of an entry of type ty for chunk
-// KC at H + en.z + KC * kcsm_slab(N, ty), made of even-padded pieces in tile
-// order: A [A t0 | A t1], REST [R t0 | R t1], FULL [A t0 | R t0 | A t1 | R t1];
-// a FULL entry runs the A band and the REST band of each tile on the same
-// staged y window (one copy of the unrolled term code per band type).
+// KC at H + en.z + KC * kcsm_slab(N, ty): one even-padded piece per tile, in
+// band_tile order.  (Phase 1 unrolls the FULL and the REST band: running FULL
+// entries as A + REST, as k_conv_mirror does, loads their x diagonals twice
+// from L2, and phase 1 is L2-bound.)
 // list = [CSR offsets (nrows + 1) | output row (nrows) | aux (nrows) |
 //         longest-first order (nrows)], aux = partner r' (phase 0) or
 //         1 if the row is seeded from B (phase 1).
@@ -812,19 +812,13 @@ __host__ __device__ constexpr int tile_terms_t(int n, int t, int kc, int ti, int
         for (int kk = 0; kk < t; ++kk) c += band_term_t(n, t, kc, sc, m3, kk, ty) ? 1 : 0;
     return c;
 }
-// offset (doubles) of the A / REST piece of tile ti within a chunk slab of type ty
-__host__ __device__ constexpr int kcsm_piece_off(int n, int t, int kc, int ti, int ty, int piece) {
+// offset (doubles) of tile ti's piece within a chunk slab of type ty
+__host__ __device__ constexpr int kcsm_piece_off(int n, int t, int kc, int ti, int ty) {
     int o = 0;
-    for (int u = 0; u < ti; ++u) {
-        if (ty != BT_REST) o += even_up(tile_terms_t(n, t, kc, u, BT_A));
-        if (ty != BT_A) o += even_up(tile_terms_t(n, t, kc, u, BT_REST));
-    }
-    if (piece == BT_REST && ty == BT_FULL) o += even_up(tile_terms_t(n, t, kc, ti, BT_A));
+    for (int u = 0; u < ti; ++u) o += even_up(tile_terms_t(n, t, kc, u, ty));
     return o;
 }
-__host__ __device__ constexpr int kcsm_slab_kc(int n, int t, int kc, int ty) {
-    return kcsm_piece_off(n, t, kc, n / t, ty, BT_A);
-}
+__host__ __device__ constexpr int kcsm_slab_kc(int n, int t, int kc, int ty) { return kcsm_piece_off(n, t, kc, n / t, ty); }
 // per-chunk stride of an entry's slab (max over chunks)
 __host__ __device__ constexpr int kcsm_slab(int n, int ty) {
     const int t = conv_tile(n);
@@ -842,27 +836,22 @@ struct KcsmLayout {
     static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
 };
 
-// one tile of a k_conv_kcsm entry: its A piece and / or its REST piece on the
-// y window in registers (x per diagonal from L2)
+// one tile of a k_conv_kcsm entry on the y window in registers (x per
+// diagonal from L2): phase 0 runs the A band, phase 1 the FULL or the REST band
 template <int N, int KC, int TI, int PHASE>
 __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const double2 (&y)[conv_tile(N)],
                                           const double2* X, const double2* hs, int ty) {
     constexpr int T = conv_tile(N), NK = N / T;
-    constexpr int oA_A = kcsm_piece_off(N, T, KC, TI, BT_A, BT_A), oA_F = kcsm_piece_off(N, T, KC, TI, BT_FULL, BT_A);
-    constexpr int oR_R = kcsm_piece_off(N, T, KC, TI, BT_REST, BT_REST);
-    constexpr int oR_F = kcsm_piece_off(N, T, KC, TI, BT_FULL, BT_REST);
     auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
     auto none = [](int, int) {};
     double2 hb = make_double2(0.0, 0.0);
-    if (ty != BT_REST) {
-        int p = 0;
-        band_tile<N, T, NK, KC, TI, BT_A>(acc, y, xat, hs + (ty == BT_A ? oA_A : oA_F) / 2, p, hb, none);
-    }
-    if constexpr (PHASE == 1) {
-        if (ty != BT_A) {
-            int p = 0;
-            band_tile<N, T, NK, KC, TI, BT_REST>(acc, y, xat, hs + (ty == BT_REST ? oR_R : oR_F) / 2, p, hb, none);
-        }
+    int p = 0;
+    if constexpr (PHASE == 0) {
+        band_tile<N, T, NK, KC, TI, BT_A>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_A) / 2, p, hb, none);
+    } else if (ty == BT_FULL) {
+        band_tile<N, T, NK, KC, TI, BT_FULL>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_FULL) / 2, p, hb, none);
+    } else {
+        band_tile<N, T, NK, KC, TI, BT_REST>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_REST) / 2, p, hb, none);
     }
 }
 
