@@ -73,9 +73,8 @@ struct boltz_ctx {
     int4* dMEnt = nullptr;
     int* dItems = nullptr;  // nitems x kItemInts, then the longest-first order
     int nitems = 0;
-    int* dListP = nullptr;  // k_conv_kcsm (N = 24, 32): phase-0 / phase-1 row lists
-    int* dListQ = nullptr;
-    int nP = 0, nQ = 0;
+    int* dListK[3] = {nullptr, nullptr, nullptr};  // k_conv_kcsm (N = 24, 32): row lists of phases 0, 1, 2
+    int nK[3] = {0, 0, 0};
     // workspace (group layout), capacity in cells (multiple of 32)
     int64_t cap = 0;
     double2* dA = nullptr;
@@ -517,53 +516,63 @@ void build_table_mirror_kcs(boltz_ctx* c, const double* G_host) {
     struct Rows {
         std::vector<int> start, row, aux;
         std::vector<long long> cost;
-    } P, Q;
+    } R[3];
     auto partner = [&](int k1, int k2) { return (k1 >= 1 && k2 >= 1) ? (n - k1) * n + (n - k2) : -1; };
-    for (int phase = 0; phase < 2; ++phase)
+    // phase 0: pair leaders' A entries; 1: pair rows' REST entries; 2: every
+    // row's FULL entries -- or, without kcsm_split, list 1 = every row's REST and
+    // FULL entries (kernel phase 3) and no list 2
+    const bool split = kcsm_split(n);
+    for (int phase = 0; phase < 3; ++phase)
         for (int k1 = 0; k1 < n; ++k1)
             for (int k2 = 0; k2 < n; ++k2) {
+                if (phase == 2 && !split) break;
                 const int r = k1 * n + k2, rm = partner(k1, k2);
                 const bool pair = rm >= 0 && rm != r;
-                Rows& R = phase == 0 ? P : Q;
-                if (phase == 0 && !(pair && r < rm)) continue;
+                if ((phase == 0 && !(pair && r < rm)) || (phase == 1 && split && !pair)) continue;
+                Rows& L = R[phase];
                 const size_t first = ent.size();
-                R.start.push_back((int)first);
-                R.row.push_back(r);
-                R.aux.push_back(phase == 0 ? rm : (pair ? 1 : 0));
-                if (phase == 0)
-                    reps(k1, k2, [&](int m1, int m2, bool in) { if (in) add(k1, k2, m1, m2, BT_A); });
-                else
-                    reps(k1, k2, [&](int m1, int m2, bool in) { add(k1, k2, m1, m2, pair && in ? BT_REST : BT_FULL); });
+                L.start.push_back((int)first);
+                L.row.push_back(r);
+                L.aux.push_back(phase == 0 ? rm : (pair ? 1 : 0));
+                reps(k1, k2, [&](int m1, int m2, bool in) {
+                    const bool interior = pair && in;
+                    if (phase == 0 && interior) add(k1, k2, m1, m2, BT_A);
+                    if (phase == 1 && interior) add(k1, k2, m1, m2, BT_REST);
+                    if ((phase == 2 || (phase == 1 && !split)) && !interior) add(k1, k2, m1, m2, BT_FULL);
+                });
                 long long w = 0;
                 for (size_t e = first; e < ent.size(); ++e) w += T.ts.slab[ent[e].w];
-                R.cost.push_back(w);
+                L.cost.push_back(w);
             }
-    auto finish = [&](Rows& R, int end) {
-        const int nr = (int)R.row.size();
-        std::vector<int> list(R.start);
+    auto finish = [&](Rows& L, int end) {
+        const int nr = (int)L.row.size();
+        std::vector<int> list(L.start);
         list.push_back(end);
-        list.insert(list.end(), R.row.begin(), R.row.end());
-        list.insert(list.end(), R.aux.begin(), R.aux.end());
+        list.insert(list.end(), L.row.begin(), L.row.end());
+        list.insert(list.end(), L.aux.begin(), L.aux.end());
         std::vector<int> order(nr);
         for (int i = 0; i < nr; ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return R.cost[a] > R.cost[b]; });
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return L.cost[a] > L.cost[b]; });
         list.insert(list.end(), order.begin(), order.end());
         return list;
     };
-    const auto lp = finish(P, Q.start.empty() ? (int)ent.size() : Q.start.front());
-    const auto lq = finish(Q, (int)ent.size());
-    c->nP = (int)P.row.size();
-    c->nQ = (int)Q.row.size();
+    std::vector<int> lists[3];
+    for (int ph = 0; ph < 3; ++ph) {
+        const int end = ph < 2 && !R[ph + 1].start.empty() ? R[ph + 1].start.front() : (int)ent.size();
+        lists[ph] = finish(R[ph], end);
+        c->nK[ph] = (int)R[ph].row.size();
+    }
     if (T.hsize >= (size_t)INT32_MAX) throw CudaError{"mirror table too large for 32-bit H offsets"};
     const size_t hbytes = T.hsize * sizeof(double);
     CK(cudaMalloc(&c->dMH, hbytes));
     CK(cudaMalloc(&c->dMEnt, ent.size() * sizeof(int4)));
-    CK(cudaMalloc(&c->dListP, lp.size() * sizeof(int)));
-    CK(cudaMalloc(&c->dListQ, lq.size() * sizeof(int)));
     CK(cudaMemcpy(c->dMEnt, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->dListP, lp.data(), lp.size() * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(c->dListQ, lq.data(), lq.size() * sizeof(int), cudaMemcpyHostToDevice));
-    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 16 + (int64_t)(lp.size() + lq.size()) * 4;
+    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 16;
+    for (int ph = 0; ph < 3; ++ph) {
+        CK(cudaMalloc(&c->dListK[ph], lists[ph].size() * sizeof(int)));
+        CK(cudaMemcpy(c->dListK[ph], lists[ph].data(), lists[ph].size() * sizeof(int), cudaMemcpyHostToDevice));
+        c->table_bytes += (int64_t)lists[ph].size() * 4;
+    }
     c->terms_mirror = (int64_t)T.hsize;
     fill_table(c, G_host, T, c->dMH);
 }
@@ -716,26 +725,39 @@ struct Launch {
                     };
                     cfg(k_conv_kcsm<N, 0, 0>);
                     cfg(k_conv_kcsm<N, KC1, 0>);
-                    cfg(k_conv_kcsm<N, 0, 1>);
-                    cfg(k_conv_kcsm<N, KC1, 1>);
+                    if constexpr (kcsm_split(N)) {
+                        cfg(k_conv_kcsm<N, 0, 1>);
+                        cfg(k_conv_kcsm<N, KC1, 1>);
+                        cfg(k_conv_kcsm<N, 0, 2>);
+                        cfg(k_conv_kcsm<N, KC1, 2>);
+                    } else {
+                        cfg(k_conv_kcsm<N, 0, 3>);
+                        cfg(k_conv_kcsm<N, KC1, 3>);
+                    }
                     configured = true;
                 }
                 const unsigned gy = (unsigned)((ng + kConvWarps - 1) / kConvWarps);
                 // longest rows first in the last column of many-wave grids (conv_row)
                 auto lpt = [&](int nrows) { return (int64_t)nrows * gy < 8 * 2 * 148 ? 0 : (int)gy - 1; };
                 Timed t_(c, KIND_CONV, s);
-                // phase 0 (pair leaders' A sums + mirror seeds), then phase 1, per k-chunk
-                k_conv_kcsm<N, 0, 0><<<dim3(c->nP, gy), kLanes * kConvWarps, smem, s>>>(
-                    c->dA, c->dB, c->dMH, c->dMEnt, c->dListP, c->nP, (int)ng, lpt(c->nP));
-                if constexpr (NK > 1)
-                    k_conv_kcsm<N, KC1, 0><<<dim3(c->nP, gy), kLanes * kConvWarps, smem, s>>>(
-                        c->dA, c->dB, c->dMH, c->dMEnt, c->dListP, c->nP, (int)ng, lpt(c->nP));
-                k_conv_kcsm<N, 0, 1><<<dim3(c->nQ, gy), kLanes * kConvWarps, smem, s>>>(
-                    c->dA, c->dB, c->dMH, c->dMEnt, c->dListQ, c->nQ, (int)ng, lpt(c->nQ));
-                if constexpr (NK > 1)
-                    k_conv_kcsm<N, KC1, 1><<<dim3(c->nQ, gy), kLanes * kConvWarps, smem, s>>>(
-                        c->dA, c->dB, c->dMH, c->dMEnt, c->dListQ, c->nQ, (int)ng, lpt(c->nQ));
-                c->launches[KIND_CONV] += 2 * NK - 1;  // 2 NK kernels under one timing bracket
+                // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
+                auto go = [&](auto kern, int ph) {
+                    kern<<<dim3(c->nK[ph], gy), kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
+                                                                                c->dListK[ph], c->nK[ph], (int)ng,
+                                                                                lpt(c->nK[ph]));
+                };
+                go(k_conv_kcsm<N, 0, 0>, 0);
+                if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 0>, 0);
+                if constexpr (kcsm_split(N)) {
+                    go(k_conv_kcsm<N, 0, 1>, 1);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 1>, 1);
+                    go(k_conv_kcsm<N, 0, 2>, 2);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
+                } else {
+                    go(k_conv_kcsm<N, 0, 3>, 1);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3>, 1);
+                }
+                c->launches[KIND_CONV] += (kcsm_split(N) ? 3 : 2) * NK - 1;  // all under one timing bracket
                 CK(cudaGetLastError());
                 return;
             }
@@ -1261,7 +1283,7 @@ int boltz_destroy(boltz_ctx* c) {
     if (!c) return BOLTZ_OK;
     cudaSetDevice(c->device);
     cudaFree(c->dH); cudaFree(c->dEnt); cudaFree(c->dRowStart);
-    cudaFree(c->dMH); cudaFree(c->dMEnt); cudaFree(c->dItems); cudaFree(c->dListP); cudaFree(c->dListQ);
+    cudaFree(c->dMH); cudaFree(c->dMEnt); cudaFree(c->dItems); for (int* l : c->dListK) cudaFree(l);
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);

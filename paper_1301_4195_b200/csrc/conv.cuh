@@ -793,16 +793,18 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
 //   phase 0 (one launch per KC, rows = pair leaders r < r'): sums A(r) over the
 //     interior input rows and writes it, raw, to chunk KC of row r of B, and
 //     its conjugate, k3-reversed, to row r' (B[r'][N - k3] = conj A[r][k3]);
-//   phase 1 (one launch per KC, rows = every output row): starts from B (pair
-//     rows) or 0, adds the FULL / REST entries and writes the chunk with s_k.
-// Launch order P(0..NK-1), Q(0..NK-1).  Slab of an entry of type ty for chunk
-// KC at H + en.z + KC * kcsm_slab(N, ty): one even-padded piece per tile, in
-// band_tile order.  (Phase 1 unrolls the FULL and the REST band: running FULL
-// entries as A + REST, as k_conv_mirror does, loads their x diagonals twice
-// from L2, and phase 1 is L2-bound.)
+//   phase 1 (one launch per KC, rows = pair rows): adds the REST entries
+//     (the rest of the interior input rows' terms) to the seed in B, raw;
+//   phase 2 (one launch per KC, rows = every output row): starts from B (pair
+//     rows) or 0, adds the FULL entries and writes the chunk with s_k.
+// Launch order: phase 0, 1, 2, each over KC = 0..NK-1; every launch unrolls
+// one band type of one chunk.  Without kcsm_split, phase 3 replaces 1 and 2
+// (REST and FULL entries of every row, typed per entry, one launch).  Slab of an entry
+// of type ty for chunk KC at H + en.z + KC * kcsm_slab(N, ty): one even-padded
+// piece per tile, in band_tile order.
 // list = [CSR offsets (nrows + 1) | output row (nrows) | aux (nrows) |
 //         longest-first order (nrows)], aux = partner r' (phase 0) or
-//         1 if the row is seeded from B (phase 1).
+//         1 if the row is seeded from B (phases 1, 2).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr int even_up(int c) { return (c + 1) & ~1; }
 __host__ __device__ constexpr int tile_terms_t(int n, int t, int kc, int ti, int ty) {
@@ -836,8 +838,16 @@ struct KcsmLayout {
     static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
 };
 
+// the band type phase PHASE runs: 0 the pair leaders' A terms, 1 REST, 2 FULL,
+// 3 REST or FULL per entry (phases 1 and 2 in one launch)
+__host__ __device__ constexpr int kcsm_type(int phase) { return phase == 0 ? BT_A : phase == 1 ? BT_REST : BT_FULL; }
+// phases 1 and 2 as separate launches (one band type unrolled per kernel) for
+// two k-chunks; one launch at N=24 (measured: N=32 339.8 -> 330.7 ms per RK2
+// step split, N=24 31.3 -> 32.8 ms)
+__host__ __device__ constexpr bool kcsm_split(int n) { return n / conv_tile(n) > 1; }
+
 // one tile of a k_conv_kcsm entry on the y window in registers (x per
-// diagonal from L2): phase 0 runs the A band, phase 1 the FULL or the REST band
+// diagonal from L2)
 template <int N, int KC, int TI, int PHASE>
 __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const double2 (&y)[conv_tile(N)],
                                           const double2* X, const double2* hs, int ty) {
@@ -846,8 +856,9 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const do
     auto none = [](int, int) {};
     double2 hb = make_double2(0.0, 0.0);
     int p = 0;
-    if constexpr (PHASE == 0) {
-        band_tile<N, T, NK, KC, TI, BT_A>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_A) / 2, p, hb, none);
+    if constexpr (PHASE < 3) {
+        constexpr int TY = kcsm_type(PHASE);
+        band_tile<N, T, NK, KC, TI, TY>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, TY) / 2, p, hb, none);
     } else if (ty == BT_FULL) {
         band_tile<N, T, NK, KC, TI, BT_FULL>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_FULL) / 2, p, hb, none);
     } else {
@@ -861,9 +872,10 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
     using LY = KcsmLayout<N>;
     constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
-    constexpr int SA = kcsm_slab(N, BT_A), SR = kcsm_slab(N, BT_REST), SF = kcsm_slab(N, BT_FULL);
-    constexpr unsigned BA = 8u * kcsm_slab_kc(N, T, KC, BT_A), BR = 8u * kcsm_slab_kc(N, T, KC, BT_REST),
-                       BF = 8u * kcsm_slab_kc(N, T, KC, BT_FULL);
+    // this chunk's part of an entry's slab (phase 3: REST or FULL per entry)
+    constexpr int TY = kcsm_type(PHASE < 3 ? PHASE : 2);
+    constexpr size_t OFF = (size_t)KC * kcsm_slab(N, TY), OFF_R = (size_t)KC * kcsm_slab(N, BT_REST);
+    constexpr unsigned BYTES = 8u * kcsm_slab_kc(N, T, KC, TY), BYTES_R = 8u * kcsm_slab_kc(N, T, KC, BT_REST);
     extern __shared__ __align__(16) char smem[];
     const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -879,7 +891,7 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     const double2* Ag = Abase + lane;
     double2* Brow = B + ((size_t)g * N3 + (size_t)row * N + KC * T) * kLanes + lane;
     double2 acc[T];
-    if (PHASE == 1 && aux) {
+    if (PHASE >= 1 && aux) {
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) acc[kk] = Brow[(size_t)kk * kLanes];
     } else {
@@ -888,12 +900,11 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     }
     auto tma_h = [&](int slot, int4 en) {
         if (lane == 0) {
-            const int w = en.w;
-            const size_t off = (size_t)(unsigned)en.z + (size_t)KC * (w == BT_A ? SA : w == BT_REST ? SR : SF);
-            const unsigned bytes = w == BT_A ? BA : w == BT_REST ? BR : BF;
+            const bool rest = PHASE == 3 && en.w == BT_REST;
+            const unsigned bytes = rest ? BYTES_R : BYTES;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, bytes);
-            bulk_g2s(hbase + slot * LY::H_BYTES, H + off, bytes, bar + slot);
+            bulk_g2s(hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z + (rest ? OFF_R : OFF), bytes, bar + slot);
         }
     };
     auto tma_y = [&](int slot, int4 en) {
@@ -924,21 +935,20 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             if (more) tma_h(cur ^ 1, nx);
             const double2* X = Ag + (size_t)en.x * kLanes;
             const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
-            const int ty = PHASE == 0 ? (int)BT_A : en.w;
             double2 y[T];
 #pragma unroll
             for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
             if constexpr (NK == 1) {
                 __syncwarp();  // every lane holds its y window: the buffer may be refilled
                 if (more) tma_y(cur ^ 1, nx);
-                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, ty);
+                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, en.w);
             } else {
-                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, ty);
+                kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, en.w);
 #pragma unroll
                 for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
                 __syncwarp();
                 if (more) tma_y(cur ^ 1, nx);
-                kcsm_tile<N, KC, (NK > 1 ? 1 : 0), PHASE>(acc, y, X, hs, ty);
+                kcsm_tile<N, KC, (NK > 1 ? 1 : 0), PHASE>(acc, y, X, hs, en.w);
             }
             if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
             en = nx;
@@ -955,6 +965,9 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             if (k3 != 0) Bm[(size_t)(N - k3) * kLanes] = make_double2(acc[kk].x, -acc[kk].y);
         }
         if (KC == NK - 1) Bm[0] = make_double2(0.0, 0.0);
+    } else if constexpr (PHASE == 1) {  // seed + REST, raw: phase 2 continues the row
+#pragma unroll
+        for (int kk = 0; kk < T; ++kk) Brow[(size_t)kk * kLanes] = acc[kk];
     } else {
         write_row<N, T>(B, g, row, KC, lane, acc);
     }
