@@ -199,8 +199,9 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * output row, or per mirror row pair, and 32-cell group), s = 1..4 = latency
  * (each row's entry list in 4s fixed segments on 4s warps + an ordered
  * reduction; small batches, N <= 16; other N keep the throughput schedule).
- * Under the throughput schedule collide / RK2 at N <= 16 use the Hermitian
- * mirror schedule (conv.cuh k_conv_mirror; env BOLTZ_MIRROR=0 disables it).
+ * Under the throughput schedule collide / RK2 at N >= 8 use the Hermitian
+ * mirror schedule (conv.cuh k_conv_mirror at N <= 16, the phased k_conv_kcsm
+ * at N = 24, 32; env BOLTZ_MIRROR=0 disables it).
  * Results are bitwise reproducible and independent of batch composition
  * within a schedule; the two schedules differ by round-off.
  */
@@ -208,7 +209,8 @@ int boltz_set_schedule(boltz_ctx* ctx, int schedule);
 /*
  * Executed K2 terms per cell eval: *plain for the throughput / latency
  * schedules and evaluate_qhat, *mirror for collide / RK2 when the Hermitian
- * mirror schedule is active (0 if not; N <= 16 with a mirror-symmetric table).
+ * mirror schedule is active (0 if not: N < 8, or a table that is not
+ * mirror-symmetric).
  * Each is the size of its folded table, i.e. every FP64 term the kernel runs.
  */
 int boltz_schedule_terms(boltz_ctx* ctx, int64_t* plain, int64_t* mirror);
