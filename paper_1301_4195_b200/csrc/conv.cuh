@@ -844,7 +844,12 @@ __host__ __device__ constexpr int kcsm_type(int phase) { return phase == 0 ? BT_
 // phases 1 and 2 as separate launches (one band type unrolled per kernel) for
 // two k-chunks; one launch at N=24 (measured: N=32 339.8 -> 330.7 ms per RK2
 // step split, N=24 31.3 -> 32.8 ms)
-__host__ __device__ constexpr bool kcsm_split(int n) { return n / conv_tile(n) > 1; }
+#ifndef BOLTZ_KCSM_SPLIT
+#define BOLTZ_KCSM_SPLIT -1  // -1: split for two k-chunks; 0 / 1 force (tuning)
+#endif
+__host__ __device__ constexpr bool kcsm_split(int n) {
+    return BOLTZ_KCSM_SPLIT >= 0 ? BOLTZ_KCSM_SPLIT == 1 : n / conv_tile(n) > 1;
+}
 
 // one tile of a k_conv_kcsm entry on the y window in registers (x per
 // diagonal from L2)
