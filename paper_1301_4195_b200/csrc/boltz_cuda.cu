@@ -68,6 +68,7 @@ struct boltz_ctx {
     int nent = 0, slab = 0;
     // Hermitian mirror schedule (conv.cuh k_conv_mirror) for collide / RK2
     bool mirror = false;
+    bool mirror2 = false;  // k_conv_mirror2 (TMEM accumulators) instead of k_conv_mirror
     int64_t terms_plain = 0, terms_mirror = 0;  // executed K2 terms per cell eval (H table sizes)
     double* dMH = nullptr;
     int4* dMEnt = nullptr;
@@ -240,6 +241,7 @@ struct TableLayout {
     std::vector<int4> entk;  // k1, k2, m1, m2
     std::vector<int2> meta;  // H offset, band type
     size_t hsize = 0;        // doubles
+    bool partner_terms = false;  // terms flagged kMirrorTermFlag (k_conv_mirror2)
 };
 
 void layout_terms_plain(int n, TableLayout& T, int& slab) {
@@ -328,10 +330,19 @@ void fill_table(boltz_ctx* c, const double* G_host, TableLayout& T, double* dH) 
             for (int k1 = 0; k1 < n; ++k1) {
                 const int e0 = kstart[k1], e1 = kstart[k1 + 1];
                 const long long total = (long long)(e1 - e0) * ts.slab_max;
-                if (total == 0) continue;
+                // partner-row terms (k_conv_mirror2) of the entries of plane n - k1 need this plane
+                const int kp = n - k1;
+                const long long total_p = T.partner_terms && kp < n ? (long long)(kstart[kp + 1] - kstart[kp]) * ts.slab_max : 0;
+                if (total == 0 && total_p == 0) continue;
                 CK(cudaMemcpy(dPlane, G_host + (size_t)k1 * plane, plane * sizeof(double), cudaMemcpyHostToDevice));
+                if (total_p) {
+                    k_build_H<<<(unsigned)((total_p + 255) / 256), 256>>>(dPlane, dH, dEntK, dMeta, dList, kstart[kp],
+                                                                          kstart[kp + 1], ts, n, w3, 1);
+                    CK(cudaGetLastError());
+                }
+                if (total == 0) continue;
                 k_build_H<<<(unsigned)((total + 255) / 256), 256>>>(dPlane, dH, dEntK, dMeta, dList, e0, e1, ts, n,
-                                                                    w3);
+                                                                    w3, 0);
                 CK(cudaGetLastError());
             }
         }
@@ -448,6 +459,114 @@ void build_table_mirror(boltz_ctx* c, const double* G_host) {
         }
     c->nitems = (int)cost.size();
     {   // longest items first (the conv_row lpt order, per item)
+        std::vector<int> order(c->nitems);
+        for (int i = 0; i < c->nitems; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+        items.insert(items.end(), order.begin(), order.end());
+    }
+    if (T.hsize >= (size_t)INT32_MAX) throw CudaError{"mirror table too large for 32-bit H offsets"};
+    const size_t hbytes = T.hsize * sizeof(double);
+    CK(cudaMalloc(&c->dMH, hbytes));
+    CK(cudaMalloc(&c->dMEnt, ent.size() * sizeof(int4)));
+    CK(cudaMalloc(&c->dItems, items.size() * sizeof(int)));
+    CK(cudaMemcpy(c->dMEnt, ent.data(), ent.size() * sizeof(int4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->dItems, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+    c->table_bytes += (int64_t)hbytes + (int64_t)ent.size() * 16 + (int64_t)items.size() * 4;
+    c->terms_mirror = (int64_t)T.hsize;
+    fill_table(c, G_host, T, c->dMH);
+}
+
+// Mirror schedule with TMEM accumulators (conv.cuh k_conv_mirror2): FULL slab
+// [A band | REST band], I slab (type id BT_A) [A band | REST | REST' of the
+// partner row, flagged].
+void layout_terms_mirror2(int n, TableLayout& T) {
+    std::vector<short2> a(m2_a(n), make_short2(-1, -1)), rest(m2_r(n), make_short2(-1, -1)), restp,
+        rband(m2_r(n), make_short2(-1, -1));
+    int pos = 0, rpos = 0;
+    for (int m3 = 0; m3 < n; ++m3)  // band_tile order of the single-tile A and REST bands
+        for (int kk = 0; kk < n; ++kk) {
+            if (band_term_t(n, n, 0, 0, m3, kk, BT_A)) a[pos++] = make_short2((short)kk, (short)m3);
+            if (band_term_t(n, n, 0, 0, m3, kk, BT_REST)) rband[rpos++] = make_short2((short)kk, (short)m3);
+        }
+    if (band_slab_type(n, BT_REST) != m2_r(n)) throw CudaError{"mirror2 REST piece size mismatch"};
+    pos = 0;
+    for (int k3 = 0; k3 < n; ++k3)  // m2_rest order
+        for (int m3 = 0; m3 < n; ++m3)
+            if (rest_term(n, k3, m3)) rest[pos++] = make_short2((short)k3, (short)m3);
+    restp = rest;
+    for (auto& t : restp)
+        if (t.x >= 0) t.x = (short)(t.x + kMirrorTermFlag);
+    T.term.clear();
+    T.ts.off[BT_FULL] = 0;
+    T.ts.slab[BT_FULL] = m2_slab(n, BT_FULL);
+    T.term.insert(T.term.end(), a.begin(), a.end());
+    T.term.insert(T.term.end(), rband.begin(), rband.end());
+    T.ts.off[BT_A] = (int)T.term.size();
+    T.ts.slab[BT_A] = m2_slab(n, BT_A);
+    T.term.insert(T.term.end(), a.begin(), a.end());
+    T.term.insert(T.term.end(), rest.begin(), rest.end());
+    T.term.insert(T.term.end(), restp.begin(), restp.end());
+    T.ts.off[BT_REST] = (int)T.term.size();
+    T.ts.slab[BT_REST] = 0;
+    T.ts.slab_max = m2_slab(n, BT_A);
+    if ((int)T.term.size() != m2_slab(n, BT_FULL) + m2_slab(n, BT_A)) throw CudaError{"mirror2 slab layout mismatch"};
+    T.partner_terms = true;
+}
+
+void build_table_mirror2(boltz_ctx* c, const double* G_host) {
+    const int n = c->n, h = n / 2;
+    TableLayout T;
+    layout_terms_mirror2(n, T);
+    std::vector<int4> ent;
+    std::vector<int> items;
+    std::vector<long long> cost;
+    auto add = [&](int k1, int k2, int m1, int m2, int ty) {
+        const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+        ent.push_back(make_int4((m1 * n + m2) * n, (s1 * n + s2) * n, (int)T.hsize, ty));
+        T.meta.push_back(make_int2((int)T.hsize, ty));
+        T.hsize += T.ts.slab[ty];
+        T.entk.push_back(make_int4(k1, k2, m1, m2));
+    };
+    auto reps = [&](int k1, int k2, auto&& fn) {
+        for (int m1 = std::max(0, k1 - h + 1); m1 <= std::min(n - 1, k1 + h); ++m1)
+            for (int m2 = std::max(0, k2 - h + 1); m2 <= std::min(n - 1, k2 + h); ++m2) {
+                const int s1 = k1 - m1 + h, s2 = k2 - m2 + h;
+                if (m1 < s1 || (m1 == s1 && m2 <= s2))
+                    fn(m1, m2, mirror_interior(n, m1) && mirror_interior(n, m2) && mirror_interior(n, s1) &&
+                                   mirror_interior(n, s2));
+            }
+    };
+    for (int k1 = 0; k1 < n; ++k1)
+        for (int k2 = 0; k2 < n; ++k2) {
+            const int r = k1 * n + k2;
+            const bool has = k1 >= 1 && k2 >= 1;
+            const int rm = has ? (n - k1) * n + (n - k2) : -1;
+            if (has && rm < r) continue;  // handled with its partner
+            const bool pair = has && rm != r;
+            const size_t first = ent.size();
+            int it[kItemInts];
+            it[0] = r;
+            it[1] = pair ? rm : -1;
+            it[2] = (int)ent.size();
+            if (!pair) {
+                reps(k1, k2, [&](int m1, int m2, bool) { add(k1, k2, m1, m2, BT_FULL); });
+                it[3] = it[2];
+                it[4] = it[5] = (int)ent.size();
+            } else {
+                reps(k1, k2, [&](int m1, int m2, bool in) { if (in) add(k1, k2, m1, m2, BT_A); });
+                it[3] = (int)ent.size();
+                reps(k1, k2, [&](int m1, int m2, bool in) { if (!in) add(k1, k2, m1, m2, BT_FULL); });
+                it[4] = (int)ent.size();
+                reps(n - k1, n - k2, [&](int m1, int m2, bool in) { if (!in) add(n - k1, n - k2, m1, m2, BT_FULL); });
+                it[5] = (int)ent.size();
+            }
+            long long w = 0;
+            for (size_t e = first; e < ent.size(); ++e) w += T.ts.slab[ent[e].w];
+            cost.push_back(w);
+            items.insert(items.end(), it, it + kItemInts);
+        }
+    c->nitems = (int)cost.size();
+    {
         std::vector<int> order(c->nitems);
         for (int i = 0; i < c->nitems; ++i) order[i] = i;
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
@@ -594,7 +713,11 @@ void build_table(boltz_ctx* c, const double* G_host) {
     if (const char* e = std::getenv("BOLTZ_MIRROR")) mirror = mirror && std::atoi(e) != 0;
     if (mirror && G_host) mirror = g_mirror_symmetric(c->n, G_host);
     if (mirror) {
-        if (mirror_pipe_n(c->n)) build_table_mirror(c, G_host);
+        // BOLTZ_MIRROR=2: the TMEM variant (k_conv_mirror2) at N = 8..16
+        c->mirror2 = mirror_pipe_n(c->n) && c->n % 4 == 0 && std::getenv("BOLTZ_MIRROR") &&
+                     std::atoi(std::getenv("BOLTZ_MIRROR")) == 2;
+        if (c->mirror2) build_table_mirror2(c, G_host);
+        else if (mirror_pipe_n(c->n)) build_table_mirror(c, G_host);
         else build_table_mirror_kcs(c, G_host);
     }
     c->mirror = mirror;
@@ -758,6 +881,26 @@ struct Launch {
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3>, 1);
                 }
                 c->launches[KIND_CONV] += (kcsm_split(N) ? 3 : 2) * NK - 1;  // all under one timing bracket
+                CK(cudaGetLastError());
+                return;
+            }
+        }
+        if constexpr (mirror_pipe_n(N) && N % 4 == 0) {
+            if (hermitian && c->mirror && c->mirror2 && c->schedule == 0) {
+                const int smem = Mirror2Layout<N>::CTA_BYTES;
+                static bool configured = false;
+                if (!configured) {
+                    CK(cudaFuncSetAttribute(k_conv_mirror2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    CK(cudaFuncSetAttribute(k_conv_mirror2<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    configured = true;
+                }
+                dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
+                int lpt = 0;
+                if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
+                Timed t_(c, KIND_CONV, s);
+                k_conv_mirror2<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dItems,
+                                                                          c->dItems + kItemInts * c->nitems, (int)ng,
+                                                                          lpt);
                 CK(cudaGetLastError());
                 return;
             }

@@ -786,6 +786,307 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
 }
 
 // ---------------------------------------------------------------------------
+// k_conv_mirror2 (single-tile rows, TMA staging, TMEM): the mirror schedule
+// with every interior input row staged once.  k_conv_mirror stages an interior
+// row three times -- A(r), REST(r), REST(r') -- because its only accumulator
+// is the register row of the output being summed.  Here an entry of an
+// interior input row (type BT_A below: "I") runs
+//   A     (diagonal-major band, registers)      -> acc        (row r)
+//   REST  (k3-major, 4 outputs per TMEM access) -> T_r  (TMEM, row r)
+//   REST' (k3-major)                             -> T_r' (TMEM, row r')
+// REST' is r' = N - r's own non-mirrored terms, computed from r's staged rows:
+// for real f, fhat(N - m) = conj fhat(m) per axis, so x'[m3'] = conj x[N - m3']
+// (m3' >= 1) and x'[0] = fhat(N - m1, N - m2, 0), one extra value per row
+// (likewise y'); its weights are r''s own (k_build_H: term.x >= kMirrorTermFlag).
+// A FULL entry (non-interior input rows; all rows of an unpaired output row)
+// runs the A and the REST band (diagonal-major) into acc.
+//   after the I entries: conj(acc[N - k3']) seeds row r' of B (k3' >= 1)
+//   after FULL(r):       acc += T_r, row r written; acc = B row r'
+//   at the end:          acc += T_r' (T_r for an unpaired row), row written
+// Slabs (doubles, even-padded pieces): FULL [A band | REST band],
+// I [A band | REST k3-major | REST' k3-major].  Items as k_conv_mirror:
+// {r, r' (-1), begin, end of I, begin of r', end}.
+// TMEM: each CTA allocates 2 x 4N 32-bit columns per lane (N <= 16: 128);
+// warp w uses lanes 32 (w % 4) .. +31; T_r at column 0, T_r' at 4N.
+// ---------------------------------------------------------------------------
+constexpr int kMirrorTermFlag = 64;  // term.x >= 64: a REST' term, k3' = x - 64, weights of q' = N - q
+__host__ __device__ inline int4 mirror_q(int n, int4 q) { return make_int4(n - q.x, n - q.y, n - q.z, n - q.w); }
+
+__host__ __device__ constexpr bool single_band(int n, int k3, int m3) {
+    const int s3 = k3 - m3 + n / 2;
+    return s3 >= 0 && s3 < n;
+}
+__host__ __device__ constexpr bool rest_term(int n, int k3, int m3) {
+    return single_band(n, k3, m3) && type_term(n, BT_REST, k3, m3);
+}
+__host__ __device__ constexpr int rest_terms(int n) {
+    int c = 0;
+    for (int k3 = 0; k3 < n; ++k3)
+        for (int m3 = 0; m3 < n; ++m3) c += rest_term(n, k3, m3) ? 1 : 0;
+    return c;
+}
+// slab pieces of k_conv_mirror2 (doubles)
+__host__ __device__ constexpr int m2_a(int n) { return band_slab_type(n, BT_A); }
+__host__ __device__ constexpr int m2_r(int n) { return (rest_terms(n) + 1) & ~1; }
+__host__ __device__ constexpr int m2_slab(int n, int ty) { return ty == BT_A ? m2_a(n) + 2 * m2_r(n) : m2_a(n) + m2_r(n); }
+__host__ __device__ constexpr int m2_tmem_cols(int n) { return 8 * n <= 32 ? 32 : 8 * n <= 64 ? 64 : 8 * n <= 128 ? 128 : 256; }
+
+template <int N>
+struct Mirror2Layout {
+    static constexpr int X_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = m2_slab(N, BT_A) * 8;
+    static constexpr int WARP_BYTES = 3 * X_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+    static constexpr int CTA_BYTES = kConvWarps * WARP_BYTES + 16;     // + the TMEM base address
+};
+
+// TMEM <-> registers, 4 complex values (16 columns) of this thread's lane
+__device__ __forceinline__ void tm_ld4c(uint32_t ta, double2 (&v)[4]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(ta));
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        v[i] = make_double2(__hiloint2double(r[4 * i + 1], r[4 * i]), __hiloint2double(r[4 * i + 3], r[4 * i + 2]));
+}
+__device__ __forceinline__ void tm_st4c(uint32_t ta, const double2 (&v)[4]) {
+    uint32_t r[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        r[4 * i] = (uint32_t)__double2loint(v[i].x);
+        r[4 * i + 1] = (uint32_t)__double2hiint(v[i].x);
+        r[4 * i + 2] = (uint32_t)__double2loint(v[i].y);
+        r[4 * i + 3] = (uint32_t)__double2hiint(v[i].y);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+        ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+          "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+
+// stores complete before TMEM is read again (tm_st4c does not wait)
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// one term of a REST pass into a (PRIME: REST' of the partner row)
+template <int N, bool PRIME, int K3, int M3>
+__device__ __forceinline__ void m2_term(double2& a, double h, const double2 (&y)[N], const double2* __restrict__ xs,
+                                        int lane, double2 X0, double2 Y0) {
+    constexpr int S3 = K3 - M3 + N / 2;
+    if constexpr (!PRIME) {
+        const double2 xm = xs[M3 * kLanes + lane];
+        const double tr = fma(xm.x, y[S3].x, -xm.y * y[S3].y);
+        const double ti = fma(xm.x, y[S3].y, xm.y * y[S3].x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else if constexpr (M3 == 0) {  // X0 * conj(y[N - s3])  (s3 >= 1 here)
+        const double2 yv = y[(N - S3) % N];
+        const double tr = fma(X0.x, yv.x, X0.y * yv.y);
+        const double ti = fma(X0.y, yv.x, -X0.x * yv.y);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else if constexpr (S3 == 0) {  // conj(x[N - m3]) * Y0
+        const double2 xm = xs[(N - M3) * kLanes + lane];
+        const double tr = fma(xm.x, Y0.x, xm.y * Y0.y);
+        const double ti = fma(xm.x, Y0.y, -xm.y * Y0.x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else {  // conj(x[N - m3] * y[N - s3])
+        const double2 xm = xs[(N - M3) * kLanes + lane];
+        const double2 yv = y[(N - S3) % N];
+        const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
+        const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(-h, ti, a.y);
+    }
+}
+
+// the REST terms of outputs k3 = 4B .. 4B+3 into a[4]; p / hb: the slab cursor
+template <int N, bool PRIME, int B, int Q = 0, int M3 = 0>
+__device__ __forceinline__ void m2_batch(double2 (&a)[4], const double2 (&y)[N], const double2* __restrict__ xs,
+                                         int lane, const double2* __restrict__ hs, int& p, double2& hb, double2 X0,
+                                         double2 Y0) {
+    if constexpr (Q < 4) {
+        if constexpr (M3 < N) {
+            if constexpr (rest_term(N, 4 * B + Q, M3)) {
+                double h;
+                if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
+                else h = hb.y;
+                ++p;
+                m2_term<N, PRIME, 4 * B + Q, M3>(a[Q], h, y, xs, lane, X0, Y0);
+            }
+            m2_batch<N, PRIME, B, Q, M3 + 1>(a, y, xs, lane, hs, p, hb, X0, Y0);
+        } else {
+            m2_batch<N, PRIME, B, Q + 1, 0>(a, y, xs, lane, hs, p, hb, X0, Y0);
+        }
+    }
+}
+
+// a REST pass (PRIME: REST' of the partner row) into the TMEM row at ta,
+// 4 outputs per TMEM access
+template <int N, bool PRIME, int B = 0>
+__device__ __forceinline__ void m2_pass(uint32_t ta, const double2 (&y)[N], const double2* __restrict__ xs, int lane,
+                                        const double2* __restrict__ hs, int& p, double2& hb, double2 X0, double2 Y0) {
+    if constexpr (B < N / 4) {
+        double2 a[4];
+        tm_ld4c(ta + 16 * B, a);
+        m2_batch<N, PRIME, B>(a, y, xs, lane, hs, p, hb, X0, Y0);
+        tm_st4c(ta + 16 * B, a);
+        m2_pass<N, PRIME, B + 1>(ta, y, xs, lane, hs, p, hb, X0, Y0);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kLanes* kConvWarps, 1)
+k_conv_mirror2(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+               const int4* __restrict__ ent, const int* __restrict__ items, const int* __restrict__ order, int ngroups,
+               int lpt_from) {
+    using PL = Mirror2Layout<N>;
+    constexpr int T = N, N3 = N * N * N, COLS = m2_tmem_cols(N);
+    extern __shared__ __align__(16) char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* tbase_s = reinterpret_cast<uint32_t*>(smem + kConvWarps * PL::WARP_BYTES);
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tbase_s)),
+                     "r"(COLS) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tbase_s + ((uint32_t)(32 * (wid & 3)) << 16);
+    const uint32_t t_r = tmem, t_rm = tmem + 4 * N;
+    const int* it = items + kItemInts * ((int)blockIdx.y >= lpt_from ? __ldg(order + blockIdx.x) : (int)blockIdx.x);
+    const int g = blockIdx.y * kConvWarps + wid;
+    if (g < ngroups) {
+        const int r = __ldg(it), rm = __ldg(it + 1);
+        const int e_begin = __ldg(it + 2), e_endI = __ldg(it + 3), e_rm = __ldg(it + 4), e_end = __ldg(it + 5);
+        char* wsm = smem + wid * PL::WARP_BYTES;
+        unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + 3 * PL::X_BYTES + 2 * PL::H_BYTES);
+        const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
+        const double2* Abase = A + (size_t)g * N3 * kLanes;
+        double2* Bm = B + ((size_t)g * N3 + (size_t)(rm < 0 ? 0 : rm) * N) * kLanes + lane;
+        auto issue = [&](int slot, int4 en) {
+            if (lane == 0) {
+                const unsigned hb = 8u * (en.w == BT_A ? m2_slab(N, BT_A) : m2_slab(N, BT_FULL));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + hb);
+                bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
+                bulk_g2s(wsm + 2 * PL::X_BYTES, Abase + (size_t)en.y * kLanes, PL::X_BYTES, bar + slot);
+                bulk_g2s(wsm + 3 * PL::X_BYTES + slot * PL::H_BYTES, H + (size_t)(unsigned)en.z, hb, bar + slot);
+            }
+        };
+        {   // both TMEM rows start at 0
+            const double2 z[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                                  make_double2(0.0, 0.0)};
+#pragma unroll
+            for (int b = 0; b < N / 4; ++b) {
+                tm_st4c(t_r + 16 * b, z);
+                tm_st4c(t_rm + 16 * b, z);
+            }
+            tm_wait_st();
+        }
+        uint32_t t_cur = t_r;
+        double2 acc[T];
+#pragma unroll
+        for (int i = 0; i < T; ++i) acc[i] = make_double2(0.0, 0.0);
+        auto add_tmem = [&](uint32_t ta) {
+            tm_wait_st();
+#pragma unroll
+            for (int b = 0; b < N / 4; ++b) {
+                double2 v[4];
+                tm_ld4c(ta + 16 * b, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[4 * b + q].x += v[q].x;
+                    acc[4 * b + q].y += v[q].y;
+                }
+            }
+        };
+        auto boundary = [&](int e) {
+            if (rm < 0) return;
+            if (e == e_endI) {  // I entries done: the conjugate of A(r), k3-reversed, seeds row r'
+                Bm[0] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int k = 1; k < N; ++k) Bm[(size_t)k * kLanes] = make_double2(acc[N - k].x, -acc[N - k].y);
+            }
+            if (e == e_rm) {  // row r complete: write it, continue with row r'
+                add_tmem(t_r);
+                write_row<N, T>(B, g, r, 0, lane, acc);
+#pragma unroll
+                for (int k = 0; k < N; ++k) acc[k] = Bm[(size_t)k * kLanes];
+                t_cur = t_rm;
+            }
+        };
+        if (e_begin < e_end) {
+            if (lane == 0) {
+                mbar_init(bar, 1);
+                mbar_init(bar + 1, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            }
+            __syncwarp();
+            int4 en = __ldg(ent + e_begin);
+            int4 en_ahead = e_begin + 1 < e_end ? __ldg(ent + e_begin + 1) : en;
+            issue(0, en);
+            mbar_wait(bar, 0);
+            double2 y[T];
+#pragma unroll
+            for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+            for (int e = e_begin; e < e_end; ++e) {
+                const int i = e - e_begin, cur = i & 1;
+                const bool more = e + 1 < e_end;
+                const int4 nx = en_ahead;
+                if (e + 2 < e_end) en_ahead = __ldg(ent + e + 2);
+                boundary(e);
+                __syncwarp();  // every lane read y (registers) and is done with slot cur^1
+                if (more) issue(cur ^ 1, nx);
+                const double2* xs = reinterpret_cast<const double2*>(wsm + cur * PL::X_BYTES);
+                const double2* hs = reinterpret_cast<const double2*>(wsm + 3 * PL::X_BYTES + cur * PL::H_BYTES);
+                auto xat = [&](int m3) { return xs[m3 * kLanes + lane]; };
+                auto none = [](int, int) {};
+                {
+                    int p = 0;
+                    double2 hb = make_double2(0.0, 0.0);
+                    band_tile<N, T, 1, 0, 0, BT_A>(acc, y, xat, hs, p, hb, none);
+                }
+                const double2 zero = make_double2(0.0, 0.0);
+                tm_wait_st();  // the previous entry's TMEM stores
+                int pr = 0;
+                double2 hbr = zero;
+                if (en.w == BT_A) {  // interior input rows: REST of r and REST' of r'
+                    const int m1 = en.x / (N * N), m2 = (en.x / N) % N, s1 = en.y / (N * N), s2 = (en.y / N) % N;
+                    const double2 X0 = ldg2(Abase + (size_t)(((N - m1) * N + (N - m2)) * N) * kLanes + lane);
+                    const double2 Y0 = ldg2(Abase + (size_t)(((N - s1) * N + (N - s2)) * N) * kLanes + lane);
+                    m2_pass<N, false>(t_r, y, xs, lane, hs + m2_a(N) / 2, pr, hbr, zero, zero);
+                    int pp = 0;
+                    double2 hbp = zero;
+                    m2_pass<N, true>(t_rm, y, xs, lane, hs + (m2_a(N) + m2_r(N)) / 2, pp, hbp, X0, Y0);
+                } else {  // FULL: the REST band into the registers too
+                    band_tile<N, T, 1, 0, 0, BT_REST>(acc, y, xat, hs + m2_a(N) / 2, pr, hbr, none);
+                }
+                if (more) {
+                    mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+#pragma unroll
+                    for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+                }
+                en = nx;
+            }
+        }
+        boundary(e_end);  // boundaries that coincide with the end of the list
+        add_tmem(t_cur);
+        write_row<N, T>(B, g, rm >= 0 ? rm : r, 0, lane, acc);
+    }
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (wid == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(COLS) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // k_conv_kcsm (N = 24, 32: the k-chunked kcs kernels, TMA staging): the
 // Hermitian mirror schedule in two phases, so that each kernel still unrolls
 // one k-chunk's code.  The k3 reversal maps chunk KC of row r onto chunk
@@ -1006,17 +1307,26 @@ __device__ __forceinline__ double folded_h(int n, double w3, int4 q, short2 km, 
 
 // from one k1-plane of the caller's dense zeta-major G:
 // Gk1[(k2*N + k3) * N^3 + m]; list[e_begin..e_end) = the entries of that plane
+// mode 0: the entries' own terms (plane k1 = q.x); mode 1: only their
+// partner-row terms (term.x >= kMirrorTermFlag, plane N - q.x), which must not
+// be touched in mode 0
 __global__ void k_build_H(const double* __restrict__ Gk1, double* __restrict__ H, const int4* __restrict__ entk,
                           const int2* __restrict__ meta, const int* __restrict__ list, int e_begin, int e_end,
-                          TermSet ts, int n, double w3) {
+                          TermSet ts, int n, double w3, int mode) {
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (tid >= (long long)(e_end - e_begin) * ts.slab_max) return;
     const int e = list[e_begin + (int)(tid / ts.slab_max)];
     const int pos = (int)(tid % ts.slab_max);
     const int2 mt = meta[e];
     if (pos >= ts.slab[mt.y]) return;
-    const int4 q = entk[e];
-    const short2 km = ts.term[ts.off[mt.y] + pos];
+    int4 q = entk[e];
+    short2 km = ts.term[ts.off[mt.y] + pos];
+    const bool partner = km.x >= kMirrorTermFlag;
+    if (partner != (mode == 1)) return;
+    if (partner) {
+        km.x -= kMirrorTermFlag;
+        q = mirror_q(n, q);
+    }
     double out = 0.0;
     if (km.x >= 0) {
         const long long n3 = (long long)n * n * n;

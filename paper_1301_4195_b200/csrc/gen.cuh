@@ -24,8 +24,12 @@ __global__ void k_gen_H(double* __restrict__ H, const int4* __restrict__ entk, c
     const int e = (int)(tid / ts.slab_max), pos = (int)(tid % ts.slab_max);
     const int2 mt = meta[e];
     if (pos >= ts.slab[mt.y]) return;
-    const int4 q = entk[e];
-    const short2 km = ts.term[ts.off[mt.y] + pos];
+    int4 q = entk[e];
+    short2 km = ts.term[ts.off[mt.y] + pos];
+    if (km.x >= kMirrorTermFlag) {  // a partner-row term (k_conv_mirror2)
+        km.x -= kMirrorTermFlag;
+        q = mirror_q(gp.n, q);
+    }
     double out = 0.0;
     if (km.x >= 0) {
         const int h = gp.n / 2;
