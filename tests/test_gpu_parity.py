@@ -373,3 +373,30 @@ def test_mirror_schedule_kcs_consistent(gpu, O, n, L, cells):
         for c in range(2):
             ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
             assert rel_max(qh[c], ref) < TOL_Q
+
+
+@pytest.mark.parametrize("n,L", [(8, 5.0), (16, 6.0)])
+def test_mirror2_tmem_schedule(gpu, O, n, L, monkeypatch):
+    """BOLTZ_MIRROR=2 (conv.cuh k_conv_mirror2: REST and the partner row's REST'
+    in TMEM, each interior input row staged once) with the host table
+    (k_build_H's partner-plane pass) and the generated one (k_gen_H): Q against
+    the oracle to 1e-10, against the default mirror schedule to round-off, and
+    bitwise independent of the batch."""
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 9, seed=71)
+    G = table(n, L)
+    with _op(n, L) as op:
+        q1 = op.collide(f)                                  # k_conv_mirror
+    monkeypatch.setenv("BOLTZ_MIRROR", "2")
+    with _op(n, L) as op:
+        plain, mirror = op.schedule_terms()
+        assert 0 < mirror < plain
+        q2 = op.collide(f)
+        assert np.array_equal(op.collide(f[3:5]), q2[3:5])
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        q3 = op.collide(f)
+    for c in range(0, 9, 4):
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q2[c], ref) < TOL_Q
+    assert rel_max(q2, q1) < 1e-12
+    assert rel_max(q3, q2) < 1e-12
