@@ -163,6 +163,12 @@ def cpu_baseline(seconds, threads=None):
     g24 = VelocityGrid.create(24, 8.0)  # cfg4's grid (Tables 2/4 are N=24)
     G24 = O.generate_table(24, 8.0, LAM, nthreads=threads)
     tables.append(table(24, 8.0, G24, scenarios.mixture_cells(g24, 3, seed=4195)))
+    del G24
+    # N=32 (SURVEY.md §8d asks for N=16 and N=32): the dense table is 8.6 GB of host memory
+    g32 = VelocityGrid.create(32, 8.0)
+    G32 = O.generate_table(32, 8.0, LAM, nthreads=threads)
+    tables.append(table(32, 8.0, G32, scenarios.mixture_cells(g32, 3, seed=4195)))
+    del G32
     return {"value": ev / el, "unit": "evals/s", "cores": threads, "kind": "port",
             "sample": f"{ev} single-cell collide() evals at N=16 (cfg2 cells 0..63, OpenMP over zeta_k, "
                       f"{threads} threads, {el:.1f} s)",
