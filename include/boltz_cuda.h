@@ -201,7 +201,8 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * reduction; small batches, N <= 16; other N keep the throughput schedule).
  * Under the throughput schedule collide / RK2 at N >= 8 use the Hermitian
  * mirror schedule (conv.cuh k_conv_mirror at N <= 16, the phased k_conv_kcsm
- * at N = 24, 32; env BOLTZ_MIRROR=0 disables it).
+ * at N = 24, 32; env BOLTZ_MIRROR=0 disables it, BOLTZ_MIRROR=2 selects the
+ * TMEM-accumulator variant k_conv_mirror2 at N = 8..16).
  * Results are bitwise reproducible and independent of batch composition
  * within a schedule; the two schedules differ by round-off.
  */
