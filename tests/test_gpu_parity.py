@@ -163,12 +163,12 @@ def test_device_generated_table_matches_host_table(gpu, O, n, L, lam):
         assert rel_max(qg[0], O.evaluate_qhat(n, L, G, fh[0], nthreads=8)) < TOL_Q
 
 
-def test_host_pipeline_matches_device_path(gpu):
+@pytest.mark.parametrize("n,L", [(8, 5.0), (24, 8.0)])
+def test_host_pipeline_matches_device_path(gpu, n, L):
     """Host-memory calls are chunked and pipelined over two copy and two compute
     streams with two workspaces; the result is bitwise the device-memory call's
-    (ragged last chunk)."""
+    (ragged last chunk).  N=8 runs k_conv_mirror, N=24 the phased k_conv_kcsm."""
     import torch
-    n, L = 8, 5.0
     grid = VelocityGrid.create(n, L)
     f = scenarios.mixture_cells(grid, 1100, seed=21)
     with _op(n, L) as op:
