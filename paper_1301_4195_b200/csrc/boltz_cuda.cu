@@ -1206,7 +1206,9 @@ template <typename Fn>
 int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
                        cudaStream_t s, double* max_imag, Fn&& fn) {
     std::vector<int64_t> bounds{0};
-    auto up32 = [](int64_t x) { return (x + kLanes - 1) / kLanes * kLanes; };
+    // chunk boundaries on whole K2 CTA columns (kConvWarps groups of 32 cells)
+    constexpr int64_t kGrain = (int64_t)kLanes * kConvWarps;
+    auto up32 = [](int64_t x) { return (x + kGrain - 1) / kGrain * kGrain; };
     // Chunk schedule (relative weights, measured best on B200 for cfg2): the first
     // H2D and the last D2H cannot overlap compute, so the edge chunks are small;
     // odd chunks run on a second stream, so each chunk's last wave overlaps the
