@@ -843,23 +843,26 @@ struct Launch {
         if constexpr (mirror_kcs_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
-                const int smem = kConvWarps * KcsmLayout<N>::WARP_BYTES;
+                const int smem_ph[4] = {kConvWarps * KcsmLayout<N, 0>::WARP_BYTES,
+                                        kConvWarps * KcsmLayout<N, 1>::WARP_BYTES,
+                                        kConvWarps * KcsmLayout<N, 2>::WARP_BYTES,
+                                        kConvWarps * KcsmLayout<N, 3>::WARP_BYTES};
                 static bool configured = false;
                 if (!configured) {
-                    auto cfg = [&](auto fn) {
-                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                    auto cfg = [&](auto fn, int ph) {
+                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ph[ph]));
                         CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                     };
-                    cfg(k_conv_kcsm<N, 0, 0>);
-                    cfg(k_conv_kcsm<N, KC1, 0>);
+                    cfg(k_conv_kcsm<N, 0, 0>, 0);
+                    cfg(k_conv_kcsm<N, KC1, 0>, 0);
                     if constexpr (kcsm_split(N)) {
-                        cfg(k_conv_kcsm<N, 0, 1>);
-                        cfg(k_conv_kcsm<N, KC1, 1>);
-                        cfg(k_conv_kcsm<N, 0, 2>);
-                        cfg(k_conv_kcsm<N, KC1, 2>);
+                        cfg(k_conv_kcsm<N, 0, 1>, 1);
+                        cfg(k_conv_kcsm<N, KC1, 1>, 1);
+                        cfg(k_conv_kcsm<N, 0, 2>, 2);
+                        cfg(k_conv_kcsm<N, KC1, 2>, 2);
                     } else {
-                        cfg(k_conv_kcsm<N, 0, 3>);
-                        cfg(k_conv_kcsm<N, KC1, 3>);
+                        cfg(k_conv_kcsm<N, 0, 3>, 3);
+                        cfg(k_conv_kcsm<N, KC1, 3>, 3);
                     }
                     configured = true;
                 }
@@ -869,7 +872,8 @@ struct Launch {
                 Timed t_(c, KIND_CONV, s);
                 // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
                 auto go = [&](auto kern, int ph) {
-                    kern<<<dim3(c->nK[ph], gy), kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
+                    const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph;  // list 1 runs phase 3 when not split
+                    kern<<<dim3(c->nK[ph], gy), kLanes * kConvWarps, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
                                                                                 c->dListK[ph], c->nK[ph], (int)ng,
                                                                                 lpt(c->nK[ph]));
                 };

@@ -1130,14 +1130,20 @@ __host__ __device__ constexpr int kcsm_slab(int n, int ty) {
     return mx;
 }
 
-template <int N>
+// per-warp shared memory of phase PHASE (its H slots sized for its band type;
+// phase 3 holds REST or FULL slabs)
+template <int N, int PHASE = 3>
 struct KcsmLayout {
     static constexpr int T = conv_tile(N);
     static constexpr int NK = N / T;
     static constexpr int Y_BYTES = N * kLanes * 16;
-    static constexpr int H_BYTES = kcsm_slab(N, BT_FULL) * 8;
+    static constexpr int H_BYTES =
+        kcsm_slab(N, PHASE == 0 ? (int)BT_A : PHASE == 1 ? (int)BT_REST : (int)BT_FULL) * 8;
     static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
 };
+#ifndef BOLTZ_KCSM_REST_MINB
+#define BOLTZ_KCSM_REST_MINB 1  // CTAs per SM the REST phase is compiled for (registers)
+#endif
 
 // the band type phase PHASE runs: 0 the pair leaders' A terms, 1 REST, 2 FULL,
 // 3 REST or FULL per entry (phases 1 and 2 in one launch)
@@ -1173,10 +1179,10 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const do
 }
 
 template <int N, int KC, int PHASE>
-__global__ void __launch_bounds__(kLanes* kConvWarps, BOLTZ_K0_MINB)
+__global__ void __launch_bounds__(kLanes* kConvWarps, PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
 k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
-    using LY = KcsmLayout<N>;
+    using LY = KcsmLayout<N, PHASE>;
     constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
     // this chunk's part of an entry's slab (phase 3: REST or FULL per entry)
     constexpr int TY = kcsm_type(PHASE < 3 ? PHASE : 2);

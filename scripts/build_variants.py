@@ -20,7 +20,9 @@ V = {
     "kcs16_m3w2": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_K0_MINB=3", "BOLTZ_CONV_WARPS=2"],
     "kcsm16": ["BOLTZ_CONV_KERNEL=3"],
     "kcsm16s": ["BOLTZ_CONV_KERNEL=3", "BOLTZ_KCSM_SPLIT=1"],
-    "kcsm24s": ["BOLTZ_KCSM_SPLIT=1"],  # N <= 16 on k_conv_kcs / the phased k_conv_kcsm mirror
+    "kcsm24s": ["BOLTZ_KCSM_SPLIT=1"],
+    "rest3": ["BOLTZ_KCSM_REST_MINB=3"],
+    "rest2": ["BOLTZ_KCSM_REST_MINB=2"],  # N <= 16 on k_conv_kcs / the phased k_conv_kcsm mirror
 }
 root = pathlib.Path(__file__).resolve().parent.parent / "variants"
 names = sys.argv[1:] or list(V)
