@@ -23,6 +23,7 @@ V = {
     "kcsm24s": ["BOLTZ_KCSM_SPLIT=1"],
     "rest3": ["BOLTZ_KCSM_REST_MINB=3"],
     "w2": ["BOLTZ_CONV_WARPS=2"],
+    "t24_12": ["BOLTZ_TILE24=12"],
     "w8": ["BOLTZ_CONV_WARPS=8"],
     "rest2": ["BOLTZ_KCSM_REST_MINB=2"],  # N <= 16 on k_conv_kcs / the phased k_conv_kcsm mirror
 }
