@@ -843,10 +843,9 @@ struct Launch {
         if constexpr (mirror_kcs_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
-                const int smem_ph[4] = {kConvWarps * KcsmLayout<N, 0>::WARP_BYTES,
-                                        kConvWarps * KcsmLayout<N, 1>::WARP_BYTES,
-                                        kConvWarps * KcsmLayout<N, 2>::WARP_BYTES,
-                                        kConvWarps * KcsmLayout<N, 3>::WARP_BYTES};
+                constexpr int W = kcsm_warps(N);
+                const int smem_ph[4] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
+                                        W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES};
                 static bool configured = false;
                 if (!configured) {
                     auto cfg = [&](auto fn, int ph) {
@@ -866,14 +865,14 @@ struct Launch {
                     }
                     configured = true;
                 }
-                const unsigned gy = (unsigned)((ng + kConvWarps - 1) / kConvWarps);
+                const unsigned gy = (unsigned)((ng + W - 1) / W);
                 // longest rows first in the last column of many-wave grids (conv_row)
                 auto lpt = [&](int nrows) { return (int64_t)nrows * gy < 8 * 2 * 148 ? 0 : (int)gy - 1; };
                 Timed t_(c, KIND_CONV, s);
                 // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
                 auto go = [&](auto kern, int ph) {
                     const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph;  // list 1 runs phase 3 when not split
-                    kern<<<dim3(c->nK[ph], gy), kLanes * kConvWarps, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
+                    kern<<<dim3(c->nK[ph], gy), kLanes * W, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
                                                                                 c->dListK[ph], c->nK[ph], (int)ng,
                                                                                 lpt(c->nK[ph]));
                 };

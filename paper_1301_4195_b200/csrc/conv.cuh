@@ -1141,6 +1141,12 @@ struct KcsmLayout {
         kcsm_slab(N, PHASE == 0 ? (int)BT_A : PHASE == 1 ? (int)BT_REST : (int)BT_FULL) * 8;
     static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
 };
+// cell groups (warps) per CTA of k_conv_kcsm: 8 at N=24 (cfg4 RK2 step 31.3 ->
+// 30.4 ms), the global kConvWarps elsewhere (8 measured +7% at N=32)
+#ifndef BOLTZ_KCSM_WARPS24
+#define BOLTZ_KCSM_WARPS24 8
+#endif
+__host__ __device__ constexpr int kcsm_warps(int n) { return n == 24 ? BOLTZ_KCSM_WARPS24 : kConvWarps; }
 #ifndef BOLTZ_KCSM_REST_MINB
 #define BOLTZ_KCSM_REST_MINB 1  // CTAs per SM the REST phase is compiled for (registers)
 #endif
@@ -1179,7 +1185,7 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const do
 }
 
 template <int N, int KC, int PHASE>
-__global__ void __launch_bounds__(kLanes* kConvWarps, PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
+__global__ void __launch_bounds__(kLanes* kcsm_warps(N), PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
 k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
     using LY = KcsmLayout<N, PHASE>;
@@ -1191,7 +1197,7 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     extern __shared__ __align__(16) char smem[];
     const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.y * kConvWarps + wid;
+    const int g = blockIdx.y * kcsm_warps(N) + wid;
     if (g >= ngroups) return;
     const int row = __ldg(list + nrows + 1 + wi), aux = __ldg(list + 2 * nrows + 1 + wi);
     const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
