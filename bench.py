@@ -37,6 +37,51 @@ sys.path.insert(0, REPO)
 PUBLISHED_EVALS_PER_S = 1.0 / 0.00408
 N_VEL, L_VEL, LAM, CELLS, DT = 16, 6.0, 1.0, 4096, 0.01
 FLOP_PER_TERM = 10  # 2 DMUL + 4 DFMA per (k, m) term, SURVEY.md §8d
+# identical in both arms, so the driver can divide them
+METRIC = "collision-operator evals/s (N=16, cfg2 two-Maxwellian cells, RK2 step; FP64)"
+# parity witnesses of the timed cfg2 batch: lanes 0 and 31, several 32-cell
+# groups, the first and last chunk of the host pipeline (1,3,3,1 x 512 cells)
+WITNESS16 = (0, 31, 32, 511, 549, 2047, 2148, 4095)
+WITNESS32 = (0, 1234)
+
+
+def workload_config(cells, world):
+    """BASELINE.json configs[1] as this bench runs it (the same dict in both arms)."""
+    return {"workload": f"cfg2: {cells} independent cells per GPU, N=16^3 on [-6,6]^3, hard spheres, "
+                        "one collision RK2 step (2 collide evals) per cell per step",
+            "cells_per_gpu": cells, "N": N_VEL, "L": L_VEL, "lambda": LAM, "dt": DT,
+            "seed": "SplitMix64 4195 (+7919 x rank), rho/u/T per mixture component",
+            "parallelism": f"cells sharded, {world} rank(s), no collective on the data path",
+            "l2": "flushed (256 MiB write) before every timed step; f 128 MiB + fhat 256 MiB > L2"}
+
+
+def host_cpu():
+    """CPU model, physical cores and logical CPUs this process may run on."""
+    cpus = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count()))
+    model, cores, cur = None, set(), {}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh.read().splitlines() + [""]:
+                if not line.strip():
+                    if cur.get("processor") is not None and int(cur["processor"]) in cpus:
+                        cores.add((cur.get("physical id", "0"), cur.get("core id", cur["processor"])))
+                    cur = {}
+                    continue
+                k, _, v = line.partition(":")
+                cur[k.strip()] = v.strip()
+                if k.strip() == "model name" and model is None:
+                    model = v.strip()
+    except OSError:
+        pass
+    return {"cpu_model": model, "physical_cores": len(cores) or len(cpus), "logical_cpus": len(cpus)}
+
+
+def pin_openmp():
+    """The reference's OpenMP run settings: one
+    thread per physical core, bound close.  Must run before libgomp loads."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    return f"OMP_PROC_BIND={os.environ['OMP_PROC_BIND']} OMP_PLACES={os.environ['OMP_PLACES']}"
 
 
 def ncu_traffic(kernel, cells):
@@ -121,12 +166,14 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU baseline
-def cpu_baseline(seconds, threads=None):
-    """Oracle port (C, OpenMP over zeta_k) on this host: evals/s at N=16."""
+def cpu_baseline(seconds, omp):
+    """Oracle port (C, OpenMP over zeta_k) on this host: evals/s at N=16,
+    plus the reference's bench_collision tables at N=16/24/32."""
     from oracle import oracle as O
     from paper_1301_4195_b200 import VelocityGrid, scenarios
     O.build()
-    threads = threads or os.cpu_count()
+    hw = host_cpu()
+    threads = hw["physical_cores"]
     grid = VelocityGrid.create(N_VEL, L_VEL)
     G = O.generate_table(N_VEL, L_VEL, LAM, nthreads=threads)
     cells = scenarios.mixture_cells(grid, 64, seed=4195)
@@ -139,13 +186,14 @@ def cpu_baseline(seconds, threads=None):
         el = time.perf_counter() - t0
         if el >= seconds or ev >= 100000:
             break
+
     # the reference's bench_collision table (Tables 1-4):
     # median wall time of one collide() per worker count, ratio to the previous
     # row and total speed-up over 1 worker
     def table(n, L, Gt, fs):
         rows, t1, prev = [], None, None
         w = 1
-        while w <= threads:
+        while True:
             reps = []
             for r in range(3):
                 t0 = time.perf_counter()
@@ -155,7 +203,9 @@ def cpu_baseline(seconds, threads=None):
             t1 = t1 or t
             rows.append({"cores": w, "time": t, "ratio": (prev / t) if prev else 1.0, "total_speedup": t1 / t})
             prev = t
-            w *= 2
+            if w == threads:
+                break
+            w = min(2 * w, threads)
         return {"columns": "cores,time,ratio,total_speedup", "N": n, "L": L, "rows": rows}
 
     tables = [table(N_VEL, L_VEL, G, cells)]
@@ -172,19 +222,23 @@ def cpu_baseline(seconds, threads=None):
     return {"value": ev / el, "unit": "evals/s", "cores": threads, "kind": "port",
             "sample": f"{ev} single-cell collide() evals at N=16 (cfg2 cells 0..63, OpenMP over zeta_k, "
                       f"{threads} threads, {el:.1f} s)",
-            "tables_1_4": tables}
+            **hw, "omp": omp, "tables_1_4": tables}
 
 
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, omp):
+    """The reference arm: the oracle port of the reference's OpenMP collision
+    path on this box's host cores, on a bounded sample of the
+    same cfg2 workload, printed under the same metric and config."""
     if rank != 0:
         return
     from oracle import oracle as O
     from paper_1301_4195_b200 import VelocityGrid, scenarios
     O.build()
-    threads = os.cpu_count()
+    hw = host_cpu()
+    threads = hw["physical_cores"]
     grid = VelocityGrid.create(N_VEL, L_VEL)
     G = O.generate_table(N_VEL, L_VEL, LAM, nthreads=threads)
-    sample = 16  # cells per step: one RK2 step (2 evals) of 16 cfg2 cells
+    sample = 16  # cells per step: one RK2 step (2 evals) of 16 of the 4096 cfg2 cells
     f = scenarios.mixture_cells(grid, sample, seed=4195)
     for _ in range(args.warmup):
         O.collision_rk2(N_VEL, L_VEL, G, f, DT, 1.0, nthreads=threads)
@@ -195,16 +249,18 @@ def run_reference(args, rank, world):
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = 2 * sample * args.steps / tot
+    desc = (f"{sample} of the {args.cells} cfg2 cells per step (cells 0..{sample - 1}), RK2 step = 2 evals per "
+            f"cell; evals/s is the per-eval rate, which is batch-size independent on the CPU (cells run one "
+            f"after another, OpenMP over zeta_k inside each eval)")
     line = {
-        "impl": "reference", "metric": "collision-operator evals/s (N=16, cfg2 two-Maxwellian cells, RK2)",
-        "value": value, "unit": "evals/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": METRIC,
+        "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / PUBLISHED_EVALS_PER_S, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg2 sample: RK2 step of {sample} cells (of 4096), N=16, L=6, lambda=1",
-                   "cells_per_step": sample},
+        "config": workload_config(args.cells, world),
+        "sample": desc,
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} cells x {args.steps} RK2 steps, oracle/boltz_oracle.c "
-                                   f"(OpenMP over zeta_k, {threads} threads)"},
+                         "sample": f"{desc}; oracle/boltz_oracle.c, {threads} threads", **hw, "omp": omp},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -213,11 +269,15 @@ def run_reference(args, rank, world):
 # ------------------------------------------------------------------- ours
 def main():
     args = parse()
+    omp = pin_openmp()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world, omp)
+    if world > 1:  # communicator init lines (ranks, transport) on stderr for the driver's check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
 
     import torch
     import torch.distributed as dist
@@ -255,6 +315,7 @@ def main():
     f_host = scenarios.mixture_cells(grid, cells, seed=4195 + 7919 * rank)
     f = torch.from_numpy(f_host).to(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    wit = [c for c in WITNESS16 if c < cells]
 
     peak = fp64_peak(local, 0.5)
 
@@ -262,34 +323,47 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(ms):
+        t = torch.tensor([ms], dtype=torch.float64, device=cdev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(step, nsteps, before_last=None):
+        """nsteps device-timed calls of step(), L2 flushed and ranks aligned
+        before each; before_last() runs (untimed) ahead of the last one."""
+        ms = []
+        for i in range(nsteps):
+            flush.zero_()  # L2 flush outside the timed events
+            if i == nsteps - 1 and before_last:
+                before_last()
+            barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        barrier()
+        return ms
+
+    stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         op.collision_rk2(f, DT)
     torch.cuda.synchronize()
     op.timing(reset=True)
     op.set_timing(True)
-    stream = torch.cuda.current_stream()
-    step_ms = []
+    snap = {}
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush.zero_()  # L2 flush outside the timed events
-            barrier()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            op.collision_rk2(f, DT)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-        barrier()
+        step_ms = timed(lambda: op.collision_rk2(f, DT), args.steps,
+                        before_last=lambda: snap.update(dev=f[wit].cpu().numpy()))
     op.set_timing(False)
     kms, klaunch = op.timing(reset=True)
-    total_ms = sum(step_ms)
-    tmax = torch.tensor([total_ms], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    total_ms = float(tmax.item())
+    total_ms = max_over_ranks(sum(step_ms))
     evals = 2 * cells * args.steps * world
     value = evals / (total_ms * 1e-3)
+    dev_after = f[wit].cpu().numpy()
 
     # roofline of the dominant kernel (K2 convolution)
     terms_plain, terms_mirror = op.schedule_terms()
@@ -299,76 +373,101 @@ def main():
     conv_ms_avg = kms["conv"] / max(conv_launches, 1)
     flop_per_launch = FLOP_PER_TERM * terms_per_eval(N_VEL) * cells
     achieved = flop_per_launch / (conv_ms_avg * 1e-3) / 1e12
+    # nominal FP64 peak at the sampled SM clock: 148 SMs x 64 DFMA/clk x 2 flop
+    sm_mhz = clk.summary()["sm_mhz"] or 1965.0
+    peak_nominal = torch.cuda.get_device_properties(dev).multi_processor_count * 64 * 2 * sm_mhz * 1e6 / 1e12
 
-    # e2e: the public API with HOST buffers (pinned), H2D + compute + D2H every step
+    # e2e: the public API with HOST buffers, H2D + compute + D2H every step;
+    # pinned (the library's pipeline overlaps copies with compute) and pageable
+    # (plain numpy / std::vector memory, what the reference's caller holds)
     pinned = torch.from_numpy(f_host).pin_memory()
     ph = pinned.numpy()
-    for _ in range(1):
+    for _ in range(args.warmup):
         op.collision_rk2(ph, DT)
-    e2e_ms = []
-    for _ in range(args.steps):
-        flush.zero_()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        op.collision_rk2(ph, DT)  # synchronous: copies in, 2 evals per cell, copies out
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(e0.elapsed_time(e1))
-    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = evals / (float(te.item()) * 1e-3)
+    e2e_ms = timed(lambda: op.collision_rk2(ph, DT), args.steps,
+                   before_last=lambda: snap.update(e2e=ph[wit].copy()))
+    e2e_value = evals / (max_over_ranks(sum(e2e_ms)) * 1e-3)
+    pg = f_host.copy()
+    for _ in range(args.warmup):
+        op.collision_rk2(pg, DT)
+    pg_ms = timed(lambda: op.collision_rk2(pg, DT), args.steps)
+    pg_value = evals / (max_over_ranks(sum(pg_ms)) * 1e-3)
+    pageable_bitwise = bool(np.array_equal(pg, ph))
 
-    # N=32 (cfg5-shaped: 2048 two-Maxwellian cells, L=8) sub-measurement
-    cfg3 = bench_cfg3(op, dev) if rank == 0 and not args.no_cfg3 else None
+    # parity witness: the last timed step of sampled cells against the oracle's
+    # collision_rk2 with the same host table G (SURVEY.md §8c bar: 1e-10)
+    parity = None
+    if rank == 0:
+        from oracle import oracle as O
+        O.build()
+        th = host_cpu()["physical_cores"]
+        r_dev = O.collision_rk2(N_VEL, L_VEL, G, snap["dev"], DT, 1.0, nthreads=th)
+        r_e2e = O.collision_rk2(N_VEL, L_VEL, G, snap["e2e"], DT, 1.0, nthreads=th)
+
+        def rel(got, ref, before):
+            return max(float(np.abs(g - r).max() / np.abs(r - b).max()) for g, r, b in zip(got, ref, before))
+        parity = {"cells": wit, "reference": "oracle collision_rk2 (same host G), last timed step",
+                  "max_rel_increment_n16_device": rel(dev_after, r_dev, snap["dev"]),
+                  "max_rel_increment_n16_e2e": rel(ph[wit], r_e2e, snap["e2e"]),
+                  "max_rel_state_n16": max(rel_state(dev_after, r_dev), rel_state(ph[wit], r_e2e))}
+
+    # cfg3 (Strang steps with the halo); on N>1 ranks strong-scaled with NCCL halo
+    cfg3 = None if args.no_cfg3 else bench_cfg3(op, dev, rank, world, backend)
 
     n32 = None
     if not args.no_n32 and rank == 0:
         op.close()
         del G
         n32 = bench_n32(args, dev, local)
+        if parity is not None and n32.get("parity"):
+            parity.update(n32.pop("parity"))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_seconds)
+        cpu = cpu_baseline(args.cpu_seconds, omp)
 
     if rank == 0:
         line = {
-            "metric": "collision-operator evals/s (N=16, cfg2; FP64)",
+            "metric": METRIC,
             "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": value / PUBLISHED_EVALS_PER_S, "dtype": "f64", "data": "synthetic",
             "vs_baseline_ref": "BASELINE.md: 245.1 evals/s = 1 / 0.00408 s per N=16 eval on 16 Stampede cores "
                                "(PAPER.md:358), other hardware",
-            "config": {"workload": f"cfg2: {cells} independent cells per GPU, N=16^3 on [-6,6]^3, hard spheres, "
-                                   "one collision RK2 step (2 collide evals) per cell per step",
-                       "cells_per_gpu": cells, "N": N_VEL, "L": L_VEL, "lambda": LAM, "dt": DT,
-                       "parallelism": f"cells sharded, {world} rank(s), no collective on the data path",
-                       "l2": "flushed (256 MiB write) before every timed step; f 128 MiB + fhat 256 MiB > L2"},
+            "config": workload_config(cells, world),
             "cells_steps_per_s": value / 2.0,
             "gpu_launches": int(sum(klaunch.values())),
             "kernel_ms": {k: round(v, 4) for k, v in kms.items()},
             "kernel_launches": klaunch,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(conv_kernel, cells),
+                         "peak_source": "builder-probed: k_dfma_probe (32 warps/SM x 8 independent DFMA chains) "
+                                        "timed in this run; MEASURED_PEAKS.json has no FP64 entry",
+                         "peak_nominal": peak_nominal,
+                         "frac_nominal": achieved / peak_nominal,
+                         "peak_nominal_source": "148 SMs x 64 DFMA/clk x 2 flop x median sampled SM clock",
                          "kernel": f"{conv_kernel} (K2)",
                          "executed_term_ratio": exec_ratio,
                          "executed_fp64_slot_fraction": achieved / peak * exec_ratio * 12 / 10,
+                         "executed_fp64_slot_fraction_nominal": achieved / peak_nominal * exec_ratio * 12 / 10,
                          "note": "achieved = 10 flop x 27/64 N^6 valid terms x cells per launch / mean launch time "
                                  "(algorithmic, SURVEY.md §8d). The kernel executes executed_term_ratio of those "
                                  "terms (pair symmetry, plus the Hermitian mirror of interior terms for collide / "
                                  "RK2, DESIGN.md §2-3; the ratio is the library's folded-table size) at 6 FP64 "
-                                 "pipe instructions (2 DMUL + 4 DFMA) each, so the FP64 pipe-slot fraction is frac "
-                                 "x executed_term_ratio x 12/10. peak = DFMA probe measured in this run "
-                                 "(MEASURED_PEAKS.json has no FP64 entry)"},
+                                 "pipe instructions (2 DMUL + 4 DFMA) each, so frac > 1 is exact work avoided, "
+                                 "and the hardware FP64 pipe-slot fraction is frac x executed_term_ratio x 12/10"},
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(cells * N_VEL ** 3 * 8),
                     "d2h_bytes_per_step": int(cells * N_VEL ** 3 * 8),
                     "path": "CollisionOperator.collision_rk2(pinned numpy) -> boltz_rk2_batch(mem=HOST)"},
+            "e2e_pageable": {"value": pg_value, "unit": "evals/s", "h2d_bytes_per_step": int(cells * N_VEL ** 3 * 8),
+                             "d2h_bytes_per_step": int(cells * N_VEL ** 3 * 8),
+                             "ratio_to_pinned": pg_value / e2e_value, "bitwise_equal_to_pinned": pageable_bitwise,
+                             "path": "CollisionOperator.collision_rk2(plain numpy) -> boltz_rk2_batch(mem=HOST)"},
             "clocks": clk.summary(),
             "setup_s": {"table_generate": round(t_gen, 3), "table_upload_fold": round(t_upload, 3)},
         }
+        if parity:
+            line["parity"] = parity
         if n32:
             line["n32"] = n32
         if cfg3:
@@ -380,74 +479,155 @@ def main():
         dist.destroy_process_group()
 
 
-def bench_cfg3(op, dev, steps=60):
-    """cfg3 (BASELINE.json configs[2]) on this rank: Nx=256 geometric cells,
-    diffuse wall T_w=2, Strang steps (SSP-RK2 transport + RK2 collision) replayed
-    as a CUDA graph of 3 steps; 1 rank (the halo path is exercised by tests)."""
+def rel_state(got, ref):
+    return max(float(np.abs(g - r).max() / np.abs(r).max()) for g, r in zip(got, ref))
+
+
+class _HostStagedHalo:
+    """BOLTZ_BENCH_DIST=gloo plumbing check only: the field goes through host
+    memory to torch.distributed gloo P2P (ranks folded onto one GPU cannot share
+    an NCCL communicator).  Not a measurement path."""
+
+    def __init__(self, rank, world):
+        from paper_1301_4195_b200.solver import TorchHalo
+        self.h = TorchHalo(rank, world)
+
+    def exchange(self, field):
+        host = field.cpu()
+        n = self.h.exchange(host)
+        field.copy_(host)
+        return n
+
+
+def bench_cfg3(op, dev, rank, world, backend, steps=60):
+    """cfg3 (BASELINE.json configs[2]): Nx=256 geometric cells, diffuse wall
+    T_w=2, Strang steps (SSP-RK2 transport + RK2 collision).  One rank: CUDA
+    graph of 3 Strang steps.  N>1 ranks: STRONG-scaled -- the 256 cells are
+    sharded by plan_decomposition and the ghosts cross ranks through the
+    library's NCCL halo (boltz_halo_exchange, captured in the same graph);
+    rank 0 then recomputes the run unsharded and compares bitwise (the
+    decomposition transparency contract)."""
     import torch
-    from paper_1301_4195_b200 import scenarios
+    import torch.distributed as dist
+    from paper_1301_4195_b200 import NcclHalo, scenarios
     from paper_1301_4195_b200.solver import Boundary, Solver1D
     grid = op.grid
-    x, dx = scenarios.geometric_grid(256, 20.0, 1.02)
-    f0 = np.tile(scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0), (256, 1))
-    op.set_schedule("latency")  # 256 cells: K2 rows split over 4 warps (DESIGN.md §3)
-    s = Solver1D(op, x, dx, f0, left=Boundary("wall", 2.0), right=Boundary("extrap"), device=dev)
+    nx = 256
+    x, dx = scenarios.geometric_grid(nx, 20.0, 1.02)
+    m0 = scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0)
+    init = lambda start, count: np.tile(m0, (count, 1))  # noqa: E731
+    op.set_schedule("latency")  # <= 256 cells per rank: K2 rows split over 4 warps (DESIGN.md §3)
+    kw = dict(left=Boundary("wall", 2.0), right=Boundary("extrap"), device=dev)
+    halo = None
+    if world > 1:
+        halo = NcclHalo(rank, world, dev.index) if backend == "nccl" else _HostStagedHalo(rank, world)
+    s = Solver1D(op, x, dx, init, rank=rank, world=world, halo=halo, **kw)
     dt = s.cfl_dt()
-    s.strang_step(dt)
+    graph = world == 1 or isinstance(halo, NcclHalo)
+    s.strang_step(dt)  # warm-up: workspace + kernel attributes
     op.timing(reset=True)
-    s.capture(dt)  # the launches of 3 Strang steps are counted here, at capture
-    _, counts = op.timing(reset=True)
-    launches_per_step = sum(counts.values()) / 3
-    s.advance(3)
+    if graph:
+        s.capture(dt)  # the launches of 3 Strang steps are counted here, at capture
+        _, counts = op.timing(reset=True)
+        launches_per_step = sum(counts.values()) / 3
+        s.advance(3)
+    else:
+        launches_per_step = None
+        for _ in range(3):
+            s.strang_step(dt)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    s.advance(steps)
+    if graph:
+        s.advance(steps)
+    else:
+        for _ in range(steps):
+            s.strang_step(dt)
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64,
+                      device=dev if backend == "nccl" else torch.device("cpu"))
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    done = 1 + 3 + steps  # Strang steps each rank has taken
+    out = {"workload": "cfg3: Nx=256 geometric (1.02) on [0,20], N=16 L=6, diffuse wall T_w=2, dt=CFL 0.9",
+           "ranks": world, "scaling": "strong" if world > 1 else None, "steps": steps, "ms_per_step": ms / steps,
+           "cells_steps_per_s": nx * steps / (ms * 1e-3), "evals_per_s": 2 * nx * steps / (ms * 1e-3),
+           "mode": ("CUDA graph of 3 Strang steps" if graph else "eager Strang steps") + ", K2 latency schedule"
+                   + (", NCCL halo (boltz_halo_exchange) inside the graph" if isinstance(halo, NcclHalo) else
+                      ", host-staged gloo halo (plumbing check, not a measurement)" if world > 1 else ""),
+           "launches_per_step_rank0": launches_per_step}
+    if world > 1:
+        n3 = grid.size()
+        # 4 ghost refreshes per Strang step (2 sub-steps x 2 stages), 2 cells x N^3 doubles each way per boundary
+        out["halo_bytes_per_step"] = {"per_boundary_each_way": 4 * 2 * n3 * 8,
+                                      "total": 4 * 2 * 2 * (world - 1) * n3 * 8}
+        parts = [None] * world if rank == 0 else None
+        dist.gather_object((s.start, s.interior.cpu().numpy()), parts, dst=0)
+        if rank == 0:
+            parts.sort(key=lambda p: p[0])
+            sharded = np.concatenate([p[1] for p in parts])
+            one = Solver1D(op, x, dx, init, rank=0, world=1, halo=None, **kw)
+            one.strang_step(dt)
+            one.run(dt, done - 1, graph=True)
+            out["bitwise_vs_1rank"] = bool(np.array_equal(sharded, one.interior.cpu().numpy()))
+            out["steps_compared"] = done
     op.set_schedule("throughput")
-    return {"workload": "cfg3: Nx=256 geometric (1.02) on [0,20], N=16 L=6, diffuse wall T_w=2, dt=CFL 0.9",
-            "steps": steps, "ms_per_step": ms / steps, "cells_steps_per_s": 256 * steps / (ms * 1e-3),
-            "evals_per_s": 2 * 256 * steps / (ms * 1e-3),
-            "mode": "async library + CUDA graph of 3 Strang steps, K2 latency schedule",
-            "launches_per_step": launches_per_step}
+    return out
 
 
 def bench_n32(args, dev, local):
+    """cfg5-shaped N=32 sub-measurement: 2048 mixture cells, RK2 steps, with a
+    parity witness of two cells of the last timed step against the oracle."""
     import torch
     from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios
     n, L, cells = 32, 8.0, 2048
+    warm, steps = max(3, args.warmup), max(5, min(args.steps, 8))
     grid = VelocityGrid.create(n, L)
     t0 = time.perf_counter()
     G = generate_table(grid, KernelSpec(LAM))
     t_gen = time.perf_counter() - t0
     op = CollisionOperator(grid, KernelSpec(LAM), G, device=local)
-    del G
     f = torch.from_numpy(scenarios.mixture_cells(grid, cells, seed=4195)).to(dev)
-    for _ in range(1):
+    for _ in range(warm):
         op.collision_rk2(f, 1e-3)
     torch.cuda.synchronize()
     op.timing(reset=True)
     op.set_timing(True)
-    steps = 2
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
+    ms = 0.0
+    wit = list(WITNESS32)
+    snap = None
+    for i in range(steps):
+        if i == steps - 1:
+            snap = f[wit].cpu().numpy()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         op.collision_rk2(f, 1e-3)
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
     kms, kl = op.timing(reset=True)
+    after = f[wit].cpu().numpy()
     op.close()
+    from oracle import oracle as O
+    O.build()
+    ref = O.collision_rk2(n, L, G, snap, 1e-3, 1.0, nthreads=host_cpu()["physical_cores"])
+    del G
     conv_avg = kms["conv"] / max(kl["conv"], 1)
-    # the workspace may split the batch: flops per launch = per-launch cells share
     flop_total = FLOP_PER_TERM * terms_per_eval(n) * cells * 2 * steps
-    return {"workload": f"cfg5-shaped: {cells} cells, N=32^3 on [-8,8]^3, lambda=1, RK2 steps",
-            "value": 2 * cells * steps / (ms * 1e-3), "unit": "evals/s", "steps": steps, "warmup": 1,
+    return {"workload": f"cfg5-shaped: {cells} cells, N=32^3 on [-8,8]^3, lambda=1, RK2 steps (dt=1e-3)",
+            "value": 2 * cells * steps / (ms * 1e-3), "unit": "evals/s", "steps": steps, "warmup": warm,
             "ms_per_step": ms / steps, "conv_tflops_algorithmic": flop_total / (kms["conv"] * 1e-3) / 1e12,
             "conv_ms_per_kernel": conv_avg, "conv_kernels_per_eval": kl["conv"] / (2 * steps),
-            "table_generate_s": round(t_gen, 2)}
+            "table_generate_s": round(t_gen, 2),
+            "parity": {"cells_n32": wit,
+                       "max_rel_increment_n32": max(float(np.abs(a - r).max() / np.abs(r - b).max())
+                                                    for a, r, b in zip(after, ref, snap)),
+                       "max_rel_state_n32": rel_state(after, ref)}}
 
 
 if __name__ == "__main__":

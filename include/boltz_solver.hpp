@@ -6,7 +6,9 @@
 //
 //   strang_step(dt) = T(dt/2) o C_RK2(dt) o T(dt/2)
 //   T(h):  SSP-RK2 of the FV step, ghost refresh before each
-//          stage: halo exchange (NCCL / loopback) + physical ends
+//          stage: halo exchange (NCCL / loopback) + physical ends; or the
+//          SPEC's literal single stage f <- S(f) with one ghost refresh
+//          (SPEC.md:342-345,471): TransportScheme::SingleStage
 //   C_RK2: boltz_rk2_batch over the rank's interior cells (cell-local)
 //
 // Field: (ncl + 4) x N^3 doubles on the device, ghosts at 0,1 and ncl+2,ncl+3
@@ -107,6 +109,12 @@ private:
     size_t n_ = 0;
 };
 
+// time integration of the transport sub-step T(h)
+enum class TransportScheme {
+    SspRk2 = 0,       // Heun: t1 = S(f), f <- f/2 + S(t1)/2 (DESIGN.md §5 item 4)
+    SingleStage = 1,  // f <- S(f), one ghost refresh per sub-step
+};
+
 class Solver1D {
 public:
     // x, dx: GLOBAL cell centres / widths; f0: this rank's interior cells,
@@ -114,9 +122,10 @@ public:
     // halo: NCCL communicator for world > 1 (nullptr with the loopback driver).
     Solver1D(CollisionOperator& op, int n, double half_width, std::span<const double> x, std::span<const double> dx,
              std::span<const double> f0, int rank = 0, int world = 1, Boundary left = {}, Boundary right = {},
-             double epsilon = 1.0, boltz_halo* halo = nullptr, cudaStream_t stream = nullptr)
+             double epsilon = 1.0, boltz_halo* halo = nullptr, cudaStream_t stream = nullptr,
+             TransportScheme scheme = TransportScheme::SspRk2)
         : op_(op), n3_((int64_t)n * n * n), L_(half_width), rank_(rank), world_(world), left_(left), right_(right),
-          eps_(epsilon), halo_(halo), s_(stream) {
+          eps_(epsilon), halo_(halo), s_(stream), scheme_(scheme) {
         cuda_check(cudaGetDevice(&device_));
         const auto plan = plan_decomposition((int64_t)x.size(), world);
         start_ = plan[rank].first;
@@ -139,6 +148,7 @@ public:
     }
 
     int64_t ncl() const { return ncl_; }
+    int transport_stages() const { return scheme_ == TransportScheme::SingleStage ? 1 : 2; }
     int64_t cell_values() const { return n3_; }
     int64_t start() const { return start_; }
     double time() const { return t_; }
@@ -182,7 +192,9 @@ public:
         check(boltz_transport_step_peer(op_.handle(), in, stage ? field_.data() : nullptr, stage ? 0.5 : 0.0,
                                         stage_out(stage), ncl_, x_ext_.data(), dx_ext_.data(), h, wl, wr, left_dst,
                                         right_dst, s_));
-        if (stage == 1) {
+        if (scheme_ == TransportScheme::SingleStage) {
+            field_.swap(tmp_);  // field = S(f)
+        } else if (stage == 1) {
             field_.swap(tmp_);
             tmp2_.swap(field_);
         }
@@ -195,10 +207,18 @@ public:
         check(boltz_store_edges(op_.handle(), interior(), ncl_, left_dst, right_dst, s_));
     }
 
-    // SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
-    // stage 1: f <- f/2 + S(t1)/2, S = one FV step after a ghost refresh
+    // stage of the transport sub-step.  SSP-RK2: stage 0: t1 = S(f);
+    // stage 1: f <- f/2 + S(t1)/2.  SingleStage: stage 0: f <- S(f).
+    // S = one FV step after a ghost refresh of its input
     void transport_stage(int stage, double h, bool exchange = true) {
         const int wl = rank_ == 0 && left_.is_wall(), wr = rank_ == world_ - 1 && right_.is_wall();
+        if (scheme_ == TransportScheme::SingleStage) {
+            fill_ghosts(exchange);
+            check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
+                                       dx_ext_.data(), h, wl, wr, s_));
+            field_.swap(tmp_);  // field = S(f)
+            return;
+        }
         if (stage == 0) {
             fill_ghosts(exchange);
             check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
@@ -217,8 +237,7 @@ public:
 
     void transport(double h) {
         if (h * L_ > dx_min_ * (1 + 1e-12)) throw Error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
-        transport_stage(0, h);
-        transport_stage(1, h);
+        for (int stage = 0; stage < transport_stages(); ++stage) transport_stage(stage, h);
     }
 
     void collide(double dt) { check(boltz_rk2_batch(op_.handle(), interior(), ncl_, dt, 1.0 / eps_, BOLTZ_MEM_DEVICE, s_)); }
@@ -353,6 +372,7 @@ private:
     double eps_;
     boltz_halo* halo_;
     cudaStream_t s_;
+    TransportScheme scheme_;
     int64_t start_ = 0, ncl_ = 0;
     double dx_min_ = 0, t_ = 0;
     double sigma_w_[2] = {0, 0};
@@ -401,7 +421,7 @@ public:
 
     void strang_step(double dt) {
         for (int half = 0; half < 2; ++half) {
-            for (int stage = 0; stage < 2; ++stage)
+            for (int stage = 0; stage < r_[0]->transport_stages(); ++stage)
                 op([&](size_t i, double* l, double* r) { r_[i]->transport_stage_peer(stage, 0.5 * dt, l, r); },
                    stage == 0 ? Kind::Stage0 : Kind::Stage1);
             if (half == 0) op([&](size_t i, double* l, double* r) { r_[i]->collide_peer(dt, l, r); }, Kind::Collide);
@@ -462,7 +482,7 @@ inline void strang_step_loopback(std::vector<Solver1D*>& ranks, double dt, cudaS
         check(boltz_halo_exchange_loopback(fields.data(), ncl.data(), (int)ranks.size(), cells, s));
     };
     for (int half = 0; half < 2; ++half) {
-        for (int stage = 0; stage < 2; ++stage) {
+        for (int stage = 0; stage < ranks[0]->transport_stages(); ++stage) {
             exchange(stage, ranks[0]->cell_values());
             for (auto* r : ranks) r->transport_stage(stage, 0.5 * dt, false);
         }

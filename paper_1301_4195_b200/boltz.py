@@ -404,15 +404,27 @@ class CollisionOperator:
             raise ConfigError(f"array of {n} values is not a whole number of cells ({per_cell} per cell)")
         return n // per_cell
 
-    def _args(self, *arrays):
+    def _args(self, *arrays, complex_idx=()):
+        """Pointers, memory kind and stream for a call. Device arrays must be
+        contiguous CUDA tensors on this operator's device, complex128 at the
+        positions in `complex_idx` and float64 elsewhere."""
         if all(_is_torch(a) for a in arrays):
             import torch
-            for a in arrays:
-                if not (a.is_cuda and a.is_contiguous() and a.dtype in (torch.float64, torch.complex128)):
-                    raise ConfigError("device arrays must be contiguous float64/complex128 CUDA tensors")
+            for i, a in enumerate(arrays):
+                want = torch.complex128 if i in complex_idx else torch.float64
+                if not (a.is_cuda and a.is_contiguous()):
+                    raise ConfigError("device arrays must be contiguous CUDA tensors")
+                if a.dtype != want:
+                    raise ConfigError(f"argument {i}: expected a {want} tensor, got {a.dtype}")
+                if a.device.index != self.device:
+                    raise ConfigError(f"argument {i} lives on cuda:{a.device.index}, the operator on cuda:{self.device}")
             return [a.data_ptr() for a in arrays], MEM_DEVICE, torch.cuda.current_stream(arrays[0].device).cuda_stream
         if any(_is_torch(a) for a in arrays):
             raise ConfigError("mix of host and device arrays")
+        for i, a in enumerate(arrays):
+            want = np.complex128 if i in complex_idx else np.float64
+            if a.dtype != want:
+                raise ConfigError(f"argument {i}: expected a {np.dtype(want)} array, got {a.dtype}")
         return [a.ctypes.data for a in arrays], MEM_HOST, None
 
     def _alloc_like(self, x, shape, complex_=False):
@@ -427,7 +439,9 @@ class CollisionOperator:
 
     def _prep(self, x, complex_=False):
         if _is_torch(x):
-            return x.contiguous()
+            return x.contiguous()  # dtype and device are checked by _args
+        if not complex_ and np.iscomplexobj(x):
+            raise ConfigError("expected real data, got a complex array")
         return self._host(x, np.complex128 if complex_ else np.float64)
 
     # -- reference operations, batched
@@ -437,7 +451,7 @@ class CollisionOperator:
         n3 = self.grid.size()
         nc = self._ncells(f, n3)
         out = self._alloc_like(f, (nc, n3), complex_=True)
-        (pf, po), mem, s = self._args(f, out)
+        (pf, po), mem, s = self._args(f, out, complex_idx=(1,))
         _check(lib().boltz_forward_batch(self._h, pf, po, nc, mem, s))
         return out
 
@@ -448,7 +462,7 @@ class CollisionOperator:
         nc = self._ncells(g, n3)
         out = self._alloc_like(g, (nc, n3))
         mi = self._alloc_like(g, (nc,))
-        (pg, po, pm), mem, s = self._args(g, out, mi)
+        (pg, po, pm), mem, s = self._args(g, out, mi, complex_idx=(0,))
         _check(lib().boltz_inverse_batch(self._h, pg, po, pm, nc, mem, s))
         return out, mi
 
@@ -458,7 +472,7 @@ class CollisionOperator:
         n3 = self.grid.size()
         nc = self._ncells(fhat, n3)
         out = self._alloc_like(fhat, (nc, n3), complex_=True)
-        (pf, po), mem, s = self._args(fhat, out)
+        (pf, po), mem, s = self._args(fhat, out, complex_idx=(0, 1))
         _check(lib().boltz_qhat_batch(self._h, pf, po, nc, mem, s))
         return out
 

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -114,6 +115,11 @@ struct boltz_ctx {
     int64_t seg_cap = 0;      // cells
     double2* dSeg2 = nullptr; // ... of the second workspace set (swap_workspace)
     int64_t seg_cap2 = 0;
+    // once a call was captured into a CUDA graph, the graph holds the workspace
+    // pointers: growing a buffer then retires the old one (freed at destroy)
+    // instead of freeing it, so a later replay never touches freed memory
+    bool graph_captured = false;
+    std::vector<void*> retired;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<int> ev_kind;
@@ -124,6 +130,35 @@ struct boltz_ctx {
 namespace {
 
 int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
+
+// frees a workspace buffer, or retires it while a captured graph may use it
+void release(boltz_ctx* c, void* p) {
+    if (!p) return;
+    if (c->graph_captured) c->retired.push_back(p);
+    else cudaFree(p);
+}
+
+// marks the context's workspace as baked into a graph when `s` is capturing
+void note_capture(boltz_ctx* c, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) c->graph_captured = true;
+}
+
+// One-time kernel configuration (cudaFuncSetAttribute) PER DEVICE: the runtime
+// keeps function attributes per device context, so one process driving several
+// GPUs (PeerGroup, boltz_halo_create_all) must opt each device in.
+struct PerDevice {
+    std::mutex m;
+    uint64_t mask = 0;
+    template <class Fn>
+    void once(int dev, Fn&& fn) {
+        std::lock_guard<std::mutex> g(m);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (mask & bit) return;
+        fn();  // throws CudaError on failure; the bit stays clear
+        mask |= bit;
+    }
+};
 
 // Brackets one kernel launch with CUDA events on its stream when timing is on.
 struct Timed {
@@ -737,7 +772,7 @@ void ensure_workspace(boltz_ctx* c, int64_t cells) {
     int64_t lim = std::max<int64_t>(kLanes, (int64_t)(gb * (1 << 30)) / per_cell / kLanes * kLanes);
     want = std::min(want, lim);
     if (want <= c->cap) return;
-    cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs); cudaFree(c->dMaxIm);
+    release(c, c->dA); release(c, c->dB); release(c, c->dFs); release(c, c->dMaxIm);
     c->dA = c->dB = nullptr; c->dFs = nullptr; c->dMaxIm = nullptr; c->cap = 0;
     CK(cudaMalloc(&c->dA, (size_t)want * n3 * 16));
     CK(cudaMalloc(&c->dB, (size_t)want * n3 * 16));
@@ -752,7 +787,9 @@ void ensure_workspace(boltz_ctx* c, int64_t cells) {
 // `cells` counts cells x schedule
 void ensure_seg(boltz_ctx* c, int64_t cells) {
     if (cells <= c->seg_cap) return;
-    cudaFree(c->dSeg); cudaFree(c->dSeg2);
+    // only the current set's scratch: the other set's may still be in use by
+    // the other compute stream (swap_workspace)
+    release(c, c->dSeg);
     c->dSeg = nullptr;
     c->seg_cap = 0;
     CK(cudaMalloc(&c->dSeg, (size_t)kConvWarps * cells * n3_of(c) * 16));
@@ -762,9 +799,11 @@ void ensure_seg(boltz_ctx* c, int64_t cells) {
 // the second workspace set (same capacity as the first)
 void ensure_workspace2(boltz_ctx* c) {
     if (c->cap2 == c->cap) return;
-    cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
-    cudaFree(c->dSeg);
+    release(c, c->dA2); release(c, c->dB2); release(c, c->dFs2); release(c, c->dMaxIm2);
+    release(c, c->dSeg2);  // the second set's scratch; ensure_seg reallocates it on demand
     c->dA2 = c->dB2 = nullptr; c->dFs2 = nullptr; c->dMaxIm2 = nullptr; c->cap2 = 0;
+    c->dSeg2 = nullptr;
+    c->seg_cap2 = 0;
     const int64_t n3 = n3_of(c);
     CK(cudaMalloc(&c->dA2, (size_t)c->cap * n3 * 16));
     CK(cudaMalloc(&c->dB2, (size_t)c->cap * n3 * 16));
@@ -788,8 +827,8 @@ void ensure_staging(boltz_ctx* c, int64_t cells) {
     if (cells <= c->stage_cap) return;
     const int64_t n3 = n3_of(c);
     for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
-        cudaFree(c->dStageIn[b]);
-        cudaFree(c->dStageOut[b]);
+        release(c, c->dStageIn[b]);
+        release(c, c->dStageOut[b]);
         c->dStageIn[b] = c->dStageOut[b] = nullptr;
     }
     c->stage_cap = 0;
@@ -816,11 +855,10 @@ struct Launch {
 #if BOLTZ_FUSED
         if constexpr (Fused<N>::FITS) {
             using F = Fused<N>;
-            static bool configured = false;
-            if (!configured) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
                 CK(cudaFuncSetAttribute(k_fwd_fused<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
-                configured = true;
-            }
+            });
             Timed t_(c, KIND_FFT, s);
             k_fwd_fused<N><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(f, c->dA, nc, scale,
                                                                                           c->dFlag);
@@ -846,8 +884,8 @@ struct Launch {
                 constexpr int W = kcsm_warps(N);
                 const int smem_ph[4] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
                                         W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES};
-                static bool configured = false;
-                if (!configured) {
+                static PerDevice configured;  // attributes are per device
+                configured.once(c->device, [&] {
                     auto cfg = [&](auto fn, int ph) {
                         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ph[ph]));
                         CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -863,8 +901,7 @@ struct Launch {
                         cfg(k_conv_kcsm<N, 0, 3>, 3);
                         cfg(k_conv_kcsm<N, KC1, 3>, 3);
                     }
-                    configured = true;
-                }
+                });
                 const unsigned gy = (unsigned)((ng + W - 1) / W);
                 // longest rows first in the last column of many-wave grids (conv_row)
                 auto lpt = [&](int nrows) { return (int64_t)nrows * gy < 8 * 2 * 148 ? 0 : (int)gy - 1; };
@@ -895,12 +932,11 @@ struct Launch {
         if constexpr (mirror_pipe_n(N) && N % 4 == 0) {
             if (hermitian && c->mirror && c->mirror2 && c->schedule == 0) {
                 const int smem = Mirror2Layout<N>::CTA_BYTES;
-                static bool configured = false;
-                if (!configured) {
+                static PerDevice configured;  // attributes are per device
+                configured.once(c->device, [&] {
                     CK(cudaFuncSetAttribute(k_conv_mirror2<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                     CK(cudaFuncSetAttribute(k_conv_mirror2<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                    configured = true;
-                }
+                });
                 dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
                 int lpt = 0;
                 if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
@@ -915,12 +951,11 @@ struct Launch {
         if constexpr (mirror_pipe_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 const int smem = kConvWarps * MirrorLayout<N>::WARP_BYTES;
-                static bool configured = false;
-                if (!configured) {
+                static PerDevice configured;  // attributes are per device
+                configured.once(c->device, [&] {
                     CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                     CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                    configured = true;
-                }
+                });
                 dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
                 // longest items first in every column: items range from single rows to
                 // row pairs (~1.6x), and LPT everywhere measured best (11.17 ms against
@@ -940,12 +975,11 @@ struct Launch {
             if (c->schedule > 0) {
                 const int S = kConvWarps * c->schedule;  // segments per row
                 const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
-                static bool configured = false;
-                if (!configured) {
+                static PerDevice configured;  // attributes are per device
+                configured.once(c->device, [&] {
                     CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                     CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                    configured = true;
-                }
+                });
                 ensure_seg(c, ng * kLanes * c->schedule);
                 Timed t_(c, KIND_CONV, s);
                 k_conv_seg<N><<<dim3(N * N, (unsigned)ng, (unsigned)c->schedule), kLanes * kConvWarps, smem, s>>>(
@@ -965,12 +999,11 @@ struct Launch {
         if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
         if constexpr (conv_kernel_for(N) == 1 && kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
             const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
-            static bool configured = false;  // per process; attributes apply to every device
-            if (!configured) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
                 CK(cudaFuncSetAttribute(k_conv_pipe<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                 CK(cudaFuncSetAttribute(k_conv_pipe<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                configured = true;
-            }
+            });
             Timed t_(c, KIND_CONV, s);
             k_conv_pipe<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart,
                                                                     (int)ng, lpt);
@@ -978,14 +1011,13 @@ struct Launch {
             using LY = KcsLayout<N>;
             const int smem = kConvWarps * LY::WARP_BYTES;
             constexpr int KC1 = NK > 1 ? 1 : 0;
-            static bool configured = false;
-            if (!configured) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
                 CK(cudaFuncSetAttribute(k_conv_kcs<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                 CK(cudaFuncSetAttribute(k_conv_kcs<N, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 CK(cudaFuncSetAttribute(k_conv_kcs<N, KC1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                 CK(cudaFuncSetAttribute(k_conv_kcs<N, KC1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                configured = true;
-            }
+            });
             dim3 g1(N * N, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
             Timed t_(c, KIND_CONV, s);
             k_conv_kcs<N, 0><<<g1, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dH, c->dEnt, c->dRowStart, (int)ng, lpt);
@@ -1022,11 +1054,10 @@ struct Launch {
             const int64_t ng = (nc + 31) / 32;
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
-            static bool configured = false;
-            if (!configured) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
                 CK(cudaFuncSetAttribute(k_inv_project<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, F::SMEM));
-                configured = true;
-            }
+            });
             Timed t_(c, KIND_PROJECT, s);
             k_inv_project<N><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(
                 c->dB, base, out, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
@@ -1050,12 +1081,11 @@ struct Launch {
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
-            static bool configured = false;
-            if (!configured) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
                 CK(cudaFuncSetAttribute(k_inv_project<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         F::SMEM));
-                configured = true;
-            }
+            });
             Timed t_(c, KIND_PROJECT, s);
             k_inv_project<N, true><<<(unsigned)(ng * kLanes / F::CPB), F::THREADS, F::SMEM, s>>>(
                 c->dB, base, nullptr, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
@@ -1187,6 +1217,7 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
     }
     if (ncells == 0) return BOLTZ_OK;
     cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
+    note_capture(c, s);
     if (mem == BOLTZ_MEM_HOST) return run_host_pipelined(c, in, out, ncells, in_elems, out_elems, s, max_imag, fn);
     ensure_workspace(c, ncells);
     const bool deferred = c->async_mode;  // flag checked at boltz_sync
@@ -1443,6 +1474,8 @@ int boltz_destroy(boltz_ctx* c) {
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
+    cudaFree(c->dSeg); cudaFree(c->dSeg2);
+    for (void* p : c->retired) cudaFree(p);
     if (c->comp2) cudaStreamDestroy(c->comp2);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -1659,6 +1692,7 @@ int boltz_fill_boundary(boltz_ctx* c, double* field, int64_t ncl, const double* 
             return BOLTZ_ERR_CONFIG;
         }
         cudaStream_t s = (cudaStream_t)stream;  // NULL = the CUDA default stream
+        note_capture(c, s);
         double vw[3] = {0, 0, 0};
         if (Vw_host3) std::memcpy(vw, Vw_host3, sizeof vw);
         double* dsig = reinterpret_cast<double*>(c->dMaxIm);

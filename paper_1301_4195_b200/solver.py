@@ -3,8 +3,11 @@ and the GPU collision RK2, with the spatial domain sharded across ranks
 (SPEC.md:372-481, PAPER.md:194-201, 383-432).
 
     strang_step(dt) = T(dt/2) o C_RK2(dt) o T(dt/2)
-    T(h): ghost fill (halo exchange / wall / extrapolation), then one explicit
-          FV step -- single stage, SURVEY Appendix A.4
+    T(h): SSP-RK2 (Heun) of the explicit FV step S:
+          t1 = S(f), f <- f/2 + S(t1)/2, each S after a ghost refresh (halo
+          exchange / wall / extrapolation) -- DESIGN.md §5 item 4.  The SPEC's
+          literal single stage, f <- S(f) with one ghost refresh
+          (SPEC.md:342-345,471), is `transport_scheme="single_stage"`.
     C_RK2(dt): boltz_rk2_batch over the rank's interior cells -- cell-local,
           no communication
 
@@ -125,8 +128,11 @@ class Solver1D:
 
     def __init__(self, op: CollisionOperator, x: np.ndarray, dx: np.ndarray, f0, *, rank: int = 0,
                  world: int = 1, left: Boundary = Boundary(), right: Boundary = Boundary(),
-                 epsilon: float = 1.0, halo=None, device=None, plan=None):
+                 epsilon: float = 1.0, halo=None, device=None, plan=None, transport_scheme: str = "ssp_rk2"):
         import torch
+        if transport_scheme not in ("ssp_rk2", "single_stage"):
+            raise ConfigError(f"transport_scheme must be 'ssp_rk2' or 'single_stage', got {transport_scheme!r}")
+        self.scheme = transport_scheme
         self.op, self.rank, self.world, self.eps = op, rank, world, epsilon
         self.left, self.right = left, right
         self.n3 = op.grid.size()
@@ -198,11 +204,22 @@ class Solver1D:
     def _walls(self):
         return (self.is_left_end and self.left.is_wall, self.is_right_end and self.right.is_wall)
 
+    @property
+    def transport_stages(self) -> int:
+        return 1 if self.scheme == "single_stage" else 2
+
     def transport_stage(self, stage: int, dt: float, exchange: bool = True) -> None:
-        """SSP-RK2 stage of the transport sub-step: stage 0: t1 = S(f);
-        stage 1: f <- f/2 + S(t1)/2, S = one FV step after a
-        ghost refresh of its input."""
+        """Stage of the transport sub-step.  SSP-RK2: stage 0: t1 = S(f);
+        stage 1: f <- f/2 + S(t1)/2.  single_stage: stage 0
+        is f <- S(f).  S = one FV step after a ghost refresh
+        of its input."""
         wl, wr = self._walls()
+        if self.scheme == "single_stage":
+            self.fill_ghosts(exchange)
+            self._track_flux(dt, wl, wr)
+            self.op.transport_step(self.field, self._tmp, self.x_ext, self.dx_ext, dt, wl, wr)
+            self.field, self._tmp = self._tmp, self.field
+            return
         if stage == 0:
             self.fill_ghosts(exchange)
             self._track_flux(dt, wl, wr)
@@ -234,16 +251,19 @@ class Solver1D:
         return f.cpu().numpy()
 
     def _track_flux(self, dt: float, wl: bool, wr: bool) -> None:
-        # SSP-RK2: f^{n+1} = f^n - dt/2 (D(f^n) + D(t1)), so each stage's face fluxes weigh dt/2
+        # SSP-RK2: f^{n+1} = f^n - dt/2 (D(f^n) + D(t1)), so each stage's face fluxes weigh dt/2;
+        # the single stage weighs its one set of fluxes dt
         if getattr(self, "_flux", None) is not None:
-            self.op.end_flux(self.field, self.x_ext, self.dx_ext, self._flux, 0.5 * dt, wl, wr)
+            w = dt if self.scheme == "single_stage" else 0.5 * dt
+            self.op.end_flux(self.field, self.x_ext, self.dx_ext, self._flux, w, wl, wr)
 
     def transport(self, dt: float, exchange: bool = True) -> None:
-        """Transport sub-step T(dt): SSP-RK2 of the FV step."""
+        """Transport sub-step T(dt): SSP-RK2 of the FV step, or
+        the SPEC's single stage (transport_scheme="single_stage")."""
         if dt * self.op.grid.half_width > float(self.dx_glob.min()) * (1 + 1e-12):
             raise ConfigError("transport: CFL violated (dt * L > min dx)")
-        self.transport_stage(0, dt, exchange)
-        self.transport_stage(1, dt, exchange)
+        for stage in range(self.transport_stages):
+            self.transport_stage(stage, dt, exchange)
 
     def collide(self, dt: float) -> None:
         interior = self.field[2:self.ncl + 2]  # contiguous rows -> in place on device
@@ -316,7 +336,7 @@ class Solver1D:
 def strang_step_loopback(solvers: Sequence[Solver1D], dt: float) -> None:
     """One Strang step of n virtual ranks in one process (LoopbackHalo)."""
     for half in (0, 1):
-        for stage in (0, 1):
+        for stage in range(solvers[0].transport_stages):
             if stage == 1:  # the stage-1 input t1 lives in _tmp until transport_stage swaps it in
                 LoopbackHalo.exchange_all([s._tmp for s in solvers])
             else:

@@ -84,7 +84,9 @@ def spatial(args, rank, world, dev):
     if world > 1 and args.halo == "nccl":
         from paper_1301_4195_b200 import NcclHalo
         halo = NcclHalo(rank, world, dev.index)  # the C ABI's NCCL halo: capturable, so graphs across ranks
-    s = Solver1D(op, x, dx, init, rank=rank, world=world, left=left, right=right, plan=plan, device=dev, halo=halo)
+    s = Solver1D(op, x, dx, init, rank=rank, world=world, left=left, right=right, plan=plan, device=dev, halo=halo,
+                 transport_scheme=args.transport)
+    mass0 = float(s.ledger()[0])  # global sum_j dx_j rho_j of the initial state (collective)
     dt = s.cfl_dt()
     # warm-up step (not timed), then the run
     s.strang_step(dt)
@@ -128,7 +130,7 @@ def spatial(args, rank, world, dev):
             "kernel_ms_rank0": {k: round(v, 3) for k, v in kms.items() if v},
             "kernel_launches_rank0": {k: v for k, v in kl.items() if v},
             "setup_s": round(t_setup, 2),
-            "mass": float((rho * dx).sum()), "mass0": float(dx.sum() * (1.0 if cfg == 3 else np.nan)),
+            "mass": float((rho * dx).sum()), "mass0": mass0, "transport": args.transport,
             "T_wall_cell": float(T[0]), "T_far": float(T[-1]), "max_abs_V1": float(np.abs(V1).max()),
         }
     return out
@@ -170,6 +172,8 @@ def main():
     p.add_argument("--steps", type=int, default=0)
     p.add_argument("--lam", type=float, default=1.0)
     p.add_argument("--mode", default="graph", choices=["graph", "eager"])
+    p.add_argument("--transport", default="ssp_rk2", choices=["ssp_rk2", "single_stage"],
+                   help="transport sub-step: SSP-RK2 (default) or the SPEC single stage (SPEC.md:342-345)")
     p.add_argument("--schedule", default="auto", choices=["auto", "throughput", "latency", "latency8"],
                    help="K2 schedule (auto: latency for <= 256 cells per rank at N <= 16)")
     p.add_argument("--halo", default="nccl", choices=["nccl", "torch"],

@@ -2,7 +2,9 @@
 // time-stepping loop in the reference's language over the C ABI.  Built and
 // checked by tests/test_cpp_solver.py against the Python driver (solver.py).
 //
-//   solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE
+//   solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE [SCHEME]
+//     SCHEME ssp (default): SSP-RK2 transport sub-steps; single: the SPEC's
+//                    single-stage transport sub-step
 //     DIR/x.bin, DIR/dx.bin: Nx doubles; DIR/f0.bin: Nx x N^3 doubles
 //     MODE nccl:     one rank, an NCCL communicator of world 1 (exchange is
 //                    then a no-op; allreduce of the ledger is exercised)
@@ -34,11 +36,12 @@ static std::vector<double> read_bin(const std::string& path) {
 }
 
 int main(int argc, char** argv) {
-    if (argc != 10) {
-        std::fprintf(stderr, "usage: solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE\n");
+    if (argc != 10 && argc != 11) {
+        std::fprintf(stderr, "usage: solver_demo DIR N L LAMBDA TW DT STEPS NRANKS MODE [SCHEME]\n");
         return 2;
     }
-    const std::string dir = argv[1], mode = argv[9];
+    const std::string dir = argv[1], mode = argv[9], scheme_name = argc == 11 ? argv[10] : "ssp";
+    const TransportScheme scheme = scheme_name == "single" ? TransportScheme::SingleStage : TransportScheme::SspRk2;
     const int n = std::atoi(argv[2]), steps = std::atoi(argv[7]), nranks = std::atoi(argv[8]);
     const double L = std::atof(argv[3]), lam = std::atof(argv[4]), Tw = std::atof(argv[5]), dt = std::atof(argv[6]);
     try {
@@ -56,7 +59,7 @@ int main(int argc, char** argv) {
             boltz_halo* halo = nullptr;
             check(boltz_halo_create(0, 1, id, 0, &halo));
             {
-                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, halo);
+                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, halo, nullptr, scheme);
                 led0 = s.ledger();
                 for (int i = 0; i < steps; ++i) s.strang_step(dt);
                 led1 = s.ledger();
@@ -79,7 +82,7 @@ int main(int argc, char** argv) {
                 ops.push_back(std::make_unique<CollisionOperator>(n, L, k, CollisionOperator::Generated{}));
                 std::span<const double> f0r(f0.data() + plan[r].first * n3, plan[r].second * n3);
                 ranks.push_back(std::make_unique<Solver1D>(*ops.back(), n, L, x, dx, f0r, r, nranks, left, right, 1.0,
-                                                           nullptr, streams[r]));
+                                                           nullptr, streams[r], scheme));
                 ptrs.push_back(ranks.back().get());
             }
             {
@@ -95,7 +98,7 @@ int main(int argc, char** argv) {
             cudaStream_t st;
             cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
             {
-                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, nullptr, st);
+                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, nullptr, st, scheme);
                 led0 = s.ledger();
                 s.run(dt, steps);
                 led1 = s.ledger();
@@ -108,7 +111,8 @@ int main(int argc, char** argv) {
             std::vector<Solver1D*> ptrs;
             for (int r = 0; r < nranks; ++r) {
                 std::span<const double> f0r(f0.data() + plan[r].first * n3, plan[r].second * n3);
-                ranks.push_back(std::make_unique<Solver1D>(op, n, L, x, dx, f0r, r, nranks, left, right));
+                ranks.push_back(std::make_unique<Solver1D>(op, n, L, x, dx, f0r, r, nranks, left, right, 1.0, nullptr,
+                                                           nullptr, scheme));
                 ptrs.push_back(ranks.back().get());
             }
             for (auto* r : ptrs) {
@@ -122,7 +126,8 @@ int main(int argc, char** argv) {
                 ptrs[r]->download(std::span<double>(out.data() + plan[r].first * n3, plan[r].second * n3));
             }
         }
-        const std::string path = dir + "/out_" + mode + "_" + std::to_string(nranks) + ".bin";
+        const std::string path =
+            dir + "/out_" + mode + "_" + std::to_string(nranks) + (argc == 11 ? "_" + scheme_name : "") + ".bin";
         std::ofstream(path, std::ios::binary).write(reinterpret_cast<const char*>(out.data()), out.size() * 8);
         std::printf("ledger mass %.17g -> %.17g\n", led0[0], led1[0]);
         return 0;

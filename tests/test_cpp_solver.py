@@ -75,3 +75,35 @@ def test_cpp_solver_matches_python_driver(gpu, tmp_path):
         got = np.fromfile(tmp_path / f"out_{mode}_{nranks}.bin").reshape(nx, -1)
         assert np.array_equal(got, ref), (mode, np.abs(got - ref).max())
         assert "ledger mass" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_solver_single_stage_matches_python_driver(gpu, tmp_path):
+    """TransportScheme::SingleStage (SPEC.md:342-345) in the C++ driver equals
+    the Python driver's transport_scheme="single_stage" bit for bit, for the
+    loopback, graph-replay and fused peer-halo modes."""
+    import torch
+    from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, scenarios
+    from paper_1301_4195_b200.solver import Boundary, Solver1D
+    _compile()
+    n, L, lam, Tw, nx, steps = 8, 5.0, 1.0, 2.0, 10, 7
+    grid = VelocityGrid.create(n, L)
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    f0 = scenarios.mixture_cells(grid, nx, seed=19)
+    x.tofile(tmp_path / "x.bin")
+    dx.tofile(tmp_path / "dx.bin")
+    np.ascontiguousarray(f0).tofile(tmp_path / "f0.bin")
+    with CollisionOperator.generated(grid, KernelSpec(lam)) as op:
+        s = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw), right=Boundary("extrap"),
+                     transport_scheme="single_stage")
+        dt = 0.5 * s.cfl_dt()
+        for _ in range(steps):
+            s.strang_step(dt)
+        ref = s.interior.cpu().numpy()
+    torch.cuda.synchronize()
+    for mode, nranks in [("loopback", 3), ("graph", 1), ("peer", 3)]:
+        r = subprocess.run([str(EXE), str(tmp_path), str(n), repr(L), repr(lam), repr(Tw), repr(dt), str(steps),
+                            str(nranks), mode, "single"], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+        got = np.fromfile(tmp_path / f"out_{mode}_{nranks}_single.bin").reshape(nx, -1)
+        assert np.array_equal(got, ref), (mode, np.abs(got - ref).max())

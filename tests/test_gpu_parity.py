@@ -400,3 +400,132 @@ def test_mirror2_tmem_schedule(gpu, O, n, L, monkeypatch):
         assert rel_max(q2[c], ref) < TOL_Q
     assert rel_max(q2, q1) < 1e-12
     assert rel_max(q3, q2) < 1e-12
+
+
+def test_n32_mirror_schedule_vs_oracle_in_a_batch(gpu, O):
+    """The N=32 metric's kernel (k_conv_kcsm<32>, phased mirror schedule) with
+    the HOST table against the oracle on three cells of a 64-cell batch: the
+    first cell (group 0, lane 0), a cell at lane 1 of group 1 and the last
+    cell (group 1, lane 31)."""
+    n, L, cells = 32, 8.0, 64
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=4195)
+    G = table(n, L)
+    with _op(n, L) as op:
+        plain, mirror = op.schedule_terms()
+        assert 0 < mirror < 0.8 * plain
+        q = op.collide(f)
+        g = f[[0, 33, 63]].copy()
+        op.collision_rk2(g, 1e-3)
+    for i, c in enumerate((0, 33, 63)):
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q[c], ref) < TOL_Q, c
+        m = O.moments(n, L, q[c])
+        assert np.abs(m[:5]).max() < TOL_CONS * O.moments(n, L, f[c])[0]
+    ref = O.collision_rk2(n, L, G, f[[0]].copy(), 1e-3, 1.0, nthreads=8)
+    assert rel_max(g[0] - f[0], ref[0] - f[0]) < 1e-9
+
+
+def test_n24_maxwell_molecules_kcsm_vs_oracle(gpu, O):
+    """cfg4's second run: N=24, L=8, Maxwell molecules (lambda=0), through the
+    phased mirror kernel k_conv_kcsm<24> with the host table, against the
+    oracle on cells of a 40-cell batch (lanes 0 and 5 of group 0, lane 7 of
+    group 1)."""
+    n, L, lam = 24, 8.0, 0.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 40, seed=97)
+    G = table(n, L, lam)
+    with _op(n, L, lam) as op:
+        plain, mirror = op.schedule_terms()
+        assert 0 < mirror < plain
+        q = op.collide(f)
+    for c in (0, 5, 39):
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q[c], ref) < TOL_Q, c
+
+
+def test_host_pipeline_cfg2_size_matches_device_path(gpu):
+    """The e2e path bench.py times: N=16 x 4096 cells through the host pipeline
+    (mirror schedule chunking 1,3,3,1 over two compute streams and three
+    staging slots) is bitwise the device-memory call, for collide and RK2."""
+    import torch
+    n, L, cells = 16, 6.0, 4096
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=4195)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        fd = torch.from_numpy(f).to(gpu)
+        qd = op.collide(fd).cpu().numpy()
+        qh = op.collide(f)
+        assert np.array_equal(qh, qd)
+        pinned = torch.from_numpy(f.copy()).pin_memory()
+        op.collision_rk2(pinned.numpy(), 0.01)
+        g = f.copy()                                     # pageable host memory
+        op.collision_rk2(g, 0.01)
+        op.collision_rk2(fd, 0.01)
+        ref = fd.cpu().numpy()
+        assert np.array_equal(pinned.numpy(), ref)
+        assert np.array_equal(g, ref)
+
+
+def test_latency_schedule_host_pipeline_large_batch(gpu):
+    """the latency schedule through the two-workspace host pipeline
+    on 2048+ cells (odd chunks use the second workspace's segment scratch) is
+    bitwise the device path, and repeated calls stay so."""
+    import torch
+    n, L, cells = 16, 6.0, 2100
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=31)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        op.set_schedule("latency")
+        qd = op.collide(torch.from_numpy(f).to(gpu)).cpu().numpy()
+        for _ in range(2):
+            qh = op.collide(f)
+            assert np.array_equal(qh, qd)
+        op.set_schedule("throughput")
+        q_thr = op.collide(f)
+        assert rel_max(qh, q_thr) < 1e-12
+
+
+def test_argument_checks(gpu):
+    """dtype and device of every array are checked against the call."""
+    import torch
+    from paper_1301_4195_b200 import ConfigError
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 2, seed=3)
+    with _op(n, L) as op:
+        with pytest.raises(ConfigError):
+            op.collide(torch.from_numpy(f).to(gpu).to(torch.complex128))
+        with pytest.raises(ConfigError):
+            op.collide(f.astype(np.complex128))
+        with pytest.raises(ConfigError):
+            op.evaluate_qhat(torch.from_numpy(f).to(gpu))  # real where complex is expected
+        with pytest.raises(ConfigError):
+            op.collision_rk2(torch.from_numpy(f).to(gpu).float(), 0.01)
+
+
+def test_graph_capture_keeps_workspace_alive(gpu):
+    """once a call is captured in a CUDA graph, a later larger batch
+    must not free the workspace the graph uses; the replay stays correct."""
+    import torch
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = torch.from_numpy(scenarios.mixture_cells(grid, 32, seed=3)).to(gpu)
+    with _op(n, L) as op:
+        ref = op.collide(f).clone()
+        out = torch.empty_like(f)
+        op.set_async(True)
+        s = torch.cuda.Stream(gpu)
+        s.wait_stream(torch.cuda.current_stream(gpu))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                out.copy_(op.collide(f))
+        op.set_async(False)
+        torch.cuda.current_stream(gpu).wait_stream(s)
+        big = torch.from_numpy(scenarios.mixture_cells(grid, 2000, seed=5)).to(gpu)
+        op.collide(big)                                  # grows the workspace
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)

@@ -54,9 +54,10 @@ def test_fill_boundary_vs_oracle(gpu, O, side, kind):
     assert abs(s - sref) <= 1e-13 * max(1.0, abs(sref))
 
 
-def _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, steps):
+def _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, steps, single_stage=False):
     """Strang step composed from the oracle's primitives,
-    transport sub-step = SSP-RK2 of the FV step."""
+    transport sub-step = SSP-RK2 of the FV step, or the SPEC's
+    single stage with one ghost refresh."""
     nx = field.shape[0] - 4
 
     def fill(f):
@@ -65,6 +66,8 @@ def _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, steps):
 
     def T(f, h):
         fill(f)
+        if single_stage:
+            return O.transport_step(n, L, f, xe, dxe, h, 1, 0)
         t1 = O.transport_step(n, L, f, xe, dxe, h, 1, 0)
         fill(t1)
         t2 = O.transport_step(n, L, t1, xe, dxe, h, 1, 0)
@@ -98,6 +101,61 @@ def test_strang_wall_problem_vs_oracle(gpu, O):
     ref = _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, 4)[2:nx + 2]
     assert rel_max(got - f0, ref - f0) < 1e-9
     assert np.abs(got - f0).max() > 1e-6  # the wall did something
+
+
+def test_strang_single_stage_transport_vs_oracle(gpu, O):
+    """The SPEC-literal Strang step: each transport sub-step is ONE FV stage
+    after one ghost refresh, against the same composition
+    of oracle primitives; and it differs from the SSP-RK2 default."""
+    n, L, nx, Tw = 8, 5.0, 10, 2.0
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    xe, dxe = scenarios.extend_ghosts(x, dx)
+    grid = VelocityGrid.create(n, L)
+    f0 = scenarios.mixture_cells(grid, nx, seed=23)
+    G = table(n, L)
+    with _op(n, L) as op:
+        s = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw), right=Boundary("extrap"),
+                     transport_scheme="single_stage")
+        dt = 0.5 * s.cfl_dt()
+        for _ in range(4):
+            s.strang_step(dt)
+        got = s.interior.cpu().numpy()
+        s2 = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw), right=Boundary("extrap"))
+        for _ in range(4):
+            s2.strang_step(dt)
+        rk = s2.interior.cpu().numpy()
+        # the graph path rotates one buffer pair per sub-step: 3 captured steps close it
+        s3 = Solver1D(op, x, dx, f0, left=Boundary("wall", Tw), right=Boundary("extrap"),
+                      transport_scheme="single_stage")
+        s3.run(dt, 4, graph=True)
+        assert np.array_equal(s3.interior.cpu().numpy(), got)
+    field = np.zeros((nx + 4, n ** 3))
+    field[2:nx + 2] = f0
+    ref = _oracle_strang(O, n, L, G, field, xe, dxe, dt, Tw, 4, single_stage=True)[2:nx + 2]
+    assert rel_max(got - f0, ref - f0) < 1e-9
+    assert rel_max(rk - f0, ref - f0) > 1e-6  # a different scheme
+
+
+def test_single_stage_loopback_transparency(gpu):
+    """Decomposition transparency of the single-stage scheme."""
+    n, L, nx, Tw = 8, 5.0, 9, 2.0
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.05)
+    grid = VelocityGrid.create(n, L)
+    f0 = scenarios.mixture_cells(grid, nx, seed=29)
+    with _op(n, L) as op:
+        kw = dict(left=Boundary("wall", Tw), transport_scheme="single_stage")
+        single = [Solver1D(op, x, dx, f0, **kw)]
+        plan = plan_decomposition(nx, 3)
+        multi = [Solver1D(op, x, dx, f0, rank=r, world=3, plan=plan, halo=False, **kw) for r in range(3)]
+        for m in multi:
+            m.halo = None
+        dt = 0.5 * single[0].cfl_dt()
+        for _ in range(3):
+            strang_step_loopback(single, dt)
+            strang_step_loopback(multi, dt)
+        a = single[0].interior.cpu().numpy()
+        b = np.concatenate([m.interior.cpu().numpy() for m in multi])
+    assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("nranks", [2, 4])
