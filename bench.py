@@ -78,7 +78,10 @@ def host_cpu():
 
 def pin_openmp():
     """The reference's OpenMP run settings: one
-    thread per physical core, bound close.  Must run before libgomp loads."""
+    thread per physical core, bound close.  Only for processes that run nothing
+    but the CPU oracle: libgomp binds its initial thread when it loads, so
+    host_cpu() must be read before, and the GPU arm's own host threads must not
+    inherit the binding (the CPU legs run in a subprocess there)."""
     os.environ.setdefault("OMP_PROC_BIND", "close")
     os.environ.setdefault("OMP_PLACES", "cores")
     return f"OMP_PROC_BIND={os.environ['OMP_PROC_BIND']} OMP_PLACES={os.environ['OMP_PLACES']}"
@@ -113,6 +116,7 @@ def parse():
     p.add_argument("--no-cfg3", action="store_true", help="skip the cfg3 Strang-step sub-measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
     return p.parse_args()
 
 
@@ -166,13 +170,22 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU baseline
-def cpu_baseline(seconds, omp):
+def cpu_baseline_subprocess(seconds):
+    """cpu_baseline() in a fresh process pinned like the reference's OpenMP run."""
+    env = dict(os.environ, OMP_PROC_BIND="close", OMP_PLACES="cores")
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-baseline-only", "--cpu-seconds",
+                        str(seconds)], capture_output=True, text=True, env=env)
+    if r.returncode != 0:
+        return {"error": r.stderr[-400:]}
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(seconds, omp, hw):
     """Oracle port (C, OpenMP over zeta_k) on this host: evals/s at N=16,
     plus the reference's bench_collision tables at N=16/24/32."""
     from oracle import oracle as O
     from paper_1301_4195_b200 import VelocityGrid, scenarios
     O.build()
-    hw = host_cpu()
     threads = hw["physical_cores"]
     grid = VelocityGrid.create(N_VEL, L_VEL)
     G = O.generate_table(N_VEL, L_VEL, LAM, nthreads=threads)
@@ -225,7 +238,7 @@ def cpu_baseline(seconds, omp):
             **hw, "omp": omp, "tables_1_4": tables}
 
 
-def run_reference(args, rank, world, omp):
+def run_reference(args, rank, world, omp, hw):
     """The reference arm: the oracle port of the reference's OpenMP collision
     path on this box's host cores, on a bounded sample of the
     same cfg2 workload, printed under the same metric and config."""
@@ -234,7 +247,6 @@ def run_reference(args, rank, world, omp):
     from oracle import oracle as O
     from paper_1301_4195_b200 import VelocityGrid, scenarios
     O.build()
-    hw = host_cpu()
     threads = hw["physical_cores"]
     grid = VelocityGrid.create(N_VEL, L_VEL)
     G = O.generate_table(N_VEL, L_VEL, LAM, nthreads=threads)
@@ -269,12 +281,15 @@ def run_reference(args, rank, world, omp):
 # ------------------------------------------------------------------- ours
 def main():
     args = parse()
-    omp = pin_openmp()
+    hw = host_cpu()  # before libgomp can bind this thread
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.cpu_baseline_only:
+        print(json.dumps(cpu_baseline(args.cpu_seconds, pin_openmp(), hw)), flush=True)
+        return
     if args.impl == "reference":
-        return run_reference(args, rank, world, omp)
+        return run_reference(args, rank, world, pin_openmp(), hw)
     if world > 1:  # communicator init lines (ranks, transport) on stderr for the driver's check
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
@@ -400,7 +415,7 @@ def main():
     if rank == 0:
         from oracle import oracle as O
         O.build()
-        th = host_cpu()["physical_cores"]
+        th = hw["physical_cores"]
         r_dev = O.collision_rk2(N_VEL, L_VEL, G, snap["dev"], DT, 1.0, nthreads=th)
         r_e2e = O.collision_rk2(N_VEL, L_VEL, G, snap["e2e"], DT, 1.0, nthreads=th)
 
@@ -418,13 +433,13 @@ def main():
     if not args.no_n32 and rank == 0:
         op.close()
         del G
-        n32 = bench_n32(args, dev, local)
+        n32 = bench_n32(args, dev, local, hw)
         if parity is not None and n32.get("parity"):
             parity.update(n32.pop("parity"))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.cpu_seconds, omp)
+        cpu = cpu_baseline_subprocess(args.cpu_seconds)
 
     if rank == 0:
         line = {
@@ -579,7 +594,7 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
     return out
 
 
-def bench_n32(args, dev, local):
+def bench_n32(args, dev, local, hw):
     """cfg5-shaped N=32 sub-measurement: 2048 mixture cells, RK2 steps, with a
     parity witness of two cells of the last timed step against the oracle."""
     import torch
@@ -615,7 +630,7 @@ def bench_n32(args, dev, local):
     op.close()
     from oracle import oracle as O
     O.build()
-    ref = O.collision_rk2(n, L, G, snap, 1e-3, 1.0, nthreads=host_cpu()["physical_cores"])
+    ref = O.collision_rk2(n, L, G, snap, 1e-3, 1.0, nthreads=hw["physical_cores"])
     del G
     conv_avg = kms["conv"] / max(kl["conv"], 1)
     flop_total = FLOP_PER_TERM * terms_per_eval(n) * cells * 2 * steps

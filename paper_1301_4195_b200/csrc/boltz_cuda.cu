@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <omp.h>
 #include <string>
 #include <vector>
 
@@ -90,6 +91,13 @@ struct boltz_ctx {
     int stage_slots = 3;
     double* dStageIn[kMaxStageSlots] = {};
     double* dStageOut[kMaxStageSlots] = {};
+    // pinned host bounce ring for PAGEABLE caller memory (run_host_pipelined):
+    // the caller's chunk is memcpy'd by host threads into pinned memory while
+    // the GPU works on the previous chunk, so the DMA keeps its pinned speed
+    int64_t bounce_cap = 0;  // cells per slot
+    double* hBounceIn[kMaxStageSlots] = {};
+    double* hBounceOut[kMaxStageSlots] = {};
+    double* hBounceMi[kMaxStageSlots] = {};
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_h2d[kMaxStageSlots] = {}, ev_comp[kMaxStageSlots] = {}, ev_d2h[kMaxStageSlots] = {};
     // second compute stream + workspace: odd host-pipeline chunks run beside even
@@ -823,6 +831,55 @@ void swap_workspace(boltz_ctx* c) {
     std::swap(c->seg_cap, c->seg_cap2);
 }
 
+// pinned bounce slots for pageable host buffers (cells per slot, both directions)
+void ensure_bounce(boltz_ctx* c, int64_t cells) {
+    if (cells <= c->bounce_cap) return;
+    const int64_t n3 = n3_of(c);
+    for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
+        if (c->hBounceIn[b]) cudaFreeHost(c->hBounceIn[b]);
+        if (c->hBounceOut[b]) cudaFreeHost(c->hBounceOut[b]);
+        if (c->hBounceMi[b]) cudaFreeHost(c->hBounceMi[b]);
+        c->hBounceIn[b] = c->hBounceOut[b] = c->hBounceMi[b] = nullptr;
+    }
+    c->bounce_cap = 0;
+    for (int b = 0; b < c->stage_slots; ++b) {
+        CK(cudaMallocHost(&c->hBounceIn[b], (size_t)cells * n3 * 16));  // complex-sized, like the device staging
+        CK(cudaMallocHost(&c->hBounceOut[b], (size_t)cells * n3 * 16));
+        CK(cudaMallocHost(&c->hBounceMi[b], (size_t)cells * 8));
+    }
+    c->bounce_cap = cells;
+}
+
+// true when p is ordinary pageable host memory (not cudaHostAlloc'd / registered)
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+// host memcpy spread over a few threads (one thread reaches ~10 GB/s)
+void host_copy(void* dst, const void* src, size_t bytes) {
+    static const int threads = [] {
+        int t = std::min(8, omp_get_num_procs());
+        if (const char* e = std::getenv("BOLTZ_COPY_THREADS")) t = std::max(1, std::atoi(e));
+        return t;
+    }();
+    constexpr size_t kBlock = 1 << 20;
+    const int64_t nb = (int64_t)((bytes + kBlock - 1) / kBlock);
+    if (threads <= 1 || nb < 4) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t b = 0; b < nb; ++b) {
+        const size_t o = (size_t)b * kBlock;
+        std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kBlock, bytes - o));
+    }
+}
+
 void ensure_staging(boltz_ctx* c, int64_t cells) {
     if (cells <= c->stage_cap) return;
     const int64_t n3 = n3_of(c);
@@ -1281,6 +1338,11 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         chunk = c->cap;
     }
     ensure_staging(c, chunk);
+    // pageable caller memory goes through the pinned bounce ring (host threads
+    // copy; the DMA engines only ever see pinned memory)
+    bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));
+    if (const char* e = std::getenv("BOLTZ_BOUNCE")) bounce_in = bounce_out = bounce_in && std::atoi(e) != 0;
+    if (bounce_in || bounce_out) ensure_bounce(c, chunk);
     CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     const int64_t nchunks = (int64_t)bounds.size() - 1;
     // odd chunks compute on comp2 with the second workspace; comp2 joins s's
@@ -1297,9 +1359,32 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         const int slot = (int)(i % K);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
         if (i >= K) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-K done reading
-        CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice,
-                           c->h2d_stream));
+        if (!bounce_in) {
+            CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8,
+                               cudaMemcpyHostToDevice, c->h2d_stream));
+        } else {
+            // the slot's pinned buffer is free once chunk i-K's H2D completed; the
+            // host copy runs in blocks, each DMA'd as soon as it is in pinned memory
+            if (i >= K) CK(cudaEventSynchronize(c->ev_h2d[slot]));
+            const size_t bytes = (size_t)nc * in_elems * 8, blk = (size_t)8 << 20;
+            const char* src = reinterpret_cast<const char*>(in + c0 * in_elems);
+            char* pin = reinterpret_cast<char*>(c->hBounceIn[slot]);
+            char* dst = reinterpret_cast<char*>(c->dStageIn[slot]);
+            for (size_t o = 0; o < bytes; o += blk) {
+                const size_t b = std::min(blk, bytes - o);
+                host_copy(pin + o, src + o, b);
+                CK(cudaMemcpyAsync(dst + o, pin + o, b, cudaMemcpyHostToDevice, c->h2d_stream));
+            }
+        }
         CK(cudaEventRecord(c->ev_h2d[slot], c->h2d_stream));
+    };
+    // pageable output: chunk i's pinned result -> the caller's memory, on the host
+    auto drain = [&](int64_t i) {
+        const int slot = (int)(i % K);
+        const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
+        CK(cudaEventSynchronize(c->ev_d2h[slot]));
+        host_copy(out + c0 * out_elems, c->hBounceOut[slot], (size_t)nc * out_elems * 8);
+        if (max_imag) std::memcpy(max_imag + c0, c->hBounceMi[slot], (size_t)nc * 8);
     };
     h2d(0);
     for (int64_t i = 0; i < nchunks; ++i) {
@@ -1312,14 +1397,23 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         if (odd) swap_workspace(c);
         fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
         CK(cudaEventRecord(c->ev_comp[slot], cs));
-        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
+        if (max_imag)
+            CK(cudaMemcpyAsync(bounce_out ? c->hBounceMi[slot] : max_imag + c0, c->dMaxIm, (size_t)nc * 8,
+                               cudaMemcpyDeviceToHost, cs));
         if (odd) swap_workspace(c);
-        if (i + 1 < nchunks) h2d(i + 1);
+        if (bounce_out) {
+            // chunk i's D2H goes to the slot's pinned buffer, which must also wait
+            // for the max|Im| copy on the compute stream
+            CK(cudaEventRecord(c->ev_comp[slot], cs));
+        }
         CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
-        CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
-                           cudaMemcpyDeviceToHost, c->d2h_stream));
+        CK(cudaMemcpyAsync(bounce_out ? c->hBounceOut[slot] : out + c0 * out_elems, c->dStageOut[slot],
+                           (size_t)nc * out_elems * 8, cudaMemcpyDeviceToHost, c->d2h_stream));
         CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
+        if (i + 1 < nchunks) h2d(i + 1);
+        if (bounce_out && i >= 1) drain(i - 1);
     }
+    if (bounce_out) drain(nchunks - 1);
     if (two) {
         CK(cudaEventRecord(c->ev_join, c->comp2));
         CK(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -1489,6 +1583,11 @@ int boltz_destroy(boltz_ctx* c) {
     if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
     if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->hFlag) cudaFreeHost(c->hFlag);
+    for (int b = 0; b < boltz_ctx::kMaxStageSlots; ++b) {
+        if (c->hBounceIn[b]) cudaFreeHost(c->hBounceIn[b]);
+        if (c->hBounceOut[b]) cudaFreeHost(c->hBounceOut[b]);
+        if (c->hBounceMi[b]) cudaFreeHost(c->hBounceMi[b]);
+    }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
     return BOLTZ_OK;
