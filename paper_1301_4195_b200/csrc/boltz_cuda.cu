@@ -2,13 +2,16 @@
 // B200 collision path.  Host orchestration only; the kernels live in
 // transforms.cuh (K1/K3), conv.cuh (K2) and transport.cuh (K4).
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <omp.h>
 #include <string>
 #include <vector>
@@ -98,6 +101,8 @@ struct boltz_ctx {
     double* hBounceIn[kMaxStageSlots] = {};
     double* hBounceOut[kMaxStageSlots] = {};
     double* hBounceMi[kMaxStageSlots] = {};
+    static constexpr int kBounceBlocks = 16;  // D2H of a slot in up to 16 blocks, one event each
+    cudaEvent_t ev_blk[kMaxStageSlots][kBounceBlocks] = {};
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_h2d[kMaxStageSlots] = {}, ev_comp[kMaxStageSlots] = {}, ev_d2h[kMaxStageSlots] = {};
     // second compute stream + workspace: odd host-pipeline chunks run beside even
@@ -843,6 +848,8 @@ void ensure_bounce(boltz_ctx* c, int64_t cells) {
     }
     c->bounce_cap = 0;
     for (int b = 0; b < c->stage_slots; ++b) {
+        for (int j = 0; j < boltz_ctx::kBounceBlocks; ++j)
+            if (!c->ev_blk[b][j]) CK(cudaEventCreateWithFlags(&c->ev_blk[b][j], cudaEventDisableTiming));
         CK(cudaMallocHost(&c->hBounceIn[b], (size_t)cells * n3 * 16));  // complex-sized, like the device staging
         CK(cudaMallocHost(&c->hBounceOut[b], (size_t)cells * n3 * 16));
         CK(cudaMallocHost(&c->hBounceMi[b], (size_t)cells * 8));
@@ -860,23 +867,64 @@ bool is_pageable(const void* p) {
     return a.type == cudaMemoryTypeUnregistered;
 }
 
-// host memcpy spread over a few threads (one thread reaches ~10 GB/s)
+// block of the bounce pipeline: host copy of block j overlaps the DMA of j-1
+size_t bounce_block() {
+    static const size_t b = [] {
+        double mb = 4.0;
+        if (const char* e = std::getenv("BOLTZ_BOUNCE_BLK_MB")) mb = std::max(0.25, std::atof(e));
+        return (size_t)(mb * (1 << 20));
+    }();
+    return b;
+}
+
+// Streaming (non-temporal) copy: the destination lines are written without
+// being read first, so a copy costs 2 bytes of DRAM traffic per byte instead
+// of 3 -- the host copies of the bounce pipeline are DRAM-bound.
+__attribute__((target("avx512f"))) void copy_stream_avx512(char* dst, const char* src, size_t bytes) {
+    size_t head = (64 - (reinterpret_cast<uintptr_t>(dst) & 63)) & 63;
+    head = std::min(head, bytes);
+    std::memcpy(dst, src, head);
+    dst += head, src += head, bytes -= head;
+    const size_t n = bytes / 256;
+    for (size_t i = 0; i < n; ++i, dst += 256, src += 256) {
+        const __m512d a = _mm512_loadu_pd(src), b = _mm512_loadu_pd(src + 64);
+        const __m512d c = _mm512_loadu_pd(src + 128), d = _mm512_loadu_pd(src + 192);
+        _mm512_stream_pd(reinterpret_cast<double*>(dst), a);
+        _mm512_stream_pd(reinterpret_cast<double*>(dst + 64), b);
+        _mm512_stream_pd(reinterpret_cast<double*>(dst + 128), c);
+        _mm512_stream_pd(reinterpret_cast<double*>(dst + 192), d);
+    }
+    std::memcpy(dst, src, bytes % 256);
+    _mm_sfence();
+}
+
+void copy_block(void* dst, const void* src, size_t bytes) {
+    static const bool nt = __builtin_cpu_supports("avx512f") &&
+                           !(std::getenv("BOLTZ_COPY_NT") && std::atoi(std::getenv("BOLTZ_COPY_NT")) == 0);
+    if (nt) copy_stream_avx512(static_cast<char*>(dst), static_cast<const char*>(src), bytes);
+    else std::memcpy(dst, src, bytes);
+}
+
+// host copy spread over a few threads (one thread reaches ~15 GB/s; B200
+// box, cfg2 pageable e2e / pinned: 2 threads 0.81, 4 threads 0.90, 8 threads
+// 0.91, 12 threads 0.92, 16 threads 0.92 with streaming stores; 0.70 / 0.83 /
+// 0.81 at 2 / 4 / 8 threads with memcpy)
 void host_copy(void* dst, const void* src, size_t bytes) {
     static const int threads = [] {
-        int t = std::min(8, omp_get_num_procs());
+        int t = std::min(12, omp_get_num_procs());
         if (const char* e = std::getenv("BOLTZ_COPY_THREADS")) t = std::max(1, std::atoi(e));
         return t;
     }();
-    constexpr size_t kBlock = 1 << 20;
+    constexpr size_t kBlock = 1 << 19;
     const int64_t nb = (int64_t)((bytes + kBlock - 1) / kBlock);
-    if (threads <= 1 || nb < 4) {
-        std::memcpy(dst, src, bytes);
+    if (threads <= 1 || nb < 2) {
+        copy_block(dst, src, bytes);
         return;
     }
 #pragma omp parallel for num_threads(threads) schedule(static)
     for (int64_t b = 0; b < nb; ++b) {
         const size_t o = (size_t)b * kBlock;
-        std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kBlock, bytes - o));
+        copy_block(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kBlock, bytes - o));
     }
 }
 
@@ -1292,7 +1340,14 @@ int run_chunked(boltz_ctx* c, const double* in, double* out, int64_t ncells, int
 // streams -- H2D of chunk i+1 (copy engine), compute of chunk i (`s` for even,
 // `comp2` with the second workspace for odd chunks), D2H of chunk i-1 (the
 // other copy engine) -- through stage_slots staging buffer pairs, so with
-// pinned host memory the PCIe traffic hides behind the kernels.
+// pinned host memory the PCIe traffic hides behind the kernels.  Pageable
+// caller memory runs the same pipeline through pinned bounce buffers, with
+// the host copies on two worker threads (run_host_bounced).
+template <typename Fn>
+int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, int out_elems, cudaStream_t s,
+                     double* max_imag, Fn& fn, const std::vector<int64_t>& bounds, bool two, bool bounce_in,
+                     bool bounce_out);
+
 template <typename Fn>
 int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncells, int in_elems, int out_elems,
                        cudaStream_t s, double* max_imag, Fn&& fn) {
@@ -1304,10 +1359,12 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     // H2D and the last D2H cannot overlap compute, so the edge chunks are small;
     // odd chunks run on a second stream, so each chunk's last wave overlaps the
     // next chunk's work.  With the mirror schedule, whose work items are row
-    // pairs and which only pays from ~1.5k cells up, fewer larger chunks win:
-    // 1,3,3,1 (621k evals/s); the plain schedule prefers 2,6,8,8,6,2 (602k).
-    // BOLTZ_HOST_CHUNKS="a,b,..." overrides.
-    std::vector<double> w = c->mirror ? std::vector<double>{1, 3, 3, 1} : std::vector<double>{2, 6, 8, 8, 6, 2};
+    // pairs and which only pays from ~1.5k cells up, large middle chunks win:
+    // 1,2,4,4,2,1 (cfg2: 651k evals/s pinned against 627-641k for 1,3,3,1; the
+    // pageable bounce path also needs the small edge chunks); the plain
+    // schedule prefers 2,6,8,8,6,2 (602k).  BOLTZ_HOST_CHUNKS="a,b,..." overrides.
+    std::vector<double> w =
+        c->mirror ? std::vector<double>{1, 2, 4, 4, 2, 1} : std::vector<double>{2, 6, 8, 8, 6, 2};
     if (const char* sched = std::getenv("BOLTZ_HOST_CHUNKS")) {
         w.clear();
         for (const char* p = sched; *p;) {
@@ -1338,19 +1395,24 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         chunk = c->cap;
     }
     ensure_staging(c, chunk);
-    // pageable caller memory goes through the pinned bounce ring (host threads
-    // copy; the DMA engines only ever see pinned memory)
-    bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));
-    if (const char* e = std::getenv("BOLTZ_BOUNCE")) bounce_in = bounce_out = bounce_in && std::atoi(e) != 0;
-    if (bounce_in || bounce_out) ensure_bounce(c, chunk);
-    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     const int64_t nchunks = (int64_t)bounds.size() - 1;
     // odd chunks compute on comp2 with the second workspace; comp2 joins s's
     // prior work first and s waits for comp2 at the end (stream semantics kept)
     bool two = nchunks > 1;
     if (const char* e = std::getenv("BOLTZ_HOST_STREAMS")) two = two && std::atoi(e) > 1;  // tuning / A-B
+    if (two) ensure_workspace2(c);
+    // pageable caller memory goes through the pinned bounce ring (host threads
+    // copy; the DMA engines only ever see pinned memory)
+    bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));
+    if (const char* e = std::getenv("BOLTZ_BOUNCE"))
+        if (std::atoi(e) == 0) bounce_in = bounce_out = false;
+    if (bounce_in || bounce_out) {
+        ensure_bounce(c, chunk);
+        return run_host_bounced(c, in, out, in_elems, out_elems, s, max_imag, fn, bounds, two, bounce_in,
+                                bounce_out);
+    }
+    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
     if (two) {
-        ensure_workspace2(c);
         CK(cudaEventRecord(c->ev_fork, s));
         CK(cudaStreamWaitEvent(c->comp2, c->ev_fork, 0));
     }
@@ -1359,32 +1421,9 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         const int slot = (int)(i % K);
         const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
         if (i >= K) CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // chunk i-K done reading
-        if (!bounce_in) {
-            CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8,
-                               cudaMemcpyHostToDevice, c->h2d_stream));
-        } else {
-            // the slot's pinned buffer is free once chunk i-K's H2D completed; the
-            // host copy runs in blocks, each DMA'd as soon as it is in pinned memory
-            if (i >= K) CK(cudaEventSynchronize(c->ev_h2d[slot]));
-            const size_t bytes = (size_t)nc * in_elems * 8, blk = (size_t)8 << 20;
-            const char* src = reinterpret_cast<const char*>(in + c0 * in_elems);
-            char* pin = reinterpret_cast<char*>(c->hBounceIn[slot]);
-            char* dst = reinterpret_cast<char*>(c->dStageIn[slot]);
-            for (size_t o = 0; o < bytes; o += blk) {
-                const size_t b = std::min(blk, bytes - o);
-                host_copy(pin + o, src + o, b);
-                CK(cudaMemcpyAsync(dst + o, pin + o, b, cudaMemcpyHostToDevice, c->h2d_stream));
-            }
-        }
+        CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, (size_t)nc * in_elems * 8, cudaMemcpyHostToDevice,
+                           c->h2d_stream));
         CK(cudaEventRecord(c->ev_h2d[slot], c->h2d_stream));
-    };
-    // pageable output: chunk i's pinned result -> the caller's memory, on the host
-    auto drain = [&](int64_t i) {
-        const int slot = (int)(i % K);
-        const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
-        CK(cudaEventSynchronize(c->ev_d2h[slot]));
-        host_copy(out + c0 * out_elems, c->hBounceOut[slot], (size_t)nc * out_elems * 8);
-        if (max_imag) std::memcpy(max_imag + c0, c->hBounceMi[slot], (size_t)nc * 8);
     };
     h2d(0);
     for (int64_t i = 0; i < nchunks; ++i) {
@@ -1397,23 +1436,189 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         if (odd) swap_workspace(c);
         fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
         CK(cudaEventRecord(c->ev_comp[slot], cs));
-        if (max_imag)
-            CK(cudaMemcpyAsync(bounce_out ? c->hBounceMi[slot] : max_imag + c0, c->dMaxIm, (size_t)nc * 8,
-                               cudaMemcpyDeviceToHost, cs));
+        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
         if (odd) swap_workspace(c);
-        if (bounce_out) {
-            // chunk i's D2H goes to the slot's pinned buffer, which must also wait
-            // for the max|Im| copy on the compute stream
-            CK(cudaEventRecord(c->ev_comp[slot], cs));
-        }
-        CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
-        CK(cudaMemcpyAsync(bounce_out ? c->hBounceOut[slot] : out + c0 * out_elems, c->dStageOut[slot],
-                           (size_t)nc * out_elems * 8, cudaMemcpyDeviceToHost, c->d2h_stream));
-        CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
         if (i + 1 < nchunks) h2d(i + 1);
-        if (bounce_out && i >= 1) drain(i - 1);
+        CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
+        CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
+                           cudaMemcpyDeviceToHost, c->d2h_stream));
+        CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
     }
-    if (bounce_out) drain(nchunks - 1);
+    if (two) {
+        CK(cudaEventRecord(c->ev_join, c->comp2));
+        CK(cudaStreamWaitEvent(s, c->ev_join, 0));
+    }
+    CK(cudaStreamSynchronize(c->d2h_stream));
+    return check_flag(c, s);
+}
+
+// Progress counters shared by the bounce pipeline's three host threads.
+struct PipeSync {
+    std::mutex m;
+    std::condition_variable cv;
+    int64_t h2d = 0;      // chunks whose H2D is enqueued (ev_h2d recorded)
+    int64_t comp = 0;     // chunks whose compute is enqueued (ev_comp recorded)
+    int64_t d2h = 0;      // chunks whose D2H is enqueued (ev_d2h recorded)
+    int64_t drained = 0;  // chunks copied out to the caller's memory
+    bool abort = false;
+    std::string err;
+    void wait(int64_t PipeSync::*ctr, int64_t v) {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return this->*ctr >= v || abort; });
+        if (abort) throw CudaError{err.empty() ? std::string("host pipeline aborted") : err};
+    }
+    void bump(int64_t PipeSync::*ctr) {
+        {
+            std::lock_guard<std::mutex> g(m);
+            ++(this->*ctr);
+        }
+        cv.notify_all();
+    }
+    void fail(const std::string& e) {
+        {
+            std::lock_guard<std::mutex> g(m);
+            if (!abort) err = e;
+            abort = true;
+        }
+        cv.notify_all();
+    }
+};
+
+// The pinned-bounce variant of run_host_pipelined for pageable caller memory.
+// Three host threads run the three pipeline legs concurrently, ordered by the
+// PipeSync counters and CUDA events:
+//   feeder  (chunk i): [pageable in -> pinned slot, in blocks] -> H2D, ev_h2d
+//   main    (chunk i): wait ev_h2d; compute on s / comp2; ev_comp
+//   drainer (chunk i): wait ev_comp; D2H into the pinned slot in blocks (one
+//                      event each); block j -> caller memory while j+1 is in flight
+// A direction whose caller memory is pinned skips its bounce copy.
+template <typename Fn>
+int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, int out_elems, cudaStream_t s,
+                     double* max_imag, Fn& fn, const std::vector<int64_t>& bounds, bool two, bool bounce_in,
+                     bool bounce_out) {
+    const int64_t nchunks = (int64_t)bounds.size() - 1;
+    const int K = c->stage_slots;
+    const size_t blk_in = bounce_block();
+    auto out_blk = [&](int64_t i) {
+        const size_t bytes = (size_t)(bounds[i + 1] - bounds[i]) * out_elems * 8;
+        return std::max(bounce_block(), (bytes + boltz_ctx::kBounceBlocks - 1) / boltz_ctx::kBounceBlocks);
+    };
+    CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
+    if (two) {
+        CK(cudaEventRecord(c->ev_fork, s));
+        CK(cudaStreamWaitEvent(c->comp2, c->ev_fork, 0));
+    }
+    // the copy streams must not run ahead of the caller's prior work on `s`
+    CK(cudaEventRecord(c->ev_join, s));
+    CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_join, 0));
+    PipeSync ps;
+    auto feeder = [&] {
+        try {
+            CK(cudaSetDevice(c->device));
+            for (int64_t i = 0; i < nchunks; ++i) {
+                const int slot = (int)(i % K);
+                const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
+                if (i >= K) {
+                    ps.wait(&PipeSync::comp, i - K + 1);  // chunk i-K's ev_comp is recorded
+                    CK(cudaStreamWaitEvent(c->h2d_stream, c->ev_comp[slot], 0));  // ... device slot free
+                }
+                const size_t bytes = (size_t)nc * in_elems * 8;
+                if (!bounce_in) {
+                    CK(cudaMemcpyAsync(c->dStageIn[slot], in + c0 * in_elems, bytes, cudaMemcpyHostToDevice,
+                                       c->h2d_stream));
+                } else {
+                    if (i >= K) CK(cudaEventSynchronize(c->ev_h2d[slot]));  // pinned slot's last DMA done
+                    const char* src = reinterpret_cast<const char*>(in + c0 * in_elems);
+                    char* pin = reinterpret_cast<char*>(c->hBounceIn[slot]);
+                    char* dst = reinterpret_cast<char*>(c->dStageIn[slot]);
+                    for (size_t o = 0; o < bytes; o += blk_in) {
+                        const size_t b = std::min(blk_in, bytes - o);
+                        host_copy(pin + o, src + o, b);
+                        CK(cudaMemcpyAsync(dst + o, pin + o, b, cudaMemcpyHostToDevice, c->h2d_stream));
+                    }
+                }
+                CK(cudaEventRecord(c->ev_h2d[slot], c->h2d_stream));
+                ps.bump(&PipeSync::h2d);
+            }
+        } catch (const CudaError& e) {
+            ps.fail(e.msg);
+        }
+    };
+    auto drainer = [&] {
+        try {
+            CK(cudaSetDevice(c->device));
+            for (int64_t i = 0; i < nchunks; ++i) {
+                const int slot = (int)(i % K);
+                const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
+                ps.wait(&PipeSync::comp, i + 1);
+                CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
+                const size_t bytes = (size_t)nc * out_elems * 8, blk = out_blk(i);
+                if (!bounce_out) {
+                    CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], bytes, cudaMemcpyDeviceToHost,
+                                       c->d2h_stream));
+                    CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
+                    ps.bump(&PipeSync::d2h);
+                    ps.bump(&PipeSync::drained);
+                    continue;
+                }
+                char* pin = reinterpret_cast<char*>(c->hBounceOut[slot]);
+                const char* src = reinterpret_cast<const char*>(c->dStageOut[slot]);
+                int j = 0;
+                for (size_t o = 0; o < bytes; o += blk, ++j) {
+                    CK(cudaMemcpyAsync(pin + o, src + o, std::min(blk, bytes - o), cudaMemcpyDeviceToHost,
+                                       c->d2h_stream));
+                    CK(cudaEventRecord(c->ev_blk[slot][j], c->d2h_stream));
+                }
+                CK(cudaEventRecord(c->ev_d2h[slot], c->d2h_stream));
+                ps.bump(&PipeSync::d2h);
+                char* dst = reinterpret_cast<char*>(out + c0 * out_elems);
+                j = 0;
+                for (size_t o = 0; o < bytes; o += blk, ++j) {
+                    CK(cudaEventSynchronize(c->ev_blk[slot][j]));
+                    host_copy(dst + o, pin + o, std::min(blk, bytes - o));
+                }
+                if (max_imag) {
+                    CK(cudaEventSynchronize(c->ev_comp[slot]));  // the max|Im| copy precedes it on the stream
+                    std::memcpy(max_imag + c0, c->hBounceMi[slot], (size_t)nc * 8);
+                }
+                ps.bump(&PipeSync::drained);
+            }
+        } catch (const CudaError& e) {
+            ps.fail(e.msg);
+        }
+    };
+    std::thread tf(feeder), td(drainer);
+    std::string err;
+    try {
+        for (int64_t i = 0; i < nchunks; ++i) {
+            const int slot = (int)(i % K);
+            const bool odd = (i & 1) && two;
+            const int64_t c0 = bounds[i], nc = bounds[i + 1] - bounds[i];
+            cudaStream_t cs = odd ? c->comp2 : s;
+            ps.wait(&PipeSync::h2d, i + 1);
+            CK(cudaStreamWaitEvent(cs, c->ev_h2d[slot], 0));
+            if (i >= K) {
+                ps.wait(&PipeSync::d2h, i - K + 1);  // chunk i-K's output left the device slot
+                CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));
+                if (bounce_out && max_imag) ps.wait(&PipeSync::drained, i - K + 1);  // pinned max|Im| slot read
+            }
+            if (odd) swap_workspace(c);
+            fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
+            if (max_imag)
+                CK(cudaMemcpyAsync(bounce_out ? c->hBounceMi[slot] : max_imag + c0, c->dMaxIm, (size_t)nc * 8,
+                                   cudaMemcpyDeviceToHost, cs));
+            CK(cudaEventRecord(c->ev_comp[slot], cs));
+            if (odd) swap_workspace(c);
+            ps.bump(&PipeSync::comp);
+        }
+    } catch (const CudaError& e) {
+        err = e.msg;
+        ps.fail(e.msg);
+    }
+    tf.join();
+    td.join();
+    if (err.empty() && ps.abort) err = ps.err;
+    if (!err.empty()) throw CudaError{err};
     if (two) {
         CK(cudaEventRecord(c->ev_join, c->comp2));
         CK(cudaStreamWaitEvent(s, c->ev_join, 0));
@@ -1587,6 +1792,8 @@ int boltz_destroy(boltz_ctx* c) {
         if (c->hBounceIn[b]) cudaFreeHost(c->hBounceIn[b]);
         if (c->hBounceOut[b]) cudaFreeHost(c->hBounceOut[b]);
         if (c->hBounceMi[b]) cudaFreeHost(c->hBounceMi[b]);
+        for (cudaEvent_t e : c->ev_blk[b])
+            if (e) cudaEventDestroy(e);
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     delete c;
