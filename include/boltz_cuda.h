@@ -84,6 +84,12 @@ int boltz_create_generated(int n, double L, double lambda, double beta, double r
                            boltz_ctx** out);
 
 /* Device bytes held by the context (folded table + workspace). */
+/* A transforms-only context (no weight table): forward / inverse / conserve /
+ * moments / marginal / transport work, collision calls return
+ * BOLTZ_ERR_CONFIG.  Backs the reference-typed boltz::SpectralTransform
+ * (fourier.hpp:28-52) of paper_1301_4195_b200/shim/fourier_cuda.cpp. */
+int boltz_create_transform(int n, double L, int device, boltz_ctx** out);
+
 int boltz_memory_bytes(const boltz_ctx* ctx, int64_t* table_bytes, int64_t* workspace_bytes);
 
 /* forward: f (ncells x N^3 real) -> fhat (ncells x N^3 complex) */

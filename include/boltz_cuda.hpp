@@ -19,8 +19,32 @@
 
 #include "boltz_cuda.h"
 
+// Errors.  Built inside the reference tree (its include directory on the
+// path, so <boltz/errors.hpp> resolves), failures are the reference's own
+// exceptions: boltz::ConfigError / IoError / NumericError (errors.hpp:9-35), and
+// CUDA / NCCL failures a boltz::Error of category 5; boltz::cuda::Error is then
+// boltz::Error itself, so a reference strang_step that catches
+// boltz::NumericError catches ours.  Standalone, boltz::cuda::Error
+// is a std::runtime_error with the same integer categories.
+#if !defined(BOLTZ_CUDA_STANDALONE_ERRORS) && __has_include(<boltz/errors.hpp>)
+#include <boltz/errors.hpp>
+#define BOLTZ_CUDA_REFERENCE_ERRORS 1
+#endif
+
 namespace boltz::cuda {
 
+#if BOLTZ_CUDA_REFERENCE_ERRORS
+using Error = boltz::Error;
+
+[[noreturn]] inline void throw_error(int category, const std::string& what) {
+    switch (category) {
+        case BOLTZ_ERR_CONFIG: throw boltz::ConfigError(what);
+        case BOLTZ_ERR_IO: throw boltz::IoError(what);
+        case BOLTZ_ERR_NUMERIC: throw boltz::NumericError(what);
+        default: throw boltz::Error(static_cast<boltz::ErrorCategory>(category), "CUDA: " + what);
+    }
+}
+#else
 // Category 2/3/4 as in boltz::ErrorCategory (errors.hpp:8-13); 5 = CUDA/NCCL.
 class Error : public std::runtime_error {
 public:
@@ -31,8 +55,14 @@ private:
     int category_;
 };
 
+[[noreturn]] inline void throw_error(int category, const std::string& what) { throw Error(category, what); }
+#endif
+
+// the integer category of either error type (2/3/4 reference, 5 CUDA/NCCL)
+inline int category_of(const Error& e) { return static_cast<int>(e.category()); }
+
 inline void check(int rc) {
-    if (rc != BOLTZ_OK) throw Error(rc, boltz_last_error());
+    if (rc != BOLTZ_OK) throw_error(rc, boltz_last_error());
 }
 
 struct Kernel {
@@ -52,7 +82,7 @@ class CollisionOperator {
 public:
     CollisionOperator(int n, double L, const Kernel& k, std::span<const double> table, int device = 0) : n_(n) {
         if (table.size() != static_cast<size_t>(n) * n * n * n * n * n)
-            throw Error(BOLTZ_ERR_CONFIG, "weight table size is not N^6");
+            throw_error(BOLTZ_ERR_CONFIG, "weight table size is not N^6");
         check(boltz_create(n, L, k.lambda, k.beta, k.r0 > 0 ? k.r0 : L, table.data(), device, &ctx_));
     }
     // the weights generated on the device (no N^6 host table)
@@ -85,12 +115,12 @@ public:
         check(boltz_conserve_batch(ctx_, q_raw.data(), q.data(), cells(q_raw.size()), BOLTZ_MEM_HOST, nullptr));
     }
     void collide(std::span<const double> f, std::span<double> q, double epsilon, double* max_imag = nullptr) {
-        if (!(epsilon > 0)) throw Error(BOLTZ_ERR_CONFIG, "collide: epsilon must be positive");
+        if (!(epsilon > 0)) throw_error(BOLTZ_ERR_CONFIG, "collide: epsilon must be positive");
         check(boltz_collide_batch(ctx_, f.data(), q.data(), cells(f.size()), 1.0 / epsilon, max_imag, BOLTZ_MEM_HOST,
                                   nullptr));
     }
     void collision_rk2(std::span<double> field, double dt, double epsilon) {
-        if (!(dt > 0 && epsilon > 0)) throw Error(BOLTZ_ERR_CONFIG, "collision_rk2: dt, epsilon must be positive");
+        if (!(dt > 0 && epsilon > 0)) throw_error(BOLTZ_ERR_CONFIG, "collision_rk2: dt, epsilon must be positive");
         check(boltz_rk2_batch(ctx_, field.data(), cells(field.size()), dt, 1.0 / epsilon, BOLTZ_MEM_HOST, nullptr));
     }
     // device-pointer variants (ordered on `stream`)
@@ -113,7 +143,7 @@ public:
 
 private:
     int64_t cells(size_t values) const {
-        if (values % cell_size()) throw Error(BOLTZ_ERR_CONFIG, "array is not a whole number of cells");
+        if (values % cell_size()) throw_error(BOLTZ_ERR_CONFIG, "array is not a whole number of cells");
         return static_cast<int64_t>(values / cell_size());
     }
     int n_;

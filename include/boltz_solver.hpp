@@ -31,13 +31,13 @@
 namespace boltz::cuda {
 
 inline void cuda_check(cudaError_t e) {
-    if (e != cudaSuccess) throw Error(BOLTZ_ERR_CUDA, cudaGetErrorString(e));
+    if (e != cudaSuccess) throw_error(BOLTZ_ERR_CUDA, cudaGetErrorString(e));
 }
 
 // plan_decomposition: (start, count) per rank, contiguous,
 // |count_r - count_s| <= 1, larger ranges first.
 inline std::vector<std::pair<int64_t, int64_t>> plan_decomposition(int64_t ncells, int nranks) {
-    if (nranks < 1 || ncells < nranks) throw Error(BOLTZ_ERR_CONFIG, "plan_decomposition: more ranks than cells");
+    if (nranks < 1 || ncells < nranks) throw_error(BOLTZ_ERR_CONFIG, "plan_decomposition: more ranks than cells");
     std::vector<std::pair<int64_t, int64_t>> out;
     const int64_t base = ncells / nranks, rem = ncells % nranks;
     int64_t s = 0;
@@ -54,7 +54,7 @@ inline std::vector<std::pair<int64_t, int64_t>> plan_decomposition(int64_t ncell
 inline void extend_ghosts(std::span<const double> x, std::span<const double> dx, std::vector<double>& xe,
                           std::vector<double>& dxe) {
     const size_t n = x.size();
-    if (n < 2 || dx.size() != n) throw Error(BOLTZ_ERR_CONFIG, "extend_ghosts: need >= 2 cells");
+    if (n < 2 || dx.size() != n) throw_error(BOLTZ_ERR_CONFIG, "extend_ghosts: need >= 2 cells");
     dxe.assign(n + 4, 0.0);
     dxe[0] = dx[1];
     dxe[1] = dx[0];
@@ -130,8 +130,8 @@ public:
         const auto plan = plan_decomposition((int64_t)x.size(), world);
         start_ = plan[rank].first;
         ncl_ = plan[rank].second;
-        if (ncl_ < 2) throw Error(BOLTZ_ERR_CONFIG, "each rank needs at least 2 cells (2-cell halo, SPEC.md:438)");
-        if ((int64_t)f0.size() != ncl_ * n3_) throw Error(BOLTZ_ERR_CONFIG, "f0 must hold this rank's ncl x N^3 values");
+        if (ncl_ < 2) throw_error(BOLTZ_ERR_CONFIG, "each rank needs at least 2 cells (2-cell halo, SPEC.md:438)");
+        if ((int64_t)f0.size() != ncl_ * n3_) throw_error(BOLTZ_ERR_CONFIG, "f0 must hold this rank's ncl x N^3 values");
         std::vector<double> xe, dxe;
         extend_ghosts(x, dx, xe, dxe);
         dx_min_ = dx[0];
@@ -185,7 +185,7 @@ public:
     // edge cells go straight into the neighbours' stage outputs (left_dst /
     // right_dst); this rank's ghosts were written by its neighbours' previous op
     void transport_stage_peer(int stage, double h, double* left_dst, double* right_dst) {
-        if (h * L_ > dx_min_ * (1 + 1e-12)) throw Error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
+        if (h * L_ > dx_min_ * (1 + 1e-12)) throw_error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
         const int wl = rank_ == 0 && left_.is_wall(), wr = rank_ == world_ - 1 && right_.is_wall();
         double* in = stage_in(stage);
         fill_physical(in);
@@ -236,7 +236,7 @@ public:
     double* stage_input(int stage) { return stage == 0 ? field_.data() : tmp_.data(); }
 
     void transport(double h) {
-        if (h * L_ > dx_min_ * (1 + 1e-12)) throw Error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
+        if (h * L_ > dx_min_ * (1 + 1e-12)) throw_error(BOLTZ_ERR_CONFIG, "transport: CFL violated (dt * L > min dx)");
         for (int stage = 0; stage < transport_stages(); ++stage) transport_stage(stage, h);
     }
 
@@ -280,7 +280,7 @@ public:
 
     // interior cells -> host (ncl x N^3)
     void download(std::span<double> out) {
-        if ((int64_t)out.size() != ncl_ * n3_) throw Error(BOLTZ_ERR_CONFIG, "download: size must be ncl x N^3");
+        if ((int64_t)out.size() != ncl_ * n3_) throw_error(BOLTZ_ERR_CONFIG, "download: size must be ncl x N^3");
         cuda_check(cudaMemcpyAsync(out.data(), interior(), out.size() * sizeof(double), cudaMemcpyDeviceToHost, s_));
         cuda_check(cudaStreamSynchronize(s_));
     }
@@ -306,7 +306,7 @@ public:
     // non-default stream and one eager step first (see run()).  The NCCL halo
     // is captured too when world > 1.  Does not advance the state.
     void capture(double dt) {
-        if (!s_) throw Error(BOLTZ_ERR_CONFIG, "capture: the solver needs a non-default stream");
+        if (!s_) throw_error(BOLTZ_ERR_CONFIG, "capture: the solver needs a non-default stream");
         const double* p0[3] = {field_.data(), tmp_.data(), tmp2_.data()};
         check(boltz_set_async(op_.handle(), 1));
         cudaGraph_t g = nullptr;
@@ -327,7 +327,7 @@ public:
         check(boltz_set_async(op_.handle(), 0));
         if (field_.data() != p0[0] || tmp_.data() != p0[1] || tmp2_.data() != p0[2]) {
             cudaGraphDestroy(g);
-            throw Error(BOLTZ_ERR_CONFIG, "capture: buffer rotation did not close after 3 steps");
+            throw_error(BOLTZ_ERR_CONFIG, "capture: buffer rotation did not close after 3 steps");
         }
         if (exec_) cudaGraphExecDestroy(exec_);
         exec_ = nullptr;
@@ -340,7 +340,7 @@ public:
     // `steps` Strang steps of the captured dt: graph replays + eager remainder;
     // numeric errors are reported once, at the end (boltz_sync)
     void advance(int steps) {
-        if (!exec_) throw Error(BOLTZ_ERR_CONFIG, "advance: capture() first");
+        if (!exec_) throw_error(BOLTZ_ERR_CONFIG, "advance: capture() first");
         check(boltz_set_async(op_.handle(), 1));
         try {
             for (int i = 0; i < steps / 3; ++i) {
@@ -396,10 +396,10 @@ private:
 class PeerGroup {
 public:
     explicit PeerGroup(std::vector<Solver1D*> ranks) : r_(std::move(ranks)) {
-        if (r_.empty()) throw Error(BOLTZ_ERR_CONFIG, "PeerGroup: no ranks");
+        if (r_.empty()) throw_error(BOLTZ_ERR_CONFIG, "PeerGroup: no ranks");
         ev_.resize(2 * r_.size());
         for (size_t i = 0; i < r_.size(); ++i) {
-            if (!r_[i]->stream()) throw Error(BOLTZ_ERR_CONFIG, "PeerGroup: every rank needs its own stream");
+            if (!r_[i]->stream()) throw_error(BOLTZ_ERR_CONFIG, "PeerGroup: every rank needs its own stream");
             cuda_check(cudaSetDevice(r_[i]->device()));
             for (int p = 0; p < 2; ++p) cuda_check(cudaEventCreateWithFlags(&ev_[2 * i + p], cudaEventDisableTiming));
             for (int d : {-1, 1}) {  // peer access to the neighbours' devices

@@ -56,5 +56,35 @@ def build(verbose: bool = False, force: bool = False, out: pathlib.Path = LIB, d
     return LIB
 
 
+REF_INCLUDE = pathlib.Path("/root/reference/proj/include")
+REF_GRID_SRC = pathlib.Path("/root/reference/proj/src/velocity_grid.cpp")
+SHIM_DEMO = PKG.parent / "tests" / "cpp" / "ref_shim_demo"
+
+
+def build_shim(force: bool = False):
+    """Compile the reference-typed drop-in (shim/fourier_cuda.cpp implementing
+    the reference's unmodified boltz::SpectralTransform, shim/collision_cuda.cpp)
+    together with the reference's own velocity_grid.cpp, compiled in place,
+    into tests/cpp/ref_shim_demo.  Needs the reference tree (this container);
+    the GPU box runs the prebuilt binary.  Returns the binary or None."""
+    if not (REF_INCLUDE.is_dir() and REF_GRID_SRC.is_file()):
+        return SHIM_DEMO if SHIM_DEMO.exists() else None
+    lib = build()
+    srcs = [PKG.parent / "tests" / "cpp" / "ref_shim_demo.cpp", PKG / "shim" / "fourier_cuda.cpp",
+            PKG / "shim" / "collision_cuda.cpp", REF_GRID_SRC]
+    deps = srcs + [lib, PKG.parent / "include" / "boltz_cuda.hpp", PKG / "shim" / "collision_cuda.hpp"]
+    if not force and SHIM_DEMO.exists() and all(p.stat().st_mtime <= SHIM_DEMO.stat().st_mtime for p in deps):
+        return SHIM_DEMO
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(REF_INCLUDE), "-I", str(PKG.parent / "include"),
+           "-I", str(PKG / "shim"), "-o", str(SHIM_DEMO), *map(str, srcs), str(lib),
+           f"-Wl,-rpath,{lib.parent}"]
+    print("[build]", " ".join(cmd), file=sys.stderr, flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("g++ failed building tests/cpp/ref_shim_demo")
+    return SHIM_DEMO
+
+
 if __name__ == "__main__":
     build(verbose="--verbose" in sys.argv, force=True)

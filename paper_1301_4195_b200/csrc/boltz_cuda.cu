@@ -1663,7 +1663,14 @@ int api(boltz_ctx* c, Body&& body) {
 
 namespace {
 int create_context(int n, double L, double lambda, double beta, double r0, int panels, const double* G_host,
-                   int device, boltz_ctx** out);
+                   int device, boltz_ctx** out, bool with_table = true);
+
+// the collision entry points need the weight table (boltz_create_transform has none)
+int need_table(const boltz_ctx* c) {
+    if (c->dH) return BOLTZ_OK;
+    set_error("this context has no weight table (boltz_create_transform): transforms only");
+    return BOLTZ_ERR_CONFIG;
+}
 }
 
 extern "C" {
@@ -1726,11 +1733,28 @@ int boltz_create_generated(int n, double L, double lambda, double beta, double r
     return create_context(n, L, lambda, beta, r0, panels, nullptr, device, out);
 }
 
+int boltz_create_transform(int n, double L, int device, boltz_ctx** out) {
+    if (!out) {
+        set_error("boltz_create_transform: out is null");
+        return BOLTZ_ERR_CONFIG;
+    }
+    *out = nullptr;
+    if (n < 4 || n % 2 != 0 || !(L > 0.0)) {
+        set_error("velocity grid: N must be even and >= 4 and L > 0");
+        return BOLTZ_ERR_CONFIG;
+    }
+    if (!supported_n(n)) {
+        set_error("boltz_create_transform: N=" + std::to_string(n) + " has no compiled kernel");
+        return BOLTZ_ERR_CONFIG;
+    }
+    return create_context(n, L, 1.0, 1.0, L, 64, nullptr, device, out, false);
+}
+
 }  // extern "C"
 
 namespace {
 int create_context(int n, double L, double lambda, double beta, double r0, int panels, const double* G_host,
-                   int device, boltz_ctx** out) {
+                   int device, boltz_ctx** out, bool with_table) {
     boltz_ctx* c = new boltz_ctx();
     c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device; c->panels = panels;
     if (const char* e = std::getenv("BOLTZ_STAGE_SLOTS"))  // tuning
@@ -1752,7 +1776,7 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
         CK(cudaMallocHost(&c->hFlag, sizeof(int)));
         fill_twiddles();
         build_projection(c);
-        build_table(c, G_host);
+        if (with_table) build_table(c, G_host);
     } catch (const CudaError& e) {
         set_error(e.msg);
         boltz_destroy(c);
@@ -1839,6 +1863,7 @@ int boltz_inverse_batch(boltz_ctx* c, const double* g, double* f, double* max_im
 
 int boltz_qhat_batch(boltz_ctx* c, const double* fhat, double* qhat, int64_t ncells, int mem, void* stream) {
     return api(c, [&] {
+        if (int rc = need_table(c)) return rc;
         const int64_t n3 = n3_of(c);
         return run_chunked(c, fhat, qhat, ncells, (int)(2 * n3), (int)(2 * n3), mem, stream, nullptr,
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
@@ -1869,6 +1894,7 @@ int boltz_conserve_batch(boltz_ctx* c, const double* q_raw, double* q, int64_t n
 int boltz_collide_batch(boltz_ctx* c, const double* f, double* q, int64_t ncells, double inv_eps, double* max_imag,
                         int mem, void* stream) {
     return api(c, [&] {
+        if (int rc = need_table(c)) return rc;
         const int64_t n3 = n3_of(c);
         return run_chunked(c, f, q, ncells, (int)n3, (int)n3, mem, stream, max_imag,
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {
@@ -1884,6 +1910,7 @@ int boltz_collide_batch(boltz_ctx* c, const double* f, double* q, int64_t ncells
 
 int boltz_rk2_batch(boltz_ctx* c, double* f, int64_t ncells, double dt, double inv_eps, int mem, void* stream) {
     return api(c, [&] {
+        if (int rc = need_table(c)) return rc;
         const int64_t n3 = n3_of(c);
         return run_chunked(c, f, f, ncells, (int)n3, (int)n3, mem, stream, nullptr,
                            [&](const double* in, double* out, int64_t nc, cudaStream_t s) {

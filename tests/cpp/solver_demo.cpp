@@ -27,7 +27,7 @@ using namespace boltz::cuda;
 
 static std::vector<double> read_bin(const std::string& path) {
     std::ifstream f(path, std::ios::binary | std::ios::ate);
-    if (!f) throw Error(BOLTZ_ERR_IO, "cannot read " + path);
+    if (!f) throw_error(BOLTZ_ERR_IO, "cannot read " + path);
     const std::streamsize n = f.tellg();
     std::vector<double> v(n / sizeof(double));
     f.seekg(0);
@@ -132,7 +132,7 @@ int main(int argc, char** argv) {
         std::printf("ledger mass %.17g -> %.17g\n", led0[0], led1[0]);
         return 0;
     } catch (const Error& e) {
-        std::fprintf(stderr, "error category %d: %s\n", e.category(), e.what());
-        return e.category();
+        std::fprintf(stderr, "error category %d: %s\n", category_of(e), e.what());
+        return category_of(e);
     }
 }

@@ -38,11 +38,11 @@ int main() {
             std::vector<double> bad(m + 1);
             op.collide(bad, bad, 1.0);
         } catch (const boltz::cuda::Error& e) {
-            std::printf("config error category %d\n", e.category());
+            std::printf("config error category %d\n", boltz::cuda::category_of(e));
         }
         return 0;
     } catch (const boltz::cuda::Error& e) {
-        std::printf("error category %d: %s\n", e.category(), e.what());
-        return e.category();
+        std::printf("error category %d: %s\n", boltz::cuda::category_of(e), e.what());
+        return boltz::cuda::category_of(e);
     }
 }
