@@ -317,13 +317,15 @@ void layout_terms_plain(int n, TableLayout& T, int& slab) {
 }
 
 void layout_terms_mirror(int n, TableLayout& T) {
-    // slab of one typed band in band_tile order (band_diag(n, 1, 0, 0, i) == i), padded to even
+    // slab of one typed band in band_tile order (band_diag(n, 1, 0, 0, i) == i;
+    // kMirrorKS kk passes, pass-major), padded to even
     auto typed = [&](int ty) {
         std::vector<short2> v(band_slab_type(n, ty), make_short2(-1, -1));
         int pos = 0;
-        for (int m3 = 0; m3 < n; ++m3)
-            for (int kk = 0; kk < n; ++kk)
-                if (band_term_t(n, n, 0, 0, m3, kk, ty)) v[pos++] = make_short2((short)kk, (short)m3);
+        for (int q = 0; q < kMirrorKS; ++q)
+            for (int m3 = 0; m3 < n; ++m3)
+                for (int kk = q * n / kMirrorKS; kk < (q + 1) * n / kMirrorKS; ++kk)
+                    if (band_term_t(n, n, 0, 0, m3, kk, ty)) v[pos++] = make_short2((short)kk, (short)m3);
         return v;
     };
     const auto a = typed(BT_A), rest = typed(BT_REST);

@@ -34,6 +34,8 @@
 
 namespace boltz_gpu {
 
+#include <type_traits>
+
 // ---------------------------------------------------------------------------
 // Band enumeration shared by the kernels (compile time) and the host table
 // builder (run time).  Tile (kc, sc): k3 in [kc*T, kc*T+T), s3 in [sc*T, sc*T+T),
@@ -150,25 +152,81 @@ __host__ __device__ constexpr int conv_kernel_for(int n) {
 }
 constexpr int kConvWarps = BOLTZ_CONV_WARPS;  // cell groups per CTA (share the row stream / H via L1)
 
+// Term arithmetic.  acc += h * x * y for complex x = a + ib (per diagonal),
+// y = c + id (per term), real h.  Default: 2 DMUL + 4 DFMA.  Gauss form
+// (BOLTZ_TERM_GAUSS): the y window holds (c, c + d, d - c) and the diagonal
+// a + b, so that with t = c (a + b)
+//   Re = t - b (c + d) = ac - bd,   Im = t + a (d - c) = ad + bc
+// costs 1 DMUL + 2 DFMA, and the accumulation 2 DFMA: 5 FP64 instructions
+// per term instead of 6 (the sums are paid once per y value and diagonal).
+#ifndef BOLTZ_TERM_GAUSS
+#define BOLTZ_TERM_GAUSS 0  // every kernel; the per-kernel defaults below win otherwise
+#endif
+struct YG {
+    double c, s, t;  // c, c + d, d - c of y = c + i d
+};
+__device__ __forceinline__ YG to_yg(double2 v) { return YG{v.x, v.x + v.y, v.y - v.x}; }
+#if BOLTZ_TERM_GAUSS
+using YElem = YG;
+__device__ __forceinline__ YG to_y(double2 v) { return to_yg(v); }
+#else
+using YElem = double2;
+__device__ __forceinline__ double2 to_y(double2 v) { return v; }
+#endif
+// k_conv_mirror: kk passes of its bands (BOLTZ_MIRROR_KS) and its term form
+#ifndef BOLTZ_MIRROR_KS
+#define BOLTZ_MIRROR_KS 1
+#endif
+// B200, cfg2 RK2 step, k_conv_mirror<16> K2 ms: 11.0 (6-instruction term) | 12.0 Gauss,
+// KS = 2 | 12.4 Gauss, KS = 4 | 11.3 KS = 2: kept at the 6-instruction term, KS = 1
+#ifndef BOLTZ_MIRROR_GAUSS
+#define BOLTZ_MIRROR_GAUSS BOLTZ_TERM_GAUSS
+#endif
+constexpr int kMirrorKS = BOLTZ_MIRROR_KS;
+
+// does diagonal m3 carry a term of tile (kc, sc), type ty, in kk pass q of ks?
+__host__ __device__ constexpr bool diag_used_q(int n, int t, int kc, int sc, int m3, int ty, int ks, int q) {
+    bool any = false;
+    for (int kk = q * t / ks; kk < (q + 1) * t / ks; ++kk) any = any || band_term_t(n, t, kc, sc, m3, kk, ty);
+    return any;
+}
+
 // one tile of terms: acc[kk] += H * x[m3] * y[j]; the x source and the
-// per-diagonal hook (x refill) are policies
-template <int N, int T, int NK, int KC, int TI, int TY = BT_FULL, typename XAt, typename AfterDiag>
-__device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[T], XAt x_at, const double2* hs,
+// per-diagonal hook (x refill) are policies.  KS > 1 walks the band in KS
+// passes over kk ranges (pass, diagonal, kk order -- the table builder lays
+// the slab out the same way), so only T / KS accumulators are live at a time
+// while x is read KS times per diagonal.
+template <int N, int T, int NK, int KC, int TI, int TY = BT_FULL, int KS = 1, typename YT, typename XAt,
+          typename AfterDiag>
+__device__ __forceinline__ void band_tile(double2 (&acc)[T], const YT (&y)[T], XAt x_at, const double2* hs,
                                           int& p, double2& hb, AfterDiag after) {
     constexpr int SC = band_tile_sc(NK, KC, TI);
+    constexpr bool GAUSS = std::is_same<YT, YG>::value;
+#pragma unroll
+    for (int q = 0; q < KS; ++q)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
         const int m3 = band_diag(N, NK, KC, TI, i);
-        if (!diag_used_t(N, T, KC, SC, m3, TY)) continue;
+        if (!diag_used_q(N, T, KC, SC, m3, TY, KS, q)) continue;
         const double2 xm = x_at(m3);
+        double xab = 0.0;
+        if constexpr (GAUSS) xab = xm.x + xm.y;
 #pragma unroll
-        for (int kk = 0; kk < T; ++kk) {
+        for (int kk = q * T / KS; kk < (q + 1) * T / KS; ++kk) {
             if (!band_term_t(N, T, KC, SC, m3, kk, TY)) continue;
             const int j = KC * T + kk - m3 + N / 2 - SC * T;  // y chunk slot
             double h;
             if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
             else h = hb.y;
             ++p;
+            if constexpr (GAUSS) {
+                const double t = y[j].c * xab;
+                const double tr = fma(-xm.y, y[j].s, t);
+                const double ti = fma(xm.x, y[j].t, t);
+                acc[kk].x = fma(h, tr, acc[kk].x);
+                acc[kk].y = fma(h, ti, acc[kk].y);
+                continue;
+            } else {
 #if BOLTZ_TERM_HX
             // b = h*x (independent of y and acc), then acc += b*y: 2 DMUL + 4 DFMA
             const double bx = h * xm.x, by = h * xm.y;
@@ -182,6 +240,7 @@ __device__ __forceinline__ void band_tile(double2 (&acc)[T], const double2 (&y)[
             acc[kk].x = fma(h, tr, acc[kk].x);
             acc[kk].y = fma(h, ti, acc[kk].y);
 #endif
+            }
         }
         after(i, m3);
     }
@@ -232,13 +291,13 @@ __device__ __forceinline__ void conv_rows(const double2* __restrict__ Ag, const 
         double2 hb = make_double2(0.0, 0.0);
         auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
         auto none = [](int, int) {};
-        double2 y[T];
+        YElem y[T];
 #pragma unroll
-        for (int j = 0; j < T; ++j) y[j] = ldg2(Y + (size_t)(band_tile_sc(NK, KC, 0) * T + j) * kLanes);
+        for (int j = 0; j < T; ++j) y[j] = to_y(ldg2(Y + (size_t)(band_tile_sc(NK, KC, 0) * T + j) * kLanes));
         band_tile<N, T, NK, KC, 0>(acc, y, xat, Hs, p, hb, none);
         if constexpr (NK == 2) {
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ldg2(Y + (size_t)(band_tile_sc(NK, KC, 1) * T + j) * kLanes);
+            for (int j = 0; j < T; ++j) y[j] = to_y(ldg2(Y + (size_t)(band_tile_sc(NK, KC, 1) * T + j) * kLanes));
             band_tile<N, T, NK, KC, 1>(acc, y, xat, Hs, p, hb, none);
         }
     }
@@ -378,9 +437,9 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
             double2 hb = make_double2(0.0, 0.0);
             auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
             auto none = [](int, int) {};
-            double2 y[T];
+            YElem y[T];
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
             if constexpr (NK == 1) {
                 __syncwarp();  // every lane holds its y chunk: the buffer may be refilled
                 if (more) tma_y(cur ^ 1, nx);
@@ -388,7 +447,7 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
             } else {
                 band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
 #pragma unroll
-                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane]);
                 __syncwarp();
                 if (more) tma_y(cur ^ 1, nx);
                 band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
@@ -420,9 +479,9 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
             double2 hb = make_double2(0.0, 0.0);
             auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
             auto none = [](int, int) {};
-            double2 y[T];
+            YElem y[T];
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
             if constexpr (NK == 1) {
                 if (more) issue_y(nx);  // own-lane slots, just read
                 cp_async_commit();
@@ -430,7 +489,7 @@ k_conv_kcs(const double2* __restrict__ A, double2* __restrict__ B, const double*
             } else {
                 band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
 #pragma unroll
-                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane]);
                 if (more) issue_y(nx);
                 cp_async_commit();
                 band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
@@ -495,9 +554,9 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
         int2 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en_next;
         issue(0, en_next, e0);
         mbar_wait(bar, 0);
-        double2 y[T];
+        YElem y[T];
 #pragma unroll
-        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+        for (int j = 0; j < T; ++j) y[j] = to_y(ys[j * kLanes + lane]);
         for (int e = e0; e < e1; ++e) {
             const int i = e - e0, cur = i & 1;
             const bool more = e + 1 < e1;
@@ -515,7 +574,7 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
             if (more) {
                 mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
 #pragma unroll
-                for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+                for (int j = 0; j < T; ++j) y[j] = to_y(ys[j * kLanes + lane]);
             }
         }
         return;
@@ -546,9 +605,9 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
     issue_y(en_next);
     cp_async_wait_all();
     __syncwarp();
-    double2 y[T];
+    YElem y[T];
 #pragma unroll
-    for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+    for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
     for (int e = e0; e < e1; ++e) {
         const int cur = (e - e0) & 1;
         const bool more = e + 1 < e1;
@@ -566,7 +625,7 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
         band_tile<N, T, NK, KC, 0>(acc, y, xat, hs, p, hb, none);
         if constexpr (NK == 2) {
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+            for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane]);
             if (more) issue_y(en_next);
             band_tile<N, T, NK, KC, 1>(acc, y, xat, hs, p, hb, none);
         }
@@ -574,7 +633,7 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
             cp_async_wait_all();
             __syncwarp();
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            for (int j = 0; j < T; ++j) y[j] = to_y(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
         }
     }
 }
@@ -748,9 +807,14 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
         int4 en_ahead = e_begin + 1 < e_end ? __ldg(ent + e_begin + 1) : en;
         issue(0, en);
         mbar_wait(bar, 0);
-        double2 y[T];
+        using YM = std::conditional_t<BOLTZ_MIRROR_GAUSS != 0, YG, double2>;
+        auto to_ym = [](double2 v) {
+            if constexpr (BOLTZ_MIRROR_GAUSS != 0) return to_yg(v);
+            else return v;
+        };
+        YM y[T];
 #pragma unroll
-        for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+        for (int j = 0; j < T; ++j) y[j] = to_ym(ys[j * kLanes + lane]);
         for (int e = e_begin; e < e_end; ++e) {
             const int i = e - e_begin, cur = i & 1;
             const bool more = e + 1 < e_end;
@@ -766,17 +830,17 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
             double2 hb = make_double2(0.0, 0.0);
             if (en.w != BT_REST) {  // warp-uniform: A, or the A half of a FULL entry
                 int p = 0;
-                band_tile<N, T, 1, 0, 0, BT_A>(acc, y, xat, hs, p, hb, none);
+                band_tile<N, T, 1, 0, 0, BT_A, kMirrorKS>(acc, y, xat, hs, p, hb, none);
             }
             if (en.w != BT_A) {  // REST, or the REST half of a FULL entry
                 int p = 0;
-                band_tile<N, T, 1, 0, 0, BT_REST>(acc, y, xat, hs + (en.w == BT_FULL ? mirror_slab(N, BT_A) / 2 : 0),
+                band_tile<N, T, 1, 0, 0, BT_REST, kMirrorKS>(acc, y, xat, hs + (en.w == BT_FULL ? mirror_slab(N, BT_A) / 2 : 0),
                                                   p, hb, none);
             }
             if (more) {
                 mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
 #pragma unroll
-                for (int j = 0; j < T; ++j) y[j] = ys[j * kLanes + lane];
+                for (int j = 0; j < T; ++j) y[j] = to_ym(ys[j * kLanes + lane]);
             }
             en = nx;
         }
@@ -1166,8 +1230,26 @@ __host__ __device__ constexpr bool kcsm_split(int n) {
 
 // one tile of a k_conv_kcsm entry on the y window in registers (x per
 // diagonal from L2)
-template <int N, int KC, int TI, int PHASE>
-__device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const double2 (&y)[conv_tile(N)],
+// Gauss term form per k_conv_kcsm kernel, by measurement on B200 (ncu launch
+// list, 2048 cells): <32,0,0> 29.3 -> 27.4 ms, <32,0,2> 27.7 -> 24.9 ms,
+// <32,0,1> 25.2 -> 25.5; the KC = 1 kernels and N = 24 spill registers with it
+// (84-896 B of stack) and run slower, so they keep the 6-instruction term.
+#ifndef BOLTZ_KCSM_GAUSS
+#define BOLTZ_KCSM_GAUSS 1
+#endif
+__host__ __device__ constexpr bool kcsm_gauss(int n, int kc, int phase) {
+    return BOLTZ_TERM_GAUSS || (BOLTZ_KCSM_GAUSS && n == 32 && kc == 0 && (phase == 0 || phase == 2));
+}
+template <int N, int KC, int PHASE>
+using KcsmY = std::conditional_t<kcsm_gauss(N, KC, PHASE), YG, double2>;
+template <typename YT>
+__device__ __forceinline__ YT to_yt(double2 v) {
+    if constexpr (std::is_same<YT, YG>::value) return to_yg(v);
+    else return v;
+}
+
+template <int N, int KC, int TI, int PHASE, typename YT>
+__device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const YT (&y)[conv_tile(N)],
                                           const double2* X, const double2* hs, int ty) {
     constexpr int T = conv_tile(N), NK = N / T;
     auto xat = [&](int m3) { return ldg2(X + (size_t)m3 * kLanes); };
@@ -1253,9 +1335,9 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             if (more) tma_h(cur ^ 1, nx);
             const double2* X = Ag + (size_t)en.x * kLanes;
             const double2* hs = reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES);
-            double2 y[T];
+            KcsmY<N, KC, PHASE> y[T];
 #pragma unroll
-            for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane];
+            for (int j = 0; j < T; ++j) y[j] = to_yt<KcsmY<N, KC, PHASE>>(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
             if constexpr (NK == 1) {
                 __syncwarp();  // every lane holds its y window: the buffer may be refilled
                 if (more) tma_y(cur ^ 1, nx);
@@ -1263,7 +1345,7 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             } else {
                 kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, en.w);
 #pragma unroll
-                for (int j = 0; j < T; ++j) y[j] = ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane];
+                for (int j = 0; j < T; ++j) y[j] = to_yt<KcsmY<N, KC, PHASE>>(ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane]);
                 __syncwarp();
                 if (more) tma_y(cur ^ 1, nx);
                 kcsm_tile<N, KC, (NK > 1 ? 1 : 0), PHASE>(acc, y, X, hs, en.w);
