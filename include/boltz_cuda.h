@@ -204,13 +204,15 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * K2 schedule (no reference counterpart): 0 = throughput (default; one warp per
  * output row, or per mirror row pair, and 32-cell group), s = 1..4 = latency
  * (each row's entry list in 4s fixed segments on 4s warps + an ordered
- * reduction; small batches, N <= 16; other N keep the throughput schedule).
+ * reduction; small batches, N <= 16; other N keep the throughput schedule),
+ * 5 = cell (lane = output k3, one CTA per (output row, cell), the cell's
+ * f-hat in shared memory: one or a few cells, N <= 16; conv.cuh k_conv_cell).
  * Under the throughput schedule collide / RK2 at N >= 8 use the Hermitian
  * mirror schedule (conv.cuh k_conv_mirror at N <= 16, the phased k_conv_kcsm
  * at N = 24, 32; env BOLTZ_MIRROR=0 disables it, BOLTZ_MIRROR=2 selects the
  * TMEM-accumulator variant k_conv_mirror2 at N = 8..16).
  * Results are bitwise reproducible and independent of batch composition
- * within a schedule; the two schedules differ by round-off.
+ * within a schedule; schedules differ by round-off.
  */
 int boltz_set_schedule(boltz_ctx* ctx, int schedule);
 /*

@@ -364,9 +364,10 @@ class CollisionOperator:
     def set_schedule(self, schedule="throughput"):
         """K2 schedule: "throughput" (default), "latency" (each row's entries in 4
         fixed segments on 4 warps: small batches, N <= 16), "latency8" (8
-        segments: a few cells), or the ABI's integer 0..4.  Bitwise
-        reproducible within a schedule; schedules differ by round-off."""
-        code = {"throughput": 0, "latency": 1, "latency8": 2}.get(schedule, schedule)
+        segments: a few cells), "cell" (lane = output k3: one or a few cells,
+        N <= 16), or the ABI's integer 0..5.  Bitwise reproducible within a
+        schedule; schedules differ by round-off."""
+        code = {"throughput": 0, "latency": 1, "latency8": 2, "cell": 5}.get(schedule, schedule)
         _check(lib().boltz_set_schedule(self._h, int(code)))
 
     # -- asynchronous mode (CUDA-graph capturable device calls)

@@ -62,6 +62,8 @@ using namespace boltz_gpu;
 // kernel classes for timing / launch counting
 enum Kind : int { KIND_CONV = 0, KIND_FFT = 1, KIND_PROJECT = 2, KIND_LAYOUT = 3, KIND_TRANSPORT = 4, kKinds = 5 };
 
+constexpr int kScheduleCell = 5;  // boltz_set_schedule: lane = output k3 (conv.cuh k_conv_cell), N <= 16
+
 struct boltz_ctx {
     int n = 0;
     double L = 0, lambda = 0, beta = 0, r0 = 0;
@@ -123,11 +125,15 @@ struct boltz_ctx {
     // per-kernel-class CUDA-event timing (bench.py roofline) and launch counts
     bool timing = false;
     bool async_mode = false;  // device-pointer calls return without a sync (boltz_set_async)
-    int schedule = 0;         // K2: 0 throughput, 1 latency (segmented rows, boltz_set_schedule)
+    int schedule = 0;         // K2: 0 throughput, 1..4 latency (segmented rows), 5 cell (boltz_set_schedule)
     double2* dSeg = nullptr;  // latency schedule's segment partials
     int64_t seg_cap = 0;      // cells
     double2* dSeg2 = nullptr; // ... of the second workspace set (swap_workspace)
     int64_t seg_cap2 = 0;
+    double2* dCell = nullptr; // cell schedule: contiguous f-hat cubes (k_cell_gather)
+    int64_t cell_cap = 0;
+    double2* dCell2 = nullptr;  // ... of the second workspace set
+    int64_t cell_cap2 = 0;
     // once a call was captured into a CUDA graph, the graph holds the workspace
     // pointers: growing a buffer then retires the old one (freed at destroy)
     // instead of freeing it, so a later replay never touches freed memory
@@ -811,6 +817,16 @@ void ensure_seg(boltz_ctx* c, int64_t cells) {
     c->seg_cap = cells;
 }
 
+// the cell schedule's contiguous f-hat cubes (cells) of the current workspace set
+void ensure_cell(boltz_ctx* c, int64_t cells) {
+    if (cells <= c->cell_cap) return;
+    release(c, c->dCell);
+    c->dCell = nullptr;
+    c->cell_cap = 0;
+    CK(cudaMalloc(&c->dCell, (size_t)cells * n3_of(c) * 16));
+    c->cell_cap = cells;
+}
+
 // the second workspace set (same capacity as the first)
 void ensure_workspace2(boltz_ctx* c) {
     if (c->cap2 == c->cap) return;
@@ -819,6 +835,9 @@ void ensure_workspace2(boltz_ctx* c) {
     c->dA2 = c->dB2 = nullptr; c->dFs2 = nullptr; c->dMaxIm2 = nullptr; c->cap2 = 0;
     c->dSeg2 = nullptr;
     c->seg_cap2 = 0;
+    release(c, c->dCell2);
+    c->dCell2 = nullptr;
+    c->cell_cap2 = 0;
     const int64_t n3 = n3_of(c);
     CK(cudaMalloc(&c->dA2, (size_t)c->cap * n3 * 16));
     CK(cudaMalloc(&c->dB2, (size_t)c->cap * n3 * 16));
@@ -836,6 +855,8 @@ void swap_workspace(boltz_ctx* c) {
     std::swap(c->dMaxIm, c->dMaxIm2);
     std::swap(c->dSeg, c->dSeg2);
     std::swap(c->seg_cap, c->seg_cap2);
+    std::swap(c->dCell, c->dCell2);
+    std::swap(c->cell_cap, c->cell_cap2);
 }
 
 // pinned bounce slots for pageable host buffers (cells per slot, both directions)
@@ -985,6 +1006,24 @@ struct Launch {
     // mirror schedule may run; evaluate_qhat of a caller's fhat never does
     static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s, bool hermitian = false) {
         const int64_t ng = (nc + 31) / 32;
+        if constexpr (conv_tile(N) == N && N <= 16) {
+            if (c->schedule == kScheduleCell) {  // one or a few cells: lane = output k3 (conv.cuh k_conv_cell)
+                using CL = CellLayout<N>;
+                static PerDevice configured;  // attributes are per device
+                configured.once(c->device, [&] {
+                    CK(cudaFuncSetAttribute(k_conv_cell<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, CL::BYTES));
+                });
+                ensure_cell(c, nc);
+                Timed t_(c, KIND_CONV, s);
+                const long long tot = nc * (long long)N3;
+                k_cell_gather<N><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(c->dA, c->dCell, (int)nc);
+                k_conv_cell<N><<<dim3(N * N, (unsigned)nc), kLanes * kCellWarps, CL::BYTES, s>>>(
+                    c->dCell, c->dB, c->dH, c->dEnt, c->dRowStart, c->slab);
+                c->launches[KIND_CONV]++;  // two kernels under one timing bracket
+                CK(cudaGetLastError());
+                return;
+            }
+        }
         if constexpr (mirror_kcs_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
@@ -1799,7 +1838,7 @@ int boltz_destroy(boltz_ctx* c) {
     cudaFree(c->dA); cudaFree(c->dB); cudaFree(c->dFs);
     cudaFree(c->dMaxIm); cudaFree(c->dFlag);
     cudaFree(c->dA2); cudaFree(c->dB2); cudaFree(c->dFs2); cudaFree(c->dMaxIm2);
-    cudaFree(c->dSeg); cudaFree(c->dSeg2);
+    cudaFree(c->dSeg); cudaFree(c->dSeg2); cudaFree(c->dCell); cudaFree(c->dCell2);
     for (void* p : c->retired) cudaFree(p);
     if (c->comp2) cudaStreamDestroy(c->comp2);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -2082,8 +2121,8 @@ int boltz_schedule_terms(boltz_ctx* c, int64_t* plain, int64_t* mirror) {
 }
 
 int boltz_set_schedule(boltz_ctx* c, int schedule) {
-    if (!c || schedule < 0 || schedule > 4) {
-        set_error("set_schedule: 0 (throughput) or 1..4 (latency: 4 x schedule segments per row)");
+    if (!c || schedule < 0 || schedule > kScheduleCell) {
+        set_error("set_schedule: 0 (throughput), 1..4 (latency: 4 x schedule segments per row) or 5 (cell)");
         return BOLTZ_ERR_CONFIG;
     }
     c->schedule = schedule;

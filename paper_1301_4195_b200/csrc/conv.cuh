@@ -725,6 +725,138 @@ k_conv_seg_reduce(const double2* __restrict__ P, double2* __restrict__ B, long l
 }
 
 // ---------------------------------------------------------------------------
+// Cell schedule (boltz_set_schedule(ctx, 5)) for one or a few cells, N <= 16:
+// lane = output k3 instead of lane = cell, so a single cell (cfg1) keeps every
+// lane busy.  A CTA owns one (output row, cell); the cell's f-hat cube is
+// staged in shared memory; warp w's lane slot q (32 / N slots of N lanes)
+// walks entries e0 + (w * P + q) + j * (8 * P) of the row's plain-table list
+// and, per diagonal m3, adds the term (k3 = lane, m3) when it is in the band:
+//   h = H[e][doff(m3) + k3 - klo(m3)]  (consecutive lanes, consecutive h),
+//   x = fhat(row m, m3) (smem broadcast), y = fhat(row s, k3 - m3 + N/2).
+// The slot partials are then added in a fixed (warp, slot) order, so results
+// are bitwise reproducible and independent of the batch; they differ from the
+// other schedules by round-off (another summation order).
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int cell_klo(int n, int m3) { return m3 - n / 2 > 0 ? m3 - n / 2 : 0; }
+__host__ __device__ constexpr int cell_khi(int n, int m3) { return m3 + n / 2 < n ? m3 + n / 2 : n; }
+// slab offset of diagonal m3 in a single-tile plain slab (layout_terms_plain order)
+__host__ __device__ constexpr int cell_doff(int n, int m3) {
+    int o = 0;
+    for (int i = 0; i < m3; ++i) o += cell_khi(n, i) - cell_klo(n, i);
+    return o;
+}
+#ifndef BOLTZ_CELL_WARPS
+#define BOLTZ_CELL_WARPS 16
+#endif
+constexpr int kCellWarps = BOLTZ_CELL_WARPS;
+template <int N>
+struct CellLayout {
+    static constexpr int P = kLanes / N;  // entry slots per warp
+    static constexpr int N3 = N * N * N;
+    static constexpr int CUBE_BYTES = N3 * 16;
+    static constexpr int RED_BYTES = kCellWarps * P * N * 16;
+    static constexpr int BYTES = CUBE_BYTES + RED_BYTES;
+};
+
+// the cells' f-hat cubes, group layout -> contiguous [cell][N^3] (k_conv_cell's input)
+template <int N>
+__global__ void __launch_bounds__(256) k_cell_gather(const double2* __restrict__ A, double2* __restrict__ C, int ncells) {
+    constexpr int N3 = N * N * N;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)ncells * N3) return;
+    const int cell = (int)(i / N3), idx = (int)(i % N3);
+    C[i] = ldg2(A + ((size_t)(cell / kLanes) * N3 + idx) * kLanes + cell % kLanes);
+}
+
+#ifndef BOLTZ_CELL_MINB
+#define BOLTZ_CELL_MINB 1
+#endif
+template <int N>
+__global__ void __launch_bounds__(kLanes* kCellWarps, BOLTZ_CELL_MINB)
+k_conv_cell(const double2* __restrict__ Cc, double2* __restrict__ B, const double* __restrict__ H,
+            const int2* __restrict__ ent, const int* __restrict__ row_start, int slab) {
+    using CL = CellLayout<N>;
+    constexpr int P = CL::P, N3 = CL::N3, S = kCellWarps * P;
+    static_assert(conv_tile(N) == N, "cell schedule: single-tile rows");
+    extern __shared__ __align__(16) char smem[];
+    double2* cube = reinterpret_cast<double2*>(smem);
+    double2* red = reinterpret_cast<double2*>(smem + CL::CUBE_BYTES);
+    const int row = blockIdx.x, cell = blockIdx.y;
+    const int g = cell / kLanes, cl = cell % kLanes;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int q = lane / N, k3 = lane % N;
+    const int e0 = __ldg(row_start + row), e1 = __ldg(row_start + row + 1);
+    // this slot's first two entries, loaded before the cube arrives
+    const int ea = e0 + w * P + q, eb = ea + S;
+    const int2 ena = (q < P && ea < e1) ? __ldg(ent + ea) : make_int2(0, 0);
+    const int2 enb = (q < P && eb < e1) ? __ldg(ent + eb) : make_int2(0, 0);
+    const double2* Cg = Cc + (size_t)cell * N3;
+    for (int i = threadIdx.x; i < N3; i += kLanes * kCellWarps) cube[i] = ldg2(Cg + i);
+    __syncthreads();
+    double2 acc = make_double2(0.0, 0.0);
+    // h of one entry for this lane: every diagonal's load issued up front
+    // (unconditional, clamped into the slab; out-of-band terms are skipped)
+    auto load_h = [&](int e, double (&hv)[N]) {
+        const double* hs = H + (size_t)e * slab;
+#pragma unroll
+        for (int m3 = 0; m3 < N; ++m3) {
+            constexpr int dummy = 0;
+            const int lo = cell_klo(N, m3), hi = cell_khi(N, m3);
+            const int o = cell_doff(N, m3) + (k3 < lo ? 0 : k3 >= hi ? hi - 1 - lo : k3 - lo) + dummy;
+            hv[m3] = __ldg(hs + o);
+        }
+    };
+    auto terms = [&](int2 en, const double (&hv)[N]) {
+        const double2* xs = cube + en.x;
+        const double2* ys = cube + en.y;
+#pragma unroll
+        for (int m3 = 0; m3 < N; ++m3) {
+            if (k3 < cell_klo(N, m3) || k3 >= cell_khi(N, m3)) continue;
+            const double2 xm = xs[m3];
+            const double2 yv = ys[k3 - m3 + N / 2];
+            const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
+            const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+            acc.x = fma(hv[m3], tr, acc.x);
+            acc.y = fma(hv[m3], ti, acc.y);
+        }
+    };
+    if (q < P) {
+        // two entries per step: 2N loads of h in flight per lane
+        int e = ea;
+        int2 en0 = ena, en1 = enb;
+        for (; e + S < e1; e += 2 * S) {
+            double h0[N], h1[N];
+            load_h(e, h0);
+            load_h(e + S, h1);
+            const int2 nx0 = e + 2 * S < e1 ? __ldg(ent + e + 2 * S) : en0;
+            const int2 nx1 = e + 3 * S < e1 ? __ldg(ent + e + 3 * S) : en1;
+            terms(en0, h0);
+            terms(en1, h1);
+            en0 = nx0;
+            en1 = nx1;
+        }
+        if (e < e1) {
+            double h0[N];
+            load_h(e, h0);
+            terms(en0, h0);
+        }
+        red[(w * P + q) * N + k3] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x < N) {
+        double2 sum = make_double2(0.0, 0.0);
+        for (int i = 0; i < S; ++i) {
+            const double2 v = red[i * N + threadIdx.x];
+            sum.x += v.x;
+            sum.y += v.y;
+        }
+        const int k1 = row / N, k2 = row % N, kk = threadIdx.x;
+        const double sg = ((k1 + k2 + kk) & 1) ? -1.0 : 1.0;  // inverse transform's input sign s_k
+        B[((size_t)g * N3 + (size_t)row * N + kk) * kLanes + cl] = make_double2(sg * sum.x, sg * sum.y);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // k_conv_mirror (single-tile rows, TMA staging): the Hermitian mirror schedule.
 // A work item is an output row r with no mirror partner (k1 = 0, k2 = 0 or
 // r = N - r), or a pair (r, r' = N - r).  Its entries are one contiguous list

@@ -529,3 +529,32 @@ def test_graph_capture_keeps_workspace_alive(gpu):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("n,L", [(4, 3.0), (6, 4.0), (8, 5.0), (12, 6.0), (16, 6.0)])
+def test_cell_schedule_vs_oracle(gpu, O, n, L):
+    """K2's cell schedule (conv.cuh k_conv_cell: lane = output k3, one CTA per
+    (output row, cell); cfg1's single cell): Q-hat and collide within 1e-10 of
+    the oracle, per-cell results bitwise independent of the batch, within
+    round-off of the throughput schedule, and the RK2 step against the oracle."""
+    import torch
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 3, seed=47)
+    G = table(n, L)
+    with _op(n, L) as op:
+        fh = op.forward(torch.from_numpy(f).to(gpu))
+        q_thr = op.evaluate_qhat(fh).cpu().numpy()
+        op.set_schedule("cell")
+        q3 = op.evaluate_qhat(fh).cpu().numpy()
+        q1 = op.evaluate_qhat(fh[2:3].contiguous()).cpu().numpy()
+        assert np.array_equal(q1[0], q3[2])
+        assert rel_max(q3, q_thr) < 1e-13
+        for c in range(3):
+            assert rel_max(q3[c], O.evaluate_qhat(n, L, G, fh[c].cpu().numpy())) < TOL_Q
+        qc = op.collide(f[:1])
+        g = f[:1].copy()
+        op.collision_rk2(g, 0.01)
+    ref, _ = O.collide(n, L, G, f[0])
+    assert rel_max(qc[0], ref) < TOL_Q
+    r2 = O.collision_rk2(n, L, G, f[:1], 0.01)
+    assert rel_max(g[0] - f[0], r2[0] - f[0]) < 1e-9
