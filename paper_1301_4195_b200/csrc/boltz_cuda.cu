@@ -24,8 +24,12 @@
 #include "transport.cuh"
 #include "probe.cuh"
 #include "fused.cuh"
+#include "line.cuh"
 #include "gen.cuh"
 
+#ifndef BOLTZ_LINE
+#define BOLTZ_LINE 1  // K1 / K3 as one cell per CTA, one FFT line per thread (line.cuh) at N = 8, 16
+#endif
 #ifndef BOLTZ_FUSED
 #define BOLTZ_FUSED 1  // single-kernel K1 / K3 when the N^3 cube fits in shared memory
 #endif
@@ -980,6 +984,20 @@ struct Launch {
         const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
         const double par = ((N / 2) & 1) ? -1.0 : 1.0;  // ((-1)^{N/2})^3
         const double scale = sv * sv * sv * par;
+#if BOLTZ_LINE
+        if constexpr (line_n(N)) {
+          if ((reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
+                CK(cudaFuncSetAttribute(k_fwd_line<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Line<N>::SMEM));
+            });
+            Timed t_(c, KIND_FFT, s);
+            k_fwd_line<N><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(f, c->dA, nc, scale, c->dFlag);
+            CK(cudaGetLastError());
+            return;
+          }
+        }
+#endif
 #if BOLTZ_FUSED
         if constexpr (Fused<N>::FITS) {
             using F = Fused<N>;
@@ -1194,6 +1212,24 @@ struct Launch {
     // group complex c->dB -> out = base + coef * P_N(Re iFFT) (user layout); max|Im| -> c->dMaxIm
     static void inverse_project(boltz_ctx* c, const double* base, double* out, int64_t nc, double coef,
                                 cudaStream_t s) {
+#if BOLTZ_LINE
+        if constexpr (line_n(N)) {
+            const int64_t ng = (nc + 31) / 32;
+            const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
+            const double par = ((N / 2) & 1) ? -1.0 : 1.0;
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
+                CK(cudaFuncSetAttribute(k_inv_line<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Line<N>::SMEM));
+            });
+            Timed t_(c, KIND_PROJECT, s);
+            k_inv_line<N, false><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(
+                c->dB, base, out, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
+                c->dFlag, nullptr, 0.0);
+            CK(cudaGetLastError());
+            return;
+        }
+#endif
 #if BOLTZ_FUSED
         if constexpr (Fused<N>::FITS) {
             using F = Fused<N>;
@@ -1220,6 +1256,27 @@ struct Launch {
     // otherwise through the user-layout scratch `fs`.
     static void inverse_project_forward(boltz_ctx* c, const double* base, double* fs, int64_t nc, double coef,
                                         cudaStream_t s) {
+#if BOLTZ_LINE
+        if constexpr (line_n(N)) {
+          if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) {
+            const int64_t ng = (nc + 31) / 32;
+            const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
+            const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
+            const double par = ((N / 2) & 1) ? -1.0 : 1.0;
+            static PerDevice configured;  // attributes are per device
+            configured.once(c->device, [&] {
+                CK(cudaFuncSetAttribute(k_inv_line<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Line<N>::SMEM));
+            });
+            Timed t_(c, KIND_PROJECT, s);
+            k_inv_line<N, true><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(
+                c->dB, base, nullptr, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
+                c->dFlag, c->dA, sv * sv * sv * par);
+            CK(cudaGetLastError());
+            return;
+          }
+        }
+#endif
 #if BOLTZ_FUSED
         if constexpr (Fused<N>::FITS) {
             using F = Fused<N>;

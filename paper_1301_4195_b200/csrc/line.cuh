@@ -1,0 +1,259 @@
+// line.cuh -- K1 / K3 with one cell per CTA and one FFT line per thread
+// (N = 8, 16), so that two or three CTAs share an SM and one CTA's HBM
+// loads overlap another's transforms.  The first axis pass runs straight from
+// global memory into registers and the last one straight from registers to
+// global memory, so a transform costs two shared-memory round trips instead of
+// the staged kernels' four (fused.cuh, which remains for N = 12, 24).
+//
+//   k_fwd_line:        user f [cell][N^3]  -> group fhat      (fourier.hpp:11-12)
+//   k_inv_line<FWD>:   group s_k*Qhat       -> out = base + coef * P_N(Re iFFT)
+//                      (+ max|Im|; inverse fourier.hpp:15-17, projection
+//                      SPEC.md:204-212, RK2 axpy SPEC.md:383-391); FWD: the
+//                      RK2 stage value goes straight on to its forward
+//                      transform into A_next, never touching HBM
+//
+// Thread t of the N^2 threads owns the lines (a, b) = (t / N, t % N) of every
+// pass: along i3 at (i1, i2) = (a, b), along i2 at (i1, i3) = (a, b), along i1 at
+// (i2, i3) = (a, b).  Moments are summed per thread over i1 (pass 3) and
+// reduced in a fixed order (shuffle tree, warps in order): deterministic and
+// independent of the batch.  Cells past ncells (the group's padding lanes)
+// read as zero.  HBM traffic per cell (N = 16): K1 32 KiB in + 64 KiB out;
+// K3 64 KiB + 32 KiB base in, 32 KiB (or, FWD, 64 KiB fhat) out.
+#pragma once
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace boltz_gpu {
+
+template <int N>
+struct Line {
+    static constexpr int N3 = N * N * N;
+    static constexpr int THREADS = N * N;
+    static constexpr int WARPS = (THREADS + 31) / 32;
+    static constexpr int ROW = N + 1;  // padded rows: the three passes are bank-conflict free
+    static constexpr int CELL = N * N * ROW;
+    static constexpr int SMEM = CELL * 16 + WARPS * 6 * 8 + 8 * 8;  // cube + reduction + lambda
+    __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
+};
+// the line kernels serve these N (THREADS = N^2 a multiple of 32: whole warps in the shuffle reduction)
+__host__ __device__ constexpr bool line_n(int n) { return n == 8 || n == 16; }
+
+// one in-smem pass along axis 1 (i2) of the lines (i1, i3) = (a, b)
+template <int N, int SIGN>
+__device__ __forceinline__ void line_pass_axis1(double2* sm, int a, int b) {
+    using LN = Line<N>;
+    double2 x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = sm[LN::at(a, j, b)];
+    RegFFT<N, SIGN, N>::run(x);
+#pragma unroll
+    for (int j = 0; j < N; ++j) sm[LN::at(a, j, b)] = x[j];
+}
+
+// grid = cells (the groups' padding lanes included); block = N^2 threads
+template <int N>
+__global__ void __launch_bounds__(Line<N>::THREADS, 2)
+k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
+           int* __restrict__ flag) {
+    using LN = Line<N>;
+    constexpr int N3 = LN::N3;
+    extern __shared__ __align__(16) double2 sm[];
+    const long long cell = blockIdx.x;
+    const bool live = cell < ncells;
+    const int t = threadIdx.x, a = t / N, b = t % N;
+    // pass 1 (axis 2, i3) from global: the line (a, b, :) is N contiguous doubles
+    double2 x[N];
+    bool bad = false;
+    const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
+    const double cab = axis_coeff(N, a) * axis_coeff(N, b);
+    double fv[N];  // the line as N / 2 16-byte loads (f is 16-byte aligned: the callers check)
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+        const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
+        fv[2 * j] = u.x;
+        fv[2 * j + 1] = u.y;
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double v = fv[j];
+        bad |= !isfinite(v);
+        double w = cab * axis_coeff(N, j);  // s_m c_m (fourier.hpp:19-22)
+        if ((a + b + j) & 1) w = -w;
+        x[j] = make_double2(v * w, 0.0);
+    }
+    if (bad) atomicOr(flag, 1);
+    RegFFT<N, -1, N>::run(x);
+#pragma unroll
+    for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+    __syncthreads();
+    line_pass_axis1<N, -1>(sm, a, b);
+    __syncthreads();
+    // pass 3 (axis 0, i1) to global: scale * par * s_k into the group layout
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+    RegFFT<N, -1, N>::run(x);
+    const long long g = cell / kLanes;
+    const int lane = (int)(cell % kLanes);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double s = ((j + a + b) & 1) ? -scale : scale;
+        A[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] = make_double2(x[j].x * s, x[j].y * s);
+    }
+}
+
+template <int N, bool FWD>
+__global__ void __launch_bounds__(Line<N>::THREADS, 2)
+k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
+           double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
+           int* __restrict__ flag, double2* __restrict__ A_next, double fwd_scale) {
+    using LN = Line<N>;
+    constexpr int N3 = LN::N3, NN = N * N;
+    extern __shared__ __align__(16) double2 sm[];
+    double* red = reinterpret_cast<double*>(sm + LN::CELL);  // [warps][6]
+    double* lam = red + LN::WARPS * 6;                       // [5]
+    const long long cell = blockIdx.x;
+    const bool live = cell < ncells;
+    const long long g = cell / kLanes;
+    const int lane = (int)(cell % kLanes);
+    const int t = threadIdx.x, a = t / N, b = t % N, wid = t >> 5, ln = t & 31;
+    // the RK2 base this thread applies at the end, prefetched now: FWD -- the
+    // line (a, b, :), contiguous; otherwise nodes t + k N^2 (coalesced)
+    double bv[N];
+    if constexpr (FWD) {  // N / 2 16-byte loads (base is 16-byte aligned: the callers check)
+        const double2* bl = reinterpret_cast<const double2*>(base + (size_t)cell * N3 + (size_t)(a * N + b) * N);
+#pragma unroll
+        for (int j = 0; j < N / 2; ++j) {
+            const double2 u = (live && base) ? ldg2(bl + j) : make_double2(0.0, 0.0);
+            bv[2 * j] = u.x;
+            bv[2 * j + 1] = u.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            bv[j] = (live && base) ? __ldg(base + (size_t)cell * N3 + (size_t)j * NN + t) : 0.0;
+    }
+    // pass 1 (axis 2, i3) from the group layout
+    double2 x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+        x[j] = live ? ldg2(B + ((size_t)g * N3 + (size_t)(a * N + b) * N + j) * kLanes + lane) : make_double2(0.0, 0.0);
+    RegFFT<N, +1, N>::run(x);
+#pragma unroll
+    for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+    __syncthreads();
+    line_pass_axis1<N, +1>(sm, a, b);
+    __syncthreads();
+    // pass 3 (axis 0, i1) in registers: Qt = Re(scale * par * s_k * z), its
+    // moments over i1 and max|Im| (the thread's (i2, i3) = (a, b) are fixed)
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+    RegFFT<N, +1, N>::run(x);
+    const double dv3 = pc.dv * pc.dv * pc.dv;
+    const double fv2 = pc.dv * (a - N / 2), fv3 = pc.dv * (b - N / 2);
+    const double fw23 = axis_coeff(N, a) * axis_coeff(N, b) * dv3;
+    const double sg23 = ((a + b) & 1) ? -scale : scale;
+    double s0 = 0.0, s1 = 0.0, s4 = 0.0, mi = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double q = x[j].x * ((j & 1) ? -sg23 : sg23);
+        sm[LN::at(j, a, b)].x = q;
+        const double v1 = pc.dv * (j - N / 2);
+        const double cq = axis_coeff(N, j) * q;
+        s0 += cq;
+        s1 = fma(v1, cq, s1);
+        s4 = fma(v1 * v1, cq, s4);
+        mi = fmax(mi, fabs(x[j].y));
+    }
+    double part[6];
+    part[0] = fw23 * s0;
+    part[1] = fw23 * s1;
+    part[2] = fv2 * part[0];
+    part[3] = fv3 * part[0];
+    part[4] = fw23 * fma(fv2 * fv2 + fv3 * fv3, s0, s4);
+    part[5] = mi * fabs(scale);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        double v = part[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = (k == 5) ? fmax(v, u) : v + u;
+        }
+        if (ln == 0) red[wid * 6 + k] = v;
+    }
+    __syncthreads();
+    if (t == 0) {
+        double m[6] = {0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < LN::WARPS; ++w)
+            for (int k = 0; k < 6; ++k) {
+                const double r = red[w * 6 + k];
+                m[k] = (k == 5) ? fmax(m[k], r) : m[k] + r;
+            }
+        for (int k = 0; k < 5; ++k) {  // lambda = (C C^T)^{-1} C Qt
+            double s = 0.0;
+            for (int c = 0; c < 5; ++c) s = fma(pc.ginv[k * 5 + c], m[c], s);
+            lam[k] = s;
+        }
+        if (maximag && live) maximag[cell] = m[5];
+    }
+    __syncthreads();
+    const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3], l4 = lam[4];
+    bool bad = false;
+    if constexpr (!FWD) {
+        // out = base + coef * (Qt - w C^T lambda) at nodes t + k N^2: i1 = k, (i2, i3) = (a, b)
+        const double cl23 = l0 + fv2 * l2 + fv3 * l3 + (fv2 * fv2 + fv3 * fv3) * l4;
+        if (live) {
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                const double v1 = pc.dv * (k - N / 2);
+                const double cl = fma(v1, fma(v1, l4, l1), cl23);
+                const double q = sm[LN::at(k, a, b)].x - axis_coeff(N, k) * fw23 * cl;
+                double v = coef * q;
+                if (base) v += bv[k];
+                bad |= !isfinite(v);
+                out[(size_t)cell * N3 + (size_t)k * NN + t] = v;
+            }
+        }
+        if (bad) atomicOr(flag, 2);
+    } else {
+        // f* = base + coef * P_N(Qt) on the line (a, b, :), times s_m c_m, and its
+        // forward transform: pass 1 in registers, pass 2 in smem, pass 3 to A_next
+        const double v1 = pc.dv * (a - N / 2), v2 = pc.dv * (b - N / 2);
+        const double cl12 = l0 + v1 * l1 + v2 * l2 + (v1 * v1 + v2 * v2) * l4;
+        const double w12 = axis_coeff(N, a) * axis_coeff(N, b);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double v3 = pc.dv * (j - N / 2);
+            const double cl = fma(v3, fma(v3, l4, l3), cl12);
+            const double q = sm[LN::at(a, b, j)].x - w12 * axis_coeff(N, j) * dv3 * cl;
+            double v = 0.0;
+            if (live) {
+                v = coef * q;
+                if (base) v += bv[j];
+                bad |= !isfinite(v);
+            }
+            double w = w12 * axis_coeff(N, j);
+            if ((a + b + j) & 1) w = -w;
+            x[j] = make_double2(v * w, 0.0);
+        }
+        if (bad) atomicOr(flag, 2);
+        RegFFT<N, -1, N>::run(x);
+        // the thread's own line: no other thread reads it after the barrier above
+#pragma unroll
+        for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+        __syncthreads();
+        line_pass_axis1<N, -1>(sm, a, b);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+        RegFFT<N, -1, N>::run(x);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double s = ((j + a + b) & 1) ? -fwd_scale : fwd_scale;
+            A_next[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] =
+                make_double2(x[j].x * s, x[j].y * s);
+        }
+    }
+}
+
+}  // namespace boltz_gpu
