@@ -118,7 +118,7 @@ __host__ __device__ constexpr int mirror_slab(int n, int ty) {
 }
 
 // Register tile width and kernel per N, chosen by measurement on B200
-// (scripts/ab_conv.py, scripts/ab_n32.sh; algorithmic TFLOP/s, round 1):
+// (scripts/dev/ab_conv.py, scripts/dev/ab_n32.sh; algorithmic TFLOP/s, round 1):
 //   N=16: T=16 k_conv_pipe 47.5 | T=16 kcs 46.4 | T=8 kcs 39.7 | T=16 k_conv 41.1
 //   N=24: T=24 kcs 45.5         | T=12 kcs 43.5 | T=24 pipe 36.0 | T=12 k_conv 34.3
 //   N=32: T=16 kcs 45.3         | T=16 k_conv 33.3 | pipe 28.8

@@ -1,8 +1,8 @@
 """Time the K2 convolution of each library variant (development aid).
-    python scripts/ab_conv.py variants/lib_*.so
+    python scripts/dev/ab_conv.py variants/lib_*.so
 Each variant runs in its own process (BOLTZ_LIB_VARIANT)."""
 import os, pathlib, subprocess, sys, json
-ROOT = pathlib.Path(__file__).resolve().parent.parent
+ROOT = pathlib.Path(__file__).resolve().parents[2]
 if len(sys.argv) > 1 and sys.argv[1] != "--child":
     for lib in sys.argv[1:]:
         env = dict(os.environ, BOLTZ_LIB_VARIANT=str(pathlib.Path(lib).resolve()))

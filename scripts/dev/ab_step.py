@@ -1,7 +1,7 @@
 """Per-kernel-class ms of one cfg2 RK2 step for each library variant (dev aid).
-    python scripts/ab_step.py variants/lib_*.so"""
+    python scripts/dev/ab_step.py variants/lib_*.so"""
 import os, pathlib, subprocess, sys, json
-ROOT = pathlib.Path(__file__).resolve().parent.parent
+ROOT = pathlib.Path(__file__).resolve().parents[2]
 if len(sys.argv) > 1 and sys.argv[1] != "--child":
     for lib in sys.argv[1:]:
         env = dict(os.environ, BOLTZ_LIB_VARIANT=str(pathlib.Path(lib).resolve()))

@@ -1,7 +1,7 @@
 """Build A/B variants of the library into variants/ (development aid)."""
 import pathlib, sys
 from concurrent.futures import ThreadPoolExecutor
-sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[2]))
 from paper_1301_4195_b200.build import build
 V = {
     "base": [],
@@ -27,7 +27,7 @@ V = {
     "w8": ["BOLTZ_CONV_WARPS=8"],
     "rest2": ["BOLTZ_KCSM_REST_MINB=2"],  # N <= 16 on k_conv_kcs / the phased k_conv_kcsm mirror
 }
-root = pathlib.Path(__file__).resolve().parent.parent / "variants"
+root = pathlib.Path(__file__).resolve().parents[2] / "variants"
 names = sys.argv[1:] or list(V)
 with ThreadPoolExecutor(4) as ex:
     list(ex.map(lambda n: build(force=True, out=root / f"lib_{n}.so", defines=V[n]), names))

@@ -1,6 +1,6 @@
 """cfg1 (one cell, N=16): K2 per eval and the 50-step RK2 run per schedule (dev aid)."""
 import sys, pathlib, time
-sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[2]))
 import torch
 from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios
 grid = VelocityGrid.create(16, 6.0)

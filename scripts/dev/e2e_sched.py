@@ -1,8 +1,8 @@
 """e2e (pinned host memory) cfg2 RK2 step time for host-pipeline chunk schedules
-(development aid).   python scripts/e2e_sched.py "1,7,7,1" "1,4,11,11,4,1" ...
+(development aid).   python scripts/dev/e2e_sched.py "1,7,7,1" "1,4,11,11,4,1" ...
 Each schedule runs in its own process (BOLTZ_HOST_CHUNKS)."""
 import os, pathlib, subprocess, sys
-ROOT = pathlib.Path(__file__).resolve().parent.parent
+ROOT = pathlib.Path(__file__).resolve().parents[2]
 if len(sys.argv) > 1 and sys.argv[1] != "--child":
     for sch in sys.argv[1:]:
         env = dict(os.environ)

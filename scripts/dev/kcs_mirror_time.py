@@ -1,7 +1,7 @@
 """N=24 / N=32 RK2 step time, mirror vs plain K2 schedule (dev aid).
 Each schedule in its own process (BOLTZ_MIRROR)."""
 import os, pathlib, subprocess, sys
-ROOT = pathlib.Path(__file__).resolve().parent.parent
+ROOT = pathlib.Path(__file__).resolve().parents[2]
 if len(sys.argv) < 2 or sys.argv[1] != "--child":
     for m in ("0", "1"):
         r = subprocess.run([sys.executable, __file__, "--child"], env=dict(os.environ, BOLTZ_MIRROR=m),

@@ -1,7 +1,7 @@
 """K2 schedules at small batches (dev aid): RK2 step time per cell count for the
-throughput and latency schedules, N=16 cfg2 cells.   python scripts/latency_time.py"""
+throughput and latency schedules, N=16 cfg2 cells.   python scripts/dev/latency_time.py"""
 import pathlib, sys
-sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[2]))
 import torch
 from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios
 grid = VelocityGrid.create(16, 6.0)

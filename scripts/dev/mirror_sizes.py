@@ -1,7 +1,7 @@
 """K2 mirror vs plain schedule by batch size (dev aid): RK2 step ms, N=16.
 Each schedule in its own process (BOLTZ_MIRROR values from argv, default 0 1)."""
 import os, pathlib, subprocess, sys
-ROOT = pathlib.Path(__file__).resolve().parent.parent
+ROOT = pathlib.Path(__file__).resolve().parents[2]
 if len(sys.argv) < 2 or sys.argv[1] != "--child":
     for m in (sys.argv[1:] or ["0", "1"]):
         r = subprocess.run([sys.executable, __file__, "--child"], env=dict(os.environ, BOLTZ_MIRROR=m),

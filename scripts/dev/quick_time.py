@@ -1,6 +1,6 @@
 """Quick device timing of the collision path (development aid)."""
 import sys, time, pathlib
-sys.path.insert(0, str(pathlib.Path(__file__).resolve().parent.parent))
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[2]))
 import numpy as np, torch
 from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios
 from paper_1301_4195_b200.build import build
