@@ -655,6 +655,21 @@ void layout_terms_kcsm(int n, TableLayout& T) {
     const int t = conv_tile(n), nk = n / t;
     int off = 0;
     for (int ty = 0; ty < kBandTypes; ++ty) {
+        if (ty == BT_REST && kcsr_n(n)) {
+            // k_conv_kcsr: the whole row's REST terms, diagonal-major, one slab
+            std::vector<short2> v(kcsr_slab(n), make_short2(-1, -1));
+            int pos = 0;
+            for (int part = 0; part < 3; ++part)  // k_conv_kcsr's visiting order
+                for (int m3 = 0; m3 < n; ++m3)
+                    for (int k3 = 0; k3 < n; ++k3)
+                        if (kcsr_part(n, part, k3, m3)) v[pos++] = make_short2((short)k3, (short)m3);
+            T.ts.off[ty] = off;
+            T.ts.slab[ty] = (int)v.size();
+            T.ts.slab_max = std::max(T.ts.slab_max, (int)v.size());
+            T.term.insert(T.term.end(), v.begin(), v.end());
+            off += (int)v.size();
+            continue;
+        }
         const int stride = kcsm_slab(n, ty);
         std::vector<short2> v((size_t)nk * stride, make_short2(-1, -1));
         for (int kc = 0; kc < nk; ++kc)
@@ -1056,6 +1071,11 @@ struct Launch {
                     };
                     cfg(k_conv_kcsm<N, 0, 0>, 0);
                     cfg(k_conv_kcsm<N, KC1, 0>, 0);
+                    if constexpr (kcsr_n(N)) {
+                        CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
+                        CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    }
                     if constexpr (kcsm_split(N)) {
                         cfg(k_conv_kcsm<N, 0, 1>, 1);
                         cfg(k_conv_kcsm<N, KC1, 1>, 1);
@@ -1079,7 +1099,14 @@ struct Launch {
                 };
                 go(k_conv_kcsm<N, 0, 0>, 0);
                 if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 0>, 0);
-                if constexpr (kcsm_split(N)) {
+                if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
+                    const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
+                    const int lr = (int64_t)c->nK[1] * gr < 8 * 2 * 148 ? 0 : (int)gr - 1;
+                    k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
+                                     s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr);
+                    go(k_conv_kcsm<N, 0, 2>, 2);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
+                } else if constexpr (kcsm_split(N)) {
                     go(k_conv_kcsm<N, 0, 1>, 1);
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 1>, 1);
                     go(k_conv_kcsm<N, 0, 2>, 2);
@@ -1088,7 +1115,7 @@ struct Launch {
                     go(k_conv_kcsm<N, 0, 3>, 1);
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3>, 1);
                 }
-                c->launches[KIND_CONV] += (kcsm_split(N) ? 3 : 2) * NK - 1;  // all under one timing bracket
+                c->launches[KIND_CONV] += kcsr_n(N) ? 2 * NK : (kcsm_split(N) ? 3 : 2) * NK - 1;  // one timing bracket
                 CK(cudaGetLastError());
                 return;
             }

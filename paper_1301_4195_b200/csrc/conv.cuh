@@ -1505,6 +1505,223 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_conv_kcsr (N = 32, replaces phase 1 of k_conv_kcsm): the REST entries of
+// the pair rows for BOTH k-chunks in one launch.  A REST entry holds few terms
+// (the non-interior ones and the k3 = 0 column: 109 at N = 32, against ~700
+// A terms) but needs the whole x and y rows, so phase 1 ran one L2-bound pass
+// per k-chunk.  Here an entry's rows are staged once for the full output row:
+// 32 accumulators in registers, x per diagonal from L2, the H slab by TMA
+// (double-buffered) and the y row by TMA into a single buffer, read in three
+// parts so that the buffer is refilled early:
+//   part 0: the edge diagonals m3 in {0, 1, N-1} (y per term from smem)
+//   part 1: the k3 = 0 column of the interior diagonals (y per term from smem)
+//   -- y[0], y[1], y[N-1] to registers; the next entry's y row is issued --
+//   part 2: the interior diagonals' remaining terms, whose s3 is 0, 1 or N-1
+// The table builder lays the slab out in exactly this order (kcsr_part).  The
+// row is seeded from B (phase 0's raw A or its mirror) and written back raw;
+// phase 2 finishes it.  Per-cell order is fixed: bitwise batch-independent.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr bool kcsr_term(int n, int k3, int m3) {
+    const int s3 = k3 - m3 + n / 2;
+    return s3 >= 0 && s3 < n && type_term(n, BT_REST, k3, m3);
+}
+// y buffers per warp: 1 -- the three parts above; 2 -- double-buffered y row
+// and one diagonal-major pass (every term in part 0).  B200, cfg5-shaped RK2
+// step (2048 cells), K2 ms: phase 1 per k-chunk 318.0 | kcsr 1 buffer, 4 warps
+// 305.8 | 2 buffers, 2 warps per CTA 299.9 | 3 warps 301.9 | 4 warps 322.5
+#ifndef BOLTZ_KCSR_YBUF
+#define BOLTZ_KCSR_YBUF 2
+#endif
+// is REST term (k3, m3) in part `part` (0, 1, 2; see above)?
+__host__ __device__ constexpr bool kcsr_part(int n, int part, int k3, int m3) {
+    if (!kcsr_term(n, k3, m3)) return false;
+    if (BOLTZ_KCSR_YBUF == 2) return part == 0;
+    const bool edge = !mirror_interior(n, m3);
+    return part == 0 ? edge : part == 1 ? (!edge && k3 == 0) : (!edge && k3 != 0);
+}
+__host__ __device__ constexpr int kcsr_slab(int n) {
+    int c = 0;
+    for (int m3 = 0; m3 < n; ++m3)
+        for (int k3 = 0; k3 < n; ++k3) c += kcsr_term(n, k3, m3) ? 1 : 0;
+    return even_up(c);
+}
+__host__ __device__ constexpr bool kcsr_diag(int n, int part, int m3) {
+    bool any = false;
+    for (int k3 = 0; k3 < n; ++k3) any = any || kcsr_part(n, part, k3, m3);
+    return any;
+}
+#ifndef BOLTZ_KCSR
+#define BOLTZ_KCSR 1  // N = 32: one full-row REST launch instead of phase 1 per k-chunk
+#endif
+__host__ __device__ constexpr bool kcsr_n(int n) { return BOLTZ_KCSR && n == 32 && kcsm_split(n); }
+#ifndef BOLTZ_KCSR_WARPS
+#define BOLTZ_KCSR_WARPS 2
+#endif
+constexpr int kKcsrWarps = BOLTZ_KCSR_WARPS;
+template <int N>
+struct KcsrLayout {
+    static constexpr int Y_BYTES = N * kLanes * 16;
+    static constexpr int H_BYTES = kcsr_slab(N) * 8;
+    static constexpr int WARP_BYTES = BOLTZ_KCSR_YBUF * Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+};
+#ifndef BOLTZ_KCSR_MINB
+#define BOLTZ_KCSR_MINB 2
+#endif
+
+// the kcsr term list as a compile-time table: term I = (k3, m3), parts in order
+template <int N>
+struct KcsrTab {
+    static constexpr int cnt() {
+        int c = 0;
+        for (int part = 0; part < 3; ++part)
+            for (int m3 = 0; m3 < N; ++m3)
+                for (int k3 = 0; k3 < N; ++k3) c += kcsr_part(N, part, k3, m3) ? 1 : 0;
+        return c;
+    }
+    static constexpr int COUNT = cnt();
+    short k3[COUNT] = {}, m3[COUNT] = {}, part[COUNT] = {};
+    constexpr KcsrTab() {
+        int c = 0;
+        for (int pt = 0; pt < 3; ++pt)
+            for (int m = 0; m < N; ++m)
+                for (int k = 0; k < N; ++k)
+                    if (kcsr_part(N, pt, k, m)) {
+                        k3[c] = (short)k;
+                        m3[c] = (short)m;
+                        part[c] = (short)pt;
+                        ++c;
+                    }
+    }
+};
+
+// one kcsr entry's terms, unrolled from the compile-time table (x loaded when
+// the diagonal changes; y from smem in parts 0 and 1, from registers in part 2)
+template <int N>
+struct KcsrEntry {
+    double2 (&acc)[N];
+    const double2* X;
+    const double2* ys;
+    const double2* hs;
+    int lane;
+    double2 xm, hb, y0, y1, yl;
+    template <int I>
+    __device__ __forceinline__ void step() {
+        constexpr KcsrTab<N> tab{};
+        constexpr int k3 = tab.k3[I], m3 = tab.m3[I], part = tab.part[I], s3 = k3 - m3 + N / 2;
+        if constexpr (I == 0 || tab.m3[I > 0 ? I - 1 : 0] != m3 || tab.part[I > 0 ? I - 1 : 0] != part)
+            xm = ldg2(X + (size_t)m3 * kLanes);
+        if constexpr ((I & 1) == 0) hb = hs[I >> 1];
+        const double h = (I & 1) ? hb.y : hb.x;
+        double2 yv;
+        if constexpr (part < 2) yv = ys[s3 * kLanes + lane];
+        else yv = s3 == 0 ? y0 : s3 == 1 ? y1 : yl;
+        const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
+        const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+        acc[k3].x = fma(h, tr, acc[k3].x);
+        acc[k3].y = fma(h, ti, acc[k3].y);
+    }
+};
+template <int I, int END>
+struct KcsrRun {
+    template <typename F>
+    __device__ __forceinline__ static void run(F& f) {
+        if constexpr (I < END) {
+            f.template step<I>();
+            KcsrRun<I + 1, END>::run(f);
+        }
+    }
+};
+template <int N>
+__host__ __device__ constexpr int kcsr_part_begin(int part) {
+    int c = 0;
+    for (int pt = 0; pt < part; ++pt)
+        for (int m = 0; m < N; ++m)
+            for (int k = 0; k < N; ++k) c += kcsr_part(N, pt, k, m) ? 1 : 0;
+    return c;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kLanes* kKcsrWarps, BOLTZ_KCSR_MINB)
+k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
+    using LY = KcsrLayout<N>;
+    constexpr int N3 = N * N * N;
+    constexpr unsigned HB = LY::H_BYTES;
+    constexpr int P2 = kcsr_part_begin<N>(2), PE = KcsrTab<N>::COUNT;
+    extern __shared__ __align__(16) char smem[];
+    const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = blockIdx.y * kKcsrWarps + wid;
+    if (g >= ngroups) return;
+    const int row = __ldg(list + nrows + 1 + wi);
+    const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
+    char* wsm = smem + wid * LY::WARP_BYTES;
+    const double2* ys0 = reinterpret_cast<const double2*>(wsm);
+    char* hbase = wsm + BOLTZ_KCSR_YBUF * LY::Y_BYTES;
+    unsigned long long* bar =
+        reinterpret_cast<unsigned long long*>(wsm + BOLTZ_KCSR_YBUF * LY::Y_BYTES + 2 * LY::H_BYTES);
+    const double2* Abase = A + (size_t)g * N3 * kLanes;
+    const double2* Ag = Abase + lane;
+    double2* Brow = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
+    double2 acc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc[k] = Brow[(size_t)k * kLanes];  // seeded: every phase-1 row is a pair row
+    auto tma_h = [&](int slot, int4 en) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, HB);
+            bulk_g2s(hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z, HB, bar + slot);
+        }
+    };
+    auto tma_y = [&](int slot, int4 en) {
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar + slot, LY::Y_BYTES);
+            bulk_g2s(const_cast<double2*>(ys0) + (BOLTZ_KCSR_YBUF == 2 ? slot * N * kLanes : 0),
+                     Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+        }
+    };
+    if (e0 < e1) {
+        if (lane == 0) {
+            mbar_init(bar, 2);
+            mbar_init(bar + 1, 2);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int4 en = __ldg(ent + e0);
+        int4 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;
+        tma_y(0, en);
+        tma_h(0, en);
+        mbar_wait(bar, 0);
+        for (int e = e0; e < e1; ++e) {
+            const int i = e - e0, cur = i & 1;
+            const bool more = e + 1 < e1;
+            const int4 nx = en_ahead;
+            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
+            __syncwarp();  // every lane finished reading H[cur^1] (and y[cur^1])
+            if (more) tma_h(cur ^ 1, nx);
+            const double2* ys = ys0 + (BOLTZ_KCSR_YBUF == 2 ? cur * N * kLanes : 0);
+            if (BOLTZ_KCSR_YBUF == 2 && more) tma_y(cur ^ 1, nx);
+            KcsrEntry<N> f{acc, Ag + (size_t)en.x * kLanes, ys,
+                           reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES), lane};
+            KcsrRun<0, P2>::run(f);  // parts 0 and 1: y from the staged row
+            if constexpr (BOLTZ_KCSR_YBUF == 1) {
+                f.y0 = ys[lane];
+                f.y1 = ys[kLanes + lane];
+                f.yl = ys[(N - 1) * kLanes + lane];
+                __syncwarp();  // every lane read the y row: the buffer may be refilled
+                if (more) tma_y(cur ^ 1, nx);
+                KcsrRun<P2, PE>::run(f);  // part 2: y[0], y[1], y[N-1] in registers
+            }
+            if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+            en = nx;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) Brow[(size_t)k * kLanes] = acc[k];  // raw: phase 2 continues the row
+}
+
 // ---- H table builder.  Entry e = output row (k1,k2) x representative input
 // row (m1,m2) (entk = {k1,k2,m1,m2}) with meta[e] = {H offset, band type};
 // term[ts.off[type] + pos] = (k3, m3) of slab position pos, or (-1,-1) for
