@@ -1533,10 +1533,15 @@ __host__ __device__ constexpr bool kcsr_term(int n, int k3, int m3) {
 #ifndef BOLTZ_KCSR_YBUF
 #define BOLTZ_KCSR_YBUF 2
 #endif
+// with 2 y buffers: part 2's y[0], y[1], y[N-1] from registers (44 of the 109
+// terms) instead of shared memory -- the kernel is shared-memory-bandwidth-bound
+#ifndef BOLTZ_KCSR_YREG
+#define BOLTZ_KCSR_YREG 0  // measured: 310.3 against 299.9 ms per RK2 step (255 registers, 32 B spilled)
+#endif
 // is REST term (k3, m3) in part `part` (0, 1, 2; see above)?
 __host__ __device__ constexpr bool kcsr_part(int n, int part, int k3, int m3) {
     if (!kcsr_term(n, k3, m3)) return false;
-    if (BOLTZ_KCSR_YBUF == 2) return part == 0;
+    if (BOLTZ_KCSR_YBUF == 2 && !BOLTZ_KCSR_YREG) return part == 0;
     const bool edge = !mirror_interior(n, m3);
     return part == 0 ? edge : part == 1 ? (!edge && k3 == 0) : (!edge && k3 != 0);
 }
@@ -1706,12 +1711,14 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
             KcsrEntry<N> f{acc, Ag + (size_t)en.x * kLanes, ys,
                            reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES), lane};
             KcsrRun<0, P2>::run(f);  // parts 0 and 1: y from the staged row
-            if constexpr (BOLTZ_KCSR_YBUF == 1) {
+            if constexpr (BOLTZ_KCSR_YBUF == 1 || BOLTZ_KCSR_YREG) {
                 f.y0 = ys[lane];
                 f.y1 = ys[kLanes + lane];
                 f.yl = ys[(N - 1) * kLanes + lane];
-                __syncwarp();  // every lane read the y row: the buffer may be refilled
-                if (more) tma_y(cur ^ 1, nx);
+                if constexpr (BOLTZ_KCSR_YBUF == 1) {
+                    __syncwarp();  // every lane read the y row: the buffer may be refilled
+                    if (more) tma_y(cur ^ 1, nx);
+                }
                 KcsrRun<P2, PE>::run(f);  // part 2: y[0], y[1], y[N-1] in registers
             }
             if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));

@@ -25,6 +25,9 @@
 
 namespace boltz_gpu {
 
+#ifndef BOLTZ_LINE_MINB
+#define BOLTZ_LINE_MINB 2  // CTAs per SM the line kernels are compiled for (registers)
+#endif
 template <int N>
 struct Line {
     static constexpr int N3 = N * N * N;
@@ -52,7 +55,7 @@ __device__ __forceinline__ void line_pass_axis1(double2* sm, int a, int b) {
 
 // grid = cells (the groups' padding lanes included); block = N^2 threads
 template <int N>
-__global__ void __launch_bounds__(Line<N>::THREADS, 2)
+__global__ void __launch_bounds__(Line<N>::THREADS, BOLTZ_LINE_MINB)
 k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
            int* __restrict__ flag) {
     using LN = Line<N>;
@@ -102,7 +105,7 @@ k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncel
 }
 
 template <int N, bool FWD>
-__global__ void __launch_bounds__(Line<N>::THREADS, 2)
+__global__ void __launch_bounds__(Line<N>::THREADS, BOLTZ_LINE_MINB)
 k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
            double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
            int* __restrict__ flag, double2* __restrict__ A_next, double fwd_scale) {
