@@ -1040,7 +1040,8 @@ struct Launch {
     static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s, bool hermitian = false) {
         const int64_t ng = (nc + 31) / 32;
         if constexpr (conv_tile(N) == N && N <= 16) {
-            if (c->schedule == kScheduleCell) {  // one or a few cells: lane = output k3 (conv.cuh k_conv_cell)
+            // one or a few cells: lane = output k3 (conv.cuh k_conv_cell); one grid row per cell
+            if (c->schedule == kScheduleCell && nc <= 65535) {
                 using CL = CellLayout<N>;
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
@@ -1163,7 +1164,7 @@ struct Launch {
         }
         if constexpr (conv_kernel_for(N) == 1 && conv_tile(N) == N &&
                       kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
-            if (c->schedule > 0) {
+            if (c->schedule > 0 && c->schedule < kScheduleCell) {
                 const int S = kConvWarps * c->schedule;  // segments per row
                 const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
                 static PerDevice configured;  // attributes are per device
