@@ -1783,6 +1783,9 @@ int api(boltz_ctx* c, Body&& body) {
     } catch (const std::bad_alloc&) {
         set_error("host allocation failed");
         return BOLTZ_ERR_CUDA;
+    } catch (const std::exception& e) {  // e.g. std::system_error from the host pipeline's threads
+        set_error(std::string("host runtime error: ") + e.what());
+        return BOLTZ_ERR_CUDA;
     }
 }
 
