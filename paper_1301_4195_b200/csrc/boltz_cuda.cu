@@ -1911,6 +1911,10 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
         set_error(e.msg);
         boltz_destroy(c);
         return BOLTZ_ERR_CUDA;
+    } catch (const std::exception& e) {  // host allocation of the table layout
+        set_error(std::string("boltz_create: ") + e.what());
+        boltz_destroy(c);
+        return BOLTZ_ERR_CUDA;
     }
     *out = c;
     return BOLTZ_OK;
