@@ -382,7 +382,7 @@ def main():
 
     # roofline of the dominant kernel (K2 convolution)
     terms_plain, terms_mirror = op.schedule_terms()
-    conv_kernel = "k_conv_mirror<16>" if terms_mirror else "k_conv_pipe<16>"
+    conv_kernel = f"{op.conv_kernel()}<{N_VEL}>"
     exec_ratio = (terms_mirror or terms_plain) / terms_per_eval(N_VEL)
     conv_launches = klaunch["conv"]
     conv_ms_avg = kms["conv"] / max(conv_launches, 1)

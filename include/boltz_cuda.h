@@ -208,9 +208,10 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * 5 = cell (lane = output k3, one CTA per (output row, cell), the cell's
  * f-hat in shared memory: one or a few cells, N <= 16; conv.cuh k_conv_cell).
  * Under the throughput schedule collide / RK2 at N >= 8 use the Hermitian
- * mirror schedule (conv.cuh k_conv_mirror at N <= 16, the phased k_conv_kcsm
- * at N = 24, 32; env BOLTZ_MIRROR=0 disables it, BOLTZ_MIRROR=2 selects the
- * TMEM-accumulator variant k_conv_mirror2 at N = 8..16).
+ * mirror schedule (conv.cuh k_conv_mirror2, with TMEM accumulators, at
+ * N = 8, 12, 16; the phased k_conv_kcsm + k_conv_kcsr at N = 24, 32; env
+ * BOLTZ_MIRROR=0 disables it, BOLTZ_MIRROR=1 selects k_conv_mirror, the
+ * register-only variant, at N <= 16).
  * Results are bitwise reproducible and independent of batch composition
  * within a schedule; schedules differ by round-off.
  */
@@ -223,6 +224,9 @@ int boltz_set_schedule(boltz_ctx* ctx, int schedule);
  * Each is the size of its folded table, i.e. every FP64 term the kernel runs.
  */
 int boltz_schedule_terms(boltz_ctx* ctx, int64_t* plain, int64_t* mirror);
+/* Name of the K2 kernel(s) collide / RK2 run under the current schedule (for
+ * the benchmark's roofline label; "" for a null context). */
+const char* boltz_conv_kernel(const boltz_ctx* ctx);
 int boltz_set_async(boltz_ctx* ctx, int enable);
 int boltz_sync(boltz_ctx* ctx, void* stream);
 

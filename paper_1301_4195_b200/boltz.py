@@ -97,6 +97,8 @@ def lib():
             "boltz_set_async": (i, [vp, i]),
             "boltz_set_schedule": (i, [vp, i]),
             "boltz_schedule_terms": (i, [vp, C.POINTER(i64), C.POINTER(i64)]),
+            "boltz_conv_kernel": (C.c_char_p, [vp]),
+            "boltz_create_transform": (i, [i, d, i, C.POINTER(vp)]),
             "boltz_sync": (i, [vp, vp]),
             "boltz_set_timing": (i, [vp, i]),
             "boltz_get_timing": (i, [vp, vp, vp, i, i]),
@@ -360,6 +362,10 @@ class CollisionOperator:
         a, b = C.c_int64(), C.c_int64()
         _check(lib().boltz_schedule_terms(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def conv_kernel(self) -> str:
+        """The K2 kernel(s) collide / RK2 run under the current schedule."""
+        return lib().boltz_conv_kernel(self._h).decode()
 
     def set_schedule(self, schedule="throughput"):
         """K2 schedule: "throughput" (default), "latency" (each row's entries in 4

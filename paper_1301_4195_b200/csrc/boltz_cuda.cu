@@ -792,9 +792,11 @@ void build_table(boltz_ctx* c, const double* G_host) {
     if (const char* e = std::getenv("BOLTZ_MIRROR")) mirror = mirror && std::atoi(e) != 0;
     if (mirror && G_host) mirror = g_mirror_symmetric(c->n, G_host);
     if (mirror) {
-        // BOLTZ_MIRROR=2: the TMEM variant (k_conv_mirror2) at N = 8..16
-        c->mirror2 = mirror_pipe_n(c->n) && c->n % 4 == 0 && std::getenv("BOLTZ_MIRROR") &&
-                     std::atoi(std::getenv("BOLTZ_MIRROR")) == 2;
+        // at N = 8..16 the TMEM variant (k_conv_mirror2) is the default (BOLTZ_MIRROR unset or 2;
+        // cfg2 with the 1,2,5,5,2,1 host chunks: value 699.9k / e2e 671.2k evals/s against 693.2k /
+        // 666.7k for k_conv_mirror); BOLTZ_MIRROR=1 selects k_conv_mirror
+        const char* me = std::getenv("BOLTZ_MIRROR");
+        c->mirror2 = mirror_pipe_n(c->n) && c->n % 4 == 0 && (!me || std::atoi(me) == 2);
         if (c->mirror2) build_table_mirror2(c, G_host);
         else if (mirror_pipe_n(c->n)) build_table_mirror(c, G_host);
         else build_table_mirror_kcs(c, G_host);
@@ -2204,6 +2206,18 @@ int boltz_marginal_batch(boltz_ctx* c, const double* f, double* g, int64_t ncell
                                CK(cudaGetLastError());
                            });
     });
+}
+
+const char* boltz_conv_kernel(const boltz_ctx* c) {
+    if (!c) return "";
+    if (c->schedule == kScheduleCell && c->n <= 16) return "k_conv_cell + k_cell_gather";
+    if (c->schedule > 0 && c->schedule < kScheduleCell && c->n <= 16) return "k_conv_seg + k_conv_seg_reduce";
+    if (c->mirror) {
+        if (c->mirror2) return "k_conv_mirror2";
+        if (mirror_pipe_n(c->n)) return "k_conv_mirror";
+        return c->n == 32 ? "k_conv_kcsm (phases 0, 2) + k_conv_kcsr" : "k_conv_kcsm";
+    }
+    return conv_kernel_for(c->n) == 1 ? "k_conv_pipe" : "k_conv_kcs";
 }
 
 int boltz_schedule_terms(boltz_ctx* c, int64_t* plain, int64_t* mirror) {

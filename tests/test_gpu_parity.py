@@ -377,7 +377,7 @@ def test_mirror_schedule_kcs_consistent(gpu, O, n, L, cells):
 
 @pytest.mark.parametrize("n,L", [(8, 5.0), (16, 6.0)])
 def test_mirror2_tmem_schedule(gpu, O, n, L, monkeypatch):
-    """BOLTZ_MIRROR=2 (conv.cuh k_conv_mirror2: REST and the partner row's REST'
+    """BOLTZ_MIRROR=2, the default at N <= 16 (conv.cuh k_conv_mirror2: REST and the partner row's REST'
     in TMEM, each interior input row staged once) with the host table
     (k_build_H's partner-plane pass) and the generated one (k_gen_H): Q against
     the oracle to 1e-10, against the default mirror schedule to round-off, and
@@ -385,8 +385,10 @@ def test_mirror2_tmem_schedule(gpu, O, n, L, monkeypatch):
     grid = VelocityGrid.create(n, L)
     f = scenarios.mixture_cells(grid, 9, seed=71)
     G = table(n, L)
+    monkeypatch.setenv("BOLTZ_MIRROR", "1")
     with _op(n, L) as op:
         q1 = op.collide(f)                                  # k_conv_mirror
+        assert rel_max(q1[0], O.collide(n, L, G, f[0], 1.0, nthreads=8)[0]) < TOL_Q
     monkeypatch.setenv("BOLTZ_MIRROR", "2")
     with _op(n, L) as op:
         plain, mirror = op.schedule_terms()
