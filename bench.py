@@ -543,7 +543,8 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
     halo = None
     if world > 1:
         halo = NcclHalo(rank, world, dev.index) if backend == "nccl" else _HostStagedHalo(rank, world)
-    s = Solver1D(op, x, dx, init, rank=rank, world=world, halo=halo, **kw)
+    # NCCL halo: the exchange overlaps the ghost-free rows of each transport stage
+    s = Solver1D(op, x, dx, init, rank=rank, world=world, halo=halo, overlap_halo=isinstance(halo, NcclHalo), **kw)
     dt = s.cfl_dt()
     graph = world == 1 or isinstance(halo, NcclHalo)
     s.strang_step(dt)  # warm-up: workspace + kernel attributes
@@ -579,7 +580,8 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
            "ranks": world, "scaling": "strong" if world > 1 else None, "steps": steps, "ms_per_step": ms / steps,
            "cells_steps_per_s": nx * steps / (ms * 1e-3), "evals_per_s": 2 * nx * steps / (ms * 1e-3),
            "mode": ("CUDA graph of 3 Strang steps" if graph else "eager Strang steps") + ", K2 latency schedule"
-                   + (", NCCL halo (boltz_halo_exchange) inside the graph" if isinstance(halo, NcclHalo) else
+                   + (", NCCL halo (boltz_halo_exchange) inside the graph, overlapped with the ghost-free rows"
+                      if isinstance(halo, NcclHalo) else
                       ", host-staged gloo halo (plumbing check, not a measurement)" if world > 1 else ""),
            "launches_per_step_rank0": launches_per_step}
     if world > 1:

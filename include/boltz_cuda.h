@@ -133,6 +133,16 @@ int boltz_transport_step(boltz_ctx* ctx, const double* field, const double* base
                          int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
                          int wall_right, void* stream);
 
+/* transport_step on the interior rows [c_begin, c_end) only (2 <= c_begin <=
+ * c_end <= ncl + 2; field rows are cells, ghosts at 0, 1, ncl + 2, ncl + 3).
+ * Rows c_begin >= 4 and c_end <= ncl read no ghost row, so they can run while
+ * the halo exchange is in flight; the left ghost rows are copied through iff
+ * c_begin == 2, the right ones iff c_end == ncl + 2.  Bitwise the rows of the
+ * whole-interior call (halo/compute overlap). */
+int boltz_transport_step_range(boltz_ctx* ctx, const double* field, const double* base, double alpha, double* out,
+                               int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                               int wall_right, int64_t c_begin, int64_t c_end, void* stream);
+
 /*
  * The halo exchange fused into the transport step (B200 peer memory; no
  * reference counterpart -- it replaces transport_step + halo_exchange,

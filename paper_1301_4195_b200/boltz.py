@@ -90,6 +90,7 @@ def lib():
             "boltz_collide_batch": (i, [vp, vp, vp, i64, d, vp, i, vp]),
             "boltz_rk2_batch": (i, [vp, vp, i64, d, d, i, vp]),
             "boltz_transport_step": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, vp]),
+            "boltz_transport_step_range": (i, [vp, vp, vp, d, vp, i64, vp, vp, d, i, i, i64, i64, vp]),
             "boltz_fill_boundary": (i, [vp, vp, i64, vp, i, i, d, vp, dp, vp]),
             "boltz_moments_batch": (i, [vp, vp, vp, i64, i, vp]),
             "boltz_marginal_batch": (i, [vp, vp, vp, i64, i, vp]),
@@ -525,17 +526,22 @@ class CollisionOperator:
 
     # -- transport (device tensors only)
     def transport_step(self, field, out, x_ext, dx_ext, dt, wall_left=False, wall_right=False, base=None,
-                       alpha=0.0):
+                       alpha=0.0, rows=None):
         """transport_step on a (ncl+4, N^3) device field:
-        out = alpha*base + (1-alpha)*step(field) (base=None: the plain step)."""
+        out = alpha*base + (1-alpha)*step(field) (base=None: the plain step).
+        rows=(c_begin, c_end): only those interior rows (boltz_transport_step_range)."""
         ncl = field.shape[0] - 4
         arrs = (field, out, x_ext, dx_ext) + ((base,) if base is not None else ())
         ptrs, mem, s = self._args(*arrs)
         if mem != MEM_DEVICE:
             raise ConfigError("transport_step takes CUDA tensors")
         pb = ptrs[4] if base is not None else None
-        _check(lib().boltz_transport_step(self._h, ptrs[0], pb, alpha, ptrs[1], ncl, ptrs[2], ptrs[3], dt,
-                                          int(wall_left), int(wall_right), s))
+        if rows is None:
+            _check(lib().boltz_transport_step(self._h, ptrs[0], pb, alpha, ptrs[1], ncl, ptrs[2], ptrs[3], dt,
+                                              int(wall_left), int(wall_right), s))
+        else:
+            _check(lib().boltz_transport_step_range(self._h, ptrs[0], pb, alpha, ptrs[1], ncl, ptrs[2], ptrs[3], dt,
+                                                    int(wall_left), int(wall_right), int(rows[0]), int(rows[1]), s))
         return out
 
     def end_flux(self, field, x_ext, dx_ext, acc, coef, wall_left=False, wall_right=False):

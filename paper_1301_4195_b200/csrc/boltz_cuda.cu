@@ -2089,6 +2089,30 @@ int boltz_transport_step(boltz_ctx* c, const double* field, const double* base, 
     });
 }
 
+int boltz_transport_step_range(boltz_ctx* c, const double* field, const double* base, double alpha, double* out,
+                               int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
+                               int wall_right, int64_t c_begin, int64_t c_end, void* stream) {
+    return api(c, [&] {
+        if (ncl < 1 || !field || !out || !x_ext || !dx_ext || out == field || (base && out == base) || c_begin < 2 ||
+            c_end > ncl + 2 || c_begin > c_end) {
+            set_error("transport_step_range: invalid arguments (need 2 <= c_begin <= c_end <= ncl + 2; out must not "
+                      "alias field/base)");
+            return BOLTZ_ERR_CONFIG;
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        {
+            Timed t_(c, KIND_TRANSPORT, s);
+            launch_transport(c->n, field, base, base ? alpha : 0.0, out, ncl, x_ext, dx_ext, dt, wall_left,
+                             wall_right, c->pc.dv, s, 0, nullptr, nullptr, c_begin, c_end);
+        }
+        CK(cudaGetLastError());
+        if (c->async_mode) return BOLTZ_OK;
+        CK(cudaStreamSynchronize(s));
+        if (c->timing) collect_timing(c);
+        return BOLTZ_OK;
+    });
+}
+
 int boltz_transport_step_peer(boltz_ctx* c, const double* field, const double* base, double alpha, double* out,
                               int64_t ncl, const double* x_ext, const double* dx_ext, double dt, int wall_left,
                               int wall_right, double* left_dst, double* right_dst, void* stream) {

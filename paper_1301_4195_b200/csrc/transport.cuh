@@ -93,12 +93,15 @@ template <int N>
 __global__ void __launch_bounds__(256)
 k_transport(const double* __restrict__ f, const double* __restrict__ base, double alpha, double* __restrict__ out,
             long long ncl, const double* __restrict__ x, const double* __restrict__ dx, double dt, int wl, int wr,
-            double dv, int peer, double* __restrict__ left_dst, double* __restrict__ right_dst) {
+            double dv, int peer, double* __restrict__ left_dst, double* __restrict__ right_dst, long long cb,
+            long long ce) {
     constexpr int N3 = N * N * N;
     constexpr int P3 = N3 / 2;  // node pairs: a thread owns nodes 2p, 2p+1 (same v1: N is even)
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    const long long c0 = 2 + (long long)blockIdx.y * kTrCells;
-    const long long c1 = c0 + kTrCells < ncl + 2 ? c0 + kTrCells : ncl + 2;  // [c0, c1) interior
+    // the launch covers interior rows [cb, ce) (the whole interior [2, ncl + 2) unless a
+    // halo-overlapped stage splits it, boltz_transport_step_range)
+    const long long c0 = cb + (long long)blockIdx.y * kTrCells;
+    const long long c1 = c0 + kTrCells < ce ? c0 + kTrCells : ce;  // [c0, c1) interior
     // per-cell geometry of cells c0-1 .. c1 (slopes) and c0 .. c1-1 (dt/dx)
     __shared__ double s_r1[kTrCells + 2], s_r2[kTrCells + 2], s_r3[kTrCells + 2], s_h[kTrCells + 2];
     __shared__ double s_lam[kTrCells];
@@ -115,8 +118,8 @@ k_transport(const double* __restrict__ f, const double* __restrict__ base, doubl
     const double2* F = reinterpret_cast<const double2*>(f);
     const double2* Bs = reinterpret_cast<const double2*>(base);
     double2* O = reinterpret_cast<double2*>(out);
-    if (!peer) {  // ghost rows copied through
-        if (blockIdx.y == 0) {
+    if (!peer) {  // ghost rows copied through (by the launch that owns the adjacent interior rows)
+        if (blockIdx.y == 0 && cb == 2) {
             O[p] = F[p];
             O[P3 + p] = F[P3 + p];
         }
@@ -325,13 +328,15 @@ k_fill_boundary(double* __restrict__ f, long long ncl, const double* __restrict_
 inline void launch_transport(int n, const double* f, const double* base, double alpha, double* out, long long ncl,
                              const double* x, const double* dx, double dt, int wl, int wr, double dv,
                              cudaStream_t s, int peer = 0, double* left_dst = nullptr,
-                             double* right_dst = nullptr) {
+                             double* right_dst = nullptr, long long cb = 2, long long ce = -1) {
+    if (ce < 0) ce = ncl + 2;
+    if (ce <= cb) return;
     switch (n) {
 #define BOLTZ_TR(N)                                                                                        \
     case N: {                                                                                              \
-        dim3 grid((N * N * N / 2 + 255) / 256, (unsigned)((ncl + kTrCells - 1) / kTrCells));              \
+        dim3 grid((N * N * N / 2 + 255) / 256, (unsigned)((ce - cb + kTrCells - 1) / kTrCells));          \
         k_transport<N><<<grid, 256, 0, s>>>(f, base, alpha, out, ncl, x, dx, dt, wl, wr, dv, peer, left_dst, \
-                                            right_dst);                                                    \
+                                            right_dst, cb, ce);                                            \
     } break;
         BOLTZ_FOR_EACH_N(BOLTZ_TR)
 #undef BOLTZ_TR

@@ -128,11 +128,14 @@ class Solver1D:
 
     def __init__(self, op: CollisionOperator, x: np.ndarray, dx: np.ndarray, f0, *, rank: int = 0,
                  world: int = 1, left: Boundary = Boundary(), right: Boundary = Boundary(),
-                 epsilon: float = 1.0, halo=None, device=None, plan=None, transport_scheme: str = "ssp_rk2"):
+                 epsilon: float = 1.0, halo=None, device=None, plan=None, transport_scheme: str = "ssp_rk2",
+                 overlap_halo: bool = False):
         import torch
         if transport_scheme not in ("ssp_rk2", "single_stage"):
             raise ConfigError(f"transport_scheme must be 'ssp_rk2' or 'single_stage', got {transport_scheme!r}")
         self.scheme = transport_scheme
+        self.overlap_halo = overlap_halo
+        self._side = None
         self.op, self.rank, self.world, self.eps = op, rank, world, epsilon
         self.left, self.right = left, right
         self.n3 = op.grid.size()
@@ -194,6 +197,9 @@ class Solver1D:
     def fill_ghosts(self, exchange: bool = True) -> None:
         if exchange and self.halo is not None:
             self.halo.exchange(self.field)
+        self._fill_physical()
+
+    def _fill_physical(self) -> None:
         if self.is_left_end:
             self.sigma_w[0] = self.op.fill_boundary(self.field, self.x_ext, 0, self.left.code(), self.left.Tw,
                                                     self.left.Vw)
@@ -215,23 +221,44 @@ class Solver1D:
         of its input."""
         wl, wr = self._walls()
         if self.scheme == "single_stage":
-            self.fill_ghosts(exchange)
-            self._track_flux(dt, wl, wr)
-            self.op.transport_step(self.field, self._tmp, self.x_ext, self.dx_ext, dt, wl, wr)
+            self._refresh_and_step(self._tmp, dt, wl, wr, exchange)
             self.field, self._tmp = self._tmp, self.field
             return
         if stage == 0:
-            self.fill_ghosts(exchange)
-            self._track_flux(dt, wl, wr)
-            self.op.transport_step(self.field, self._tmp, self.x_ext, self.dx_ext, dt, wl, wr)
+            self._refresh_and_step(self._tmp, dt, wl, wr, exchange)
         else:
             self.field, self._tmp = self._tmp, self.field  # field = t1, _tmp = f^n
-            self.fill_ghosts(exchange)
-            self._track_flux(dt, wl, wr)
             out = self._tmp2
-            self.op.transport_step(self.field, out, self.x_ext, self.dx_ext, dt, wl, wr, base=self._tmp, alpha=0.5)
+            self._refresh_and_step(out, dt, wl, wr, exchange, base=self._tmp, alpha=0.5)
             self._tmp2 = self.field
             self.field = out
+
+    def _refresh_and_step(self, out, dt, wl, wr, exchange, base=None, alpha=0.0) -> None:
+        """Ghost refresh of self.field, then out = [alpha base + (1-alpha)] S(field).
+        With overlap_halo (NcclHalo, >= 6 cells per rank) the exchange runs on a
+        side stream while the rows that read no ghost ([4, ncl)) are updated,
+        and the four edge rows follow once it has landed: bitwise the same rows
+        (boltz_transport_step_range), the exchange hidden behind the interior
+        update."""
+        args = (self.x_ext, self.dx_ext, dt, wl, wr)
+        if not (exchange and self.overlap_halo and isinstance(self.halo, NcclHalo) and self.ncl >= 6):
+            self.fill_ghosts(exchange)
+            self._track_flux(dt, wl, wr)
+            self.op.transport_step(self.field, out, *args, base=base, alpha=alpha)
+            return
+        import torch
+        main = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            self.halo.exchange(self.field)
+        self._fill_physical()  # the physical ends' ghost rows: disjoint from the exchanged ones
+        self.op.transport_step(self.field, out, *args, base=base, alpha=alpha, rows=(4, self.ncl))
+        main.wait_stream(self._side)
+        self._track_flux(dt, wl, wr)  # reads the end faces, whose ghosts may have come over the halo
+        self.op.transport_step(self.field, out, *args, base=base, alpha=alpha, rows=(2, 4))
+        self.op.transport_step(self.field, out, *args, base=base, alpha=alpha, rows=(self.ncl, self.ncl + 2))
 
     def track_boundary_flux(self, enable: bool = True) -> None:
         """Accumulate the end-face fluxes of every FV stage (boltz_end_flux) so

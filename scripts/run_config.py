@@ -85,7 +85,7 @@ def spatial(args, rank, world, dev):
         from paper_1301_4195_b200 import NcclHalo
         halo = NcclHalo(rank, world, dev.index)  # the C ABI's NCCL halo: capturable, so graphs across ranks
     s = Solver1D(op, x, dx, init, rank=rank, world=world, left=left, right=right, plan=plan, device=dev, halo=halo,
-                 transport_scheme=args.transport)
+                 transport_scheme=args.transport, overlap_halo=args.overlap and halo is not None)
     mass0 = float(s.ledger()[0])  # global sum_j dx_j rho_j of the initial state (collective)
     dt = s.cfl_dt()
     # warm-up step (not timed), then the run
@@ -199,6 +199,8 @@ def main():
                    help="transport sub-step: SSP-RK2 (default) or the SPEC single stage (SPEC.md:342-345)")
     p.add_argument("--schedule", default="auto", choices=["auto", "throughput", "latency", "latency8", "cell"],
                    help="K2 schedule (auto: latency for <= 256 cells per rank at N <= 16)")
+    p.add_argument("--no-overlap", dest="overlap", action="store_false",
+                   help="NCCL halo: do not overlap the exchange with the ghost-free transport rows")
     p.add_argument("--halo", default="nccl", choices=["nccl", "torch"],
                    help="multi-rank halo: the library's NCCL halo (graph-capturable) or torch.distributed P2P")
     args = p.parse_args()

@@ -275,6 +275,69 @@ def test_nccl_halo_graph_run_matches_eager(gpu):
         halo.close()
 
 
+@pytest.mark.parametrize("scheme", ["ssp_rk2", "single_stage"])
+def test_halo_overlap_bitwise(gpu, scheme):
+    """SURVEY §8f rank 2, halo/compute overlap: with overlap_halo the NCCL
+    exchange runs on a side stream while the rows that read no ghost are
+    updated (boltz_transport_step_range), then the four edge rows.  World 1
+    (the exchange is a no-op; the streams, the split launches and the graph
+    capture are real): eager and graph-replayed steps are bitwise the plain
+    driver's, and so is the boundary-flux ledger."""
+    import torch
+    from paper_1301_4195_b200 import NcclHalo
+    n, L, nx = 8, 5.0, 14
+    grid = VelocityGrid.create(n, L)
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    f0 = scenarios.mixture_cells(grid, nx, seed=43)
+    kw = dict(left=Boundary("wall", 2.0), right=Boundary("extrap"), transport_scheme=scheme)
+    with _op(n, L) as op:
+        a = Solver1D(op, x, dx, f0, **kw)
+        a.track_boundary_flux()
+        dt = 0.5 * a.cfl_dt()
+        for _ in range(7):
+            a.strang_step(dt)
+        ref, ref_flux = a.interior.cpu().numpy(), a.boundary_flux()
+        halo = NcclHalo(0, 1, 0)
+        b = Solver1D(op, x, dx, f0, halo=halo, overlap_halo=True, **kw)
+        b.track_boundary_flux()
+        for _ in range(7):
+            b.strang_step(dt)
+        torch.cuda.synchronize()
+        assert np.array_equal(b.interior.cpu().numpy(), ref)
+        assert np.array_equal(b.boundary_flux(), ref_flux)
+        c = Solver1D(op, x, dx, f0, halo=halo, overlap_halo=True, **kw)
+        c.run(dt, 7)
+        assert getattr(c, "graph_replays", 0) == 2
+        assert np.array_equal(c.interior.cpu().numpy(), ref)
+        halo.close()
+
+
+def test_transport_step_rows_split_bitwise(gpu):
+    """boltz_transport_step_range: rows [4, ncl) + [2, 4) + [ncl, ncl + 2) are
+    bitwise the whole-interior step (ghost rows copied by the edge launches);
+    bad ranges are ConfigErrors."""
+    import torch
+    from paper_1301_4195_b200 import ConfigError
+    n, L, nx = 8, 5.0, 11
+    x, dx = scenarios.geometric_grid(nx, 3.0, 1.15)
+    xe, dxe = scenarios.extend_ghosts(x, dx)
+    rng = np.random.default_rng(5)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(gpu)  # noqa: E731
+    field, base = d(rng.random((nx + 4, n ** 3))), d(rng.random((nx + 4, n ** 3)))
+    with _op(n, L) as op:
+        dt = 0.8 * dx.min() / L
+        for kw in (dict(), dict(base=base, alpha=0.5)):
+            full = torch.empty_like(field)
+            op.transport_step(field, full, d(xe), d(dxe), dt, True, False, **kw)
+            part = torch.full_like(field, float("nan"))
+            for rows in ((4, nx), (2, 4), (nx, nx + 2)):
+                op.transport_step(field, part, d(xe), d(dxe), dt, True, False, rows=rows, **kw)
+            assert torch.equal(part, full)
+        for rows in ((1, 4), (4, nx + 3), (5, 4)):
+            with pytest.raises(ConfigError):
+                op.transport_step(field, part, d(xe), d(dxe), dt, rows=rows)
+
+
 def test_new_abi_entries_reject_bad_arguments(gpu):
     """ConfigError (category 2) for the peer transport, the edge store and the
     schedule setter on invalid input (no CUDA call is made)."""
