@@ -1586,6 +1586,8 @@ struct KcsrTab {
     }
     static constexpr int COUNT = cnt();
     short k3[COUNT] = {}, m3[COUNT] = {}, part[COUNT] = {};
+    bool dstart[COUNT] = {};  // term I opens a diagonal (a new x value)
+    short xnext[COUNT] = {};  // at a diagonal start: m3 of the next diagonal (-1: none)
     constexpr KcsrTab() {
         int c = 0;
         for (int pt = 0; pt < 3; ++pt)
@@ -1597,11 +1599,24 @@ struct KcsrTab {
                         part[c] = (short)pt;
                         ++c;
                     }
+        for (int i = 0; i < COUNT; ++i) dstart[i] = i == 0 || m3[i - 1] != m3[i] || part[i - 1] != part[i];
+        for (int i = 0; i < COUNT; ++i) {
+            xnext[i] = -1;
+            if (!dstart[i]) continue;
+            for (int j = i + 1; j < COUNT; ++j)
+                if (dstart[j]) {
+                    xnext[i] = m3[j];
+                    break;
+                }
+        }
     }
 };
 
 // one kcsr entry's terms, unrolled from the compile-time table (x loaded when
 // the diagonal changes; y from smem in parts 0 and 1, from registers in part 2)
+#ifndef BOLTZ_KCSR_XPF
+#define BOLTZ_KCSR_XPF 0  // measured: 314 against 305 ms per N=32 RK2 step (255 registers, 40 B spilled)
+#endif
 template <int N>
 struct KcsrEntry {
     double2 (&acc)[N];
@@ -1609,13 +1624,22 @@ struct KcsrEntry {
     const double2* ys;
     const double2* hs;
     int lane;
-    double2 xm, hb, y0, y1, yl;
+    double2 xm, xn, hb, y0, y1, yl;
     template <int I>
     __device__ __forceinline__ void step() {
         constexpr KcsrTab<N> tab{};
         constexpr int k3 = tab.k3[I], m3 = tab.m3[I], part = tab.part[I], s3 = k3 - m3 + N / 2;
-        if constexpr (I == 0 || tab.m3[I > 0 ? I - 1 : 0] != m3 || tab.part[I > 0 ? I - 1 : 0] != part)
-            xm = ldg2(X + (size_t)m3 * kLanes);
+        if constexpr (tab.dstart[I]) {
+            // x one diagonal ahead (BOLTZ_KCSR_XPF): the load of the next diagonal's x
+            // is in flight while this diagonal's terms run
+            if constexpr (BOLTZ_KCSR_XPF) {
+                if constexpr (I == 0) xm = ldg2(X + (size_t)m3 * kLanes);
+                else xm = xn;
+                if constexpr (tab.xnext[I] >= 0) xn = ldg2(X + (size_t)tab.xnext[I] * kLanes);
+            } else {
+                xm = ldg2(X + (size_t)m3 * kLanes);
+            }
+        }
         if constexpr ((I & 1) == 0) hb = hs[I >> 1];
         const double h = (I & 1) ? hb.y : hb.x;
         double2 yv;
