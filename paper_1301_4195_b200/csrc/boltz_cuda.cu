@@ -676,11 +676,14 @@ void layout_terms_kcsm(int n, TableLayout& T) {
             for (int ti = 0; ti < nk; ++ti) {
                 const int sc = band_tile_sc(nk, kc, ti);
                 int pos = kc * stride + kcsm_piece_off(n, t, kc, ti, ty);
-                for (int i = 0; i < n; ++i) {  // band_tile's visiting order
-                    const int m3 = band_diag(n, nk, kc, ti, i);
-                    for (int kk = 0; kk < t; ++kk)
-                        if (band_term_t(n, t, kc, sc, m3, kk, ty)) v[pos++] = make_short2((short)(kc * t + kk), (short)m3);
-                }
+                const int ks = kcsm_ks(n, kc, ty);
+                for (int q = 0; q < ks; ++q)  // band_tile's visiting order (kk passes, then diagonals)
+                    for (int i = 0; i < n; ++i) {
+                        const int m3 = band_diag(n, nk, kc, ti, i);
+                        for (int kk = q * t / ks; kk < (q + 1) * t / ks; ++kk)
+                            if (band_term_t(n, t, kc, sc, m3, kk, ty))
+                                v[pos++] = make_short2((short)(kc * t + kk), (short)m3);
+                    }
             }
         T.ts.off[ty] = off;
         T.ts.slab[ty] = nk * stride;

@@ -1369,8 +1369,22 @@ __host__ __device__ constexpr bool kcsm_split(int n) {
 #ifndef BOLTZ_KCSM_GAUSS
 #define BOLTZ_KCSM_GAUSS 1
 #endif
+// chunk-1 kernels (kc = 1, N = 32): kk passes of the band (band_tile KS) and the
+// Gauss form there (dev knobs, off): the passes do not relieve the registers --
+// ptxas: KS = 2 255 registers + 72 B stack; KS = 2 + Gauss 255 + 536 B; Gauss
+// alone 255 + 64 / 112 B (the 6-instruction term: 244 / 242, no stack)
+#ifndef BOLTZ_KCSM_KS1
+#define BOLTZ_KCSM_KS1 1
+#endif
+#ifndef BOLTZ_KCSM_GAUSS1
+#define BOLTZ_KCSM_GAUSS1 0
+#endif
+__host__ __device__ constexpr int kcsm_ks(int n, int kc, int ty) {
+    return (n == 32 && kc == 1 && (ty == BT_A || ty == BT_FULL)) ? BOLTZ_KCSM_KS1 : 1;
+}
 __host__ __device__ constexpr bool kcsm_gauss(int n, int kc, int phase) {
-    return BOLTZ_TERM_GAUSS || (BOLTZ_KCSM_GAUSS && n == 32 && kc == 0 && (phase == 0 || phase == 2));
+    return BOLTZ_TERM_GAUSS || (BOLTZ_KCSM_GAUSS && n == 32 && kc == 0 && (phase == 0 || phase == 2)) ||
+           (BOLTZ_KCSM_GAUSS1 && n == 32 && kc == 1 && (phase == 0 || phase == 2));
 }
 template <int N, int KC, int PHASE>
 using KcsmY = std::conditional_t<kcsm_gauss(N, KC, PHASE), YG, double2>;
@@ -1390,7 +1404,8 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const YT
     int p = 0;
     if constexpr (PHASE < 3) {
         constexpr int TY = kcsm_type(PHASE);
-        band_tile<N, T, NK, KC, TI, TY>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, TY) / 2, p, hb, none);
+        band_tile<N, T, NK, KC, TI, TY, kcsm_ks(N, KC, TY)>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, TY) / 2, p,
+                                                           hb, none);
     } else if (ty == BT_FULL) {
         band_tile<N, T, NK, KC, TI, BT_FULL>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, BT_FULL) / 2, p, hb, none);
     } else {
