@@ -1012,7 +1012,7 @@ struct Launch {
                 CK(cudaFuncSetAttribute(k_fwd_line<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Line<N>::SMEM));
             });
             Timed t_(c, KIND_FFT, s);
-            k_fwd_line<N><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(f, c->dA, nc, scale, c->dFlag);
+            k_fwd_line<N><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(f, c->dA, nc, scale, c->dFlag);
             CK(cudaGetLastError());
             return;
           }
@@ -1256,7 +1256,7 @@ struct Launch {
                                         Line<N>::SMEM));
             });
             Timed t_(c, KIND_PROJECT, s);
-            k_inv_line<N, false><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(
+            k_inv_line<N, false><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(
                 c->dB, base, out, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
                 c->dFlag, nullptr, 0.0);
             CK(cudaGetLastError());
@@ -1302,7 +1302,7 @@ struct Launch {
                                         Line<N>::SMEM));
             });
             Timed t_(c, KIND_PROJECT, s);
-            k_inv_line<N, true><<<(unsigned)(ng * kLanes), Line<N>::THREADS, Line<N>::SMEM, s>>>(
+            k_inv_line<N, true><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(
                 c->dB, base, nullptr, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
                 c->dFlag, c->dA, sv * sv * sv * par);
             CK(cudaGetLastError());

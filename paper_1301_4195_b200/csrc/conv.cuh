@@ -51,8 +51,11 @@ __host__ __device__ constexpr bool band_term(int n, int t, int kc, int sc, int m
     return s3 >= sc * t && s3 < sc * t + t;
 }
 __host__ __device__ constexpr int band_tile_sc(int nk, int kc, int ti) { return nk == 2 ? (ti == 0 ? 1 - kc : kc) : ti; }
+#ifndef BOLTZ_DIAG_REV
+#define BOLTZ_DIAG_REV 1  // the chunk-1 square tile walks its diagonals in reverse (x-slot refill order)
+#endif
 __host__ __device__ constexpr int band_diag(int n, int nk, int kc, int ti, int i) {
-    return (nk == 2 && ti == 1 && kc == 1) ? n - 1 - i : i;
+    return (BOLTZ_DIAG_REV && nk == 2 && ti == 1 && kc == 1) ? n - 1 - i : i;
 }
 __host__ __device__ constexpr int band_kc_terms(int n, int t, int kc) {
     int c = 0;

@@ -1,6 +1,5 @@
-// line.cuh -- K1 / K3 with one cell per CTA and one FFT line per thread
-// (N = 8, 16), so that two or three CTAs share an SM and one CTA's HBM
-// loads overlap another's transforms.  The first axis pass runs straight from
+// line.cuh -- K1 / K3 with one FFT line per thread and two adjacent cells per
+// CTA (N = 8, 16; BOLTZ_LINE_CPB=1: one cell per CTA, two CTAs per SM).  The first axis pass runs straight from
 // global memory into registers and the last one straight from registers to
 // global memory, so a transform costs two shared-memory round trips instead of
 // the staged kernels' four (fused.cuh, which remains for N = 12, 24).
@@ -26,19 +25,32 @@
 namespace boltz_gpu {
 
 #ifndef BOLTZ_LINE_MINB
-#define BOLTZ_LINE_MINB 2  // CTAs per SM the line kernels are compiled for (registers)
+#define BOLTZ_LINE_MINB 2  // CTAs per SM the line kernels are compiled for (registers), one cell per CTA
 #endif
+// cells per CTA: 1, or 2 adjacent cells of a group handled by the two half-warps
+// of every warp (lanes 0-15 and 16-31 take the same 16 lines of the two cells),
+// so that each group-layout access is a whole 32-byte sector (two 16-byte
+// lanes) instead of half of one
+#ifndef BOLTZ_LINE_CPB
+#define BOLTZ_LINE_CPB 2  // cfg2 RK2 step: K1 0.182 -> 0.168 ms, K3 0.523 -> 0.497 ms against one cell per CTA
+#endif
+constexpr int kLineCPB = BOLTZ_LINE_CPB;
 template <int N>
 struct Line {
     static constexpr int N3 = N * N * N;
-    static constexpr int THREADS = N * N;
+    static constexpr int CPB = kLineCPB;
+    static constexpr int THREADS = N * N * CPB;
     static constexpr int WARPS = (THREADS + 31) / 32;
     static constexpr int ROW = N + 1;  // padded rows: the three passes are bank-conflict free
     static constexpr int CELL = N * N * ROW;
-    static constexpr int SMEM = CELL * 16 + WARPS * 6 * 8 + 8 * 8;  // cube + reduction + lambda
+    static constexpr int SMEM = CPB * CELL * 16 + WARPS * CPB * 6 * 8 + CPB * 8 * 8;  // cubes + reduction + lambda
     __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
+    // thread t -> (cell of the CTA, line): with 2 cells the half-warps split by cell
+    __device__ static int sub(int t) { return CPB == 2 ? (t >> 4) & 1 : 0; }
+    __device__ static int line(int t) { return CPB == 2 ? ((t >> 5) << 4) | (t & 15) : t; }
+    static constexpr unsigned MINB = CPB == 2 ? 1 : BOLTZ_LINE_MINB;
 };
-// the line kernels serve these N (THREADS = N^2 a multiple of 32: whole warps in the shuffle reduction)
+// the line kernels serve these N (N^2 a multiple of 32: whole warps in the shuffle reduction)
 __host__ __device__ constexpr bool line_n(int n) { return n == 8 || n == 16; }
 
 // one in-smem pass along axis 1 (i2) of the lines (i1, i3) = (a, b)
@@ -53,17 +65,18 @@ __device__ __forceinline__ void line_pass_axis1(double2* sm, int a, int b) {
     for (int j = 0; j < N; ++j) sm[LN::at(a, j, b)] = x[j];
 }
 
-// grid = cells (the groups' padding lanes included); block = N^2 threads
+// grid = cells / CPB (the groups' padding lanes included); block = CPB N^2 threads
 template <int N>
-__global__ void __launch_bounds__(Line<N>::THREADS, BOLTZ_LINE_MINB)
+__global__ void __launch_bounds__(Line<N>::THREADS, Line<N>::MINB)
 k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
            int* __restrict__ flag) {
     using LN = Line<N>;
     constexpr int N3 = LN::N3;
-    extern __shared__ __align__(16) double2 sm[];
-    const long long cell = blockIdx.x;
+    extern __shared__ __align__(16) double2 smem_line[];
+    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
+    double2* sm = smem_line + sub * LN::CELL;
+    const long long cell = (long long)blockIdx.x * LN::CPB + sub;
     const bool live = cell < ncells;
-    const int t = threadIdx.x, a = t / N, b = t % N;
     // pass 1 (axis 2, i3) from global: the line (a, b, :) is N contiguous doubles
     double2 x[N];
     bool bad = false;
@@ -105,22 +118,23 @@ k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncel
 }
 
 template <int N, bool FWD>
-__global__ void __launch_bounds__(Line<N>::THREADS, BOLTZ_LINE_MINB)
+__global__ void __launch_bounds__(Line<N>::THREADS, Line<N>::MINB)
 k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
            double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
            int* __restrict__ flag, double2* __restrict__ A_next, double fwd_scale) {
     using LN = Line<N>;
-    constexpr int N3 = LN::N3, NN = N * N;
-    extern __shared__ __align__(16) double2 sm[];
-    double* red = reinterpret_cast<double*>(sm + LN::CELL);  // [warps][6]
-    double* lam = red + LN::WARPS * 6;                       // [5]
-    const long long cell = blockIdx.x;
+    constexpr int N3 = LN::N3, NN = N * N, CPB = LN::CPB;
+    extern __shared__ __align__(16) double2 smem_line[];
+    double* red = reinterpret_cast<double*>(smem_line + CPB * LN::CELL);  // [warps][CPB][6]
+    double* lam = red + LN::WARPS * CPB * 6;                             // [CPB][8]
+    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N, wid = t >> 5;
+    double2* sm = smem_line + sub * LN::CELL;
+    const long long cell = (long long)blockIdx.x * CPB + sub;
     const bool live = cell < ncells;
     const long long g = cell / kLanes;
     const int lane = (int)(cell % kLanes);
-    const int t = threadIdx.x, a = t / N, b = t % N, wid = t >> 5, ln = t & 31;
     // the RK2 base this thread applies at the end, prefetched now: FWD -- the
-    // line (a, b, :), contiguous; otherwise nodes t + k N^2 (coalesced)
+    // line (a, b, :), contiguous; otherwise nodes ln + k N^2 (coalesced)
     double bv[N];
     if constexpr (FWD) {  // N / 2 16-byte loads (base is 16-byte aligned: the callers check)
         const double2* bl = reinterpret_cast<const double2*>(base + (size_t)cell * N3 + (size_t)(a * N + b) * N);
@@ -133,7 +147,7 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
     } else {
 #pragma unroll
         for (int j = 0; j < N; ++j)
-            bv[j] = (live && base) ? __ldg(base + (size_t)cell * N3 + (size_t)j * NN + t) : 0.0;
+            bv[j] = (live && base) ? __ldg(base + (size_t)cell * N3 + (size_t)j * NN + ln) : 0.0;
     }
     // pass 1 (axis 2, i3) from the group layout
     double2 x[N];
@@ -174,36 +188,41 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
     part[3] = fv3 * part[0];
     part[4] = fw23 * fma(fv2 * fv2 + fv3 * fv3, s0, s4);
     part[5] = mi * fabs(scale);
+    // shuffle tree over the lanes of this cell (a whole warp, or a half-warp with 2 cells)
+    constexpr int O0 = CPB == 2 ? 8 : 16, LANES = CPB == 2 ? 16 : 32;
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         double v = part[k];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = O0; o > 0; o >>= 1) {
             const double u = __shfl_xor_sync(0xffffffffu, v, o);
             v = (k == 5) ? fmax(v, u) : v + u;
         }
-        if (ln == 0) red[wid * 6 + k] = v;
+        if ((t & (LANES - 1)) == 0) red[(wid * CPB + sub) * 6 + k] = v;
     }
     __syncthreads();
-    if (t == 0) {
+    if (t < CPB) {
+        const int c = t;
+        const long long cl = (long long)blockIdx.x * CPB + c;
         double m[6] = {0, 0, 0, 0, 0, 0};
         for (int w = 0; w < LN::WARPS; ++w)
             for (int k = 0; k < 6; ++k) {
-                const double r = red[w * 6 + k];
+                const double r = red[(w * CPB + c) * 6 + k];
                 m[k] = (k == 5) ? fmax(m[k], r) : m[k] + r;
             }
         for (int k = 0; k < 5; ++k) {  // lambda = (C C^T)^{-1} C Qt
             double s = 0.0;
-            for (int c = 0; c < 5; ++c) s = fma(pc.ginv[k * 5 + c], m[c], s);
-            lam[k] = s;
+            for (int q = 0; q < 5; ++q) s = fma(pc.ginv[k * 5 + q], m[q], s);
+            lam[c * 8 + k] = s;
         }
-        if (maximag && live) maximag[cell] = m[5];
+        if (maximag && cl < ncells) maximag[cl] = m[5];
     }
     __syncthreads();
-    const double l0 = lam[0], l1 = lam[1], l2 = lam[2], l3 = lam[3], l4 = lam[4];
+    const double l0 = lam[sub * 8 + 0], l1 = lam[sub * 8 + 1], l2 = lam[sub * 8 + 2], l3 = lam[sub * 8 + 3],
+                 l4 = lam[sub * 8 + 4];
     bool bad = false;
     if constexpr (!FWD) {
-        // out = base + coef * (Qt - w C^T lambda) at nodes t + k N^2: i1 = k, (i2, i3) = (a, b)
+        // out = base + coef * (Qt - w C^T lambda) at nodes ln + k N^2: i1 = k, (i2, i3) = (a, b)
         const double cl23 = l0 + fv2 * l2 + fv3 * l3 + (fv2 * fv2 + fv3 * fv3) * l4;
         if (live) {
 #pragma unroll
@@ -214,7 +233,7 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
                 double v = coef * q;
                 if (base) v += bv[k];
                 bad |= !isfinite(v);
-                out[(size_t)cell * N3 + (size_t)k * NN + t] = v;
+                out[(size_t)cell * N3 + (size_t)k * NN + ln] = v;
             }
         }
         if (bad) atomicOr(flag, 2);
