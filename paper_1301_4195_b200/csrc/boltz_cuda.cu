@@ -130,6 +130,7 @@ struct boltz_ctx {
     bool timing = false;
     bool async_mode = false;  // device-pointer calls return without a sync (boltz_set_async)
     int schedule = 0;         // K2: 0 throughput, 1..4 latency (segmented rows), 5 cell (boltz_set_schedule)
+    int line_cpb = 2;         // cells per CTA of the line K1/K3 (1 inside the two-stream host pipeline)
     double2* dSeg = nullptr;  // latency schedule's segment partials
     int64_t seg_cap = 0;      // cells
     double2* dSeg2 = nullptr; // ... of the second workspace set (swap_workspace)
@@ -153,6 +154,17 @@ struct boltz_ctx {
 namespace {
 
 int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
+
+// the dynamic shared-memory opt-in of kernel `fn` on `device`, once per (kernel, device)
+void configure_smem(const void* fn, int device, int bytes) {
+    static std::mutex m;
+    static std::vector<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> g(m);
+    for (const auto& d : done)
+        if (d.first == fn && d.second == device) return;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.emplace_back(fn, device);
+}
 
 // frees a workspace buffer, or retires it while a captured graph may use it
 void release(boltz_ctx* c, void* p) {
@@ -998,6 +1010,24 @@ struct Launch {
     static constexpr int N3 = N * N * N;
     static dim3 pass_grid(int64_t ngroups) { return dim3((N * N + 7) / 8, (unsigned)ngroups); }
 
+#if BOLTZ_LINE
+    // a line kernel (line.cuh) with CPB = c->line_cpb cells per CTA: 2 for
+    // device-memory calls, 1 inside the two-stream host pipeline
+    template <typename K1, typename K2, typename... Args>
+    static void launch_line(boltz_ctx* c, K1 k1, K2 k2, int64_t nc, cudaStream_t s, Args... args) {
+        const int64_t ng = (nc + 31) / 32;
+        auto go = [&](auto kern, auto cpb) {
+            using LN = Line<N, decltype(cpb)::value>;
+            // keyed by the kernel itself: kernels of one signature share this lambda
+            configure_smem(reinterpret_cast<const void*>(kern), c->device, LN::SMEM);
+            kern<<<(unsigned)(ng * kLanes / LN::CPB), LN::THREADS, LN::SMEM, s>>>(args...);
+        };
+        if (c->line_cpb == 2) go(k2, std::integral_constant<int, 2>{});
+        else go(k1, std::integral_constant<int, 1>{});
+        CK(cudaGetLastError());
+    }
+#endif
+
     // user real f (device, nc cells) -> group complex fhat in c->dA
     static void forward(boltz_ctx* c, const double* f, int64_t nc, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
@@ -1007,13 +1037,8 @@ struct Launch {
 #if BOLTZ_LINE
         if constexpr (line_n(N)) {
           if ((reinterpret_cast<uintptr_t>(f) & 15) == 0) {
-            static PerDevice configured;  // attributes are per device
-            configured.once(c->device, [&] {
-                CK(cudaFuncSetAttribute(k_fwd_line<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Line<N>::SMEM));
-            });
             Timed t_(c, KIND_FFT, s);
-            k_fwd_line<N><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(f, c->dA, nc, scale, c->dFlag);
-            CK(cudaGetLastError());
+            launch_line(c, k_fwd_line<N, 1>, k_fwd_line<N, 2>, nc, s, f, c->dA, (long long)nc, scale, c->dFlag);
             return;
           }
         }
@@ -1247,19 +1272,12 @@ struct Launch {
                                 cudaStream_t s) {
 #if BOLTZ_LINE
         if constexpr (line_n(N)) {
-            const int64_t ng = (nc + 31) / 32;
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
-            static PerDevice configured;  // attributes are per device
-            configured.once(c->device, [&] {
-                CK(cudaFuncSetAttribute(k_inv_line<N, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Line<N>::SMEM));
-            });
             Timed t_(c, KIND_PROJECT, s);
-            k_inv_line<N, false><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(
-                c->dB, base, out, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
-                c->dFlag, nullptr, 0.0);
-            CK(cudaGetLastError());
+            launch_line(c, k_inv_line<N, false, 1>, k_inv_line<N, false, 2>, nc, s, (const double2*)c->dB, base, out,
+                        reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef, c->pc, c->dFlag,
+                        (double2*)nullptr, 0.0);
             return;
         }
 #endif
@@ -1292,20 +1310,13 @@ struct Launch {
 #if BOLTZ_LINE
         if constexpr (line_n(N)) {
           if ((reinterpret_cast<uintptr_t>(base) & 15) == 0) {
-            const int64_t ng = (nc + 31) / 32;
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
-            static PerDevice configured;  // attributes are per device
-            configured.once(c->device, [&] {
-                CK(cudaFuncSetAttribute(k_inv_line<N, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        Line<N>::SMEM));
-            });
             Timed t_(c, KIND_PROJECT, s);
-            k_inv_line<N, true><<<(unsigned)(ng * kLanes / Line<N>::CPB), Line<N>::THREADS, Line<N>::SMEM, s>>>(
-                c->dB, base, nullptr, reinterpret_cast<double*>(c->dMaxIm), nc, sz * sz * sz * par, coef, c->pc,
-                c->dFlag, c->dA, sv * sv * sv * par);
-            CK(cudaGetLastError());
+            launch_line(c, k_inv_line<N, true, 1>, k_inv_line<N, true, 2>, nc, s, (const double2*)c->dB, base,
+                        (double*)nullptr, reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef,
+                        c->pc, c->dFlag, c->dA, sv * sv * sv * par);
             return;
           }
         }
@@ -1533,6 +1544,14 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     bool two = nchunks > 1;
     if (const char* e = std::getenv("BOLTZ_HOST_STREAMS")) two = two && std::atoi(e) > 1;  // tuning / A-B
     if (two) ensure_workspace2(c);
+    // two compute streams: one-cell line K1/K3 CTAs, so that the other stream's
+    // K2 CTAs still fit beside them on an SM (restored on return)
+    struct CpbGuard {
+        boltz_ctx* c;
+        int old;
+        ~CpbGuard() { c->line_cpb = old; }
+    } cpb_guard{c, c->line_cpb};
+    if (two) c->line_cpb = 1;
     // pageable caller memory goes through the pinned bounce ring (host threads
     // copy; the DMA engines only ever see pinned memory)
     bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));

@@ -14,8 +14,9 @@
 // Thread t of the N^2 threads owns the lines (a, b) = (t / N, t % N) of every
 // pass: along i3 at (i1, i2) = (a, b), along i2 at (i1, i3) = (a, b), along i1 at
 // (i2, i3) = (a, b).  Moments are summed per thread over i1 (pass 3) and
-// reduced in a fixed order (shuffle tree, warps in order): deterministic and
-// independent of the batch.  Cells past ncells (the group's padding lanes)
+// reduced in a fixed order (a shuffle tree per 16 consecutive lines, then the
+// 16-line partials in line order): deterministic, independent of the batch and
+// of the cells-per-CTA variant.  Cells past ncells (the group's padding lanes)
 // read as zero.  HBM traffic per cell (N = 16): K1 32 KiB in + 64 KiB out;
 // K3 64 KiB + 32 KiB base in, 32 KiB (or, FWD, 64 KiB fhat) out.
 #pragma once
@@ -31,19 +32,20 @@ namespace boltz_gpu {
 // of every warp (lanes 0-15 and 16-31 take the same 16 lines of the two cells),
 // so that each group-layout access is a whole 32-byte sector (two 16-byte
 // lanes) instead of half of one
-#ifndef BOLTZ_LINE_CPB
-#define BOLTZ_LINE_CPB 2  // cfg2 RK2 step: K1 0.182 -> 0.168 ms, K3 0.523 -> 0.497 ms against one cell per CTA
-#endif
-constexpr int kLineCPB = BOLTZ_LINE_CPB;
-template <int N>
+// (the launcher picks: 2 for device-memory calls -- cfg2 RK2 step K1 0.182 ->
+// 0.168 ms, K3 0.523 -> 0.497 ms -- and 1 inside the two-stream host pipeline,
+// where the 141 KB two-cell CTA would keep the other stream's K2 off the SM:
+// e2e 657k against 661-670k evals/s with it)
+template <int N, int CPB_ = 1>
 struct Line {
     static constexpr int N3 = N * N * N;
-    static constexpr int CPB = kLineCPB;
+    static constexpr int CPB = CPB_;
     static constexpr int THREADS = N * N * CPB;
     static constexpr int WARPS = (THREADS + 31) / 32;
     static constexpr int ROW = N + 1;  // padded rows: the three passes are bank-conflict free
     static constexpr int CELL = N * N * ROW;
-    static constexpr int SMEM = CPB * CELL * 16 + WARPS * CPB * 6 * 8 + CPB * 8 * 8;  // cubes + reduction + lambda
+    static constexpr int HW = N * N / 16;  // 16-line groups per cell (the moments' reduction units)
+    static constexpr int SMEM = CPB * CELL * 16 + CPB * HW * 6 * 8 + CPB * 8 * 8;  // cubes + reduction + lambda
     __device__ static int at(int i1, int i2, int i3) { return (i1 * N + i2) * ROW + i3; }
     // thread t -> (cell of the CTA, line): with 2 cells the half-warps split by cell
     __device__ static int sub(int t) { return CPB == 2 ? (t >> 4) & 1 : 0; }
@@ -66,11 +68,11 @@ __device__ __forceinline__ void line_pass_axis1(double2* sm, int a, int b) {
 }
 
 // grid = cells / CPB (the groups' padding lanes included); block = CPB N^2 threads
-template <int N>
-__global__ void __launch_bounds__(Line<N>::THREADS, Line<N>::MINB)
+template <int N, int CPB>
+__global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
 k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
            int* __restrict__ flag) {
-    using LN = Line<N>;
+    using LN = Line<N, CPB>;
     constexpr int N3 = LN::N3;
     extern __shared__ __align__(16) double2 smem_line[];
     const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
@@ -117,17 +119,17 @@ k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncel
     }
 }
 
-template <int N, bool FWD>
-__global__ void __launch_bounds__(Line<N>::THREADS, Line<N>::MINB)
+template <int N, bool FWD, int CPB>
+__global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
 k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
            double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
            int* __restrict__ flag, double2* __restrict__ A_next, double fwd_scale) {
-    using LN = Line<N>;
-    constexpr int N3 = LN::N3, NN = N * N, CPB = LN::CPB;
+    using LN = Line<N, CPB>;
+    constexpr int N3 = LN::N3, NN = N * N;
     extern __shared__ __align__(16) double2 smem_line[];
-    double* red = reinterpret_cast<double*>(smem_line + CPB * LN::CELL);  // [warps][CPB][6]
-    double* lam = red + LN::WARPS * CPB * 6;                             // [CPB][8]
-    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N, wid = t >> 5;
+    double* red = reinterpret_cast<double*>(smem_line + CPB * LN::CELL);  // [CPB][HW][6]
+    double* lam = red + CPB * LN::HW * 6;                                // [CPB][8]
+    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
     double2* sm = smem_line + sub * LN::CELL;
     const long long cell = (long long)blockIdx.x * CPB + sub;
     const bool live = cell < ncells;
@@ -188,26 +190,27 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
     part[3] = fv3 * part[0];
     part[4] = fw23 * fma(fv2 * fv2 + fv3 * fv3, s0, s4);
     part[5] = mi * fabs(scale);
-    // shuffle tree over the lanes of this cell (a whole warp, or a half-warp with 2 cells)
-    constexpr int O0 = CPB == 2 ? 8 : 16, LANES = CPB == 2 ? 16 : 32;
+    // shuffle tree over each half-warp (16 consecutive lines of one cell), then
+    // the 16-line partials in line order: the same arithmetic for 1 and 2 cells
+    // per CTA, so both variants give bitwise the same cell
 #pragma unroll
     for (int k = 0; k < 6; ++k) {
         double v = part[k];
 #pragma unroll
-        for (int o = O0; o > 0; o >>= 1) {
+        for (int o = 8; o > 0; o >>= 1) {
             const double u = __shfl_xor_sync(0xffffffffu, v, o);
             v = (k == 5) ? fmax(v, u) : v + u;
         }
-        if ((t & (LANES - 1)) == 0) red[(wid * CPB + sub) * 6 + k] = v;
+        if ((ln & 15) == 0) red[(sub * LN::HW + (ln >> 4)) * 6 + k] = v;
     }
     __syncthreads();
     if (t < CPB) {
         const int c = t;
         const long long cl = (long long)blockIdx.x * CPB + c;
         double m[6] = {0, 0, 0, 0, 0, 0};
-        for (int w = 0; w < LN::WARPS; ++w)
+        for (int h = 0; h < LN::HW; ++h)
             for (int k = 0; k < 6; ++k) {
-                const double r = red[(w * CPB + c) * 6 + k];
+                const double r = red[(c * LN::HW + h) * 6 + k];
                 m[k] = (k == 5) ? fmax(m[k], r) : m[k] + r;
             }
         for (int k = 0; k < 5; ++k) {  // lambda = (C C^T)^{-1} C Qt
