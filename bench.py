@@ -420,7 +420,8 @@ def main():
         r_e2e = O.collision_rk2(N_VEL, L_VEL, G, snap["e2e"], DT, 1.0, nthreads=th)
 
         def rel(got, ref, before):
-            return max(float(np.abs(g - r).max() / np.abs(r - b).max()) for g, r, b in zip(got, ref, before))
+            return max(float(np.abs(g - r).max() / max(np.abs(r - b).max(), 1e-300))
+                       for g, r, b in zip(got, ref, before))
         parity = {"cells": wit, "reference": "oracle collision_rk2 (same host G), last timed step",
                   "max_rel_increment_n16_device": rel(dev_after, r_dev, snap["dev"]),
                   "max_rel_increment_n16_e2e": rel(ph[wit], r_e2e, snap["e2e"]),
@@ -502,7 +503,7 @@ def main():
 
 
 def rel_state(got, ref):
-    return max(float(np.abs(g - r).max() / np.abs(r).max()) for g, r in zip(got, ref))
+    return max(float(np.abs(g - r).max() / max(np.abs(r).max(), 1e-300)) for g, r in zip(got, ref))
 
 
 class _HostStagedHalo:
@@ -649,7 +650,7 @@ def bench_n32(args, dev, local, hw):
             "conv_ms_per_kernel": conv_avg, "conv_kernels_per_eval": kl["conv"] / (2 * steps),
             "table_generate_s": round(t_gen, 2),
             "parity": {"cells_n32": wit,
-                       "max_rel_increment_n32": max(float(np.abs(a - r).max() / np.abs(r - b).max())
+                       "max_rel_increment_n32": max(float(np.abs(a - r).max() / max(np.abs(r - b).max(), 1e-300))
                                                     for a, r, b in zip(after, ref, snap)),
                        "max_rel_state_n32": rel_state(after, ref)}}
 

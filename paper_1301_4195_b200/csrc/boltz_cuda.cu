@@ -1738,7 +1738,14 @@ int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, 
             ps.fail(e.msg);
         }
     };
-    std::thread tf(feeder), td(drainer);
+    std::thread tf(feeder), td;
+    try {
+        td = std::thread(drainer);
+    } catch (...) {  // the feeder is running: stop it before reporting
+        ps.fail("host pipeline: could not start the drainer thread");
+        tf.join();
+        throw;
+    }
     std::string err;
     try {
         for (int64_t i = 0; i < nchunks; ++i) {
