@@ -213,23 +213,53 @@ public:
     void transport_stage(int stage, double h, bool exchange = true) {
         const int wl = rank_ == 0 && left_.is_wall(), wr = rank_ == world_ - 1 && right_.is_wall();
         if (scheme_ == TransportScheme::SingleStage) {
-            fill_ghosts(exchange);
-            check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
-                                       dx_ext_.data(), h, wl, wr, s_));
+            refresh_and_step(tmp_.data(), nullptr, 0.0, h, wl, wr, exchange);
             field_.swap(tmp_);  // field = S(f)
             return;
         }
         if (stage == 0) {
-            fill_ghosts(exchange);
-            check(boltz_transport_step(op_.handle(), field_.data(), nullptr, 0.0, tmp_.data(), ncl_, x_ext_.data(),
-                                       dx_ext_.data(), h, wl, wr, s_));
+            refresh_and_step(tmp_.data(), nullptr, 0.0, h, wl, wr, exchange);
         } else {
             field_.swap(tmp_);  // field = t1, tmp = f^n
-            fill_ghosts(exchange);
-            check(boltz_transport_step(op_.handle(), field_.data(), tmp_.data(), 0.5, tmp2_.data(), ncl_,
-                                       x_ext_.data(), dx_ext_.data(), h, wl, wr, s_));
+            refresh_and_step(tmp2_.data(), tmp_.data(), 0.5, h, wl, wr, exchange);
             tmp2_.swap(field_);  // field = out, tmp2 = t1
         }
+    }
+
+    // Halo/compute overlap (the NCCL halo, >= 6 cells per rank): each transport
+    // stage runs the exchange on a side stream while the rows that read no ghost
+    // ([4, ncl)) are updated, then the four edge rows -- bitwise the plain stage
+    // (boltz_transport_step_range; paper_1301_4195_b200/solver.py overlap_halo).
+    void set_overlap_halo(bool on) {
+        overlap_ = on;
+        if (on && !side_) {
+            cuda_check(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            cuda_check(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+            cuda_check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        }
+    }
+
+    // ghost refresh of the field, then out = [alpha base + (1 - alpha)] S(field)
+    void refresh_and_step(double* out, const double* base, double alpha, double h, int wl, int wr, bool exchange) {
+        if (!(exchange && overlap_ && halo_ && ncl_ >= 6)) {
+            fill_ghosts(exchange);
+            check(boltz_transport_step(op_.handle(), field_.data(), base, alpha, out, ncl_, x_ext_.data(),
+                                       dx_ext_.data(), h, wl, wr, s_));
+            return;
+        }
+        cuda_check(cudaEventRecord(ev_fork_, s_));
+        cuda_check(cudaStreamWaitEvent(side_, ev_fork_, 0));
+        check(boltz_halo_exchange(halo_, field_.data(), ncl_, n3_, side_));
+        cuda_check(cudaEventRecord(ev_join_, side_));
+        fill_physical(field_.data());  // the physical ends' ghost rows: disjoint from the exchanged ones
+        auto rows = [&](int64_t b, int64_t e) {
+            check(boltz_transport_step_range(op_.handle(), field_.data(), base, alpha, out, ncl_, x_ext_.data(),
+                                             dx_ext_.data(), h, wl, wr, b, e, s_));
+        };
+        rows(4, ncl_);
+        cuda_check(cudaStreamWaitEvent(s_, ev_join_, 0));
+        rows(2, 4);
+        rows(ncl_, ncl_ + 2);
     }
 
     // field of the loopback driver's stage-1 exchange (t1 lives in tmp until the stage swaps it in)
@@ -358,6 +388,11 @@ public:
 
     ~Solver1D() {
         if (exec_) cudaGraphExecDestroy(exec_);
+        if (side_) {
+            cudaStreamDestroy(side_);
+            cudaEventDestroy(ev_fork_);
+            cudaEventDestroy(ev_join_);
+        }
     }
     Solver1D(const Solver1D&) = delete;
     Solver1D& operator=(const Solver1D&) = delete;
@@ -380,6 +415,9 @@ private:
     DeviceArray<double> x_ext_, dx_ext_, field_, tmp_, tmp2_, red_;
     cudaGraphExec_t exec_ = nullptr;
     double graph_dt_ = 0;
+    bool overlap_ = false;
+    cudaStream_t side_ = nullptr;
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
 };
 
 // One process driving the ranks of a sharded domain in lockstep -- several

@@ -8,6 +8,8 @@
 //     DIR/x.bin, DIR/dx.bin: Nx doubles; DIR/f0.bin: Nx x N^3 doubles
 //     MODE nccl:     one rank, an NCCL communicator of world 1 (exchange is
 //                    then a no-op; allreduce of the ledger is exercised)
+//     MODE nccl_overlap: the same with the halo/compute overlap (side stream,
+//                    split transport rows) and CUDA-graph replay
 //     MODE loopback: NRANKS virtual ranks of one device
 //     MODE peer:     NRANKS ranks of one device, each with its own context and
 //                    stream, halo fused into the transport kernels (PeerGroup)
@@ -53,15 +55,22 @@ int main(int argc, char** argv) {
         Boundary left{Boundary::Wall, Tw}, right{Boundary::Extrap, 1.0};
         std::vector<double> out(nx * n3);
         std::array<double, 3> led0{}, led1{};
-        if (mode == "nccl") {
+        if (mode == "nccl" || mode == "nccl_overlap") {
             unsigned char id[BOLTZ_HALO_ID_BYTES];
             check(boltz_halo_unique_id(id));
             boltz_halo* halo = nullptr;
             check(boltz_halo_create(0, 1, id, 0, &halo));
+            cudaStream_t st = nullptr;  // graph replay needs a non-default stream
+            if (mode == "nccl_overlap") cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
             {
-                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, halo, nullptr, scheme);
+                Solver1D s(op, n, L, x, dx, f0, 0, 1, left, right, 1.0, halo, st, scheme);
                 led0 = s.ledger();
-                for (int i = 0; i < steps; ++i) s.strang_step(dt);
+                if (mode == "nccl_overlap") {  // halo on a side stream beside the ghost-free rows, graph replay
+                    s.set_overlap_halo(true);
+                    s.run(dt, steps);
+                } else {
+                    for (int i = 0; i < steps; ++i) s.strang_step(dt);
+                }
                 led1 = s.ledger();
                 s.download(out);
                 // the ledger all-reduce of a world-1 communicator is the identity
@@ -70,6 +79,7 @@ int main(int argc, char** argv) {
                 check(boltz_halo_allreduce_sum(halo, buf.data(), 3, nullptr));
                 cuda_check(cudaDeviceSynchronize());
             }
+            if (st) cuda_check(cudaStreamDestroy(st));
             check(boltz_halo_destroy(halo));
         } else if (mode == "peer") {
             const auto plan = plan_decomposition((int64_t)nx, nranks);

@@ -68,7 +68,7 @@ def test_cpp_solver_matches_python_driver(gpu, tmp_path):
             s.strang_step(dt)
         ref = s.interior.cpu().numpy()
     torch.cuda.synchronize()
-    for mode, nranks in [("nccl", 1), ("loopback", 3), ("graph", 1), ("peer", 3), ("peer", 5)]:
+    for mode, nranks in [("nccl", 1), ("nccl_overlap", 1), ("loopback", 3), ("graph", 1), ("peer", 3), ("peer", 5)]:
         r = subprocess.run([str(EXE), str(tmp_path), str(n), repr(L), repr(lam), repr(Tw), repr(dt), str(steps),
                             str(nranks), mode], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
