@@ -560,3 +560,19 @@ def test_cell_schedule_vs_oracle(gpu, O, n, L):
     assert rel_max(qc[0], ref) < TOL_Q
     r2 = O.collision_rk2(n, L, G, f[:1], 0.01)
     assert rel_max(g[0] - f[0], r2[0] - f[0]) < 1e-9
+
+
+def test_n32_maxwell_molecules_kcsr_vs_oracle(gpu, O):
+    """N=32 with Maxwell molecules (lambda=0): the phased mirror schedule with
+    the Gauss-form chunk-0 kernels and the full-row REST launch (k_conv_kcsr),
+    host table, against the oracle on two cells of a 40-cell batch."""
+    n, L, lam = 32, 8.0, 0.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 40, seed=131)
+    G = table(n, L, lam)
+    with _op(n, L, lam) as op:
+        assert "kcsr" in op.conv_kernel()
+        q = op.collide(f)
+    for c in (3, 38):
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q[c], ref) < TOL_Q, c
