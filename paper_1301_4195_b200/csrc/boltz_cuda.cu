@@ -1502,12 +1502,13 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     // odd chunks run on a second stream, so each chunk's last wave overlaps the
     // next chunk's work.  With the mirror schedule, whose work items are row
     // pairs and which only pays from ~1.5k cells up, large middle chunks win:
-    // 1,2,5,5,2,1 (cfg2 e2e pinned / pageable, k evals/s: 657 / 607; 1,2,4,4,2,1
-    // 651 / 608; 0.5,1.5,4,4,1.5,0.5 656 / 603; 1,3,5,5,3,1 644 / 582; 1,3,3,1
-    // 627-641 / -; the pageable bounce path needs the small edge chunks); the
-    // plain schedule prefers 2,6,8,8,6,2 (602k).  BOLTZ_HOST_CHUNKS="a,b,..." overrides.
-    std::vector<double> w =
-        c->mirror ? std::vector<double>{1, 2, 5, 5, 2, 1} : std::vector<double>{2, 6, 8, 8, 6, 2};
+    // 1,2,3,5,5,3,2,1 (cfg2 e2e pinned / pageable, k evals/s, two runs: 671.7 /
+    // 618.5; 1,2,5,5,2,1 669.9 / 612.8; 1,2,4,4,2,1 668.4 / 618.6; 1,2,6,6,2,1
+    // 666.0 / 605.8; 0.5,1.5,5,5,1.5,0.5 660.3 / 586; round 1's 1,3,3,1 627-641;
+    // the pageable bounce path needs the small edge chunks); the plain schedule
+    // prefers 2,6,8,8,6,2 (602k).  BOLTZ_HOST_CHUNKS="a,b,..." overrides.
+    std::vector<double> w = c->mirror ? std::vector<double>{1, 2, 3, 5, 5, 3, 2, 1}
+                                      : std::vector<double>{2, 6, 8, 8, 6, 2};
     if (const char* sched = std::getenv("BOLTZ_HOST_CHUNKS")) {
         w.clear();
         for (const char* p = sched; *p;) {

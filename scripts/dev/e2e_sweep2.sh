@@ -1,0 +1,6 @@
+# e2e pinned / pageable across host chunk schedules and staging slots (current build)
+run() { env "$@" python bench.py --steps 20 --warmup 5 --no-n32 --no-cfg3 --no-cpu-baseline 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print('$*',round(d['value']),round(d['e2e']['value']),round(d['e2e_pageable']['value']))"; }
+for r in 1 2; do
+for ch in 1,2,5,5,2,1 1,2,4,4,2,1 1,2,6,6,2,1 1,2,3,5,5,3,2,1 0.5,1.5,5,5,1.5,0.5; do run BOLTZ_HOST_CHUNKS=$ch; done
+run BOLTZ_STAGE_SLOTS=4
+done
