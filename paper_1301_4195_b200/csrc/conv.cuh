@@ -22,13 +22,23 @@
 //    (SPEC.md:233); results are independent of batch composition.
 //
 // Kernels (per-N choice by measurement, see conv_kernel_for):
-//  k_conv_pipe  N <= 16: per-warp cp.async ring -- the next row pair's x row,
-//               y row and H slab stream into shared memory while the current
-//               one computes.
+//  evaluate_qhat (any fhat) -- the plain pair-symmetric fold:
+//  k_conv_pipe  N <= 16: per-warp TMA ring -- the next row pair's x row, y row
+//               and H slab stream into shared memory while the current one
+//               computes.
 //  k_conv_kcs   N = 24, 32: one kernel per k-chunk (halves the unrolled code);
 //               y row and H slab staged one row ahead (H is DRAM-resident at
 //               N=32), x read from L2.
 //  k_conv       no staging, direct loads: the plain statement of the order.
+//  collide / RK2 (fhat of a real f) -- the Hermitian mirror schedule:
+//  k_conv_mirror2  N = 8..16 (default): row-pair items, REST and the partner
+//               row's REST' accumulated in TMEM; k_conv_mirror without TMEM.
+//  k_conv_kcsm  N = 24, 32: phases per k-chunk (A of the pair leaders; FULL;
+//               REST at N = 24), the chunk-0 kernels at N = 32 in the Gauss
+//               5-instruction term form; k_conv_kcsr: N = 32's REST entries for
+//               both k-chunks in one launch.
+//  small batches: k_conv_seg (+ reduce; rows split over warps) and k_conv_cell
+//               (lane = output k3, one or a few cells).
 #pragma once
 #include "common.cuh"
 
