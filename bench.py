@@ -437,6 +437,13 @@ def main():
             cfg3 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
             op.set_schedule("throughput")
 
+    cfg1 = None
+    if rank == 0 and not args.no_cfg3:
+        try:
+            cfg1 = bench_cfg1(op, dev)
+        except Exception as exc:  # noqa: BLE001
+            cfg1 = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     n32 = None
     if not args.no_n32 and rank == 0:
         op.close()
@@ -495,6 +502,8 @@ def main():
             line["n32"] = n32
         if cfg3:
             line["cfg3"] = cfg3
+        if cfg1:
+            line["cfg1"] = cfg1
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
@@ -602,6 +611,46 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
             out["steps_compared"] = done
     op.set_schedule("throughput")
     return out
+
+
+def bench_cfg1(op, dev, steps=50):
+    """cfg1 (BASELINE.json configs[0]): one cell, N=16, the two-Maxwellian
+    state with noise, 50 RK2 steps of dt = 0.01 -- K2 in the cell schedule
+    (lane = output k3), one RK2 step captured in a CUDA graph and replayed."""
+    import torch
+    from paper_1301_4195_b200 import scenarios
+    f0 = scenarios.config1_initial(op.grid)
+    f = torch.from_numpy(f0.reshape(1, -1).copy()).to(dev)
+    op.set_schedule("cell")
+    try:
+        op.collision_rk2(f, 0.01)  # warm-up: workspace, attributes
+        op.set_async(True)
+        st = torch.cuda.Stream(dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(g, stream=st):
+                op.collision_rk2(f, 0.01)
+        torch.cuda.current_stream(dev).wait_stream(st)
+        for _ in range(3):
+            g.replay()
+        op.sync()
+        f.copy_(torch.from_numpy(f0.reshape(1, -1)).to(dev))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            g.replay()
+        e1.record()
+        op.sync()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    finally:
+        op.set_async(False)
+        op.set_schedule("throughput")
+    return {"workload": "cfg1: one cell, N=16^3 on [-6,6]^3, hard spheres, 50 RK2 steps of dt=0.01",
+            "steps": steps, "ms": ms, "evals_per_s": 2 * steps / (ms * 1e-3),
+            "mode": "K2 cell schedule (lane = output k3), CUDA graph of one RK2 step replayed"}
 
 
 def bench_n32(args, dev, local, hw):
