@@ -987,6 +987,18 @@ void host_copy(void* dst, const void* src, size_t bytes) {
     }
 }
 
+// the second workspace set for one chunk's enqueue, swapped back even if it throws
+struct WorkspaceSwap {
+    boltz_ctx* c;
+    bool on;
+    WorkspaceSwap(boltz_ctx* c_, bool on_) : c(c_), on(on_) {
+        if (on) swap_workspace(c);
+    }
+    ~WorkspaceSwap() {
+        if (on) swap_workspace(c);
+    }
+};
+
 void ensure_staging(boltz_ctx* c, int64_t cells) {
     if (cells <= c->stage_cap) return;
     const int64_t n3 = n3_of(c);
@@ -1585,11 +1597,12 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         cudaStream_t cs = odd ? c->comp2 : s;
         CK(cudaStreamWaitEvent(cs, c->ev_h2d[slot], 0));
         if (i >= K) CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));  // chunk i-K's output left the slot
-        if (odd) swap_workspace(c);
-        fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
-        CK(cudaEventRecord(c->ev_comp[slot], cs));
-        if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
-        if (odd) swap_workspace(c);
+        {
+            WorkspaceSwap ws(c, odd);
+            fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
+            CK(cudaEventRecord(c->ev_comp[slot], cs));
+            if (max_imag) CK(cudaMemcpyAsync(max_imag + c0, c->dMaxIm, (size_t)nc * 8, cudaMemcpyDeviceToHost, cs));
+        }
         if (i + 1 < nchunks) h2d(i + 1);
         CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_comp[slot], 0));
         CK(cudaMemcpyAsync(out + c0 * out_elems, c->dStageOut[slot], (size_t)nc * out_elems * 8,
@@ -1761,13 +1774,14 @@ int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, 
                 CK(cudaStreamWaitEvent(cs, c->ev_d2h[slot], 0));
                 if (bounce_out && max_imag) ps.wait(&PipeSync::drained, i - K + 1);  // pinned max|Im| slot read
             }
-            if (odd) swap_workspace(c);
-            fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
-            if (max_imag)
-                CK(cudaMemcpyAsync(bounce_out ? c->hBounceMi[slot] : max_imag + c0, c->dMaxIm, (size_t)nc * 8,
-                                   cudaMemcpyDeviceToHost, cs));
-            CK(cudaEventRecord(c->ev_comp[slot], cs));
-            if (odd) swap_workspace(c);
+            {
+                WorkspaceSwap ws(c, odd);
+                fn(c->dStageIn[slot], c->dStageOut[slot], nc, cs);
+                if (max_imag)
+                    CK(cudaMemcpyAsync(bounce_out ? c->hBounceMi[slot] : max_imag + c0, c->dMaxIm, (size_t)nc * 8,
+                                       cudaMemcpyDeviceToHost, cs));
+                CK(cudaEventRecord(c->ev_comp[slot], cs));
+            }
             ps.bump(&PipeSync::comp);
         }
     } catch (const CudaError& e) {
