@@ -576,3 +576,24 @@ def test_n32_maxwell_molecules_kcsr_vs_oracle(gpu, O):
     for c in (3, 38):
         ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
         assert rel_max(q[c], ref) < TOL_Q, c
+
+
+def test_host_pipeline_mixed_pinned_pageable(gpu):
+    """The bounce ring per direction: pinned input with pageable output (and
+    max|Im|), pageable input with a pinned output, all bitwise the device call."""
+    import torch
+    n, L, cells = 16, 6.0, 3000
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=171)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        qd, mid = op.collide(torch.from_numpy(f).to(gpu), with_max_imag=True)
+        qd, mid = qd.cpu().numpy(), mid.cpu().numpy()
+        fin = torch.from_numpy(f.copy()).pin_memory().numpy()
+        q1, m1 = op.collide(fin, with_max_imag=True)          # pinned in, pageable out
+        assert np.array_equal(q1, qd) and np.array_equal(m1, mid)
+        from paper_1301_4195_b200.boltz import MEM_HOST, _check, lib
+        qout = torch.empty((cells, n ** 3), dtype=torch.float64).pin_memory()
+        mout = torch.empty(cells, dtype=torch.float64).pin_memory()
+        _check(lib().boltz_collide_batch(op._h, f.ctypes.data, qout.data_ptr(), cells, 1.0, mout.data_ptr(),
+                                         MEM_HOST, None))                     # pageable in, pinned out
+        assert np.array_equal(qout.numpy(), qd) and np.array_equal(mout.numpy(), mid)
