@@ -668,13 +668,11 @@ void layout_terms_kcsm(int n, TableLayout& T) {
     int off = 0;
     for (int ty = 0; ty < kBandTypes; ++ty) {
         if (ty == BT_REST && kcsr_n(n)) {
-            // k_conv_kcsr: the whole row's REST terms, diagonal-major, one slab
+            // k_conv_kcsr: the whole row's REST terms in one slab, in the kernel's
+            // visiting order (its compile-time table; kcsr_n(n) implies n == 32)
             std::vector<short2> v(kcsr_slab(n), make_short2(-1, -1));
-            int pos = 0;
-            for (int part = 0; part < 3; ++part)  // k_conv_kcsr's visiting order
-                for (int m3 = 0; m3 < n; ++m3)
-                    for (int k3 = 0; k3 < n; ++k3)
-                        if (kcsr_part(n, part, k3, m3)) v[pos++] = make_short2((short)k3, (short)m3);
+            static constexpr KcsrTab<32> tab{};
+            for (int i = 0; i < tab.COUNT; ++i) v[i] = make_short2(tab.k3[i], tab.m3[i]);
             T.ts.off[ty] = off;
             T.ts.slab[ty] = (int)v.size();
             T.ts.slab_max = std::max(T.ts.slab_max, (int)v.size());

@@ -1592,58 +1592,98 @@ __host__ __device__ constexpr bool kcsr_n(int n) { return BOLTZ_KCSR && n == 32 
 #define BOLTZ_KCSR_WARPS 2
 #endif
 constexpr int kKcsrWarps = BOLTZ_KCSR_WARPS;
+// term order: see KcsrTab
+#ifndef BOLTZ_KCSR_ORDER
+#define BOLTZ_KCSR_ORDER 2
+#endif
 template <int N>
 struct KcsrLayout {
     static constexpr int Y_BYTES = N * kLanes * 16;
     static constexpr int H_BYTES = kcsr_slab(N) * 8;
-    static constexpr int WARP_BYTES = BOLTZ_KCSR_YBUF * Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+    // ORDER 2: the edge diagonals' x (m3 = 0, 1, N-1) are staged with the y row
+    static constexpr int XE_BYTES = (BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF == 2) ? 3 * kLanes * 16 : 0;
+    static constexpr int WARP_BYTES = BOLTZ_KCSR_YBUF * (Y_BYTES + XE_BYTES) + 2 * H_BYTES + 16;  // + 2 mbarriers
 };
 #ifndef BOLTZ_KCSR_MINB
 #define BOLTZ_KCSR_MINB 2
 #endif
 
-// the kcsr term list as a compile-time table: term I = (k3, m3), parts in order
+// the kcsr term list as a compile-time table, in the kernel's visiting order.
+// Per term: where x comes from (xsrc 0/1/2: the edge diagonals m3 = 0, 1, N-1
+// held in registers for the whole entry; 3: xm, loaded when xload) and where y
+// comes from (ysrc 0/1/2: y[0], y[1], y[N-1] in registers; 3: yc, loaded from
+// the staged row when yload).
+//   BOLTZ_KCSR_ORDER 1: diagonal-major by part (x per diagonal, y per term)
+//   BOLTZ_KCSR_ORDER 2: s3-major over the edge diagonals, so that one staged
+//     y[s3] feeds every edge term on it and the k3 = 0 term that needs it,
+//     whose diagonal's other terms follow (y from registers); then the
+//     remaining interior diagonals.  45 -> 32 y loads + 3, against 109.
 template <int N>
 struct KcsrTab {
     static constexpr int cnt() {
         int c = 0;
-        for (int part = 0; part < 3; ++part)
-            for (int m3 = 0; m3 < N; ++m3)
-                for (int k3 = 0; k3 < N; ++k3) c += kcsr_part(N, part, k3, m3) ? 1 : 0;
+        for (int m3 = 0; m3 < N; ++m3)
+            for (int k3 = 0; k3 < N; ++k3) c += kcsr_term(N, k3, m3) ? 1 : 0;
         return c;
     }
     static constexpr int COUNT = cnt();
+    static constexpr int yreg(int s3) { return s3 == 0 ? 0 : s3 == 1 ? 1 : s3 == N - 1 ? 2 : 3; }
+    static constexpr int xreg(int m3) { return m3 == 0 ? 0 : m3 == 1 ? 1 : m3 == N - 1 ? 2 : 3; }
     short k3[COUNT] = {}, m3[COUNT] = {}, part[COUNT] = {};
-    bool dstart[COUNT] = {};  // term I opens a diagonal (a new x value)
-    short xnext[COUNT] = {};  // at a diagonal start: m3 of the next diagonal (-1: none)
+    signed char xsrc[COUNT] = {}, ysrc[COUNT] = {};
+    bool xload[COUNT] = {}, yload[COUNT] = {};
+    bool done[N * N] = {};
+    int c = 0;
+    constexpr void emit(int k, int m, int pt) {
+        k3[c] = (short)k;
+        m3[c] = (short)m;
+        part[c] = (short)pt;
+        done[m * N + k] = true;
+        ++c;
+    }
     constexpr KcsrTab() {
-        int c = 0;
-        for (int pt = 0; pt < 3; ++pt)
+        if (BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF == 2) {
+            const int edges[3] = {0, 1, N - 1};
+            for (int s = 0; s < N; ++s) {
+                for (int e = 0; e < 3; ++e) {
+                    const int m = edges[e], k = s + m - N / 2;
+                    if (k >= 0 && k < N && kcsr_term(N, k, m)) emit(k, m, 2);
+                }
+                if (yreg(s) != 3) continue;
+                for (int m = 2; m <= N - 2; ++m) {  // interior terms on this staged y[s]
+                    const int k = s + m - N / 2;
+                    if (k < 0 || k >= N || !kcsr_term(N, k, m) || done[m * N + k]) continue;
+                    emit(k, m, 2);
+                    for (int k2 = 0; k2 < N; ++k2)  // the rest of diagonal m: y from registers
+                        if (kcsr_term(N, k2, m) && !done[m * N + k2] && yreg(k2 - m + N / 2) != 3) emit(k2, m, 2);
+                }
+            }
             for (int m = 0; m < N; ++m)
                 for (int k = 0; k < N; ++k)
-                    if (kcsr_part(N, pt, k, m)) {
-                        k3[c] = (short)k;
-                        m3[c] = (short)m;
-                        part[c] = (short)pt;
-                        ++c;
-                    }
-        for (int i = 0; i < COUNT; ++i) dstart[i] = i == 0 || m3[i - 1] != m3[i] || part[i - 1] != part[i];
+                    if (kcsr_term(N, k, m) && !done[m * N + k]) emit(k, m, 2);
+        } else {
+            for (int pt = 0; pt < 3; ++pt)
+                for (int m = 0; m < N; ++m)
+                    for (int k = 0; k < N; ++k)
+                        if (kcsr_part(N, pt, k, m)) emit(k, m, pt);
+        }
+        const bool regs = BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF == 2;
+        int xm = -1, yc = -1;
         for (int i = 0; i < COUNT; ++i) {
-            xnext[i] = -1;
-            if (!dstart[i]) continue;
-            for (int j = i + 1; j < COUNT; ++j)
-                if (dstart[j]) {
-                    xnext[i] = m3[j];
-                    break;
-                }
+            const int s = k3[i] - m3[i] + N / 2;
+            xsrc[i] = (signed char)(regs ? xreg(m3[i]) : 3);
+            ysrc[i] = (signed char)(regs || part[i] == 2 ? yreg(s) : 3);
+            xload[i] = xsrc[i] == 3 && m3[i] != xm;
+            if (xload[i]) xm = m3[i];
+            yload[i] = ysrc[i] == 3 && (!regs || s != yc);
+            if (yload[i]) yc = s;
         }
     }
 };
-
-// one kcsr entry's terms, unrolled from the compile-time table (x loaded when
-// the diagonal changes; y from smem in parts 0 and 1, from registers in part 2)
+// ORDER 1 loads x when the diagonal changes and y per term from the staged row
+// in parts 0 and 1 (from registers in part 2); ORDER 2 as the table says.
 #ifndef BOLTZ_KCSR_XPF
-#define BOLTZ_KCSR_XPF 0  // measured: 314 against 305 ms per N=32 RK2 step (255 registers, 40 B spilled)
+#define BOLTZ_KCSR_XPF 0  // (removed) x one diagonal ahead: 314 against 305 ms per N=32 RK2 step, spills
 #endif
 template <int N>
 struct KcsrEntry {
@@ -1652,29 +1692,20 @@ struct KcsrEntry {
     const double2* ys;
     const double2* hs;
     int lane;
-    double2 xm, xn, hb, y0, y1, yl;
+    double2 xm, yc, hb, xa, xb, xc, y0, y1, yl;
     template <int I>
     __device__ __forceinline__ void step() {
         constexpr KcsrTab<N> tab{};
-        constexpr int k3 = tab.k3[I], m3 = tab.m3[I], part = tab.part[I], s3 = k3 - m3 + N / 2;
-        if constexpr (tab.dstart[I]) {
-            // x one diagonal ahead (BOLTZ_KCSR_XPF): the load of the next diagonal's x
-            // is in flight while this diagonal's terms run
-            if constexpr (BOLTZ_KCSR_XPF) {
-                if constexpr (I == 0) xm = ldg2(X + (size_t)m3 * kLanes);
-                else xm = xn;
-                if constexpr (tab.xnext[I] >= 0) xn = ldg2(X + (size_t)tab.xnext[I] * kLanes);
-            } else {
-                xm = ldg2(X + (size_t)m3 * kLanes);
-            }
-        }
+        constexpr int k3 = tab.k3[I], m3 = tab.m3[I], s3 = k3 - m3 + N / 2;
+        constexpr int xs = tab.xsrc[I], ysr = tab.ysrc[I];
+        if constexpr (tab.xload[I]) xm = ldg2(X + (size_t)m3 * kLanes);
+        if constexpr (tab.yload[I]) yc = ys[s3 * kLanes + lane];
         if constexpr ((I & 1) == 0) hb = hs[I >> 1];
         const double h = (I & 1) ? hb.y : hb.x;
-        double2 yv;
-        if constexpr (part < 2) yv = ys[s3 * kLanes + lane];
-        else yv = s3 == 0 ? y0 : s3 == 1 ? y1 : yl;
-        const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
-        const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+        const double2 xv = xs == 0 ? xa : xs == 1 ? xb : xs == 2 ? xc : xm;
+        const double2 yv = ysr == 0 ? y0 : ysr == 1 ? y1 : ysr == 2 ? yl : yc;
+        const double tr = fma(xv.x, yv.x, -xv.y * yv.y);
+        const double ti = fma(xv.x, yv.y, xv.y * yv.x);
         acc[k3].x = fma(h, tr, acc[k3].x);
         acc[k3].y = fma(h, ti, acc[k3].y);
     }
@@ -1715,9 +1746,9 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
     const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
     char* wsm = smem + wid * LY::WARP_BYTES;
     const double2* ys0 = reinterpret_cast<const double2*>(wsm);
-    char* hbase = wsm + BOLTZ_KCSR_YBUF * LY::Y_BYTES;
-    unsigned long long* bar =
-        reinterpret_cast<unsigned long long*>(wsm + BOLTZ_KCSR_YBUF * LY::Y_BYTES + 2 * LY::H_BYTES);
+    char* xebase = wsm + BOLTZ_KCSR_YBUF * LY::Y_BYTES;
+    char* hbase = xebase + BOLTZ_KCSR_YBUF * LY::XE_BYTES;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(hbase + 2 * LY::H_BYTES);
     const double2* Abase = A + (size_t)g * N3 * kLanes;
     const double2* Ag = Abase + lane;
     double2* Brow = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
@@ -1734,10 +1765,28 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
     auto tma_y = [&](int slot, int4 en) {
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(bar + slot, LY::Y_BYTES);
+            mbar_expect_tx(bar + slot, LY::Y_BYTES + LY::XE_BYTES);
             bulk_g2s(const_cast<double2*>(ys0) + (BOLTZ_KCSR_YBUF == 2 ? slot * N * kLanes : 0),
                      Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+            if constexpr (LY::XE_BYTES > 0) {
+                char* xe = xebase + slot * LY::XE_BYTES;
+                bulk_g2s(xe, Abase + (size_t)en.x * kLanes, 2 * kLanes * 16, bar + slot);
+                bulk_g2s(xe + 2 * kLanes * 16, Abase + (size_t)(en.x + N - 1) * kLanes, kLanes * 16, bar + slot);
+            }
         }
+    };
+    // the entry list through a 32-entry window, lane j holding entry wb + j: an
+    // entry is one shuffle away instead of a dependent L2 load per entry
+    int wb = e0;
+    int4 win = e0 + lane < e1 ? __ldg(ent + e0 + lane) : make_int4(0, 0, 0, 0);
+    auto entry = [&](int e) {
+        if (e - wb >= 32) {
+            wb += 32;
+            win = wb + lane < e1 ? __ldg(ent + wb + lane) : make_int4(0, 0, 0, 0);
+        }
+        const int j = e - wb;
+        return make_int4(__shfl_sync(0xffffffffu, win.x, j), __shfl_sync(0xffffffffu, win.y, j),
+                         __shfl_sync(0xffffffffu, win.z, j), __shfl_sync(0xffffffffu, win.w, j));
     };
     if (e0 < e1) {
         if (lane == 0) {
@@ -1746,22 +1795,29 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
-        int4 en = __ldg(ent + e0);
-        int4 en_ahead = e0 + 1 < e1 ? __ldg(ent + e0 + 1) : en;
+        int4 en = entry(e0);
         tma_y(0, en);
         tma_h(0, en);
         mbar_wait(bar, 0);
         for (int e = e0; e < e1; ++e) {
             const int i = e - e0, cur = i & 1;
             const bool more = e + 1 < e1;
-            const int4 nx = en_ahead;
-            if (e + 2 < e1) en_ahead = __ldg(ent + e + 2);
+            const int4 nx = more ? entry(e + 1) : en;
             __syncwarp();  // every lane finished reading H[cur^1] (and y[cur^1])
             if (more) tma_h(cur ^ 1, nx);
             const double2* ys = ys0 + (BOLTZ_KCSR_YBUF == 2 ? cur * N * kLanes : 0);
             if (BOLTZ_KCSR_YBUF == 2 && more) tma_y(cur ^ 1, nx);
             KcsrEntry<N> f{acc, Ag + (size_t)en.x * kLanes, ys,
                            reinterpret_cast<const double2*>(hbase + cur * LY::H_BYTES), lane};
+            if constexpr (LY::XE_BYTES > 0) {
+                const double2* xe = reinterpret_cast<const double2*>(xebase + cur * LY::XE_BYTES);
+                f.xa = xe[lane];
+                f.xb = xe[kLanes + lane];
+                f.xc = xe[2 * kLanes + lane];
+                f.y0 = ys[lane];
+                f.y1 = ys[kLanes + lane];
+                f.yl = ys[(N - 1) * kLanes + lane];
+            }
             KcsrRun<0, P2>::run(f);  // parts 0 and 1: y from the staged row
             if constexpr (BOLTZ_KCSR_YBUF == 1 || BOLTZ_KCSR_YREG) {
                 f.y0 = ys[lane];

@@ -25,6 +25,7 @@ V = {
     "w2": ["BOLTZ_CONV_WARPS=2"],
     "t24_12": ["BOLTZ_TILE24=12"],
     "w8": ["BOLTZ_CONV_WARPS=8"],
+    "ord1": ["BOLTZ_KCSR_ORDER=1"],  # k_conv_kcsr diagonal-major (round-2 order)
     "rest2": ["BOLTZ_KCSM_REST_MINB=2"],  # N <= 16 on k_conv_kcs / the phased k_conv_kcsm mirror
 }
 root = pathlib.Path(__file__).resolve().parents[2] / "variants"
