@@ -131,6 +131,7 @@ struct boltz_ctx {
     bool async_mode = false;  // device-pointer calls return without a sync (boltz_set_async)
     int schedule = 0;         // K2: 0 throughput, 1..4 latency (segmented rows), 5 cell (boltz_set_schedule)
     int line_cpb = 2;         // cells per CTA of the line K1/K3 (1 inside the two-stream host pipeline)
+    int num_sms = 148;        // of the context's device (grid-stride kernels)
     double2* dSeg = nullptr;  // latency schedule's segment partials
     int64_t seg_cap = 0;      // cells
     double2* dSeg2 = nullptr; // ... of the second workspace set (swap_workspace)
@@ -156,6 +157,33 @@ namespace {
 int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
 
 // the dynamic shared-memory opt-in of kernel `fn` on `device`, once per (kernel, device)
+// the group array X[g][idx][lane] (double2) as a 2D TMA tensor of doubles
+// {2 kLanes, groups N^3}, rows 512 bytes apart; box = one i1 plane (N^2 rows)
+// of cpb adjacent cells (line.cuh k_fwd_line_tma)
+CUtensorMap make_group_tmap(void* X, int64_t ngroups, int n3, int cpb) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError{"cuTensorMapEncodeTiled unavailable"};
+        return reinterpret_cast<Encode>(fn);
+    }();
+    const int nn = (int)std::lround(std::cbrt((double)n3)) * (int)std::lround(std::cbrt((double)n3));
+    CUtensorMap m;
+    const cuuint64_t dim[2] = {2 * kLanes, (cuuint64_t)ngroups * n3};
+    const cuuint64_t stride[1] = {2 * kLanes * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * cpb), (cuuint32_t)nn};
+    const cuuint32_t estride[2] = {1, 1};
+    const CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, X, dim, stride, box, estride,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+    return m;
+}
+
 void configure_smem(const void* fn, int device, int bytes) {
     static std::mutex m;
     static std::vector<std::pair<const void*, int>> done;
@@ -1023,14 +1051,21 @@ struct Launch {
 #if BOLTZ_LINE
     // a line kernel (line.cuh) with CPB = c->line_cpb cells per CTA: 2 for
     // device-memory calls, 1 inside the two-stream host pipeline
+    // persist: a grid-stride kernel (k_fwd_line), launched as the CTAs that are resident at once
     template <typename K1, typename K2, typename... Args>
-    static void launch_line(boltz_ctx* c, K1 k1, K2 k2, int64_t nc, cudaStream_t s, Args... args) {
+    static void launch_line(boltz_ctx* c, bool persist, K1 k1, K2 k2, int64_t nc, cudaStream_t s, Args... args) {
         const int64_t ng = (nc + 31) / 32;
         auto go = [&](auto kern, auto cpb) {
             using LN = Line<N, decltype(cpb)::value>;
             // keyed by the kernel itself: kernels of one signature share this lambda
             configure_smem(reinterpret_cast<const void*>(kern), c->device, LN::SMEM);
-            kern<<<(unsigned)(ng * kLanes / LN::CPB), LN::THREADS, LN::SMEM, s>>>(args...);
+            int64_t grid = ng * kLanes / LN::CPB;
+            if (persist) {
+                int per_sm = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LN::THREADS, LN::SMEM));
+                grid = std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * c->num_sms);
+            }
+            kern<<<(unsigned)grid, LN::THREADS, LN::SMEM, s>>>(args...);
         };
         if (c->line_cpb == 2) go(k2, std::integral_constant<int, 2>{});
         else go(k1, std::integral_constant<int, 1>{});
@@ -1048,7 +1083,14 @@ struct Launch {
         if constexpr (line_n(N)) {
           if ((reinterpret_cast<uintptr_t>(f) & 15) == 0) {
             Timed t_(c, KIND_FFT, s);
-            launch_line(c, k_fwd_line<N, 1>, k_fwd_line<N, 2>, nc, s, f, c->dA, (long long)nc, scale, c->dFlag);
+            if (BOLTZ_LINE_TMA) {
+                const CUtensorMap tm = make_group_tmap(c->dA, (nc + 31) / 32, N3, c->line_cpb);
+                launch_line(c, true, k_fwd_line_tma<N, 1>, k_fwd_line_tma<N, 2>, nc, s, f, tm, (long long)nc, scale,
+                            c->dFlag);
+            } else {
+                launch_line(c, BOLTZ_LINE_PERSIST != 0, k_fwd_line<N, 1>, k_fwd_line<N, 2>, nc, s, f, c->dA,
+                            (long long)nc, scale, c->dFlag);
+            }
             return;
           }
         }
@@ -1285,9 +1327,9 @@ struct Launch {
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
             Timed t_(c, KIND_PROJECT, s);
-            launch_line(c, k_inv_line<N, false, 1>, k_inv_line<N, false, 2>, nc, s, (const double2*)c->dB, base, out,
+            launch_line(c, false, k_inv_line<N, false, 1>, k_inv_line<N, false, 2>, nc, s, (const double2*)c->dB, base, out,
                         reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef, c->pc, c->dFlag,
-                        (double2*)nullptr, 0.0);
+                        (double2*)nullptr, CUtensorMap{}, 0.0);
             return;
         }
 #endif
@@ -1324,9 +1366,11 @@ struct Launch {
             const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
             Timed t_(c, KIND_PROJECT, s);
-            launch_line(c, k_inv_line<N, true, 1>, k_inv_line<N, true, 2>, nc, s, (const double2*)c->dB, base,
+            launch_line(c, false, k_inv_line<N, true, 1>, k_inv_line<N, true, 2>, nc, s, (const double2*)c->dB, base,
                         (double*)nullptr, reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef,
-                        c->pc, c->dFlag, c->dA, sv * sv * sv * par);
+                        c->pc, c->dFlag, c->dA,
+                        BOLTZ_LINE_TMA ? make_group_tmap(c->dA, (nc + 31) / 32, N3, c->line_cpb) : CUtensorMap{},
+                        sv * sv * sv * par);
             return;
           }
         }
@@ -1935,6 +1979,7 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
         c->stage_slots = std::min(boltz_ctx::kMaxStageSlots, std::max(2, std::atoi(e)));
     try {
         CK(cudaSetDevice(device));
+        CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         CK(cudaMalloc(&c->dFlag, sizeof(int)));
         CK(cudaMemset(c->dFlag, 0, sizeof(int)));
         CK(cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));

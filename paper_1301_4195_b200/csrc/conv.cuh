@@ -1736,7 +1736,8 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
     using LY = KcsrLayout<N>;
     constexpr int N3 = N * N * N;
     constexpr unsigned HB = LY::H_BYTES;
-    constexpr int P2 = kcsr_part_begin<N>(2), PE = KcsrTab<N>::COUNT;
+    constexpr int P2 = kcsr_part_begin<N>(2);
+    [[maybe_unused]] constexpr int PE = KcsrTab<N>::COUNT;
     extern __shared__ __align__(16) char smem[];
     const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

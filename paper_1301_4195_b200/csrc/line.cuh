@@ -20,6 +20,7 @@
 // read as zero.  HBM traffic per cell (N = 16): K1 32 KiB in + 64 KiB out;
 // K3 64 KiB + 32 KiB base in, 32 KiB (or, FWD, 64 KiB fhat) out.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the group-layout stores of BOLTZ_LINE_TMA)
 #include "common.cuh"
 #include "fft.cuh"
 
@@ -67,7 +68,13 @@ __device__ __forceinline__ void line_pass_axis1(double2* sm, int a, int b) {
     for (int j = 0; j < N; ++j) sm[LN::at(a, j, b)] = x[j];
 }
 
-// grid = cells / CPB (the groups' padding lanes included); block = CPB N^2 threads
+// BOLTZ_LINE_PERSIST: K1 runs a grid-stride loop over its blocks of CPB cells
+// (grid = the resident CTAs), loading the next block's lines while the current
+// one is in passes 2 and 3
+#ifndef BOLTZ_LINE_PERSIST
+#define BOLTZ_LINE_PERSIST 1
+#endif
+// blocks = cells / CPB (the groups' padding lanes included); block = CPB N^2 threads
 template <int N, int CPB>
 __global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
 k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncells, double scale,
@@ -77,56 +84,161 @@ k_fwd_line(const double* __restrict__ f, double2* __restrict__ A, long long ncel
     extern __shared__ __align__(16) double2 smem_line[];
     const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
     double2* sm = smem_line + sub * LN::CELL;
-    const long long cell = (long long)blockIdx.x * LN::CPB + sub;
-    const bool live = cell < ncells;
-    // pass 1 (axis 2, i3) from global: the line (a, b, :) is N contiguous doubles
-    double2 x[N];
-    bool bad = false;
-    const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
+    const long long nblk = (ncells + kLanes - 1) / kLanes * kLanes / CPB;
+    const long long stride = BOLTZ_LINE_PERSIST ? gridDim.x : nblk;
     const double cab = axis_coeff(N, a) * axis_coeff(N, b);
-    double fv[N];  // the line as N / 2 16-byte loads (f is 16-byte aligned: the callers check)
+    // pass 1 (axis 2, i3) from global: the line (a, b, :) is N contiguous doubles,
+    // loaded as N / 2 16-byte loads (f is 16-byte aligned: the callers check)
+    double fv[N];
+    auto load = [&](long long blk) {
+        const long long cell = blk * CPB + sub;
+        const bool live = blk < nblk && cell < ncells;
+        const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
 #pragma unroll
-    for (int j = 0; j < N / 2; ++j) {
-        const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
-        fv[2 * j] = u.x;
-        fv[2 * j + 1] = u.y;
+        for (int j = 0; j < N / 2; ++j) {
+            const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
+            fv[2 * j] = u.x;
+            fv[2 * j + 1] = u.y;
+        }
+    };
+    load(blockIdx.x);
+    for (long long blk = blockIdx.x; blk < nblk; blk += stride) {
+        const long long cell = blk * CPB + sub;
+        double2 x[N];
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double v = fv[j];
+            bad |= !isfinite(v);
+            double w = cab * axis_coeff(N, j);  // s_m c_m (fourier.hpp:19-22)
+            if ((a + b + j) & 1) w = -w;
+            x[j] = make_double2(v * w, 0.0);
+        }
+        if (bad) atomicOr(flag, 1);
+        if (BOLTZ_LINE_PERSIST) load(blk + stride);  // in flight through passes 2 and 3
+        RegFFT<N, -1, N>::run(x);
+#pragma unroll
+        for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+        __syncthreads();
+        line_pass_axis1<N, -1>(sm, a, b);
+        __syncthreads();
+        // pass 3 (axis 0, i1) to global: scale * par * s_k into the group layout
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+        RegFFT<N, -1, N>::run(x);
+        const long long g = cell / kLanes;
+        const int lane = (int)(cell % kLanes);
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double s = ((j + a + b) & 1) ? -scale : scale;
+            A[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] = make_double2(x[j].x * s, x[j].y * s);
+        }
+        if (BOLTZ_LINE_PERSIST) __syncthreads();  // every pass-3 read done before the next pass 1 writes
     }
+}
+
+// BOLTZ_LINE_TMA: the group-layout output of a line kernel leaves through
+// shared memory by 2D TMA tensor stores (one per i1 plane) instead of 16-byte
+// per-lane stores, each of which touches N^2 / 16 separate 128-byte lines
+#ifndef BOLTZ_LINE_TMA
+#define BOLTZ_LINE_TMA 1
+#endif
+// the group array X[g][idx][lane] as a 2D tensor of doubles: {2 kLanes, groups N^3}
+// (host: make_group_tmap); one box = one i1 plane of CPB adjacent cells
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// K1 with the output by TMA (grid-stride over blocks of CPB cells, as k_fwd_line).
+// After pass 3 the block's values go to a dense staging image of its group
+// rows -- plane j (idx j N^2 .. j N^2 + N^2 - 1) x CPB cells, 16 bytes each --
+// over the cube, and thread 0 stores the N planes; the next block waits for
+// those reads before it rewrites the cube.
+template <int N, int CPB>
+__global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
+k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap tmA, long long ncells,
+               double scale, int* __restrict__ flag) {
+    using LN = Line<N, CPB>;
+    constexpr int N3 = LN::N3, NN = N * N;
+    static_assert(N3 * CPB <= CPB * LN::CELL, "the staging image fits over the cubes");
+    extern __shared__ __align__(128) double2 smem_line_tma[];  // TMA: 128-byte aligned
+    double2* smem_line = smem_line_tma;
+    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
+    double2* sm = smem_line + sub * LN::CELL;
+    const long long nblk = (ncells + kLanes - 1) / kLanes * kLanes / CPB;
+    const double cab = axis_coeff(N, a) * axis_coeff(N, b);
+    double fv[N];
+    auto load = [&](long long blk) {
+        const long long cell = blk * CPB + sub;
+        const bool live = blk < nblk && cell < ncells;
+        const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const double v = fv[j];
-        bad |= !isfinite(v);
-        double w = cab * axis_coeff(N, j);  // s_m c_m (fourier.hpp:19-22)
-        if ((a + b + j) & 1) w = -w;
-        x[j] = make_double2(v * w, 0.0);
+        for (int j = 0; j < N / 2; ++j) {
+            const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
+            fv[2 * j] = u.x;
+            fv[2 * j + 1] = u.y;
+        }
+    };
+    load(blockIdx.x);
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        double2 x[N];
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double v = fv[j];
+            bad |= !isfinite(v);
+            double w = cab * axis_coeff(N, j);  // s_m c_m (fourier.hpp:19-22)
+            if ((a + b + j) & 1) w = -w;
+            x[j] = make_double2(v * w, 0.0);
+        }
+        if (bad) atomicOr(flag, 1);
+        load(blk + gridDim.x);  // in flight through passes 2 and 3
+        RegFFT<N, -1, N>::run(x);
+        if (blk != blockIdx.x) {  // the previous block's stores have read the staging image
+            if (t == 0) bulk_wait_read();
+            __syncthreads();
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+        __syncthreads();
+        line_pass_axis1<N, -1>(sm, a, b);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+        RegFFT<N, -1, N>::run(x);
+        __syncthreads();  // every pass-3 read done: the cubes become the staging image
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double s = ((j + a + b) & 1) ? -scale : scale;
+            smem_line[(j * NN + ln) * CPB + sub] = make_double2(x[j].x * s, x[j].y * s);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+            const long long cell0 = blk * CPB;
+            const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
+#pragma unroll 1
+            for (int j = 0; j < N; ++j) tma_store_2d(&tmA, smem_line + j * NN * CPB, c0, row0 + j * NN);
+            bulk_commit();
+        }
     }
-    if (bad) atomicOr(flag, 1);
-    RegFFT<N, -1, N>::run(x);
-#pragma unroll
-    for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
-    __syncthreads();
-    line_pass_axis1<N, -1>(sm, a, b);
-    __syncthreads();
-    // pass 3 (axis 0, i1) to global: scale * par * s_k into the group layout
-#pragma unroll
-    for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
-    RegFFT<N, -1, N>::run(x);
-    const long long g = cell / kLanes;
-    const int lane = (int)(cell % kLanes);
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const double s = ((j + a + b) & 1) ? -scale : scale;
-        A[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] = make_double2(x[j].x * s, x[j].y * s);
-    }
+    if (t == 0) bulk_wait_all();
 }
 
 template <int N, bool FWD, int CPB>
 __global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
 k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, double* __restrict__ out,
            double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
-           int* __restrict__ flag, double2* __restrict__ A_next, double fwd_scale) {
+           int* __restrict__ flag, double2* __restrict__ A_next, const __grid_constant__ CUtensorMap tmNext,
+           double fwd_scale) {
     using LN = Line<N, CPB>;
     constexpr int N3 = LN::N3, NN = N * N;
-    extern __shared__ __align__(16) double2 smem_line[];
+    extern __shared__ __align__(128) double2 smem_line_tma[];  // TMA (FWD): 128-byte aligned
+    double2* smem_line = smem_line_tma;
     double* red = reinterpret_cast<double*>(smem_line + CPB * LN::CELL);  // [CPB][HW][6]
     double* lam = red + CPB * LN::HW * 6;                                // [CPB][8]
     const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
@@ -272,11 +384,30 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
 #pragma unroll
         for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
         RegFFT<N, -1, N>::run(x);
+        if constexpr (BOLTZ_LINE_TMA) {  // through a staging image over the cubes, as k_fwd_line_tma
+            __syncthreads();
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-            const double s = ((j + a + b) & 1) ? -fwd_scale : fwd_scale;
-            A_next[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] =
-                make_double2(x[j].x * s, x[j].y * s);
+            for (int j = 0; j < N; ++j) {
+                const double s = ((j + a + b) & 1) ? -fwd_scale : fwd_scale;
+                smem_line[(j * NN + ln) * CPB + sub] = make_double2(x[j].x * s, x[j].y * s);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (t == 0) {
+                const long long cell0 = (long long)blockIdx.x * CPB;
+                const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
+#pragma unroll 1
+                for (int j = 0; j < N; ++j) tma_store_2d(&tmNext, smem_line + j * NN * CPB, c0, row0 + j * NN);
+                bulk_commit();
+                bulk_wait_all();
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double s = ((j + a + b) & 1) ? -fwd_scale : fwd_scale;
+                A_next[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] =
+                    make_double2(x[j].x * s, x[j].y * s);
+            }
         }
     }
 }
