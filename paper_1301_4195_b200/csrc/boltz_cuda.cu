@@ -160,17 +160,21 @@ int64_t n3_of(const boltz_ctx* c) { return (int64_t)c->n * c->n * c->n; }
 // the group array X[g][idx][lane] (double2) as a 2D TMA tensor of doubles
 // {2 kLanes, groups N^3}, rows 512 bytes apart; box = one i1 plane (N^2 rows)
 // of cpb adjacent cells (line.cuh k_fwd_line_tma)
-CUtensorMap make_group_tmap(void* X, int64_t ngroups, int n3, int cpb) {
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+using TmapEncode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Encode encode = [] {
+TmapEncode tmap_encode() {  // the driver's cuTensorMapEncodeTiled, through the runtime (no -lcuda)
+    static TmapEncode encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q;
         CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
         if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError{"cuTensorMapEncodeTiled unavailable"};
-        return reinterpret_cast<Encode>(fn);
+        return reinterpret_cast<TmapEncode>(fn);
     }();
+    return encode;
+}
+CUtensorMap make_group_tmap(void* X, int64_t ngroups, int n3, int cpb) {
+    const TmapEncode encode = tmap_encode();
     const int nn = (int)std::lround(std::cbrt((double)n3)) * (int)std::lround(std::cbrt((double)n3));
     CUtensorMap m;
     const cuuint64_t dim[2] = {2 * kLanes, (cuuint64_t)ngroups * n3};
@@ -181,6 +185,25 @@ CUtensorMap make_group_tmap(void* X, int64_t ngroups, int n3, int cpb) {
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+    return m;
+}
+
+// a user array [cell][N^3] (double) as a 2D TMA tensor {N, cells N^2}: one row
+// per line, box = one cell, 128-byte (N = 16) / 64-byte (N = 8) swizzle
+// (line.cuh k_fwd_line_tma, swz<N>)
+CUtensorMap make_cells_tmap(const double* f, int64_t ncells, int n) {
+    CUtensorMap m;
+    const cuuint64_t dim[2] = {(cuuint64_t)n, (cuuint64_t)ncells * n * n};
+    const cuuint64_t stride[1] = {(cuuint64_t)n * sizeof(double)};
+    const cuuint32_t box[2] = {(cuuint32_t)n, (cuuint32_t)(n * n)};
+    const cuuint32_t estride[2] = {1, 1};
+    const CUtensorMapSwizzle sw = n * 8 >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : n * 8 >= 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                : CU_TENSOR_MAP_SWIZZLE_32B;
+    const CUresult r = tmap_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(f), dim, stride,
+                                     box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{"cuTensorMapEncodeTiled (cells) failed: " + std::to_string((int)r)};
     return m;
 }
 
@@ -1052,20 +1075,22 @@ struct Launch {
     // a line kernel (line.cuh) with CPB = c->line_cpb cells per CTA: 2 for
     // device-memory calls, 1 inside the two-stream host pipeline
     // persist: a grid-stride kernel (k_fwd_line), launched as the CTAs that are resident at once
+    // (persist kernels are the TMA K1: their shared memory adds the f image, LineTma)
     template <typename K1, typename K2, typename... Args>
     static void launch_line(boltz_ctx* c, bool persist, K1 k1, K2 k2, int64_t nc, cudaStream_t s, Args... args) {
         const int64_t ng = (nc + 31) / 32;
         auto go = [&](auto kern, auto cpb) {
             using LN = Line<N, decltype(cpb)::value>;
+            const int smem = persist && BOLTZ_LINE_TMA ? LineTma<N, decltype(cpb)::value>::SMEM : LN::SMEM;
             // keyed by the kernel itself: kernels of one signature share this lambda
-            configure_smem(reinterpret_cast<const void*>(kern), c->device, LN::SMEM);
+            configure_smem(reinterpret_cast<const void*>(kern), c->device, smem);
             int64_t grid = ng * kLanes / LN::CPB;
             if (persist) {
                 int per_sm = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LN::THREADS, LN::SMEM));
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LN::THREADS, smem));
                 grid = std::min<int64_t>(grid, (int64_t)std::max(per_sm, 1) * c->num_sms);
             }
-            kern<<<(unsigned)grid, LN::THREADS, LN::SMEM, s>>>(args...);
+            kern<<<(unsigned)grid, LN::THREADS, smem, s>>>(args...);
         };
         if (c->line_cpb == 2) go(k2, std::integral_constant<int, 2>{});
         else go(k1, std::integral_constant<int, 1>{});
@@ -1085,8 +1110,9 @@ struct Launch {
             Timed t_(c, KIND_FFT, s);
             if (BOLTZ_LINE_TMA) {
                 const CUtensorMap tm = make_group_tmap(c->dA, (nc + 31) / 32, N3, c->line_cpb);
-                launch_line(c, true, k_fwd_line_tma<N, 1>, k_fwd_line_tma<N, 2>, nc, s, f, tm, (long long)nc, scale,
-                            c->dFlag);
+                const CUtensorMap tf = BOLTZ_LINE_TMA_LOAD ? make_cells_tmap(f, nc, N) : CUtensorMap{};
+                launch_line(c, true, k_fwd_line_tma<N, 1>, k_fwd_line_tma<N, 2>, nc, s, f, tf, tm, (long long)nc,
+                            scale, c->dFlag);
             } else {
                 launch_line(c, BOLTZ_LINE_PERSIST != 0, k_fwd_line<N, 1>, k_fwd_line<N, 2>, nc, s, f, c->dA,
                             (long long)nc, scale, c->dFlag);

@@ -153,6 +153,32 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// a user array [cell][N^3] as a 2D TMA tensor of doubles {N, cells N^2}: row =
+// one line (a, b, :) of N doubles, box = one cell (N^2 rows), landed with the
+// 128-byte (N = 16) or 64-byte (N = 8) swizzle so that lanes reading chunk c of
+// consecutive lines hit distinct banks (host: make_cells_tmap)
+template <int N>
+__device__ __forceinline__ int swz(int byte) {
+    constexpr int mask = N * 8 >= 128 ? 7 : N * 8 >= 64 ? 3 : 1;
+    return byte ^ (((byte >> 7) & mask) << 4);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+// BOLTZ_LINE_TMA_LOAD: K1 also takes f by TMA (swizzled, one box per cell), the
+// next block's box issued as soon as the current one is in registers
+#ifndef BOLTZ_LINE_TMA_LOAD
+#define BOLTZ_LINE_TMA_LOAD 1
+#endif
+template <int N, int CPB>
+struct LineTma {
+    static constexpr int F_BYTES = CPB * N * N * N * 8;             // the f image (swizzled lines)
+    static constexpr int SMEM = Line<N, CPB>::SMEM + (BOLTZ_LINE_TMA_LOAD ? F_BYTES + 1024 + 16 : 0);
+};
+
 // K1 with the output by TMA (grid-stride over blocks of CPB cells, as k_fwd_line).
 // After pass 3 the block's values go to a dense staging image of its group
 // rows -- plane j (idx j N^2 .. j N^2 + N^2 - 1) x CPB cells, 16 bytes each --
@@ -160,8 +186,8 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 // those reads before it rewrites the cube.
 template <int N, int CPB>
 __global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
-k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap tmA, long long ncells,
-               double scale, int* __restrict__ flag) {
+k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap tmF,
+               const __grid_constant__ CUtensorMap tmA, long long ncells, double scale, int* __restrict__ flag) {
     using LN = Line<N, CPB>;
     constexpr int N3 = LN::N3, NN = N * N;
     static_assert(N3 * CPB <= CPB * LN::CELL, "the staging image fits over the cubes");
@@ -172,18 +198,53 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
     const long long nblk = (ncells + kLanes - 1) / kLanes * kLanes / CPB;
     const double cab = axis_coeff(N, a) * axis_coeff(N, b);
     double fv[N];
-    auto load = [&](long long blk) {
-        const long long cell = blk * CPB + sub;
-        const bool live = blk < nblk && cell < ncells;
-        const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
+    // the f image: after the cubes, 1024-byte aligned (the swizzle atom)
+    char* fimg = reinterpret_cast<char*>(smem_line + CPB * LN::CELL);
+    fimg += (1024 - (smem_u32(fimg) & 1023)) & 1023;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(fimg + LineTma<N, CPB>::F_BYTES);
+    unsigned phase = 0;
+    auto issue = [&](long long blk) {  // thread 0: the CPB cells of block blk (rows past the tensor read as 0)
+        if (blk >= nblk) return;
+        mbar_expect_tx(bar, LineTma<N, CPB>::F_BYTES);
 #pragma unroll
-        for (int j = 0; j < N / 2; ++j) {
-            const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
-            fv[2 * j] = u.x;
-            fv[2 * j + 1] = u.y;
+        for (int c = 0; c < CPB; ++c) tma_load_2d(fimg + c * N3 * 8, &tmF, 0, (int)((blk * CPB + c) * NN), bar);
+    };
+    auto load = [&](long long blk) {
+        if constexpr (BOLTZ_LINE_TMA_LOAD) {
+            mbar_wait(bar, phase);
+            phase ^= 1;
+            const char* line = fimg + sub * N3 * 8;
+#pragma unroll
+            for (int j = 0; j < N / 2; ++j) {
+                const double2 u = *reinterpret_cast<const double2*>(line + swz<N>(ln * N * 8 + j * 16));
+                fv[2 * j] = u.x;
+                fv[2 * j + 1] = u.y;
+            }
+        } else {
+            const long long cell = blk * CPB + sub;
+            const bool live = blk < nblk && cell < ncells;
+            const double2* fl = reinterpret_cast<const double2*>(f + (size_t)cell * N3 + (size_t)(a * N + b) * N);
+#pragma unroll
+            for (int j = 0; j < N / 2; ++j) {
+                const double2 u = live ? ldg2(fl + j) : make_double2(0.0, 0.0);
+                fv[2 * j] = u.x;
+                fv[2 * j + 1] = u.y;
+            }
         }
     };
-    load(blockIdx.x);
+    if constexpr (BOLTZ_LINE_TMA_LOAD) {
+        if (t == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (t == 0) issue(blockIdx.x);
+        load(blockIdx.x);
+        __syncthreads();  // every thread holds its lines: the image may be refilled
+        if (t == 0) issue(blockIdx.x + gridDim.x);
+    } else {
+        load(blockIdx.x);
+    }
     for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         double2 x[N];
         bool bad = false;
@@ -196,7 +257,7 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
             x[j] = make_double2(v * w, 0.0);
         }
         if (bad) atomicOr(flag, 1);
-        load(blk + gridDim.x);  // in flight through passes 2 and 3
+        if constexpr (!BOLTZ_LINE_TMA_LOAD) load(blk + gridDim.x);  // in flight through passes 2 and 3
         RegFFT<N, -1, N>::run(x);
         if (blk != blockIdx.x) {  // the previous block's stores have read the staging image
             if (t == 0) bulk_wait_read();
@@ -217,6 +278,9 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
             smem_line[(j * NN + ln) * CPB + sub] = make_double2(x[j].x * s, x[j].y * s);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if constexpr (BOLTZ_LINE_TMA_LOAD) {
+            if (blk + gridDim.x < nblk) load(blk + gridDim.x);  // the next block's lines (landed meanwhile)
+        }
         __syncthreads();
         if (t == 0) {
             const long long cell0 = blk * CPB;
@@ -224,6 +288,7 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
 #pragma unroll 1
             for (int j = 0; j < N; ++j) tma_store_2d(&tmA, smem_line + j * NN * CPB, c0, row0 + j * NN);
             bulk_commit();
+            if constexpr (BOLTZ_LINE_TMA_LOAD) issue(blk + 2 * (long long)gridDim.x);
         }
     }
     if (t == 0) bulk_wait_all();
