@@ -1098,6 +1098,33 @@ struct Launch {
     }
 #endif
 
+    // K3 by k_inv_line2 (all I/O by TMA): group c->dB -> out (FWD: -> c->dA)
+    template <bool FWD>
+    static void launch_inv2(boltz_ctx* c, const double* base, double* out, int64_t nc, double scale, double coef,
+                            double fwd_scale, cudaStream_t s) {
+        const int64_t ng = (nc + 31) / 32;
+        auto go = [&](auto kern, auto cpb) {
+            constexpr int CPB = decltype(cpb)::value;
+            using LN = Line<N, CPB>;
+            const int smem = LineInv<N, CPB>::SMEM;
+            configure_smem(reinterpret_cast<const void*>(kern), c->device, smem);
+            const CUtensorMap tB = make_group_tmap(c->dB, ng, N3, CPB);
+            const CUtensorMap tBase = base ? make_cells_tmap(base, nc, N) : CUtensorMap{};
+            const CUtensorMap tOut = FWD ? CUtensorMap{} : make_cells_tmap(out, nc, N);
+            const CUtensorMap tNext = FWD ? make_group_tmap(c->dA, ng, N3, CPB) : CUtensorMap{};
+            kern<<<(unsigned)(ng * kLanes / CPB), LN::THREADS, smem, s>>>(
+                tB, tBase, tOut, tNext, base ? 1 : 0, reinterpret_cast<double*>(c->dMaxIm), (long long)nc, scale,
+                coef, c->pc, c->dFlag, fwd_scale);
+        };
+        // one cell per CTA, two CTAs per SM: one CTA's TMA loads overlap the other's
+        // transforms (cfg2 RK2 step, B200: fused K3 267 -> 198 us, final 191 -> 159 us
+        // against two cells per CTA); BOLTZ_LINE_INV2_CPB=2 for the comparison
+        static const int cpb = std::getenv("BOLTZ_LINE_INV2_CPB") && std::atoi(std::getenv("BOLTZ_LINE_INV2_CPB")) == 2 ? 2 : 1;
+        if (cpb == 2) go(k_inv_line2<N, FWD, 2>, std::integral_constant<int, 2>{});
+        else go(k_inv_line2<N, FWD, 1>, std::integral_constant<int, 1>{});
+        CK(cudaGetLastError());
+    }
+
     // user real f (device, nc cells) -> group complex fhat in c->dA
     static void forward(boltz_ctx* c, const double* f, int64_t nc, cudaStream_t s) {
         const int64_t ng = (nc + 31) / 32;
@@ -1353,6 +1380,10 @@ struct Launch {
             const double sz = (kPi / c->L) / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
             Timed t_(c, KIND_PROJECT, s);
+            if (BOLTZ_LINE_INV2 && ((reinterpret_cast<uintptr_t>(base) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+                launch_inv2<false>(c, base, out, nc, sz * sz * sz * par, coef, 0.0, s);
+                return;
+            }
             launch_line(c, false, k_inv_line<N, false, 1>, k_inv_line<N, false, 2>, nc, s, (const double2*)c->dB, base, out,
                         reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef, c->pc, c->dFlag,
                         (double2*)nullptr, CUtensorMap{}, 0.0);
@@ -1392,6 +1423,10 @@ struct Launch {
             const double sv = c->pc.dv / std::sqrt(2.0 * kPi);
             const double par = ((N / 2) & 1) ? -1.0 : 1.0;
             Timed t_(c, KIND_PROJECT, s);
+            if (BOLTZ_LINE_INV2) {
+                launch_inv2<true>(c, base, nullptr, nc, sz * sz * sz * par, coef, sv * sv * sv * par, s);
+                return;
+            }
             launch_line(c, false, k_inv_line<N, true, 1>, k_inv_line<N, true, 2>, nc, s, (const double2*)c->dB, base,
                         (double*)nullptr, reinterpret_cast<double*>(c->dMaxIm), (long long)nc, sz * sz * sz * par, coef,
                         c->pc, c->dFlag, c->dA,
@@ -2001,6 +2036,8 @@ int create_context(int n, double L, double lambda, double beta, double r0, int p
                    int device, boltz_ctx** out, bool with_table) {
     boltz_ctx* c = new boltz_ctx();
     c->n = n; c->L = L; c->lambda = lambda; c->beta = beta; c->r0 = r0; c->device = device; c->panels = panels;
+    if (const char* e = std::getenv("BOLTZ_LINE_CPB"))  // tuning: cells per CTA of the line kernels, device calls
+        c->line_cpb = std::atoi(e) == 1 ? 1 : 2;
     if (const char* e = std::getenv("BOLTZ_STAGE_SLOTS"))  // tuning
         c->stage_slots = std::min(boltz_ctx::kMaxStageSlots, std::max(2, std::atoi(e)));
     try {

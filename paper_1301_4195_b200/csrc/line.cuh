@@ -173,6 +173,9 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 #ifndef BOLTZ_LINE_TMA_LOAD
 #define BOLTZ_LINE_TMA_LOAD 1
 #endif
+#ifndef BOLTZ_LINE_WAR_FENCE
+#define BOLTZ_LINE_WAR_FENCE 1
+#endif
 template <int N, int CPB>
 struct LineTma {
     static constexpr int F_BYTES = CPB * N * N * N * 8;             // the f image (swizzled lines)
@@ -240,6 +243,7 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
         __syncthreads();
         if (t == 0) issue(blockIdx.x);
         load(blockIdx.x);
+        if (BOLTZ_LINE_WAR_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();  // every thread holds its lines: the image may be refilled
         if (t == 0) issue(blockIdx.x + gridDim.x);
     } else {
@@ -280,6 +284,7 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if constexpr (BOLTZ_LINE_TMA_LOAD) {
             if (blk + gridDim.x < nblk) load(blk + gridDim.x);  // the next block's lines (landed meanwhile)
+            if (BOLTZ_LINE_WAR_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();
         if (t == 0) {
@@ -473,6 +478,205 @@ k_inv_line(const double2* __restrict__ B, const double* __restrict__ base, doubl
                 A_next[((size_t)g * N3 + (size_t)(j * N + a) * N + b) * kLanes + lane] =
                     make_double2(x[j].x * s, x[j].y * s);
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3 with every HBM access by TMA (BOLTZ_LINE_INV2, N = 8, 16 with 16-byte
+// aligned user arrays).  The passes run i1, i2, i3 -- the reverse of
+// k_inv_line -- so that pass 1 reads the group rows plane by plane (one TMA box
+// per i1 plane, landed on the cubes) and pass 3 leaves each thread the line
+// (i1, i2, :) that the projection, the RK2 axpy, the user-layout base / out
+// (swizzled line images, one TMA box per cell) and the fused forward
+// transform's first pass all want.  Moments: per thread over i3, then the same
+// fixed-order reduction as k_inv_line.
+// ---------------------------------------------------------------------------
+#ifndef BOLTZ_LINE_INV2
+#define BOLTZ_LINE_INV2 1
+#endif
+template <int N, int CPB>
+struct LineInv {
+    static constexpr int F_BYTES = CPB * N * N * N * 8;  // base image / out staging (swizzled lines)
+    static constexpr int SMEM = Line<N, CPB>::SMEM + F_BYTES + 1024 + 16;
+};
+
+template <int N, bool FWD, int CPB>
+__global__ void __launch_bounds__(Line<N, CPB>::THREADS, Line<N, CPB>::MINB)
+k_inv_line2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBase,
+            const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmNext, int has_base,
+            double* __restrict__ maximag, long long ncells, double scale, double coef, ProjConst pc,
+            int* __restrict__ flag, double fwd_scale) {
+    using LN = Line<N, CPB>;
+    constexpr int N3 = LN::N3, NN = N * N;
+    constexpr unsigned F_BYTES = LineInv<N, CPB>::F_BYTES;
+    static_assert(N3 * CPB <= CPB * LN::CELL, "the group image fits over the cubes");
+    extern __shared__ __align__(128) double2 smem_line_tma[];
+    double2* cubes = smem_line_tma;
+    double* red = reinterpret_cast<double*>(cubes + CPB * LN::CELL);  // [CPB][HW][6]
+    double* lam = red + CPB * LN::HW * 6;                            // [CPB][8]
+    char* img = reinterpret_cast<char*>(lam + CPB * 8);
+    img += (1024 - (smem_u32(img) & 1023)) & 1023;
+    unsigned long long* bar = reinterpret_cast<unsigned long long*>(img + F_BYTES);
+    const int t = threadIdx.x, sub = LN::sub(t), ln = LN::line(t), a = ln / N, b = ln % N;
+    double2* sm = cubes + sub * LN::CELL;
+    const long long cell0 = (long long)blockIdx.x * CPB, cell = cell0 + sub;
+    const bool live = cell < ncells;
+    const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
+    char* myline = img + sub * N3 * 8;  // this cell's line image; the thread's line is row ln
+    if (t == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(bar, (unsigned)(N3 * CPB * 16) + (has_base ? F_BYTES : 0u));
+#pragma unroll 1
+        for (int j = 0; j < N; ++j) tma_load_2d(cubes + j * NN * CPB, &tmB, c0, row0 + j * NN, bar);
+        if (has_base)
+#pragma unroll 1
+            for (int c = 0; c < CPB; ++c) tma_load_2d(img + c * N3 * 8, &tmBase, 0, (int)((cell0 + c) * NN), bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    // pass 1 (axis 0, i1) from the group image: thread ln = (i2, i3)
+    double2 x[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = cubes[(j * NN + ln) * CPB + sub];
+    double bv[N];  // the RK2 base on the thread's pass-3 line (i1, i2) = (a, b)
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+        const double2 u = has_base ? *reinterpret_cast<const double2*>(myline + swz<N>(ln * N * 8 + j * 16))
+                                   : make_double2(0.0, 0.0);
+        bv[2 * j] = u.x;
+        bv[2 * j + 1] = u.y;
+    }
+    __syncthreads();  // the group image is consumed: the cubes take its place
+    RegFFT<N, +1, N>::run(x);
+#pragma unroll
+    for (int j = 0; j < N; ++j) sm[LN::at(j, a, b)] = x[j];
+    __syncthreads();
+    line_pass_axis1<N, +1>(sm, a, b);
+    __syncthreads();
+    // pass 3 (axis 2, i3) in registers: Qt = Re(scale * par * s_k * z) on the line
+    // (i1, i2) = (a, b), its moments over i3 and max|Im|
+#pragma unroll
+    for (int j = 0; j < N; ++j) x[j] = sm[LN::at(a, b, j)];
+    RegFFT<N, +1, N>::run(x);
+    const double dv3 = pc.dv * pc.dv * pc.dv;
+    const double v1 = pc.dv * (a - N / 2), v2 = pc.dv * (b - N / 2);
+    const double w12 = axis_coeff(N, a) * axis_coeff(N, b);
+    const double fw12 = w12 * dv3;
+    const double sg12 = ((a + b) & 1) ? -scale : scale;
+    double s0 = 0.0, s3 = 0.0, s4 = 0.0, mi = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double q = x[j].x * ((j & 1) ? -sg12 : sg12);
+        x[j].x = q;
+        const double v3 = pc.dv * (j - N / 2);
+        const double cq = axis_coeff(N, j) * q;
+        s0 += cq;
+        s3 = fma(v3, cq, s3);
+        s4 = fma(v3 * v3, cq, s4);
+        mi = fmax(mi, fabs(x[j].y));
+    }
+    double part[6];
+    part[0] = fw12 * s0;
+    part[1] = v1 * part[0];
+    part[2] = v2 * part[0];
+    part[3] = fw12 * s3;
+    part[4] = fw12 * fma(v1 * v1 + v2 * v2, s0, s4);
+    part[5] = mi * fabs(scale);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        double v = part[k];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+            const double u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = (k == 5) ? fmax(v, u) : v + u;
+        }
+        if ((ln & 15) == 0) red[(sub * LN::HW + (ln >> 4)) * 6 + k] = v;
+    }
+    __syncthreads();
+    if (t < CPB) {
+        const int c = t;
+        const long long cl = cell0 + c;
+        double m[6] = {0, 0, 0, 0, 0, 0};
+        for (int h = 0; h < LN::HW; ++h)
+            for (int k = 0; k < 6; ++k) {
+                const double r = red[(c * LN::HW + h) * 6 + k];
+                m[k] = (k == 5) ? fmax(m[k], r) : m[k] + r;
+            }
+        for (int k = 0; k < 5; ++k) {  // lambda = (C C^T)^{-1} C Qt
+            double s = 0.0;
+            for (int q = 0; q < 5; ++q) s = fma(pc.ginv[k * 5 + q], m[q], s);
+            lam[c * 8 + k] = s;
+        }
+        if (maximag && cl < ncells) maximag[cl] = m[5];
+    }
+    __syncthreads();
+    const double l0 = lam[sub * 8 + 0], l1 = lam[sub * 8 + 1], l2 = lam[sub * 8 + 2], l3 = lam[sub * 8 + 3],
+                 l4 = lam[sub * 8 + 4];
+    // out / f* = base + coef * (Qt - w C^T lambda) on the line
+    const double cl12 = l0 + v1 * l1 + v2 * l2 + (v1 * v1 + v2 * v2) * l4;
+    bool bad = false;
+    double v[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double v3 = pc.dv * (j - N / 2);
+        const double cl = fma(v3, fma(v3, l4, l3), cl12);
+        const double q = x[j].x - w12 * axis_coeff(N, j) * dv3 * cl;
+        double r = 0.0;
+        if (live) {
+            r = coef * q;
+            if (has_base) r += bv[j];
+            bad |= !isfinite(r);
+        }
+        v[j] = r;
+    }
+    if (bad) atomicOr(flag, 2);
+    if constexpr (!FWD) {
+        // the line into its place in the image (only this thread touched it), then one box per cell
+#pragma unroll
+        for (int j = 0; j < N / 2; ++j)
+            *reinterpret_cast<double2*>(myline + swz<N>(ln * N * 8 + j * 16)) = make_double2(v[2 * j], v[2 * j + 1]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+#pragma unroll 1
+            for (int c = 0; c < CPB; ++c) tma_store_2d(&tmOut, img + c * N3 * 8, 0, (int)((cell0 + c) * NN));
+            bulk_commit();
+            bulk_wait_all();
+        }
+    } else {
+        // f* times s_m c_m and its forward transform: pass 1 in registers, pass 2
+        // in smem, pass 3 to the staging image, stored by TMA into A_next
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            double w = w12 * axis_coeff(N, j);
+            if ((a + b + j) & 1) w = -w;
+            x[j] = make_double2(v[j] * w, 0.0);
+        }
+        RegFFT<N, -1, N>::run(x);
+        // the thread's own line: no other thread reads it after the barrier above
+#pragma unroll
+        for (int j = 0; j < N; ++j) sm[LN::at(a, b, j)] = x[j];
+        __syncthreads();
+        line_pass_axis1<N, -1>(sm, a, b);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[j] = sm[LN::at(j, a, b)];
+        RegFFT<N, -1, N>::run(x);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double s = ((j + a + b) & 1) ? -fwd_scale : fwd_scale;
+            cubes[(j * NN + ln) * CPB + sub] = make_double2(x[j].x * s, x[j].y * s);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (t == 0) {
+#pragma unroll 1
+            for (int j = 0; j < N; ++j) tma_store_2d(&tmNext, cubes + j * NN * CPB, c0, row0 + j * NN);
+            bulk_commit();
+            bulk_wait_all();
         }
     }
 }

@@ -469,6 +469,22 @@ def test_host_pipeline_cfg2_size_matches_device_path(gpu):
         assert np.array_equal(g, ref)
 
 
+def test_host_pipeline_repeatable_across_seeds(gpu):
+    """Repeated collide through the two-stream host pipeline against the device
+    path, bitwise, over 12 inputs: catches intermittent races between the TMA
+    staging of the line kernels and the other stream's kernels (a missing
+    proxy fence failed about one input in fifteen)."""
+    import torch
+    n, L, cells = 16, 6.0, 4096
+    grid = VelocityGrid.create(n, L)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as op:
+        for r in range(12):
+            f = scenarios.mixture_cells(grid, cells, seed=1000 + r)
+            qd = op.collide(torch.from_numpy(f).to(gpu)).cpu().numpy()
+            qh = op.collide(f)
+            assert np.array_equal(qh, qd), r
+
+
 def test_latency_schedule_host_pipeline_large_batch(gpu):
     """the latency schedule through the two-workspace host pipeline
     on 2048+ cells (odd chunks use the second workspace's segment scratch) is
