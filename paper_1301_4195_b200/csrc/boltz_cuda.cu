@@ -1667,7 +1667,10 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
         int old;
         ~CpbGuard() { c->line_cpb = old; }
     } cpb_guard{c, c->line_cpb};
-    if (two) c->line_cpb = 1;
+    if (two) {
+        static const int pipe_cpb = std::getenv("BOLTZ_PIPE_LINE_CPB") ? std::atoi(std::getenv("BOLTZ_PIPE_LINE_CPB")) : 1;
+        c->line_cpb = pipe_cpb == 2 ? 2 : 1;  // tuning / A-B: K1's cells per CTA inside the pipeline
+    }
     // pageable caller memory goes through the pinned bounce ring (host threads
     // copy; the DMA engines only ever see pinned memory)
     bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));
