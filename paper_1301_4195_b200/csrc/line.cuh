@@ -1,19 +1,22 @@
-// line.cuh -- K1 / K3 with one FFT line per thread and two adjacent cells per
-// CTA (N = 8, 16; BOLTZ_LINE_CPB=1: one cell per CTA, two CTAs per SM).  The first axis pass runs straight from
-// global memory into registers and the last one straight from registers to
-// global memory, so a transform costs two shared-memory round trips instead of
+// line.cuh -- K1 / K3 with one FFT line per thread (N = 8, 16).  The first axis
+// pass runs from the loaded data into registers and the last one from registers
+// to the output, so a transform costs two shared-memory round trips instead of
 // the staged kernels' four (fused.cuh, which remains for N = 12, 24).
 //
-//   k_fwd_line:        user f [cell][N^3]  -> group fhat      (fourier.hpp:11-12)
-//   k_inv_line<FWD>:   group s_k*Qhat       -> out = base + coef * P_N(Re iFFT)
+//   k_fwd_line_tma:    user f [cell][N^3]  -> group fhat      (fourier.hpp:11-12)
+//   k_inv_line2<FWD>:  group s_k*Qhat       -> out = base + coef * P_N(Re iFFT)
 //                      (+ max|Im|; inverse fourier.hpp:15-17, projection
 //                      SPEC.md:204-212, RK2 axpy SPEC.md:383-391); FWD: the
 //                      RK2 stage value goes straight on to its forward
 //                      transform into A_next, never touching HBM
+// Both move every HBM byte by TMA (2D tensor maps built per call on the host:
+// make_group_tmap, make_cells_tmap in boltz_cuda.cu).  k_fwd_line / k_inv_line
+// are the same transforms with per-lane loads and stores (BOLTZ_LINE_TMA=0,
+// BOLTZ_LINE_INV2=0, and user arrays that are not 16-byte aligned).
 //
 // Thread t of the N^2 threads owns the lines (a, b) = (t / N, t % N) of every
 // pass: along i3 at (i1, i2) = (a, b), along i2 at (i1, i3) = (a, b), along i1 at
-// (i2, i3) = (a, b).  Moments are summed per thread over i1 (pass 3) and
+// (i2, i3) = (a, b).  Moments are summed per thread over the last pass's axis and
 // reduced in a fixed order (a shuffle tree per 16 consecutive lines, then the
 // 16-line partials in line order): deterministic, independent of the batch and
 // of the cells-per-CTA variant.  Cells past ncells (the group's padding lanes)
