@@ -839,6 +839,28 @@ void build_table_mirror_kcs(boltz_ctx* c, const double* G_host) {
     fill_table(c, G_host, T, c->dMH);
 }
 
+// First cell-group column of the mirror kernels' joint longest-first tail
+// (conv.cuh mirror_unit): the last BOLTZ_LPT_TAIL columns -- 4 for grids of 16
+// or more columns (cfg2, 4096 cells: K2 5.469 -> 5.315 ms, value 714k -> 733k
+// evals/s), else 1, i.e. every column longest-first on its own (the host
+// pipeline's chunks: e2e 696.6k with 1 against 690-695k with 2-6).  Items
+// range from single rows to row pairs (~1.6x) and the earlier columns take them
+// longest-first each (measured best in round 1: 11.17 ms against 11.26 in the
+// last column only and 11.49 never).  BOLTZ_LPT_FROM overrides (tuning).
+// joint longest-first tail columns of the k-chunked kernels (k_conv_kcsm,
+// k_conv_kcsr) on many-wave grids; 1 = the last column only
+inline int kcs_lpt_tail() {
+    const char* e = std::getenv("BOLTZ_LPT_TAIL_KCS");
+    return e ? std::max(1, std::atoi(e)) : 1;
+}
+inline int mirror_lpt_from(int columns) {
+    int tail = columns >= 16 ? 4 : 1;
+    if (const char* e = std::getenv("BOLTZ_LPT_TAIL")) tail = std::max(1, std::atoi(e));
+    int from = std::max(0, columns - tail);
+    if (const char* e = std::getenv("BOLTZ_LPT_FROM")) from = std::max(0, std::atoi(e));
+    return from;
+}
+
 // the mirror schedule runs where the convolution is the single-tile TMA pipe
 // (k_conv_mirror) or the k-chunked TMA kcs kernel (k_conv_kcsm)
 constexpr bool mirror_pipe_n(int n) {
@@ -1223,23 +1245,26 @@ struct Launch {
                     }
                 });
                 const unsigned gy = (unsigned)((ng + W - 1) / W);
-                // longest rows first in the last column of many-wave grids (conv_row)
-                auto lpt = [&](int nrows) { return (int64_t)nrows * gy < 8 * 2 * 148 ? 0 : (int)gy - 1; };
+                // longest rows first: every column (each on its own) for grids a few waves
+                // deep, else the last kcs_lpt_tail() columns jointly (conv.cuh lpt_unit)
+                auto few = [&](int nrows, unsigned cols) { return (int64_t)nrows * cols < 8 * 2 * 148; };
+                auto lpt = [&](int nrows) { return few(nrows, gy) ? (int)gy : std::max(0, (int)gy - kcs_lpt_tail()); };
                 Timed t_(c, KIND_CONV, s);
                 // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
                 auto go = [&](auto kern, int ph) {
                     const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph;  // list 1 runs phase 3 when not split
                     kern<<<dim3(c->nK[ph], gy), kLanes * W, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
                                                                                 c->dListK[ph], c->nK[ph], (int)ng,
-                                                                                lpt(c->nK[ph]));
+                                                                                lpt(c->nK[ph]), (int)few(c->nK[ph], gy));
                 };
                 go(k_conv_kcsm<N, 0, 0>, 0);
                 if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 0>, 0);
                 if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
                     const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
-                    const int lr = (int64_t)c->nK[1] * gr < 8 * 2 * 148 ? 0 : (int)gr - 1;
+                    const bool fr = few(c->nK[1], gr);
+                    const int lr = fr ? (int)gr : std::max(0, (int)gr - kcs_lpt_tail());
                     k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
-                                     s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr);
+                                     s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
                     go(k_conv_kcsm<N, 0, 2>, 2);
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
                 } else if constexpr (kcsm_split(N)) {
@@ -1265,8 +1290,7 @@ struct Launch {
                     CK(cudaFuncSetAttribute(k_conv_mirror2<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 });
                 dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-                int lpt = 0;
-                if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
+                const int lpt = mirror_lpt_from((int)grid.y);
                 Timed t_(c, KIND_CONV, s);
                 k_conv_mirror2<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dItems,
                                                                           c->dItems + kItemInts * c->nitems, (int)ng,
@@ -1284,11 +1308,7 @@ struct Launch {
                     CK(cudaFuncSetAttribute(k_conv_mirror<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 });
                 dim3 grid((unsigned)c->nitems, (unsigned)((ng + kConvWarps - 1) / kConvWarps));
-                // longest items first in every column: items range from single rows to
-                // row pairs (~1.6x), and LPT everywhere measured best (11.17 ms against
-                // 11.26 in the last column only and 11.49 never)
-                int lpt = 0;
-                if (const char* e = std::getenv("BOLTZ_LPT_FROM")) lpt = std::atoi(e);  // tuning
+                const int lpt = mirror_lpt_from((int)grid.y);
                 Timed t_(c, KIND_CONV, s);
                 k_conv_mirror<N><<<grid, kLanes * kConvWarps, smem, s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dItems,
                                                                          c->dItems + kItemInts * c->nitems, (int)ng,

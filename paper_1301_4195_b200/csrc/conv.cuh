@@ -930,6 +930,24 @@ k_conv_cell(const double2* __restrict__ Cc, double2* __restrict__ B, const doubl
 // ---------------------------------------------------------------------------
 constexpr int kItemInts = 6;
 
+// A CTA's (item or row-list index, cell-group column).  Columns below lpt_from
+// take the items longest-first (head_lpt: blockIdx.x indexes `order`) or in
+// their natural, L2-friendly order (k_conv_kcsm / k_conv_kcsr); the last
+// gridDim.y - lpt_from columns are scheduled jointly: their CTAs walk the items
+// longest-first with the columns innermost, so the final waves hold the
+// shortest items of every tail column (a list schedule closer to LPT over the
+// whole tail; the tail columns' f-hat stays L2-resident).  lpt_from >= gridDim.y:
+// every column longest-first.  The assignment does not change any result.
+__device__ __forceinline__ int2 lpt_unit(const int* __restrict__ order, int lpt_from, bool head_lpt) {
+    if ((int)blockIdx.y < lpt_from) return make_int2(head_lpt ? __ldg(order + blockIdx.x) : (int)blockIdx.x, (int)blockIdx.y);
+    const int k = (int)gridDim.y - lpt_from;
+    const int u = ((int)blockIdx.y - lpt_from) * (int)gridDim.x + (int)blockIdx.x;
+    return make_int2(__ldg(order + u / k), lpt_from + u % k);
+}
+__device__ __forceinline__ int2 mirror_unit(const int* __restrict__ order, int lpt_from) {
+    return lpt_unit(order, lpt_from, true);
+}
+
 template <int N>
 struct MirrorLayout {
     static constexpr int X_BYTES = N * kLanes * 16;
@@ -946,9 +964,10 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
     static_assert(PipeLayout<N>::TMA, "the mirror schedule runs on the TMA pipe (single-tile rows)");
     constexpr int T = N, N3 = N * N * N;
     extern __shared__ __align__(16) char smem[];
-    const int* it = items + kItemInts * ((int)blockIdx.y >= lpt_from ? __ldg(order + blockIdx.x) : (int)blockIdx.x);
+    const int2 unit = mirror_unit(order, lpt_from);
+    const int* it = items + kItemInts * unit.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.y * kConvWarps + wid;
+    const int g = unit.y * kConvWarps + wid;
     if (g >= ngroups) return;
     const int r = __ldg(it), rm = __ldg(it + 1);
     const int e_begin = __ldg(it + 2), e_endA = __ldg(it + 3), e_rm = __ldg(it + 4), e_end = __ldg(it + 5);
@@ -1211,8 +1230,9 @@ k_conv_mirror2(const double2* __restrict__ A, double2* __restrict__ B, const dou
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tbase_s + ((uint32_t)(32 * (wid & 3)) << 16);
     const uint32_t t_r = tmem, t_rm = tmem + 4 * N;
-    const int* it = items + kItemInts * ((int)blockIdx.y >= lpt_from ? __ldg(order + blockIdx.x) : (int)blockIdx.x);
-    const int g = blockIdx.y * kConvWarps + wid;
+    const int2 unit = mirror_unit(order, lpt_from);
+    const int* it = items + kItemInts * unit.x;
+    const int g = unit.y * kConvWarps + wid;
     if (g < ngroups) {
         const int r = __ldg(it), rm = __ldg(it + 1);
         const int e_begin = __ldg(it + 2), e_endI = __ldg(it + 3), e_rm = __ldg(it + 4), e_end = __ldg(it + 5);
@@ -1473,7 +1493,7 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const YT
 template <int N, int KC, int PHASE>
 __global__ void __launch_bounds__(kLanes* kcsm_warps(N), PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
 k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
+            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from, int head_lpt) {
     using LY = KcsmLayout<N, PHASE>;
     constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
     // this chunk's part of an entry's slab (phase 3: REST or FULL per entry)
@@ -1481,9 +1501,10 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     constexpr size_t OFF = (size_t)KC * kcsm_slab(N, TY), OFF_R = (size_t)KC * kcsm_slab(N, BT_REST);
     constexpr unsigned BYTES = 8u * kcsm_slab_kc(N, T, KC, TY), BYTES_R = 8u * kcsm_slab_kc(N, T, KC, BT_REST);
     extern __shared__ __align__(16) char smem[];
-    const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
+    const int2 unit = lpt_unit(list + 3 * nrows + 1, lpt_from, head_lpt);
+    const int wi = unit.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.y * kcsm_warps(N) + wid;
+    const int g = unit.y * kcsm_warps(N) + wid;
     if (g >= ngroups) return;
     const int row = __ldg(list + nrows + 1 + wi), aux = __ldg(list + 2 * nrows + 1 + wi);
     const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
@@ -1775,16 +1796,17 @@ __host__ __device__ constexpr int kcsr_part_begin(int part) {
 template <int N>
 __global__ void __launch_bounds__(kLanes* kKcsrWarps, BOLTZ_KCSR_MINB)
 k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
-            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from) {
+            const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from, int head_lpt) {
     using LY = KcsrLayout<N>;
     constexpr int N3 = N * N * N;
     constexpr unsigned HB = LY::H_BYTES;
     constexpr int P2 = kcsr_part_begin<N>(2);
     [[maybe_unused]] constexpr int PE = KcsrTab<N>::COUNT;
     extern __shared__ __align__(16) char smem[];
-    const int wi = (int)blockIdx.y >= lpt_from ? __ldg(list + 3 * nrows + 1 + blockIdx.x) : (int)blockIdx.x;
+    const int2 unit = lpt_unit(list + 3 * nrows + 1, lpt_from, head_lpt);
+    const int wi = unit.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = blockIdx.y * kKcsrWarps + wid;
+    const int g = unit.y * kKcsrWarps + wid;
     if (g >= ngroups) return;
     const int row = __ldg(list + nrows + 1 + wi);
     const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
