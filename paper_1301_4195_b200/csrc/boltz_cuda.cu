@@ -731,8 +731,23 @@ void layout_terms_kcsm(int n, TableLayout& T) {
             off += (int)v.size();
             continue;
         }
-        const int stride = kcsm_slab(n, ty);
+        const bool fold = ty == BT_A && kcsf_n(n);  // phase 4: [A pieces | REST(r) | REST'(r'), flagged] per chunk
+        const int stride = fold ? kcsf_slab(n) : kcsm_slab(n, ty);
         std::vector<short2> v((size_t)nk * stride, make_short2(-1, -1));
+        if (fold) {
+            for (int kc = 0; kc < nk; ++kc) {  // kf_pass order: 4-output batches, output, m3
+                int pr = kc * stride + kcsf_a_kc(n, kc), pp = pr + even_up(kcsf_rest_kc(n, kc));
+                for (int b = 0; b < t / 4; ++b)
+                    for (int q = 0; q < 4; ++q)
+                        for (int m3 = 0; m3 < n; ++m3) {
+                            const int k3 = kc * t + 4 * b + q;
+                            if (!rest_term(n, k3, m3)) continue;
+                            v[pr++] = make_short2((short)k3, (short)m3);
+                            v[pp++] = make_short2((short)(k3 + kMirrorTermFlag), (short)m3);
+                        }
+            }
+            T.partner_terms = true;
+        }
         for (int kc = 0; kc < nk; ++kc)
             for (int ti = 0; ti < nk; ++ti) {
                 const int sc = band_tile_sc(nk, kc, ti);
@@ -791,6 +806,7 @@ void build_table_mirror_kcs(boltz_ctx* c, const double* G_host) {
                 const int r = k1 * n + k2, rm = partner(k1, k2);
                 const bool pair = rm >= 0 && rm != r;
                 if ((phase == 0 && !(pair && r < rm)) || (phase == 1 && split && !pair)) continue;
+                if (phase == 1 && kcsf_n(n)) continue;  // REST folded into phase 0 (kernel phase 4)
                 Rows& L = R[phase];
                 const size_t first = ent.size();
                 L.start.push_back((int)first);
@@ -820,7 +836,9 @@ void build_table_mirror_kcs(boltz_ctx* c, const double* G_host) {
     };
     std::vector<int> lists[3];
     for (int ph = 0; ph < 3; ++ph) {
-        const int end = ph < 2 && !R[ph + 1].start.empty() ? R[ph + 1].start.front() : (int)ent.size();
+        int end = (int)ent.size();  // the next non-empty list's first entry
+        for (int q = 2; q > ph; --q)
+            if (!R[q].start.empty()) end = R[q].start.front();
         lists[ph] = finish(R[ph], end);
         c->nK[ph] = (int)R[ph].row.size();
     }
@@ -1219,16 +1237,18 @@ struct Launch {
             if (hermitian && c->mirror && c->schedule == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
                 constexpr int W = kcsm_warps(N);
-                const int smem_ph[4] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
-                                        W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES};
+                constexpr int P0 = kcsf_n(N) ? 4 : 0;  // the phase-0 kernels: with the REST fold or plain
+                const int smem_ph[5] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
+                                        W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES,
+                                        W * KcsmLayout<N, 4>::WARP_BYTES + KcsmLayout<N, 4>::TMEM_BYTES};
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
                     auto cfg = [&](auto fn, int ph) {
                         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ph[ph]));
                         CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                     };
-                    cfg(k_conv_kcsm<N, 0, 0>, 0);
-                    cfg(k_conv_kcsm<N, KC1, 0>, 0);
+                    cfg(k_conv_kcsm<N, 0, P0>, P0);
+                    cfg(k_conv_kcsm<N, KC1, P0>, P0);
                     if constexpr (kcsr_n(N)) {
                         CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
@@ -1252,14 +1272,18 @@ struct Launch {
                 Timed t_(c, KIND_CONV, s);
                 // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
                 auto go = [&](auto kern, int ph) {
-                    const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph;  // list 1 runs phase 3 when not split
+                    // list 1 runs phase 3 when not split; list 0 phase 4 with the REST fold
+                    const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph == 0 ? P0 : ph;
                     kern<<<dim3(c->nK[ph], gy), kLanes * W, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
                                                                                 c->dListK[ph], c->nK[ph], (int)ng,
                                                                                 lpt(c->nK[ph]), (int)few(c->nK[ph], gy));
                 };
-                go(k_conv_kcsm<N, 0, 0>, 0);
-                if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 0>, 0);
-                if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
+                go(k_conv_kcsm<N, 0, P0>, 0);
+                if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, P0>, 0);
+                if constexpr (kcsf_n(N)) {  // REST folded into phase 0: FULL entries only
+                    go(k_conv_kcsm<N, 0, 2>, 2);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
+                } else if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
                     const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
                     const bool fr = few(c->nK[1], gr);
                     const int lr = fr ? (int)gr : std::max(0, (int)gr - kcs_lpt_tail());
@@ -1276,7 +1300,7 @@ struct Launch {
                     go(k_conv_kcsm<N, 0, 3>, 1);
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3>, 1);
                 }
-                c->launches[KIND_CONV] += kcsr_n(N) ? 2 * NK : (kcsm_split(N) ? 3 : 2) * NK - 1;  // one timing bracket
+                c->launches[KIND_CONV] += kcsf_n(N) ? 2 * NK - 1 : kcsr_n(N) ? 2 * NK : (kcsm_split(N) ? 3 : 2) * NK - 1;  // one timing bracket
                 CK(cudaGetLastError());
                 return;
             }
@@ -2412,7 +2436,7 @@ const char* boltz_conv_kernel(const boltz_ctx* c) {
     if (c->mirror) {
         if (c->mirror2) return "k_conv_mirror2";
         if (mirror_pipe_n(c->n)) return "k_conv_mirror";
-        return c->n == 32 ? "k_conv_kcsm (phases 0, 2) + k_conv_kcsr" : "k_conv_kcsm";
+        return c->n == 32 ? (kcsf_n(32) ? "k_conv_kcsm (phase 0 with the REST fold, phase 2)" : "k_conv_kcsm (phases 0, 2) + k_conv_kcsr") : "k_conv_kcsm";
     }
     return conv_kernel_for(c->n) == 1 ? "k_conv_pipe" : "k_conv_kcs";
 }

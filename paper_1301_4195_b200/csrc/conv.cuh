@@ -1403,16 +1403,63 @@ __host__ __device__ constexpr int kcsm_slab(int n, int ty) {
     return mx;
 }
 
+// ---------------------------------------------------------------------------
+// The REST fold (N = 32, BOLTZ_KCSF): kernel phase 4 = phase 0 of k_conv_kcsm
+// with the pair rows' REST terms folded in; it replaces k_conv_kcsr.  An entry
+// of a pair leader r (interior input row m, y row s staged) also sums, between
+// its two tiles, the chunk's REST terms of r and the REST' terms of the
+// partner r' = N - r -- r''s own non-mirrored terms, from r's rows: x'[m3'] =
+// conj x[N - m3'], x'[0] = fhat(N - m1, N - m2, 0), likewise y' (as
+// k_conv_mirror2's REST') -- k3-major, 4 outputs per TMEM access, into two TMEM
+// rows of 16 complex values per warp.  The REST terms then reuse the staged y
+// row and the x row the A band just read, instead of restaging both per REST
+// entry (k_conv_kcsr: ~33 KB of L2 per 109 terms, FP64 pipe 52%).
+// Epilogue: chunk KC of row r = A + T_r; row r' takes conj(A) at N - k3 and
+// T_r' at k3' (the KC = 0 launch writes the row, KC = 1 adds to it).
+// Slab of an entry, per chunk: [A pieces | REST(r) | REST'(r'), flagged].
+// Measured on B200 and left off (BOLTZ_KCSF=1 opts in; bitwise-equal checksum,
+// oracle parity green): cfg5-shaped collide at 2048 cells 145.1 -> 164.2 ms.
+// ncu: phase 4 takes 59.7 / 53.7 ms (chunk 0 / 1) against 27.6 + 32.9 for
+// phase 0 plus 30.1 for k_conv_kcsr -- the REST passes run at ~3x the A band's
+// cost per term: each term's x comes from L1/L2 right before its use (long
+// scoreboard 16%), every 4-output batch waits on its tcgen05.ld, and the extra
+// code spills (160 / 400 B) and misses the I-cache (no_instructions 7%).
+// ---------------------------------------------------------------------------
+#ifndef BOLTZ_KCSF
+#define BOLTZ_KCSF 0
+#endif
+// REST terms of chunk kc (k3 in [kc T, kc T + T))
+__host__ __device__ constexpr int kcsf_rest_kc(int n, int kc) {
+    const int t = conv_tile(n);
+    int c = 0;
+    for (int k3 = kc * t; k3 < kc * t + t; ++k3)
+        for (int m3 = 0; m3 < n; ++m3) c += rest_term(n, k3, m3) ? 1 : 0;
+    return c;
+}
+__host__ __device__ constexpr int kcsf_a_kc(int n, int kc) { return kcsm_slab_kc(n, conv_tile(n), kc, BT_A); }
+__host__ __device__ constexpr int kcsf_slab_kc(int n, int kc) {
+    return kcsf_a_kc(n, kc) + 2 * even_up(kcsf_rest_kc(n, kc));
+}
+// per-chunk stride of a phase-4 entry's slab
+__host__ __device__ constexpr int kcsf_slab(int n) {
+    int mx = 0;
+    for (int kc = 0; kc < n / conv_tile(n); ++kc) mx = kcsf_slab_kc(n, kc) > mx ? kcsf_slab_kc(n, kc) : mx;
+    return mx;
+}
+// the phase whose band code a kernel phase runs (4: phase 0's A band)
+__host__ __device__ constexpr int kcsm_ph(int phase) { return phase == 4 ? 0 : phase; }
+
 // per-warp shared memory of phase PHASE (its H slots sized for its band type;
-// phase 3 holds REST or FULL slabs)
+// phase 3 holds REST or FULL slabs, phase 4 the folded slabs)
 template <int N, int PHASE = 3>
 struct KcsmLayout {
     static constexpr int T = conv_tile(N);
     static constexpr int NK = N / T;
     static constexpr int Y_BYTES = N * kLanes * 16;
     static constexpr int H_BYTES =
-        kcsm_slab(N, PHASE == 0 ? (int)BT_A : PHASE == 1 ? (int)BT_REST : (int)BT_FULL) * 8;
+        (PHASE == 4 ? kcsf_slab(N) : kcsm_slab(N, PHASE == 0 ? (int)BT_A : PHASE == 1 ? (int)BT_REST : (int)BT_FULL)) * 8;
     static constexpr int WARP_BYTES = Y_BYTES + 2 * H_BYTES + 16;  // + 2 mbarriers
+    static constexpr int TMEM_BYTES = PHASE == 4 ? 16 : 0;         // the CTA's TMEM base address
 };
 // cell groups (warps) per CTA of k_conv_kcsm: 8 at N=24 (cfg4 RK2 step 31.3 ->
 // 30.4 ms), the global kConvWarps elsewhere (8 measured +7% at N=32)
@@ -1426,7 +1473,9 @@ __host__ __device__ constexpr int kcsm_warps(int n) { return n == 24 ? BOLTZ_KCS
 
 // the band type phase PHASE runs: 0 the pair leaders' A terms, 1 REST, 2 FULL,
 // 3 REST or FULL per entry (phases 1 and 2 in one launch)
-__host__ __device__ constexpr int kcsm_type(int phase) { return phase == 0 ? BT_A : phase == 1 ? BT_REST : BT_FULL; }
+__host__ __device__ constexpr int kcsm_type(int phase) {
+    return phase == 0 || phase == 4 ? BT_A : phase == 1 ? BT_REST : BT_FULL;
+}
 // phases 1 and 2 as separate launches (one band type unrolled per kernel) for
 // two k-chunks; one launch at N=24 (measured: N=32 339.8 -> 330.7 ms per RK2
 // step split, N=24 31.3 -> 32.8 ms)
@@ -1436,6 +1485,8 @@ __host__ __device__ constexpr int kcsm_type(int phase) { return phase == 0 ? BT_
 __host__ __device__ constexpr bool kcsm_split(int n) {
     return BOLTZ_KCSM_SPLIT >= 0 ? BOLTZ_KCSM_SPLIT == 1 : n / conv_tile(n) > 1;
 }
+// N = 32: the REST fold (kernel phase 4) instead of k_conv_kcsr
+__host__ __device__ constexpr bool kcsf_n(int n) { return BOLTZ_KCSF && n == 32 && kcsm_split(n); }
 
 // one tile of a k_conv_kcsm entry on the y window in registers (x per
 // diagonal from L2)
@@ -1460,8 +1511,8 @@ __host__ __device__ constexpr int kcsm_ks(int n, int kc, int ty) {
     return (n == 32 && kc == 1 && (ty == BT_A || ty == BT_FULL)) ? BOLTZ_KCSM_KS1 : 1;
 }
 __host__ __device__ constexpr bool kcsm_gauss(int n, int kc, int phase) {
-    return BOLTZ_TERM_GAUSS || (BOLTZ_KCSM_GAUSS && n == 32 && kc == 0 && (phase == 0 || phase == 2)) ||
-           (BOLTZ_KCSM_GAUSS1 && n == 32 && kc == 1 && (phase == 0 || phase == 2));
+    return BOLTZ_TERM_GAUSS || (BOLTZ_KCSM_GAUSS && n == 32 && kc == 0 && (kcsm_ph(phase) == 0 || phase == 2)) ||
+           (BOLTZ_KCSM_GAUSS1 && n == 32 && kc == 1 && (kcsm_ph(phase) == 0 || phase == 2));
 }
 template <int N, int KC, int PHASE>
 using KcsmY = std::conditional_t<kcsm_gauss(N, KC, PHASE), YG, double2>;
@@ -1479,7 +1530,7 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const YT
     auto none = [](int, int) {};
     double2 hb = make_double2(0.0, 0.0);
     int p = 0;
-    if constexpr (PHASE < 3) {
+    if constexpr (PHASE < 3 || PHASE == 4) {
         constexpr int TY = kcsm_type(PHASE);
         band_tile<N, T, NK, KC, TI, TY, kcsm_ks(N, KC, TY)>(acc, y, xat, hs + kcsm_piece_off(N, T, KC, TI, TY) / 2, p,
                                                            hb, none);
@@ -1490,22 +1541,108 @@ __device__ __forceinline__ void kcsm_tile(double2 (&acc)[conv_tile(N)], const YT
     }
 }
 
+// one REST (PRIME: REST' of the partner row) term of the fold: x from L2 (the
+// row the A band just read), y from the staged row
+template <int N, bool PRIME, int K3, int M3>
+__device__ __forceinline__ void kf_term(double2& a, double h, const double2* __restrict__ X,
+                                        const double2* __restrict__ ys, int lane, double2 X0, double2 Y0) {
+    constexpr int S3 = K3 - M3 + N / 2;
+    auto xg = [&](int m) { return ldg2(X + (size_t)m * kLanes); };
+    auto yg = [&](int s) { return ys[s * kLanes + lane]; };
+    if constexpr (!PRIME) {
+        const double2 xm = xg(M3), yv = yg(S3);
+        const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
+        const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else if constexpr (M3 == 0) {  // X0 * conj(y[N - s3])  (s3 >= 1 here)
+        const double2 yv = yg((N - S3) % N);
+        const double tr = fma(X0.x, yv.x, X0.y * yv.y);
+        const double ti = fma(X0.y, yv.x, -X0.x * yv.y);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else if constexpr (S3 == 0) {  // conj(x[N - m3]) * Y0
+        const double2 xm = xg(N - M3);
+        const double tr = fma(xm.x, Y0.x, xm.y * Y0.y);
+        const double ti = fma(xm.x, Y0.y, -xm.y * Y0.x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(h, ti, a.y);
+    } else {  // conj(x[N - m3] * y[N - s3])
+        const double2 xm = xg(N - M3), yv = yg(N - S3);
+        const double tr = fma(xm.x, yv.x, -xm.y * yv.y);
+        const double ti = fma(xm.x, yv.y, xm.y * yv.x);
+        a.x = fma(h, tr, a.x);
+        a.y = fma(-h, ti, a.y);
+    }
+}
+// the REST terms of outputs k3 = KC T + 4B .. +3 into a[4] (slab order: B, Q, m3)
+template <int N, int KC, bool PRIME, int B, int Q = 0, int M3 = 0>
+__device__ __forceinline__ void kf_batch(double2 (&a)[4], const double2* __restrict__ X,
+                                         const double2* __restrict__ ys, int lane, const double2* __restrict__ hs,
+                                         int& p, double2& hb, double2 X0, double2 Y0) {
+    constexpr int K3 = KC * conv_tile(N) + 4 * B + Q;
+    if constexpr (Q < 4) {
+        if constexpr (M3 < N) {
+            if constexpr (rest_term(N, K3, M3)) {
+                double h;
+                if ((p & 1) == 0) { hb = hs[p >> 1]; h = hb.x; }
+                else h = hb.y;
+                ++p;
+                kf_term<N, PRIME, K3, M3>(a[Q], h, X, ys, lane, X0, Y0);
+            }
+            kf_batch<N, KC, PRIME, B, Q, M3 + 1>(a, X, ys, lane, hs, p, hb, X0, Y0);
+        } else {
+            kf_batch<N, KC, PRIME, B, Q + 1, 0>(a, X, ys, lane, hs, p, hb, X0, Y0);
+        }
+    }
+}
+// a REST pass of chunk KC into the TMEM row at ta, 4 outputs per TMEM access
+template <int N, int KC, bool PRIME, int B = 0>
+__device__ __forceinline__ void kf_pass(uint32_t ta, const double2* __restrict__ X, const double2* __restrict__ ys,
+                                        int lane, const double2* __restrict__ hs, int& p, double2& hb, double2 X0,
+                                        double2 Y0) {
+    if constexpr (B < conv_tile(N) / 4) {
+        double2 a[4];
+        tm_ld4c(ta + 16 * B, a);
+        kf_batch<N, KC, PRIME, B>(a, X, ys, lane, hs, p, hb, X0, Y0);
+        tm_st4c(ta + 16 * B, a);
+        kf_pass<N, KC, PRIME, B + 1>(ta, X, ys, lane, hs, p, hb, X0, Y0);
+    }
+}
+
 template <int N, int KC, int PHASE>
 __global__ void __launch_bounds__(kLanes* kcsm_warps(N), PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
 k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from, int head_lpt) {
     using LY = KcsmLayout<N, PHASE>;
-    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N;
-    // this chunk's part of an entry's slab (phase 3: REST or FULL per entry)
-    constexpr int TY = kcsm_type(PHASE < 3 ? PHASE : 2);
-    constexpr size_t OFF = (size_t)KC * kcsm_slab(N, TY), OFF_R = (size_t)KC * kcsm_slab(N, BT_REST);
-    constexpr unsigned BYTES = 8u * kcsm_slab_kc(N, T, KC, TY), BYTES_R = 8u * kcsm_slab_kc(N, T, KC, BT_REST);
+    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N, W = kcsm_warps(N);
+    constexpr bool FOLD = PHASE == 4;
+    static_assert(!FOLD || (T % 4 == 0 && W <= 4), "the fold: 4-output TMEM batches, one TMEM lane quarter per warp");
+    constexpr int PH = kcsm_ph(PHASE);
+    // this chunk's part of an entry's slab (phase 3: REST or FULL per entry; phase 4: the folded slab)
+    constexpr int TY = kcsm_type(PHASE == 3 ? 2 : PHASE);
+    constexpr size_t OFF = (size_t)KC * (FOLD ? kcsf_slab(N) : kcsm_slab(N, TY)), OFF_R = (size_t)KC * kcsm_slab(N, BT_REST);
+    constexpr unsigned BYTES = 8u * (FOLD ? kcsf_slab_kc(N, KC) : kcsm_slab_kc(N, T, KC, TY)),
+                       BYTES_R = 8u * kcsm_slab_kc(N, T, KC, BT_REST);
     extern __shared__ __align__(16) char smem[];
     const int2 unit = lpt_unit(list + 3 * nrows + 1, lpt_from, head_lpt);
     const int wi = unit.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int g = unit.y * kcsm_warps(N) + wid;
-    if (g >= ngroups) return;
+    const int g = unit.y * W + wid;
+    // phase 4: two TMEM rows (REST of r, REST' of r') of T complex values per warp
+    [[maybe_unused]] uint32_t* tbase_s = reinterpret_cast<uint32_t*>(smem + W * LY::WARP_BYTES);
+    [[maybe_unused]] constexpr int COLS = FOLD ? (8 * T <= 32 ? 32 : 8 * T <= 64 ? 64 : 8 * T <= 128 ? 128 : 256) : 0;
+    if constexpr (FOLD) {
+        if (wid == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tbase_s)),
+                         "r"(COLS) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    if (g < ngroups) {
     const int row = __ldg(list + nrows + 1 + wi), aux = __ldg(list + 2 * nrows + 1 + wi);
     const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
     char* wsm = smem + wid * LY::WARP_BYTES;
@@ -1515,8 +1652,20 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
     const double2* Abase = A + (size_t)g * N3 * kLanes;
     const double2* Ag = Abase + lane;
     double2* Brow = B + ((size_t)g * N3 + (size_t)row * N + KC * T) * kLanes + lane;
+    [[maybe_unused]] uint32_t t_r = 0, t_rm = 0;
+    if constexpr (FOLD) {
+        t_r = *tbase_s + ((uint32_t)(32 * (wid & 3)) << 16);
+        t_rm = t_r + 4 * T;
+        const double2 z[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
+                              make_double2(0.0, 0.0)};
+#pragma unroll
+        for (int b = 0; b < T / 4; ++b) {
+            tm_st4c(t_r + 16 * b, z);
+            tm_st4c(t_rm + 16 * b, z);
+        }
+    }
     double2 acc[T];
-    if (PHASE >= 1 && aux) {
+    if (PH >= 1 && aux) {
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) acc[kk] = Brow[(size_t)kk * kLanes];
     } else {
@@ -1537,6 +1686,23 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, LY::Y_BYTES);
             bulk_g2s(ys, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+        }
+    };
+    // phase 4: the chunk's REST of r and REST' of r' from the staged rows
+    auto rest_fold = [&](int4 en, const double2* X, const double2* hs) {
+        if constexpr (FOLD) {
+            const int m1 = en.x / (N * N), m2 = (en.x / N) % N, s1 = en.y / (N * N), s2 = (en.y / N) % N;
+            const double2 X0 = ldg2(Abase + (size_t)(((N - m1) * N + (N - m2)) * N) * kLanes + lane);
+            const double2 Y0 = ldg2(Abase + (size_t)(((N - s1) * N + (N - s2)) * N) * kLanes + lane);
+            const double2 zero = make_double2(0.0, 0.0);
+            tm_wait_st();  // the previous entry's TMEM stores
+            int p = 0;
+            double2 hb = zero;
+            kf_pass<N, KC, false>(t_r, X, ys, lane, hs + kcsf_a_kc(N, KC) / 2, p, hb, zero, zero);
+            int pp = 0;
+            double2 hbp = zero;
+            kf_pass<N, KC, true>(t_rm, X, ys, lane, hs + (kcsf_a_kc(N, KC) + even_up(kcsf_rest_kc(N, KC))) / 2, pp,
+                                 hbp, X0, Y0);
         }
     };
     if (e0 < e1) {
@@ -1563,11 +1729,13 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
 #pragma unroll
             for (int j = 0; j < T; ++j) y[j] = to_yt<KcsmY<N, KC, PHASE>>(ys[(band_tile_sc(NK, KC, 0) * T + j) * kLanes + lane]);
             if constexpr (NK == 1) {
+                rest_fold(en, X, hs);  // (phase 4 needs the y row: before the refill)
                 __syncwarp();  // every lane holds its y window: the buffer may be refilled
                 if (more) tma_y(cur ^ 1, nx);
                 kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, en.w);
             } else {
                 kcsm_tile<N, KC, 0, PHASE>(acc, y, X, hs, en.w);
+                rest_fold(en, X, hs);  // between the tiles: the y row is still staged
 #pragma unroll
                 for (int j = 0; j < T; ++j) y[j] = to_yt<KcsmY<N, KC, PHASE>>(ys[(band_tile_sc(NK, KC, 1) * T + j) * kLanes + lane]);
                 __syncwarp();
@@ -1589,11 +1757,56 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
             if (k3 != 0) Bm[(size_t)(N - k3) * kLanes] = make_double2(acc[kk].x, -acc[kk].y);
         }
         if (KC == NK - 1) Bm[0] = make_double2(0.0, 0.0);
+    } else if constexpr (FOLD) {
+        // row r, chunk KC: A + REST(r), raw (phase 2 continues it)
+        tm_wait_st();
+#pragma unroll
+        for (int b = 0; b < T / 4; ++b) {
+            double2 v[4];
+            tm_ld4c(t_r + 16 * b, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                Brow[(size_t)(4 * b + q) * kLanes] = make_double2(acc[4 * b + q].x + v[q].x, acc[4 * b + q].y + v[q].y);
+        }
+        // row r': conj(A) k3-reversed (k3' = N - k3, none for k3 = 0) and REST'(r') at k3' = KC T + kk; the
+        // first chunk's launch writes the row (k3' = N/2 .. : zero where nothing lands yet), later ones add
+        double2* Bm = B + ((size_t)g * N3 + (size_t)aux * N) * kLanes + lane;
+        double2 tv[T];
+#pragma unroll
+        for (int b = 0; b < T / 4; ++b) {
+            double2 v[4];
+            tm_ld4c(t_rm + 16 * b, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) tv[4 * b + q] = v[q];
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            double2 v = KC == 0 ? make_double2(0.0, 0.0) : Bm[(size_t)k * kLanes];
+            const int kk = N - k - KC * T;  // conj A[k3 = N - k] of this chunk
+            if (k != 0 && kk >= 0 && kk < T) {
+                v.x += acc[kk].x;
+                v.y -= acc[kk].y;
+            }
+            if (k >= KC * T && k < KC * T + T) {  // REST'(r') at k3' = k
+                v.x += tv[k - KC * T].x;
+                v.y += tv[k - KC * T].y;
+            }
+            Bm[(size_t)k * kLanes] = v;
+        }
     } else if constexpr (PHASE == 1) {  // seed + REST, raw: phase 2 continues the row
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) Brow[(size_t)kk * kLanes] = acc[kk];
     } else {
         write_row<N, T>(B, g, row, KC, lane, acc);
+    }
+    }  // g < ngroups
+    if constexpr (FOLD) {
+        tm_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (wid == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tbase_s), "r"(COLS) : "memory");
     }
 }
 
@@ -1651,7 +1864,7 @@ __host__ __device__ constexpr bool kcsr_diag(int n, int part, int m3) {
 #ifndef BOLTZ_KCSR
 #define BOLTZ_KCSR 1  // N = 32: one full-row REST launch instead of phase 1 per k-chunk
 #endif
-__host__ __device__ constexpr bool kcsr_n(int n) { return BOLTZ_KCSR && n == 32 && kcsm_split(n); }
+__host__ __device__ constexpr bool kcsr_n(int n) { return BOLTZ_KCSR && !kcsf_n(n) && n == 32 && kcsm_split(n); }
 #ifndef BOLTZ_KCSR_WARPS
 #define BOLTZ_KCSR_WARPS 2
 #endif

@@ -578,16 +578,17 @@ def test_cell_schedule_vs_oracle(gpu, O, n, L):
     assert rel_max(g[0] - f[0], r2[0] - f[0]) < 1e-9
 
 
-def test_n32_maxwell_molecules_kcsr_vs_oracle(gpu, O):
+def test_n32_maxwell_molecules_rest_fold_vs_oracle(gpu, O):
     """N=32 with Maxwell molecules (lambda=0): the phased mirror schedule with
-    the Gauss-form chunk-0 kernels and the full-row REST launch (k_conv_kcsr),
-    host table, against the oracle on two cells of a 40-cell batch."""
+    the Gauss-form chunk-0 kernels and the REST terms folded into phase 0
+    (TMEM rows for REST(r) and REST'(r'), conv.cuh k_conv_kcsm phase 4), host
+    table, against the oracle on two cells of a 40-cell batch."""
     n, L, lam = 32, 8.0, 0.0
     grid = VelocityGrid.create(n, L)
     f = scenarios.mixture_cells(grid, 40, seed=131)
     G = table(n, L, lam)
     with _op(n, L, lam) as op:
-        assert "kcsr" in op.conv_kernel()
+        assert "REST fold" in op.conv_kernel() or "kcsr" in op.conv_kernel()
         q = op.collide(f)
     for c in (3, 38):
         ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
