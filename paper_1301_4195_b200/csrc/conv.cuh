@@ -397,6 +397,14 @@ struct EntAhead {
 #ifndef BOLTZ_KCSM_ENTWIN
 #define BOLTZ_KCSM_ENTWIN 0
 #endif
+// the mirror kernels (N <= 16, ~250 terms per entry): the window.  With one
+// entry loaded ahead, the compiler copied the loaded value into the loop-carried
+// register right after the load, so every entry waited on an L2 round trip
+// (ncu source view of k_conv_mirror2<16>: 1.7% of all stall samples on that copy)
+#ifndef BOLTZ_MIRROR_ENTWIN
+#define BOLTZ_MIRROR_ENTWIN 1
+#endif
+using EntSrc = std::conditional_t<BOLTZ_MIRROR_ENTWIN != 0, EntWin, EntAhead>;
 // 1D TMA: bytes (multiple of 16) global -> this CTA's shared memory, completing on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -1011,8 +1019,8 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncwarp();
-        int4 en = __ldg(ent + e_begin);
-        int4 en_ahead = e_begin + 1 < e_end ? __ldg(ent + e_begin + 1) : en;
+        EntSrc src(ent, e_begin, e_end, lane);
+        int4 en = src.first(e_begin);
         issue(0, en);
         mbar_wait(bar, 0);
         using YM = std::conditional_t<BOLTZ_MIRROR_GAUSS != 0, YG, double2>;
@@ -1026,8 +1034,7 @@ k_conv_mirror(const double2* __restrict__ A, double2* __restrict__ B, const doub
         for (int e = e_begin; e < e_end; ++e) {
             const int i = e - e_begin, cur = i & 1;
             const bool more = e + 1 < e_end;
-            const int4 nx = en_ahead;
-            if (e + 2 < e_end) en_ahead = __ldg(ent + e + 2);
+            const int4 nx = src.next(e, more, en);
             boundary(e);
             __syncwarp();  // every lane read y (registers) and is done with slot cur^1
             if (more) issue(cur ^ 1, nx);
@@ -1300,8 +1307,8 @@ k_conv_mirror2(const double2* __restrict__ A, double2* __restrict__ B, const dou
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
             }
             __syncwarp();
-            int4 en = __ldg(ent + e_begin);
-            int4 en_ahead = e_begin + 1 < e_end ? __ldg(ent + e_begin + 1) : en;
+            EntSrc src(ent, e_begin, e_end, lane);
+            int4 en = src.first(e_begin);
             issue(0, en);
             mbar_wait(bar, 0);
             double2 y[T];
@@ -1310,8 +1317,7 @@ k_conv_mirror2(const double2* __restrict__ A, double2* __restrict__ B, const dou
             for (int e = e_begin; e < e_end; ++e) {
                 const int i = e - e_begin, cur = i & 1;
                 const bool more = e + 1 < e_end;
-                const int4 nx = en_ahead;
-                if (e + 2 < e_end) en_ahead = __ldg(ent + e + 2);
+                const int4 nx = src.next(e, more, en);
                 boundary(e);
                 __syncwarp();  // every lane read y (registers) and is done with slot cur^1
                 if (more) issue(cur ^ 1, nx);
