@@ -1250,9 +1250,15 @@ struct Launch {
                     cfg(k_conv_kcsm<N, 0, P0>, P0);
                     cfg(k_conv_kcsm<N, KC1, P0>, P0);
                     if constexpr (kcsr_n(N)) {
-                        CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
-                        CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                        if constexpr (BOLTZ_KCSR_YBUF == 4) {
+                            CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    KcsrqLayout<N>::WARP_BYTES * kKcsrWarps));
+                            CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                        } else {
+                            CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
+                            CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                        }
                     }
                     if constexpr (kcsm_split(N)) {
                         cfg(k_conv_kcsm<N, 0, 1>, 1);
@@ -1287,8 +1293,13 @@ struct Launch {
                     const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
                     const bool fr = few(c->nK[1], gr);
                     const int lr = fr ? (int)gr : std::max(0, (int)gr - kcs_lpt_tail());
-                    k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
-                                     s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
+                    if constexpr (BOLTZ_KCSR_YBUF == 4)  // one y row per warp, refilled by quarters
+                        k_conv_kcsrq<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps,
+                                          KcsrqLayout<N>::WARP_BYTES * kKcsrWarps, s>>>(
+                            c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
+                    else
+                        k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
+                                         s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
                     go(k_conv_kcsm<N, 0, 2>, 2);
                     if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
                 } else if constexpr (kcsm_split(N)) {

@@ -1841,6 +1841,7 @@ __host__ __device__ constexpr bool kcsr_term(int n, int k3, int m3) {
 // and one diagonal-major pass (every term in part 0).  B200, cfg5-shaped RK2
 // step (2048 cells), K2 ms: phase 1 per k-chunk 318.0 | kcsr 1 buffer, 4 warps
 // 305.8 | 2 buffers, 2 warps per CTA 299.9 | 3 warps 301.9 | 4 warps 322.5
+// 4 -- k_conv_kcsrq: one y row refilled by quarters (below; measured no gain)
 #ifndef BOLTZ_KCSR_YBUF
 #define BOLTZ_KCSR_YBUF 2
 #endif
@@ -1852,7 +1853,7 @@ __host__ __device__ constexpr bool kcsr_term(int n, int k3, int m3) {
 // is REST term (k3, m3) in part `part` (0, 1, 2; see above)?
 __host__ __device__ constexpr bool kcsr_part(int n, int part, int k3, int m3) {
     if (!kcsr_term(n, k3, m3)) return false;
-    if (BOLTZ_KCSR_YBUF == 2 && !BOLTZ_KCSR_YREG) return part == 0;
+    if (BOLTZ_KCSR_YBUF >= 2 && !BOLTZ_KCSR_YREG) return part == 0;
     const bool edge = !mirror_interior(n, m3);
     return part == 0 ? edge : part == 1 ? (!edge && k3 == 0) : (!edge && k3 != 0);
 }
@@ -1915,6 +1916,8 @@ struct KcsrTab {
     short k3[COUNT] = {}, m3[COUNT] = {}, part[COUNT] = {};
     signed char xsrc[COUNT] = {}, ysrc[COUNT] = {};
     bool xload[COUNT] = {}, yload[COUNT] = {};
+    // k_conv_kcsrq: first / one-past-last term loading the staged y of quarter q (s3 in [qN/4, (q+1)N/4))
+    int qbeg[4] = {}, qend[4] = {};
     bool done[N * N] = {};
     int c = 0;
     constexpr void emit(int k, int m, int pt) {
@@ -1925,7 +1928,7 @@ struct KcsrTab {
         ++c;
     }
     constexpr KcsrTab() {
-        if (BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF == 2) {
+        if (BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF >= 2) {
             const int edges[3] = {0, 1, N - 1};
             for (int s = 0; s < N; ++s) {
                 for (int e = 0; e < 3; ++e) {
@@ -1950,7 +1953,7 @@ struct KcsrTab {
                     for (int k = 0; k < N; ++k)
                         if (kcsr_part(N, pt, k, m)) emit(k, m, pt);
         }
-        const bool regs = BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF == 2;
+        const bool regs = BOLTZ_KCSR_ORDER == 2 && BOLTZ_KCSR_YBUF >= 2;
         int xm = -1, yc = -1;
         for (int i = 0; i < COUNT; ++i) {
             const int s = k3[i] - m3[i] + N / 2;
@@ -1961,7 +1964,26 @@ struct KcsrTab {
             yload[i] = ysrc[i] == 3 && (!regs || s != yc);
             if (yload[i]) yc = s;
         }
+        // quarter bounds (monotone: the staged y is read in s3 order); a quarter without
+        // staged reads collapses onto the previous bound
+        int last = 1;  // y[0], y[1] are read from quarter 0 before the first term
+        for (int q = 0; q < 4; ++q) {
+            qbeg[q] = -1;
+            qend[q] = last;
+            for (int i = 0; i < COUNT; ++i) {
+                const int s = k3[i] - m3[i] + N / 2;
+                if (!yload[i] || s / (N / 4) != q) continue;
+                if (qbeg[q] < 0) qbeg[q] = i;
+                qend[q] = i + 1;
+            }
+            if (qbeg[q] < 0) qbeg[q] = last;       // no staged read: wait and refill at the same point
+            if (q > 0 && qbeg[q] < last) qmono = false;  // a quarter read before the previous one is done
+            if (qend[q] < qbeg[q]) qend[q] = qbeg[q];
+            last = qend[q];
+        }
+        qbeg[0] = 0;
     }
+    bool qmono = true;
 };
 // ORDER 1 loads x when the diagonal changes and y per term from the staged row
 // in parts 0 and 1 (from registers in part 2); ORDER 2 as the table says.
@@ -2104,6 +2126,136 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
                 KcsrRun<P2, PE>::run(f);  // part 2: y[0], y[1], y[N-1] in registers
             }
             if (more) mbar_wait(bar + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
+            en = nx;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) Brow[(size_t)k * kLanes] = acc[k];  // raw: phase 2 continues the row
+}
+
+// ---------------------------------------------------------------------------
+// k_conv_kcsrq (BOLTZ_KCSR_YBUF 4): k_conv_kcsr with ONE y row per warp,
+// refilled by quarters.  The s3-grouped term order reads the staged y in s3
+// order, so quarter q of the next entry's y row is issued as soon as the
+// current entry has read its quarter q (KcsrTab qend), a whole entry ahead of
+// its use; the edge rows x[0], x[1], x[N-1] and y[N-1] (read from the start)
+// ride with the H slab in a double-buffered slot.  22.3 KB per warp instead of
+// 37.6 KB: 8 warps per SM (register-bound) instead of 6 (shared-memory-bound).
+// Measured on B200 (cfg5-shaped collide, 2048 cells, two runs): 145.0 / 145.6
+// against 144.9 / 144.9 ms with k_conv_kcsr -- the extra warps buy nothing, so
+// the REST launch is bound by L2 throughput (67%), not by latency; opt-in
+// (BOLTZ_KCSR_YBUF=4), oracle parity and the checksum as k_conv_kcsr.
+// ---------------------------------------------------------------------------
+template <int N>
+struct KcsrqLayout {
+    static constexpr int Y_BYTES = N * kLanes * 16;  // one y row
+    static constexpr int Q_BYTES = Y_BYTES / 4;
+    static constexpr int XE_BYTES = 4 * kLanes * 16;  // x[0], x[1], x[N-1], y[N-1]
+    static constexpr int H_BYTES = (kcsr_slab(N) * 8 + 15) / 16 * 16;
+    static constexpr int SLOT_BYTES = XE_BYTES + H_BYTES;
+    static constexpr int WARP_BYTES = Y_BYTES + 2 * SLOT_BYTES + 6 * 8;  // + 2 slot and 4 quarter mbarriers
+};
+#ifndef BOLTZ_KCSRQ_MINB
+#define BOLTZ_KCSRQ_MINB 4
+#endif
+template <int N>
+__global__ void __launch_bounds__(kLanes* kKcsrWarps, BOLTZ_KCSRQ_MINB)
+k_conv_kcsrq(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
+             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from,
+             int head_lpt) {
+    using LY = KcsrqLayout<N>;
+    constexpr KcsrTab<N> tab{};
+    static_assert(tab.qmono, "k_conv_kcsrq: the staged y must be read in quarter order");
+    constexpr int PE = KcsrTab<N>::COUNT;
+    constexpr int QB1 = tab.qbeg[1], QB2 = tab.qbeg[2], QB3 = tab.qbeg[3];
+    constexpr int QE0 = tab.qend[0], QE1 = tab.qend[1], QE2 = tab.qend[2], QE3 = tab.qend[3];
+    constexpr int N3 = N * N * N, QS = N / 4;
+    constexpr unsigned HB = kcsr_slab(N) * 8;
+    extern __shared__ __align__(16) char smem[];
+    const int2 unit = lpt_unit(list + 3 * nrows + 1, lpt_from, head_lpt);
+    const int wi = unit.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int g = unit.y * kKcsrWarps + wid;
+    if (g >= ngroups) return;
+    const int row = __ldg(list + nrows + 1 + wi);
+    const int e0 = __ldg(list + wi), e1 = __ldg(list + wi + 1);
+    char* wsm = smem + wid * LY::WARP_BYTES;
+    double2* ys = reinterpret_cast<double2*>(wsm);
+    char* slots = wsm + LY::Y_BYTES;
+    unsigned long long* barE = reinterpret_cast<unsigned long long*>(slots + 2 * LY::SLOT_BYTES);
+    unsigned long long* barQ = barE + 2;
+    const double2* Abase = A + (size_t)g * N3 * kLanes;
+    const double2* Ag = Abase + lane;
+    double2* Brow = B + ((size_t)g * N3 + (size_t)row * N) * kLanes + lane;
+    double2 acc[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) acc[k] = Brow[(size_t)k * kLanes];  // seeded: every REST row is a pair row
+    auto tma_slot = [&](int slot, int4 en) {  // the edge rows + the H slab of entry en
+        if (lane == 0) {
+            char* sl = slots + slot * LY::SLOT_BYTES;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(barE + slot, LY::XE_BYTES + HB);
+            bulk_g2s(sl, Abase + (size_t)en.x * kLanes, 2 * kLanes * 16, barE + slot);
+            bulk_g2s(sl + 2 * kLanes * 16, Abase + (size_t)(en.x + N - 1) * kLanes, kLanes * 16, barE + slot);
+            bulk_g2s(sl + 3 * kLanes * 16, Abase + (size_t)(en.y + N - 1) * kLanes, kLanes * 16, barE + slot);
+            bulk_g2s(sl + LY::XE_BYTES, H + (size_t)(unsigned)en.z, HB, barE + slot);
+        }
+    };
+    auto tma_q = [&](int q, int4 en) {  // quarter q of entry en's y row
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(barQ + q, LY::Q_BYTES);
+            bulk_g2s(ys + q * QS * kLanes, Abase + (size_t)(en.y + q * QS) * kLanes, LY::Q_BYTES, barQ + q);
+        }
+    };
+    EntWin win(ent, e0, e1, lane);
+    if (e0 < e1) {
+        if (lane == 0) {
+            for (int b = 0; b < 6; ++b) mbar_init(barE + b, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        int4 en = win.get(e0);
+        tma_slot(0, en);
+        for (int q = 0; q < 4; ++q) tma_q(q, en);
+        mbar_wait(barE, 0);
+        for (int e = e0; e < e1; ++e) {
+            const int i = e - e0, cur = i & 1;
+            const unsigned qp = (unsigned)(i & 1);  // each quarter barrier completes once per entry
+            const bool more = e + 1 < e1;
+            const int4 nx = more ? win.get(e + 1) : en;
+            __syncwarp();  // every lane finished with slot cur^1 (entry i-1)
+            if (more) tma_slot(cur ^ 1, nx);
+            const double2* xe = reinterpret_cast<const double2*>(slots + cur * LY::SLOT_BYTES);
+            KcsrEntry<N> f{acc, Ag + (size_t)en.x * kLanes, ys,
+                           reinterpret_cast<const double2*>(slots + cur * LY::SLOT_BYTES + LY::XE_BYTES), lane};
+            f.xa = xe[lane];
+            f.xb = xe[kLanes + lane];
+            f.xc = xe[2 * kLanes + lane];
+            f.yl = xe[3 * kLanes + lane];
+            mbar_wait(barQ, qp);
+            f.y0 = ys[lane];
+            f.y1 = ys[kLanes + lane];
+            auto refill = [&](int q) {
+                __syncwarp();  // every lane has read quarter q of this entry's y
+                if (more) tma_q(q, nx);
+            };
+            KcsrRun<0, QE0>::run(f);
+            refill(0);
+            KcsrRun<QE0, QB1>::run(f);
+            mbar_wait(barQ + 1, qp);
+            KcsrRun<QB1, QE1>::run(f);
+            refill(1);
+            KcsrRun<QE1, QB2>::run(f);
+            mbar_wait(barQ + 2, qp);
+            KcsrRun<QB2, QE2>::run(f);
+            refill(2);
+            KcsrRun<QE2, QB3>::run(f);
+            mbar_wait(barQ + 3, qp);
+            KcsrRun<QB3, QE3>::run(f);
+            refill(3);
+            KcsrRun<QE3, PE>::run(f);
+            if (more) mbar_wait(barE + (cur ^ 1), (unsigned)(((i + 1) >> 1) & 1));
             en = nx;
         }
     }
