@@ -614,3 +614,25 @@ def test_host_pipeline_mixed_pinned_pageable(gpu):
         _check(lib().boltz_collide_batch(op._h, f.ctypes.data, qout.data_ptr(), cells, 1.0, mout.data_ptr(),
                                          MEM_HOST, None))                     # pageable in, pinned out
         assert np.array_equal(qout.numpy(), qd) and np.array_equal(mout.numpy(), mid)
+
+
+def test_joint_lpt_tail_ragged_batch(gpu, O):
+    """N=16 at 4128 cells: 33 cell-group columns, so the mirror kernel's joint
+    longest-first tail (conv.cuh lpt_unit, the last 4 columns) runs with a
+    partial last column.  Bitwise the same cells split into two launches (one
+    of them below the tail threshold), and the tail cells against the oracle."""
+    import torch
+    n, L, cells = 16, 6.0, 4128
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, cells, seed=77)
+    G = table(n, L, 1.0)
+    with _op(n, L) as op:
+        fd = torch.from_numpy(f).to(gpu)
+        q_all = op.collide(fd).cpu().numpy()
+        q_a = op.collide(fd[:1056].contiguous()).cpu().numpy()   # 33 groups: 9 columns, no joint tail
+        q_b = op.collide(fd[1056:].contiguous()).cpu().numpy()   # 96 groups: 24 columns
+    assert np.array_equal(q_all[:1056], q_a)
+    assert np.array_equal(q_all[1056:], q_b)
+    for c in (3711, 4096, 4127):  # cells of the joint tail's columns, the last one partial
+        ref, _ = O.collide(n, L, G, f[c], 1.0, nthreads=8)
+        assert rel_max(q_all[c], ref) < TOL_Q, c
