@@ -810,8 +810,11 @@ __host__ __device__ constexpr int cell_doff(int n, int m3) {
     for (int i = 0; i < m3; ++i) o += cell_khi(n, i) - cell_klo(n, i);
     return o;
 }
+// warps per (row, cell) CTA; B200, cfg1 (50 RK2 steps as graph replays, two
+// runs): 4 warps 2.87 / 2.89 ms, 8: 3.33 / 3.34, 16: 2.98 / 2.98 (16 with 64
+// registers: 3.07 / 3.08)
 #ifndef BOLTZ_CELL_WARPS
-#define BOLTZ_CELL_WARPS 16
+#define BOLTZ_CELL_WARPS 4
 #endif
 constexpr int kCellWarps = BOLTZ_CELL_WARPS;
 template <int N>
