@@ -410,6 +410,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+// Three 1D TMA copies onto one mbarrier (expect_tx of their total) issued by one
+// elected lane; called by the whole, converged warp.  Replaces an `if (lane ==
+// 0)` block, which ptxas wraps in a divergent ELECT loop per copy (ncu source
+// view of k_conv_mirror2<16>: ~2% of all stall samples on that issue code).
+#ifndef BOLTZ_TMA_ELECT
+#define BOLTZ_TMA_ELECT 1
+#endif
+__device__ __forceinline__ void bulk_g2s3_elect(unsigned long long* bar, void* d0, const void* s0, unsigned b0,
+                                                void* d1, const void* s1, unsigned b1, void* d2, const void* s2,
+                                                unsigned b2) {
+    asm volatile(
+        "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+        " @p fence.proxy.async.shared::cta;\n"
+        " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %4, [%0];\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%5], [%6], %7, [%0];\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%8], [%9], %10, [%0];\n}"
+        ::"r"(smem_u32(bar)), "r"(b0 + b1 + b2), "r"(smem_u32(d0)), "l"(s0), "r"(b0), "r"(smem_u32(d1)), "l"(s1),
+          "r"(b1), "r"(smem_u32(d2)), "l"(s2), "r"(b2)
+        : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // k_conv_kcs: one k-chunk per kernel; the y row and the H slab of the next row
@@ -1251,9 +1272,13 @@ k_conv_mirror2(const double2* __restrict__ A, double2* __restrict__ B, const dou
         const double2* ys = reinterpret_cast<const double2*>(wsm + 2 * PL::X_BYTES);
         const double2* Abase = A + (size_t)g * N3 * kLanes;
         double2* Bm = B + ((size_t)g * N3 + (size_t)(rm < 0 ? 0 : rm) * N) * kLanes + lane;
-        auto issue = [&](int slot, int4 en) {
-            if (lane == 0) {
-                const unsigned hb = 8u * (en.w == BT_A ? m2_slab(N, BT_A) : m2_slab(N, BT_FULL));
+        auto issue = [&](int slot, int4 en) {  // the whole warp (converged)
+            const unsigned hb = 8u * (en.w == BT_A ? m2_slab(N, BT_A) : m2_slab(N, BT_FULL));
+            if constexpr (BOLTZ_TMA_ELECT) {
+                bulk_g2s3_elect(bar + slot, wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES,
+                                wsm + 2 * PL::X_BYTES, Abase + (size_t)en.y * kLanes, PL::X_BYTES,
+                                wsm + 3 * PL::X_BYTES + slot * PL::H_BYTES, H + (size_t)(unsigned)en.z, hb);
+            } else if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + hb);
                 bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
