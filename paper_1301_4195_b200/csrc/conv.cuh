@@ -417,6 +417,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 #ifndef BOLTZ_TMA_ELECT
 #define BOLTZ_TMA_ELECT 1
 #endif
+// one copy: expect_tx of its bytes + the copy, by one elected lane
+__device__ __forceinline__ void bulk_g2s1_elect(unsigned long long* bar, void* d0, const void* s0, unsigned b0) {
+    asm volatile(
+        "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+        " @p fence.proxy.async.shared::cta;\n"
+        " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+        " @p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%2], [%3], %1, [%0];\n}"
+        ::"r"(smem_u32(bar)), "r"(b0), "r"(smem_u32(d0)), "l"(s0)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_g2s3_elect(unsigned long long* bar, void* d0, const void* s0, unsigned b0,
                                                 void* d1, const void* s1, unsigned b1, void* d2, const void* s2,
                                                 unsigned b2) {
@@ -1706,17 +1716,22 @@ k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double
 #pragma unroll
         for (int kk = 0; kk < T; ++kk) acc[kk] = make_double2(0.0, 0.0);
     }
-    auto tma_h = [&](int slot, int4 en) {
-        if (lane == 0) {
-            const bool rest = PHASE == 3 && en.w == BT_REST;
-            const unsigned bytes = rest ? BYTES_R : BYTES;
+    auto tma_h = [&](int slot, int4 en) {  // the whole warp (converged)
+        const bool rest = PHASE == 3 && en.w == BT_REST;
+        const unsigned bytes = rest ? BYTES_R : BYTES;
+        if constexpr (BOLTZ_TMA_ELECT) {
+            bulk_g2s1_elect(bar + slot, hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z + (rest ? OFF_R : OFF),
+                            bytes);
+        } else if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, bytes);
             bulk_g2s(hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z + (rest ? OFF_R : OFF), bytes, bar + slot);
         }
     };
-    auto tma_y = [&](int slot, int4 en) {
-        if (lane == 0) {
+    auto tma_y = [&](int slot, int4 en) {  // the whole warp (converged)
+        if constexpr (BOLTZ_TMA_ELECT) {
+            bulk_g2s1_elect(bar + slot, ys, Abase + (size_t)en.y * kLanes, LY::Y_BYTES);
+        } else if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, LY::Y_BYTES);
             bulk_g2s(ys, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
@@ -2090,19 +2105,26 @@ k_conv_kcsr(const double2* __restrict__ A, double2* __restrict__ B, const double
     double2 acc[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) acc[k] = Brow[(size_t)k * kLanes];  // seeded: every phase-1 row is a pair row
-    auto tma_h = [&](int slot, int4 en) {
-        if (lane == 0) {
+    auto tma_h = [&](int slot, int4 en) {  // the whole warp (converged)
+        if constexpr (BOLTZ_TMA_ELECT) {
+            bulk_g2s1_elect(bar + slot, hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z, HB);
+        } else if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, HB);
             bulk_g2s(hbase + slot * LY::H_BYTES, H + (size_t)(unsigned)en.z, HB, bar + slot);
         }
     };
-    auto tma_y = [&](int slot, int4 en) {
-        if (lane == 0) {
+    auto tma_y = [&](int slot, int4 en) {  // the whole warp (converged)
+        double2* yd = const_cast<double2*>(ys0) + (BOLTZ_KCSR_YBUF == 2 ? slot * N * kLanes : 0);
+        if constexpr (BOLTZ_TMA_ELECT && LY::XE_BYTES > 0) {
+            char* xe = xebase + slot * LY::XE_BYTES;
+            bulk_g2s3_elect(bar + slot, yd, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, xe,
+                            Abase + (size_t)en.x * kLanes, 2 * kLanes * 16, xe + 2 * kLanes * 16,
+                            Abase + (size_t)(en.x + N - 1) * kLanes, kLanes * 16);
+        } else if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(bar + slot, LY::Y_BYTES + LY::XE_BYTES);
-            bulk_g2s(const_cast<double2*>(ys0) + (BOLTZ_KCSR_YBUF == 2 ? slot * N * kLanes : 0),
-                     Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
+            bulk_g2s(yd, Abase + (size_t)en.y * kLanes, LY::Y_BYTES, bar + slot);
             if constexpr (LY::XE_BYTES > 0) {
                 char* xe = xebase + slot * LY::XE_BYTES;
                 bulk_g2s(xe, Abase + (size_t)en.x * kLanes, 2 * kLanes * 16, bar + slot);
