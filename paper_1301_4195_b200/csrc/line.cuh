@@ -29,6 +29,17 @@
 
 namespace boltz_gpu {
 
+// the line kernels' TMA plane loads / stores issued by every warp's elected
+// lane (2 planes per warp at N = 16) instead of one thread issuing all of them.
+// B200, cfg2 RK2 step (three runs): K3 (k_inv_line2, both launches) 0.360 ->
+// 0.350 ms; K1's per-block plane stores lost (0.107 -> 0.114 ms), so K1 keeps
+// thread 0 (BOLTZ_LINE_SPREAD_K1)
+#ifndef BOLTZ_LINE_SPREAD
+#define BOLTZ_LINE_SPREAD 1
+#endif
+#ifndef BOLTZ_LINE_SPREAD_K1
+#define BOLTZ_LINE_SPREAD_K1 0
+#endif
 #ifndef BOLTZ_LINE_MINB
 #define BOLTZ_LINE_MINB 2  // CTAs per SM the line kernels are compiled for (registers), one cell per CTA
 #endif
@@ -152,6 +163,26 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                  ::"l"(map), "r"(c0), "r"(c1), "r"(smem_u32(src)) : "memory");
 }
+// the same copies issued by one elected lane of a converged warp (the predicate
+// inside the asm: no divergent single-thread region around the TMA instruction)
+__device__ __forceinline__ void tma_store_2d_elect(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+                 " @p cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n}"
+                 ::"l"(map), "r"(c0), "r"(c1), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit_elect() {
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n @p cp.async.bulk.commit_group;\n}" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_elect() {
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n @p cp.async.bulk.wait_group.read 0;\n}" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all_elect() {
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n @p cp.async.bulk.wait_group 0;\n}" ::: "memory");
+}
+__device__ __forceinline__ void bulk_commit_wait_all_elect() {
+    asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+                 " @p cp.async.bulk.commit_group;\n @p cp.async.bulk.wait_group 0;\n}" ::: "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -164,6 +195,13 @@ template <int N>
 __device__ __forceinline__ int swz(int byte) {
     constexpr int mask = N * 8 >= 128 ? 7 : N * 8 >= 64 ? 3 : 1;
     return byte ^ (((byte >> 7) & mask) << 4);
+}
+__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                  unsigned long long* bar) {
+    asm volatile(
+        "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+        " @p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n}"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             unsigned long long* bar) {
@@ -267,7 +305,8 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
         if constexpr (!BOLTZ_LINE_TMA_LOAD) load(blk + gridDim.x);  // in flight through passes 2 and 3
         RegFFT<N, -1, N>::run(x);
         if (blk != blockIdx.x) {  // the previous block's stores have read the staging image
-            if (t == 0) bulk_wait_read();
+            if constexpr (BOLTZ_LINE_SPREAD_K1) bulk_wait_read_elect();  // every warp's own stores
+            else if (t == 0) bulk_wait_read();
             __syncthreads();
         }
 #pragma unroll
@@ -290,7 +329,14 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
             if (BOLTZ_LINE_WAR_FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();
-        if (t == 0) {
+        if constexpr (BOLTZ_LINE_SPREAD_K1) {  // each warp's elected lane stores its planes
+            const long long cell0 = blk * CPB;
+            const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
+            for (int j = t >> 5; j < N; j += LN::WARPS) tma_store_2d_elect(&tmA, smem_line + j * NN * CPB, c0, row0 + j * NN);
+            bulk_commit_elect();
+            if constexpr (BOLTZ_LINE_TMA_LOAD)
+                if (t == 0) issue(blk + 2 * (long long)gridDim.x);
+        } else if (t == 0) {
             const long long cell0 = blk * CPB;
             const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
 #pragma unroll 1
@@ -299,7 +345,8 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
             if constexpr (BOLTZ_LINE_TMA_LOAD) issue(blk + 2 * (long long)gridDim.x);
         }
     }
-    if (t == 0) bulk_wait_all();
+    if constexpr (BOLTZ_LINE_SPREAD_K1) bulk_wait_all_elect();
+    else if (t == 0) bulk_wait_all();
 }
 
 template <int N, bool FWD, int CPB>
@@ -527,17 +574,35 @@ k_inv_line2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUt
     const bool live = cell < ncells;
     const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
     char* myline = img + sub * N3 * 8;  // this cell's line image; the thread's line is row ln
-    if (t == 0) {
-        mbar_init(bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(bar, (unsigned)(N3 * CPB * 16) + (has_base ? F_BYTES : 0u));
+    if constexpr (BOLTZ_LINE_SPREAD) {
+        // the barrier (expecting every byte) first, then each warp's elected lane
+        // issues its share of the plane loads
+        constexpr int W = LN::WARPS;
+        if (t == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(bar, (unsigned)(N3 * CPB * 16) + (has_base ? F_BYTES : 0u));
+        }
+        __syncthreads();
+        const int w = t >> 5;
+#pragma unroll
+        for (int j = w; j < N; j += W) tma_load_2d_elect(cubes + j * NN * CPB, &tmB, c0, row0 + j * NN, bar);
+        if (has_base && w == W - 1)
+#pragma unroll
+            for (int c = 0; c < CPB; ++c) tma_load_2d_elect(img + c * N3 * 8, &tmBase, 0, (int)((cell0 + c) * NN), bar);
+    } else {
+        if (t == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            mbar_expect_tx(bar, (unsigned)(N3 * CPB * 16) + (has_base ? F_BYTES : 0u));
 #pragma unroll 1
-        for (int j = 0; j < N; ++j) tma_load_2d(cubes + j * NN * CPB, &tmB, c0, row0 + j * NN, bar);
-        if (has_base)
+            for (int j = 0; j < N; ++j) tma_load_2d(cubes + j * NN * CPB, &tmB, c0, row0 + j * NN, bar);
+            if (has_base)
 #pragma unroll 1
-            for (int c = 0; c < CPB; ++c) tma_load_2d(img + c * N3 * 8, &tmBase, 0, (int)((cell0 + c) * NN), bar);
+                for (int c = 0; c < CPB; ++c) tma_load_2d(img + c * N3 * 8, &tmBase, 0, (int)((cell0 + c) * NN), bar);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     mbar_wait(bar, 0);
     // pass 1 (axis 0, i1) from the group image: thread ln = (i2, i3)
     double2 x[N];
@@ -675,7 +740,12 @@ k_inv_line2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUt
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        if (t == 0) {
+        if constexpr (BOLTZ_LINE_SPREAD) {  // each warp's elected lane stores its planes
+            const int w = t >> 5;
+#pragma unroll
+            for (int j = w; j < N; j += LN::WARPS) tma_store_2d_elect(&tmNext, cubes + j * NN * CPB, c0, row0 + j * NN);
+            bulk_commit_wait_all_elect();
+        } else if (t == 0) {
 #pragma unroll 1
             for (int j = 0; j < N; ++j) tma_store_2d(&tmNext, cubes + j * NN * CPB, c0, row0 + j * NN);
             bulk_commit();
