@@ -40,6 +40,12 @@ namespace boltz_gpu {
 #ifndef BOLTZ_LINE_SPREAD_K1
 #define BOLTZ_LINE_SPREAD_K1 0
 #endif
+// K1's plane stores from warp 0 with the predicate inside the asm (elect.sync
+// picks lane 0 of the converged warp: thread 0, which waits on the bulk group);
+// measured slower too (K1 0.108 -> 0.114 ms), off
+#ifndef BOLTZ_LINE_K1_ELECT
+#define BOLTZ_LINE_K1_ELECT 0
+#endif
 #ifndef BOLTZ_LINE_MINB
 #define BOLTZ_LINE_MINB 2  // CTAs per SM the line kernels are compiled for (registers), one cell per CTA
 #endif
@@ -336,7 +342,15 @@ k_fwd_line_tma(const double* __restrict__ f, const __grid_constant__ CUtensorMap
             bulk_commit_elect();
             if constexpr (BOLTZ_LINE_TMA_LOAD)
                 if (t == 0) issue(blk + 2 * (long long)gridDim.x);
-        } else if (t == 0) {
+        } else if (BOLTZ_LINE_K1_ELECT && t < 32) {  // warp 0, the stores by its elected lane (= thread 0)
+            const long long cell0 = blk * CPB;
+            const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
+#pragma unroll
+            for (int j = 0; j < N; ++j) tma_store_2d_elect(&tmA, smem_line + j * NN * CPB, c0, row0 + j * NN);
+            bulk_commit_elect();
+            if constexpr (BOLTZ_LINE_TMA_LOAD)
+                if (t == 0) issue(blk + 2 * (long long)gridDim.x);
+        } else if (!BOLTZ_LINE_K1_ELECT && t == 0) {
             const long long cell0 = blk * CPB;
             const int c0 = (int)(cell0 % kLanes) * 2, row0 = (int)(cell0 / kLanes) * N3;
 #pragma unroll 1
@@ -707,7 +721,11 @@ k_inv_line2(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUt
             *reinterpret_cast<double2*>(myline + swz<N>(ln * N * 8 + j * 16)) = make_double2(v[2 * j], v[2 * j + 1]);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
-        if (t == 0) {
+        if (BOLTZ_LINE_SPREAD && t < 32) {  // warp 0, predicate inside the asm
+#pragma unroll
+            for (int c = 0; c < CPB; ++c) tma_store_2d_elect(&tmOut, img + c * N3 * 8, 0, (int)((cell0 + c) * NN));
+            bulk_commit_wait_all_elect();
+        } else if (!BOLTZ_LINE_SPREAD && t == 0) {
 #pragma unroll 1
             for (int c = 0; c < CPB; ++c) tma_store_2d(&tmOut, img + c * N3 * 8, 0, (int)((cell0 + c) * NN));
             bulk_commit();
