@@ -674,16 +674,19 @@ def bench_n32(args, dev, local, hw):
     ms = 0.0
     wit = list(WITNESS32)
     snap = None
-    for i in range(steps):
-        if i == steps - 1:
-            snap = f[wit].cpu().numpy()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        op.collision_rk2(f, 1e-3)
-        e1.record()
-        torch.cuda.synchronize()
-        ms += e0.elapsed_time(e1)
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            if i == steps - 1:
+                snap = f[wit].cpu().numpy()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            op.collision_rk2(f, 1e-3)
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    ms = sum(step_ms)
     kms, kl = op.timing(reset=True)
     after = f[wit].cpu().numpy()
     op.close()
@@ -697,7 +700,7 @@ def bench_n32(args, dev, local, hw):
             "value": 2 * cells * steps / (ms * 1e-3), "unit": "evals/s", "steps": steps, "warmup": warm,
             "ms_per_step": ms / steps, "conv_tflops_algorithmic": flop_total / (kms["conv"] * 1e-3) / 1e12,
             "conv_ms_per_kernel": conv_avg, "conv_kernels_per_eval": kl["conv"] / (2 * steps),
-            "table_generate_s": round(t_gen, 2),
+            "table_generate_s": round(t_gen, 2), "step_ms": [round(x, 2) for x in step_ms], "clocks": clk.summary(),
             "parity": {"cells_n32": wit,
                        "max_rel_increment_n32": max(float(np.abs(a - r).max() / max(np.abs(r - b).max(), 1e-300))
                                                     for a, r, b in zip(after, ref, snap)),
