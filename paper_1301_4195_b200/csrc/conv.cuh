@@ -629,8 +629,12 @@ __device__ __forceinline__ void pipe_rows(char* wsm, const double2* __restrict__
         // slot's mbarrier (slot = entry parity); every lane waits on the parity
         unsigned long long* bar = reinterpret_cast<unsigned long long*>(wsm + 3 * PL::X_BYTES + 2 * PL::H_BYTES);
         const double2* Abase = Ag - lane;
-        auto issue = [&](int slot, int2 en, int e) {
-            if (lane == 0) {
+        auto issue = [&](int slot, int2 en, int e) {  // the whole warp (converged)
+            if constexpr (BOLTZ_TMA_ELECT) {
+                bulk_g2s3_elect(bar + slot, wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES,
+                                wsm + 2 * PL::X_BYTES, Abase + (size_t)en.y * kLanes, PL::X_BYTES,
+                                wsm + 3 * PL::X_BYTES + slot * PL::H_BYTES, H + (size_t)e * PL::SLAB_KC, PL::H_BYTES);
+            } else if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of the slot are done
                 mbar_expect_tx(bar + slot, 2 * PL::X_BYTES + PL::H_BYTES);
                 bulk_g2s(wsm + slot * PL::X_BYTES, Abase + (size_t)en.x * kLanes, PL::X_BYTES, bar + slot);
