@@ -1236,80 +1236,90 @@ struct Launch {
         if constexpr (mirror_kcs_n(N)) {
             if (hermitian && c->mirror && c->schedule == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
-                constexpr int W = kcsm_warps(N);
-                constexpr int P0 = kcsf_n(N) ? 4 : 0;  // the phase-0 kernels: with the REST fold or plain
-                const int smem_ph[5] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
-                                        W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES,
-                                        W * KcsmLayout<N, 4>::WARP_BYTES + KcsmLayout<N, 4>::TMEM_BYTES};
-                static PerDevice configured;  // attributes are per device
-                configured.once(c->device, [&] {
-                    auto cfg = [&](auto fn, int ph) {
-                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ph[ph]));
-                        CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                    };
-                    cfg(k_conv_kcsm<N, 0, P0>, P0);
-                    cfg(k_conv_kcsm<N, KC1, P0>, P0);
-                    if constexpr (kcsr_n(N)) {
-                        if constexpr (BOLTZ_KCSR_YBUF == 4) {
-                            CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    KcsrqLayout<N>::WARP_BYTES * kKcsrWarps));
-                            CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                        } else {
-                            CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                    KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
-                            CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                // 8-warp CTAs at N = 24 (kcsm_warps) unless the batch has at most kConvWarps
+                // groups: then kConvWarps-warp CTAs, so no CTA carries idle warps' shared memory
+                auto run = [&](auto wtag) {
+                    constexpr int W = decltype(wtag)::value;
+                    constexpr int P0 = kcsf_n(N) ? 4 : 0;  // the phase-0 kernels: with the REST fold or plain
+                    const int smem_ph[5] = {W * KcsmLayout<N, 0>::WARP_BYTES, W * KcsmLayout<N, 1>::WARP_BYTES,
+                                            W * KcsmLayout<N, 2>::WARP_BYTES, W * KcsmLayout<N, 3>::WARP_BYTES,
+                                            W * KcsmLayout<N, 4>::WARP_BYTES + KcsmLayout<N, 4>::TMEM_BYTES};
+                    static PerDevice configured;  // attributes are per device
+                    configured.once(c->device, [&] {
+                        auto cfg = [&](auto fn, int ph) {
+                            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ph[ph]));
+                            CK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                        };
+                        cfg(k_conv_kcsm<N, 0, P0, W>, P0);
+                        cfg(k_conv_kcsm<N, KC1, P0, W>, P0);
+                        if constexpr (kcsr_n(N)) {
+                            if constexpr (BOLTZ_KCSR_YBUF == 4) {
+                                CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        KcsrqLayout<N>::WARP_BYTES * kKcsrWarps));
+                                CK(cudaFuncSetAttribute(k_conv_kcsrq<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                            } else {
+                                CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        KcsrLayout<N>::WARP_BYTES * kKcsrWarps));
+                                CK(cudaFuncSetAttribute(k_conv_kcsr<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                            }
                         }
-                    }
-                    if constexpr (kcsm_split(N)) {
-                        cfg(k_conv_kcsm<N, 0, 1>, 1);
-                        cfg(k_conv_kcsm<N, KC1, 1>, 1);
-                        cfg(k_conv_kcsm<N, 0, 2>, 2);
-                        cfg(k_conv_kcsm<N, KC1, 2>, 2);
+                        if constexpr (kcsm_split(N)) {
+                            cfg(k_conv_kcsm<N, 0, 1, W>, 1);
+                            cfg(k_conv_kcsm<N, KC1, 1, W>, 1);
+                            cfg(k_conv_kcsm<N, 0, 2, W>, 2);
+                            cfg(k_conv_kcsm<N, KC1, 2, W>, 2);
+                        } else {
+                            cfg(k_conv_kcsm<N, 0, 3, W>, 3);
+                            cfg(k_conv_kcsm<N, KC1, 3, W>, 3);
+                        }
+                    });
+                    const unsigned gy = (unsigned)((ng + W - 1) / W);
+                    // longest rows first: every column (each on its own) for grids a few waves
+                    // deep, else the last kcs_lpt_tail() columns jointly (conv.cuh lpt_unit)
+                    auto few = [&](int nrows, unsigned cols) { return (int64_t)nrows * cols < 8 * 2 * 148; };
+                    auto lpt = [&](int nrows) { return few(nrows, gy) ? (int)gy : std::max(0, (int)gy - kcs_lpt_tail()); };
+                    Timed t_(c, KIND_CONV, s);
+                    // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
+                    auto go = [&](auto kern, int ph) {
+                        // list 1 runs phase 3 when not split; list 0 phase 4 with the REST fold
+                        const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph == 0 ? P0 : ph;
+                        kern<<<dim3(c->nK[ph], gy), kLanes * W, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
+                                                                                    c->dListK[ph], c->nK[ph], (int)ng,
+                                                                                    lpt(c->nK[ph]), (int)few(c->nK[ph], gy));
+                    };
+                    go(k_conv_kcsm<N, 0, P0, W>, 0);
+                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, P0, W>, 0);
+                    if constexpr (kcsf_n(N)) {  // REST folded into phase 0: FULL entries only
+                        go(k_conv_kcsm<N, 0, 2, W>, 2);
+                        if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2, W>, 2);
+                    } else if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
+                        const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
+                        const bool fr = few(c->nK[1], gr);
+                        const int lr = fr ? (int)gr : std::max(0, (int)gr - kcs_lpt_tail());
+                        if constexpr (BOLTZ_KCSR_YBUF == 4)  // one y row per warp, refilled by quarters
+                            k_conv_kcsrq<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps,
+                                              KcsrqLayout<N>::WARP_BYTES * kKcsrWarps, s>>>(
+                                c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
+                        else
+                            k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
+                                             s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
+                        go(k_conv_kcsm<N, 0, 2, W>, 2);
+                        if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2, W>, 2);
+                    } else if constexpr (kcsm_split(N)) {
+                        go(k_conv_kcsm<N, 0, 1, W>, 1);
+                        if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 1, W>, 1);
+                        go(k_conv_kcsm<N, 0, 2, W>, 2);
+                        if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2, W>, 2);
                     } else {
-                        cfg(k_conv_kcsm<N, 0, 3>, 3);
-                        cfg(k_conv_kcsm<N, KC1, 3>, 3);
+                        go(k_conv_kcsm<N, 0, 3, W>, 1);
+                        if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3, W>, 1);
                     }
-                });
-                const unsigned gy = (unsigned)((ng + W - 1) / W);
-                // longest rows first: every column (each on its own) for grids a few waves
-                // deep, else the last kcs_lpt_tail() columns jointly (conv.cuh lpt_unit)
-                auto few = [&](int nrows, unsigned cols) { return (int64_t)nrows * cols < 8 * 2 * 148; };
-                auto lpt = [&](int nrows) { return few(nrows, gy) ? (int)gy : std::max(0, (int)gy - kcs_lpt_tail()); };
-                Timed t_(c, KIND_CONV, s);
-                // phase 0 (pair leaders' A sums + mirror seeds), 1 (REST), 2 (FULL, final), per k-chunk
-                auto go = [&](auto kern, int ph) {
-                    // list 1 runs phase 3 when not split; list 0 phase 4 with the REST fold
-                    const int kph = ph == 1 && !kcsm_split(N) ? 3 : ph == 0 ? P0 : ph;
-                    kern<<<dim3(c->nK[ph], gy), kLanes * W, smem_ph[kph], s>>>(c->dA, c->dB, c->dMH, c->dMEnt,
-                                                                                c->dListK[ph], c->nK[ph], (int)ng,
-                                                                                lpt(c->nK[ph]), (int)few(c->nK[ph], gy));
                 };
-                go(k_conv_kcsm<N, 0, P0>, 0);
-                if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, P0>, 0);
-                if constexpr (kcsf_n(N)) {  // REST folded into phase 0: FULL entries only
-                    go(k_conv_kcsm<N, 0, 2>, 2);
-                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
-                } else if constexpr (kcsr_n(N)) {  // the pair rows' REST entries, both k-chunks in one launch
-                    const unsigned gr = (unsigned)((ng + kKcsrWarps - 1) / kKcsrWarps);
-                    const bool fr = few(c->nK[1], gr);
-                    const int lr = fr ? (int)gr : std::max(0, (int)gr - kcs_lpt_tail());
-                    if constexpr (BOLTZ_KCSR_YBUF == 4)  // one y row per warp, refilled by quarters
-                        k_conv_kcsrq<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps,
-                                          KcsrqLayout<N>::WARP_BYTES * kKcsrWarps, s>>>(
-                            c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
-                    else
-                        k_conv_kcsr<N><<<dim3(c->nK[1], gr), kLanes * kKcsrWarps, KcsrLayout<N>::WARP_BYTES * kKcsrWarps,
-                                         s>>>(c->dA, c->dB, c->dMH, c->dMEnt, c->dListK[1], c->nK[1], (int)ng, lr, (int)fr);
-                    go(k_conv_kcsm<N, 0, 2>, 2);
-                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
-                } else if constexpr (kcsm_split(N)) {
-                    go(k_conv_kcsm<N, 0, 1>, 1);
-                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 1>, 1);
-                    go(k_conv_kcsm<N, 0, 2>, 2);
-                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 2>, 2);
+                if constexpr (kcsm_warps(N) != kConvWarps) {
+                    if (ng <= kConvWarps) run(std::integral_constant<int, kConvWarps>{});
+                    else run(std::integral_constant<int, kcsm_warps(N)>{});
                 } else {
-                    go(k_conv_kcsm<N, 0, 3>, 1);
-                    if constexpr (NK > 1) go(k_conv_kcsm<N, KC1, 3>, 1);
+                    run(std::integral_constant<int, kConvWarps>{});
                 }
                 c->launches[KIND_CONV] += kcsf_n(N) ? 2 * NK - 1 : kcsr_n(N) ? 2 * NK : (kcsm_split(N) ? 3 : 2) * NK - 1;  // one timing bracket
                 CK(cudaGetLastError());

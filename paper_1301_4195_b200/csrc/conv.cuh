@@ -1658,12 +1658,14 @@ __device__ __forceinline__ void kf_pass(uint32_t ta, const double2* __restrict__
     }
 }
 
-template <int N, int KC, int PHASE>
-__global__ void __launch_bounds__(kLanes* kcsm_warps(N), PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
+// WW: cell groups (warps) per CTA -- kcsm_warps(N), or kConvWarps at N = 24 for
+// batches of at most kConvWarps groups, where 8-warp CTAs would run half empty
+template <int N, int KC, int PHASE, int WW = kcsm_warps(N)>
+__global__ void __launch_bounds__(kLanes* WW, PHASE == 1 ? BOLTZ_KCSM_REST_MINB : BOLTZ_K0_MINB)
 k_conv_kcsm(const double2* __restrict__ A, double2* __restrict__ B, const double* __restrict__ H,
             const int4* __restrict__ ent, const int* __restrict__ list, int nrows, int ngroups, int lpt_from, int head_lpt) {
     using LY = KcsmLayout<N, PHASE>;
-    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N, W = kcsm_warps(N);
+    constexpr int T = LY::T, NK = LY::NK, N3 = N * N * N, W = WW;
     constexpr bool FOLD = PHASE == 4;
     static_assert(!FOLD || (T % 4 == 0 && W <= 4), "the fold: 4-output TMEM batches, one TMEM lane quarter per warp");
     constexpr int PH = kcsm_ph(PHASE);

@@ -446,6 +446,28 @@ def test_n24_maxwell_molecules_kcsm_vs_oracle(gpu, O):
         assert rel_max(q[c], ref) < TOL_Q, c
 
 
+def test_n24_small_batch_cta_shape_bitwise(gpu, O):
+    """N=24 batches of at most 4 cell groups run k_conv_kcsm with 4-warp CTAs
+    instead of 8 (the 8-rank cfg4 shard is 128 cells): the first 128 cells of a
+    200-cell batch (8-warp CTAs) are bitwise the same cells collided alone
+    (4-warp CTAs), for collide and an RK2 step; cell 127 against the oracle."""
+    import torch
+    n, L, lam = 24, 8.0, 1.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 200, seed=2424)
+    with _op(n, L, lam) as op:
+        big = op.collide(torch.from_numpy(f).to(gpu)).cpu().numpy()
+        small = op.collide(torch.from_numpy(f[:128].copy()).to(gpu)).cpu().numpy()
+        assert np.array_equal(big[:128], small)
+        fb = torch.from_numpy(f).to(gpu)
+        fs = torch.from_numpy(f[:128].copy()).to(gpu)
+        op.collision_rk2(fb, 1e-3)
+        op.collision_rk2(fs, 1e-3)
+        assert torch.equal(fb[:128], fs)
+    ref, _ = O.collide(n, L, table(n, L, lam), f[127], 1.0, nthreads=8)
+    assert rel_max(small[127], ref) < TOL_Q
+
+
 def test_host_pipeline_cfg2_size_matches_device_path(gpu):
     """The e2e path bench.py times: N=16 x 4096 cells through the host pipeline
     (mirror schedule chunking 1,3,3,1 over two compute streams and three
