@@ -542,13 +542,16 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
     import torch
     import torch.distributed as dist
     from paper_1301_4195_b200 import NcclHalo, scenarios
-    from paper_1301_4195_b200.solver import Boundary, Solver1D
+    from paper_1301_4195_b200.solver import Boundary, Solver1D, k2_schedule, plan_decomposition
     grid = op.grid
     nx = 256
     x, dx = scenarios.geometric_grid(nx, 20.0, 1.02)
     m0 = scenarios.maxwellian(grid, 1.0, (0, 0, 0), 1.0)
     init = lambda start, count: np.tile(m0, (count, 1))  # noqa: E731
-    op.set_schedule("latency")  # <= 256 cells per rank: K2 rows split over 4 warps
+    # K2 rows split into fixed segments: 4 (<= 256 cells per rank) or 8 (<= 64: the 8-rank shard); one schedule for
+    # every rank and for the one-rank recomputation, so bitwise_vs_1rank holds
+    sched = k2_schedule(grid.n, max(c for _, c in plan_decomposition(nx, world)))
+    op.set_schedule(sched)
     kw = dict(left=Boundary("wall", 2.0), right=Boundary("extrap"), device=dev)
     halo = None
     if world > 1:
@@ -589,7 +592,7 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
     out = {"workload": "cfg3: Nx=256 geometric (1.02) on [0,20], N=16 L=6, diffuse wall T_w=2, dt=CFL 0.9",
            "ranks": world, "scaling": "strong" if world > 1 else None, "steps": steps, "ms_per_step": ms / steps,
            "cells_steps_per_s": nx * steps / (ms * 1e-3), "evals_per_s": 2 * nx * steps / (ms * 1e-3),
-           "mode": ("CUDA graph of 3 Strang steps" if graph else "eager Strang steps") + ", K2 latency schedule"
+           "mode": ("CUDA graph of 3 Strang steps" if graph else "eager Strang steps") + f", K2 {sched} schedule"
                    + (", NCCL halo (boltz_halo_exchange) inside the graph, overlapped with the ghost-free rows"
                       if isinstance(halo, NcclHalo) else
                       ", host-staged gloo halo (plumbing check, not a measurement)" if world > 1 else ""),

@@ -47,6 +47,21 @@ def plan_decomposition(ncells: int, nranks: int) -> List[Tuple[int, int]]:
     return out
 
 
+def k2_schedule(n: int, cells_per_rank: int) -> str:
+    """The K2 schedule for a rank's collision batch (CollisionOperator.set_schedule).
+    Small batches at N <= 16 split each row's entries into fixed segments:
+    8 up to 64 cells, 4 up to 256 (B200, ms per RK2 step, schedules 1 / 2:
+    32 cells 0.235 / 0.196, 64 cells 0.296 / 0.291, 128 cells 0.491 / 0.500,
+    256 cells 0.893 / 0.914; `scripts/dev/sched_sweep.py`).  Every rank of a run
+    must use the same schedule for the decomposition to stay bitwise transparent
+    (SPEC.md:465), so callers pick it from the largest rank's cell count."""
+    if n <= 16 and cells_per_rank <= 64:
+        return "latency8"
+    if n <= 16 and cells_per_rank <= 256:
+        return "latency"
+    return "throughput"
+
+
 def predict_speedup(n: int, p: int, N: int, M: int, T_mem: float, T_flop: float, C: float) -> float:
     """The paper's leading-order speed-up model of the decomposed solver
     (§4.2; reference SPEC.md:454-462): n processes of p cores, N^3

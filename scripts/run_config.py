@@ -26,7 +26,7 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios  # noqa: E402
-from paper_1301_4195_b200.solver import Boundary, Solver1D, plan_decomposition  # noqa: E402
+from paper_1301_4195_b200.solver import Boundary, Solver1D, k2_schedule, plan_decomposition  # noqa: E402
 
 
 def moments_np(grid, f):
@@ -65,8 +65,8 @@ def spatial(args, rank, world, dev):
     del G
     if args.schedule != "auto":
         op.set_schedule(args.schedule)
-    elif n <= 16 and -(-nx // world) <= 256:  # small per-rank batches: rows split over warps
-        op.set_schedule("latency")
+    else:  # small per-rank batches: rows split over warps (the same schedule on every rank)
+        op.set_schedule(k2_schedule(n, -(-nx // world)))
     t_setup = time.perf_counter() - t0
 
     def init(start, count):

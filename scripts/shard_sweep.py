@@ -22,7 +22,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_1301_4195_b200 import CollisionOperator, KernelSpec, VelocityGrid, generate_table, scenarios  # noqa: E402
-from paper_1301_4195_b200.solver import Boundary, Solver1D, plan_decomposition  # noqa: E402
+from paper_1301_4195_b200.solver import Boundary, Solver1D, k2_schedule, plan_decomposition  # noqa: E402
 
 CFG = {  # BASELINE.json configs[2..4] (as scripts/run_config.py)
     3: dict(n=16, L=6.0, lam=1.0, nx=256, steps=60),
@@ -57,7 +57,7 @@ def sweep(cfg, ranks):
     for w in ranks:
         plan = plan_decomposition(nx, w)
         cnt = max(p[1] for p in plan) if isinstance(plan[0], (tuple, list)) else max(plan)
-        op.set_schedule("latency" if n <= 16 and cnt <= 256 else "throughput")
+        op.set_schedule(k2_schedule(n, cnt))
         s = Solver1D(op, x[:cnt], dx[:cnt], init, left=left, right=Boundary("extrap"), device=torch.device("cuda", 0))
         dt = s.cfl_dt()
         s.strang_step(dt)  # warm-up: workspace, kernel attributes
@@ -75,6 +75,7 @@ def sweep(cfg, ranks):
                           "ms_per_strang_step": round(ms, 4), "compute_speedup_bound": round(base / ms, 3),
                           "compute_efficiency_bound": round(base / ms / w, 3),
                           "halo_bytes_per_boundary_each_way_per_step": 4 * 2 * n ** 3 * 8 if w > 1 else 0,
+                          "k2_schedule": k2_schedule(n, cnt),
                           "mode": "CUDA graph of 3 Strang steps, one GPU, shard of rank 0's size"}), flush=True)
         del s
     op.close()

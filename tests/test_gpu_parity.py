@@ -270,9 +270,10 @@ def test_workspace_limit_chunks_bitwise(gpu, monkeypatch):
         assert op.memory_bytes()[1] < 64 << 20  # (table, workspace) bytes
 
 
+@pytest.mark.parametrize("sched", ["latency", "latency8"])
 @pytest.mark.parametrize("n,L", [(8, 5.0), (16, 6.0)])
-def test_latency_schedule_vs_oracle_and_batch_invariance(gpu, O, n, L):
-    """K2's latency schedule (rows split into 4 fixed segments on 4 warps,
+def test_latency_schedule_vs_oracle_and_batch_invariance(gpu, O, n, L, sched):
+    """K2's latency schedules (rows split into 4 or 8 fixed segments on 4 warps,
     ordered reduction): Q-hat within 1e-10 of the oracle; per-cell results
     bitwise independent of the batch (1 cell, 37 cells, 37 cells permuted);
     within round-off of the throughput schedule."""
@@ -283,7 +284,7 @@ def test_latency_schedule_vs_oracle_and_batch_invariance(gpu, O, n, L):
     with _op(n, L) as op:
         fh = op.forward(torch.from_numpy(f).to(gpu))
         q_thr = op.evaluate_qhat(fh).cpu().numpy()
-        op.set_schedule("latency")
+        op.set_schedule(sched)
         q_all = op.evaluate_qhat(fh).cpu().numpy()
         q_one = op.evaluate_qhat(fh[5:6].contiguous()).cpu().numpy()
         perm = torch.arange(36, -1, -1, device=gpu)
