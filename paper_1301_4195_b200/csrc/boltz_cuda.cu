@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <omp.h>
@@ -68,6 +69,51 @@ enum Kind : int { KIND_CONV = 0, KIND_FFT = 1, KIND_PROJECT = 2, KIND_LAYOUT = 3
 
 constexpr int kScheduleCell = 5;  // boltz_set_schedule: lane = output k3 (conv.cuh k_conv_cell), N <= 16
 
+// A host thread that lives as long as its context and runs one job at a time.
+// The bounce pipeline's feeder and drainer legs run on two of these instead of
+// on per-call std::threads: thread start-up leaves the timed call, and libgomp
+// keeps each leg's copy team (host_copy) alive from one call to the next.
+struct JobThread {
+    std::thread th;
+    std::mutex m;
+    std::condition_variable cv;
+    std::function<void()> job;
+    bool busy = false, stop = false;
+    void start(std::function<void()> f) {
+        std::unique_lock<std::mutex> lk(m);
+        if (!th.joinable()) th = std::thread([this] { loop(); });
+        job = std::move(f);
+        busy = true;
+        lk.unlock();
+        cv.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lk(m);
+        cv.wait(lk, [&] { return !busy; });
+    }
+    void loop() {
+        std::unique_lock<std::mutex> lk(m);
+        for (;;) {
+            cv.wait(lk, [&] { return busy || stop; });
+            if (stop) return;
+            std::function<void()> f = std::move(job);
+            lk.unlock();
+            f();  // the legs catch their own errors (PipeSync::fail)
+            lk.lock();
+            busy = false;
+            cv.notify_all();
+        }
+    }
+    ~JobThread() {
+        {
+            std::lock_guard<std::mutex> g(m);
+            stop = true;
+        }
+        cv.notify_all();
+        if (th.joinable()) th.join();
+    }
+};
+
 struct boltz_ctx {
     int n = 0;
     double L = 0, lambda = 0, beta = 0, r0 = 0;
@@ -109,6 +155,7 @@ struct boltz_ctx {
     double* hBounceMi[kMaxStageSlots] = {};
     static constexpr int kBounceBlocks = 16;  // D2H of a slot in up to 16 blocks, one event each
     cudaEvent_t ev_blk[kMaxStageSlots][kBounceBlocks] = {};
+    JobThread feeder_thread, drainer_thread;  // the bounce pipeline's two host legs
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
     cudaEvent_t ev_h2d[kMaxStageSlots] = {}, ev_comp[kMaxStageSlots] = {}, ev_d2h[kMaxStageSlots] = {};
     // second compute stream + workspace: odd host-pipeline chunks run beside even
@@ -1923,12 +1970,27 @@ int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, 
             ps.fail(e.msg);
         }
     };
-    std::thread tf(feeder), td;
+    static const bool persistent = !(std::getenv("BOLTZ_BOUNCE_PERSIST") && std::atoi(std::getenv("BOLTZ_BOUNCE_PERSIST")) == 0);
+    std::thread tf, td;
+    bool fed = false, drained = false;
+    auto join_legs = [&] {
+        if (persistent) {
+            if (fed) c->feeder_thread.wait();
+            if (drained) c->drainer_thread.wait();
+        } else {
+            if (tf.joinable()) tf.join();
+            if (td.joinable()) td.join();
+        }
+        fed = drained = false;
+    };
     try {
-        td = std::thread(drainer);
-    } catch (...) {  // the feeder is running: stop it before reporting
-        ps.fail("host pipeline: could not start the drainer thread");
-        tf.join();
+        if (persistent) c->feeder_thread.start(feeder); else tf = std::thread(feeder);
+        fed = true;
+        if (persistent) c->drainer_thread.start(drainer); else td = std::thread(drainer);
+        drained = true;
+    } catch (...) {  // a leg may be running: stop it before reporting
+        ps.fail("host pipeline: could not start a host thread");
+        join_legs();
         throw;
     }
     std::string err;
@@ -1959,8 +2021,7 @@ int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, 
         err = e.msg;
         ps.fail(e.msg);
     }
-    tf.join();
-    td.join();
+    join_legs();
     if (err.empty() && ps.abort) err = ps.err;
     if (!err.empty()) throw CudaError{err};
     if (two) {
