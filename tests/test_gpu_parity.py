@@ -639,6 +639,34 @@ def test_host_pipeline_mixed_pinned_pageable(gpu):
         assert np.array_equal(qout.numpy(), qd) and np.array_equal(mout.numpy(), mid)
 
 
+def test_bounce_threads_persist_across_calls_errors_and_contexts(gpu):
+    """The pageable bounce pipeline's feeder and drainer are two host threads
+    owned by the context (boltz_cuda.cu JobThread).  They must survive a
+    NumericError reported by a pipelined call, serve batches of different sizes, and not
+    be shared between two operators used alternately; every good call is
+    bitwise the device-memory call."""
+    import torch
+    n, L = 8, 5.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 2600, seed=99)
+    fd = torch.from_numpy(f).to(gpu)
+    with CollisionOperator.generated(grid, KernelSpec(1.0)) as a, CollisionOperator.generated(grid, KernelSpec(0.0)) as b:
+        qa = a.collide(fd).cpu().numpy()
+        qb = b.collide(fd).cpu().numpy()
+        for cells in (2600, 1100, 2048, 1025):
+            assert np.array_equal(a.collide(f[:cells].copy()), qa[:cells])   # pageable in and out
+            assert np.array_equal(b.collide(f[:cells].copy()), qb[:cells])
+        bad = f.copy()
+        bad[1500, 7] = np.nan                                  # lands in a middle chunk
+        with pytest.raises(NumericError):
+            a.collide(bad)
+        assert np.array_equal(a.collide(f.copy()), qa)          # the same threads serve the next call
+        g = f.copy()
+        a.collision_rk2(g, 0.01)
+        a.collision_rk2(fd, 0.01)
+        assert np.array_equal(g, fd.cpu().numpy())
+
+
 def test_joint_lpt_tail_ragged_batch(gpu, O):
     """N=16 at 4128 cells: 33 cell-group columns, so the mirror kernel's joint
     longest-first tail (conv.cuh lpt_unit, the last 4 columns) runs with a
