@@ -1101,12 +1101,14 @@ void copy_block(void* dst, const void* src, size_t bytes) {
 }
 
 // host copy spread over a few threads (one thread reaches ~15 GB/s; B200
-// box, cfg2 pageable e2e / pinned: 2 threads 0.81, 4 threads 0.90, 8 threads
-// 0.91, 12 threads 0.92, 16 threads 0.92 with streaming stores; 0.70 / 0.83 /
-// 0.81 at 2 / 4 / 8 threads with memcpy)
+// box, cfg2 pageable e2e / pinned with the persistent pipeline threads and
+// streaming stores: 4 threads 0.951, 6 0.946, 8 0.943, 12 0.944, 16 0.948 --
+// flat, so the default is the small team, which leaves the caller's cores
+// alone; with per-call threads it was 0.81 / 0.90 / 0.91 / 0.92 at 2 / 4 / 8 /
+// 12, and with memcpy instead of streaming stores 0.70 / 0.83 / 0.81 at 2 / 4 / 8)
 void host_copy(void* dst, const void* src, size_t bytes) {
     static const int threads = [] {
-        int t = std::min(12, omp_get_num_procs());
+        int t = std::min(6, omp_get_num_procs());
         if (const char* e = std::getenv("BOLTZ_COPY_THREADS")) t = std::max(1, std::atoi(e));
         return t;
     }();
