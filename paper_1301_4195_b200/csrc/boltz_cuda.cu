@@ -1985,6 +1985,17 @@ int run_host_bounced(boltz_ctx* c, const double* in, double* out, int in_elems, 
         }
         fed = drained = false;
     };
+    // any other unwinding (e.g. std::bad_alloc on the calling thread) must not
+    // leave a leg running on this frame's captures
+    struct LegGuard {
+        std::function<void()> f;
+        ~LegGuard() { f(); }
+    } leg_guard{[&] {
+        if (fed || drained) {
+            ps.fail("host pipeline unwound");
+            join_legs();
+        }
+    }};
     try {
         if (persistent) c->feeder_thread.start(feeder); else tf = std::thread(feeder);
         fed = true;
