@@ -604,6 +604,11 @@ def bench_cfg3(op, dev, rank, world, backend, steps=60):
                                       "total": 4 * 2 * 2 * (world - 1) * n3 * 8}
         parts = [None] * world if rank == 0 else None
         dist.gather_object((s.start, s.interior.cpu().numpy()), parts, dst=0)
+        # every rank tears the communicator down here, together and in order: the graph that holds the
+        # captured exchanges first, then ncclCommDestroy (which waits for such graphs, and for the peers)
+        s.release_graph()
+        if isinstance(halo, NcclHalo):
+            halo.close()
         if rank == 0:
             parts.sort(key=lambda p: p[0])
             sharded = np.concatenate([p[1] for p in parts])

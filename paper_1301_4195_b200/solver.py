@@ -374,6 +374,16 @@ class Solver1D:
             self.op.set_async(False)
         self.graph_replays = getattr(self, "graph_replays", 0) + steps // 3
 
+    def release_graph(self) -> None:
+        """Drop the captured graph (after the device has drained).  Call it on
+        every rank BEFORE closing an NcclHalo whose exchanges the graph holds:
+        NCCL keeps a communicator alive, and ncclCommDestroy waiting, while a
+        captured graph still references it."""
+        import torch
+        torch.cuda.synchronize(self.device)
+        self._graph = None
+        self._graph_dt = None
+
 
 def strang_step_loopback(solvers: Sequence[Solver1D], dt: float) -> None:
     """One Strang step of n virtual ranks in one process (LoopbackHalo)."""
