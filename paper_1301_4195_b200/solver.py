@@ -338,8 +338,10 @@ class Solver1D:
         self.capture(dt)
         self.advance(steps - 1)
 
-    def capture(self, dt: float) -> None:
-        """Capture three Strang steps of size dt into a CUDA graph (not executed)."""
+    def capture(self, dt: float, capture_error_mode: Optional[str] = None) -> None:
+        """Capture three Strang steps of size dt into a CUDA graph (not executed).
+        capture_error_mode: torch.cuda.graph's; default "global" on one rank,
+        "thread_local" on several."""
         import torch
         self.op.set_async(True)
         stream = torch.cuda.Stream(self.device)
@@ -347,9 +349,12 @@ class Solver1D:
         g = torch.cuda.CUDAGraph()
         ptrs = [t.data_ptr() for t in (self.field, self._tmp, self._tmp2)]
         t0 = self.t
+        # multi-rank: NCCL's own helper threads may make CUDA calls while this thread captures;
+        # thread-local capture mode keeps those from invalidating the capture
+        mode = capture_error_mode or ("thread_local" if self.world > 1 else "global")
         try:
             with torch.cuda.stream(stream):
-                with torch.cuda.graph(g, stream=stream):
+                with torch.cuda.graph(g, stream=stream, capture_error_mode=mode):
                     for _ in range(3):
                         self.strang_step(dt)
         finally:

@@ -275,6 +275,41 @@ def test_nccl_halo_graph_run_matches_eager(gpu):
         halo.close()
 
 
+def test_multirank_capture_mode_and_teardown_order(gpu):
+    """What bench.py's multi-rank cfg3 does around its graph, on one rank: the
+    Strang steps captured in torch's thread-local capture mode (the mode used
+    on several ranks, where NCCL's helper threads may call CUDA while this
+    thread captures) with the overlapped NCCL halo, replayed bitwise equal to
+    eager steps; then the teardown order -- release_graph() before
+    NcclHalo.close() -- after which the solver still steps eagerly."""
+    from paper_1301_4195_b200 import NcclHalo
+    n, L, nx = 8, 5.0, 14
+    grid = VelocityGrid.create(n, L)
+    x, dx = scenarios.geometric_grid(nx, 2.0, 1.1)
+    f0 = scenarios.mixture_cells(grid, nx, seed=47)
+    kw = dict(left=Boundary("wall", 2.0), right=Boundary("extrap"))
+    with _op(n, L) as op:
+        a = Solver1D(op, x, dx, f0, **kw)
+        dt = a.cfl_dt()
+        for _ in range(7):
+            a.strang_step(dt)
+        ref = a.interior.cpu().numpy()
+        halo = NcclHalo(0, 1, 0)
+        b = Solver1D(op, x, dx, f0, halo=halo, overlap_halo=True, **kw)
+        b.strang_step(dt)
+        b.capture(dt, capture_error_mode="thread_local")
+        b.advance(6)
+        assert getattr(b, "graph_replays", 0) == 2
+        assert np.array_equal(b.interior.cpu().numpy(), ref)
+        b.release_graph()
+        halo.close()
+        halo.close()                                   # idempotent
+        b.halo = None
+        b.strang_step(dt)
+        a.strang_step(dt)
+        assert np.array_equal(b.interior.cpu().numpy(), a.interior.cpu().numpy())
+
+
 @pytest.mark.parametrize("scheme", ["ssp_rk2", "single_stage"])
 def test_halo_overlap_bitwise(gpu, scheme):
     """SURVEY §8f rank 2, halo/compute overlap: with overlap_halo the NCCL
