@@ -217,6 +217,13 @@ int boltz_marginal_batch(boltz_ctx* ctx, const double* f, double* g, int64_t nce
  * reduction; small batches, N <= 16; other N keep the throughput schedule),
  * 5 = cell (lane = output k3, one CTA per (output row, cell), the cell's
  * f-hat in shared memory: one or a few cells, N <= 16; conv.cuh k_conv_cell).
+ * 6 = auto: chosen per call from the batch size at N <= 16 (<= 4 cells: cell;
+ * <= 64: latency with 8 segments; <= 256: latency with 4; else throughput) --
+ * for callers that, like the reference's strang_step, pass
+ * one or a few cells per call; a one-cell host-memory collide at N = 16 takes
+ * 99 us under it against 447 us under the throughput schedule.  With auto the
+ * summation order depends on the batch size, so results are reproducible per
+ * batch size only.
  * Under the throughput schedule collide / RK2 at N >= 8 use the Hermitian
  * mirror schedule (conv.cuh k_conv_mirror2, with TMEM accumulators, at
  * N = 8, 12, 16; the phased k_conv_kcsm + k_conv_kcsr at N = 24, 32; env

@@ -372,9 +372,11 @@ class CollisionOperator:
         """K2 schedule: "throughput" (default), "latency" (each row's entries in 4
         fixed segments on 4 warps: small batches, N <= 16), "latency8" (8
         segments: a few cells), "cell" (lane = output k3: one or a few cells,
-        N <= 16), or the ABI's integer 0..5.  Bitwise reproducible within a
-        schedule; schedules differ by round-off."""
-        code = {"throughput": 0, "latency": 1, "latency8": 2, "cell": 5}.get(schedule, schedule)
+        N <= 16), "auto" (picked per call from the batch size: cell up to 4
+        cells, latency8 up to 64, latency up to 256, else throughput), or the
+        ABI's integer 0..6.  Bitwise reproducible within a schedule; schedules
+        differ by round-off."""
+        code = {"throughput": 0, "latency": 1, "latency8": 2, "cell": 5, "auto": 6}.get(schedule, schedule)
         _check(lib().boltz_set_schedule(self._h, int(code)))
 
     # -- asynchronous mode (CUDA-graph capturable device calls)

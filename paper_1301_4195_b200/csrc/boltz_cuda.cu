@@ -68,6 +68,7 @@ using namespace boltz_gpu;
 enum Kind : int { KIND_CONV = 0, KIND_FFT = 1, KIND_PROJECT = 2, KIND_LAYOUT = 3, KIND_TRANSPORT = 4, kKinds = 5 };
 
 constexpr int kScheduleCell = 5;  // boltz_set_schedule: lane = output k3 (conv.cuh k_conv_cell), N <= 16
+constexpr int kScheduleAuto = 6;  // boltz_set_schedule: chosen per call from the batch size (effective_schedule)
 
 // A host thread that lives as long as its context and runs one job at a time.
 // The bounce pipeline's feeder and drainer legs run on two of these instead of
@@ -271,7 +272,25 @@ void release(boltz_ctx* c, void* p) {
     else cudaFree(p);
 }
 
+// The K2 schedule a batch of nc cells runs under.  kScheduleAuto picks it per
+// call (B200, host-memory collide, us per call at N = 16, throughput / 4
+// segments / 8 segments / cell: 1 cell 447 / 170 / 150 / 99, 4 cells 463 / 180 /
+// 161 / 134, 8 cells 464 / 198 / 176 / 185, 64 cells 579 / 359 / 360 / 633;
+// profiles/r2_small_host_calls.txt; 128 and 256 cells: solver.k2_schedule).
+// The reference calls its operator one cell at a time, so the
+// reference-typed shim runs under it.
+int effective_schedule(const boltz_ctx* c, int64_t nc);
+
 // marks the context's workspace as baked into a graph when `s` is capturing
+int effective_schedule(const boltz_ctx* c, int64_t nc) {
+    if (c->schedule != kScheduleAuto) return c->schedule;
+    if (c->n > 16) return 0;
+    if (nc <= 4) return kScheduleCell;
+    if (nc <= 64) return 2;
+    if (nc <= 256) return 1;
+    return 0;
+}
+
 void note_capture(boltz_ctx* c, cudaStream_t s) {
     cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) c->graph_captured = true;
@@ -1263,9 +1282,10 @@ struct Launch {
     // mirror schedule may run; evaluate_qhat of a caller's fhat never does
     static void conv(boltz_ctx* c, int64_t nc, cudaStream_t s, bool hermitian = false) {
         const int64_t ng = (nc + 31) / 32;
+        const int sched = effective_schedule(c, nc);
         if constexpr (conv_tile(N) == N && N <= 16) {
             // one or a few cells: lane = output k3 (conv.cuh k_conv_cell); one grid row per cell
-            if (c->schedule == kScheduleCell && nc <= 65535) {
+            if (sched == kScheduleCell && nc <= 65535) {
                 using CL = CellLayout<N>;
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
@@ -1283,7 +1303,7 @@ struct Launch {
             }
         }
         if constexpr (mirror_kcs_n(N)) {
-            if (hermitian && c->mirror && c->schedule == 0) {
+            if (hermitian && c->mirror && sched == 0) {
                 constexpr int NK = N / conv_tile(N), KC1 = NK > 1 ? 1 : 0;
                 // 8-warp CTAs at N = 24 (kcsm_warps) unless the batch has at most kConvWarps
                 // groups: then kConvWarps-warp CTAs, so no CTA carries idle warps' shared memory
@@ -1376,7 +1396,7 @@ struct Launch {
             }
         }
         if constexpr (mirror_pipe_n(N) && N % 4 == 0) {
-            if (hermitian && c->mirror && c->mirror2 && c->schedule == 0) {
+            if (hermitian && c->mirror && c->mirror2 && sched == 0) {
                 const int smem = Mirror2Layout<N>::CTA_BYTES;
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
@@ -1394,7 +1414,7 @@ struct Launch {
             }
         }
         if constexpr (mirror_pipe_n(N)) {
-            if (hermitian && c->mirror && c->schedule == 0) {
+            if (hermitian && c->mirror && sched == 0) {
                 const int smem = kConvWarps * MirrorLayout<N>::WARP_BYTES;
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
@@ -1413,17 +1433,17 @@ struct Launch {
         }
         if constexpr (conv_kernel_for(N) == 1 && conv_tile(N) == N &&
                       kConvWarps * PipeLayout<N>::WARP_BYTES <= 220 * 1024) {
-            if (c->schedule > 0 && c->schedule < kScheduleCell) {
-                const int S = kConvWarps * c->schedule;  // segments per row
+            if (sched > 0 && sched < kScheduleCell) {
+                const int S = kConvWarps * sched;  // segments per row
                 const int smem = kConvWarps * PipeLayout<N>::WARP_BYTES;
                 static PerDevice configured;  // attributes are per device
                 configured.once(c->device, [&] {
                     CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
                     CK(cudaFuncSetAttribute(k_conv_seg<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
                 });
-                ensure_seg(c, ng * kLanes * c->schedule);
+                ensure_seg(c, ng * kLanes * sched);
                 Timed t_(c, KIND_CONV, s);
-                k_conv_seg<N><<<dim3(N * N, (unsigned)ng, (unsigned)c->schedule), kLanes * kConvWarps, smem, s>>>(
+                k_conv_seg<N><<<dim3(N * N, (unsigned)ng, (unsigned)sched), kLanes * kConvWarps, smem, s>>>(
                     c->dA, c->dSeg, c->dH, c->dEnt, c->dRowStart, (int)ng, S);
                 const long long total = ng * N3 * kLanes;
                 k_conv_seg_reduce<N><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(c->dSeg, c->dB, ng, S);
@@ -2526,6 +2546,7 @@ int boltz_marginal_batch(boltz_ctx* c, const double* f, double* g, int64_t ncell
 
 const char* boltz_conv_kernel(const boltz_ctx* c) {
     if (!c) return "";
+    if (c->schedule == kScheduleAuto && c->n <= 16) return "auto: k_conv_cell / k_conv_seg / mirror by batch size";
     if (c->schedule == kScheduleCell && c->n <= 16) return "k_conv_cell + k_cell_gather";
     if (c->schedule > 0 && c->schedule < kScheduleCell && c->n <= 16) return "k_conv_seg + k_conv_seg_reduce";
     if (c->mirror) {
@@ -2544,8 +2565,8 @@ int boltz_schedule_terms(boltz_ctx* c, int64_t* plain, int64_t* mirror) {
 }
 
 int boltz_set_schedule(boltz_ctx* c, int schedule) {
-    if (!c || schedule < 0 || schedule > kScheduleCell) {
-        set_error("set_schedule: 0 (throughput), 1..4 (latency: 4 x schedule segments per row) or 5 (cell)");
+    if (!c || schedule < 0 || schedule > kScheduleAuto) {
+        set_error("set_schedule: 0 (throughput), 1..4 (latency: 4 x schedule segments per row), 5 (cell) or 6 (auto)");
         return BOLTZ_ERR_CONFIG;
     }
     c->schedule = schedule;

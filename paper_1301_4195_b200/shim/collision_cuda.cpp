@@ -32,11 +32,14 @@ CollisionGpu::CollisionGpu(const VelocityGrid& grid, const GpuKernelSpec& k, std
     if (G.size() != n3 * n3) throw ConfigError("CollisionGpu: weight table must hold N^6 values");
     gpu_check(boltz_create(grid.n, grid.half_width, k.lambda, k.beta, r0_of(grid, k), G.data(), device, &ctx_),
               "CollisionGpu");
+    // the reference passes one cell per call: K2 schedule by batch size
+    gpu_check(boltz_set_schedule(ctx_, 6), "CollisionGpu");
 }
 
 CollisionGpu::CollisionGpu(const VelocityGrid& grid, const GpuKernelSpec& k, int device) : grid_(grid) {
     gpu_check(boltz_create_generated(grid.n, grid.half_width, k.lambda, k.beta, r0_of(grid, k), 64, device, &ctx_),
               "CollisionGpu");
+    gpu_check(boltz_set_schedule(ctx_, 6), "CollisionGpu");
 }
 
 CollisionGpu::~CollisionGpu() { boltz_destroy(ctx_); }

@@ -667,6 +667,41 @@ def test_bounce_threads_persist_across_calls_errors_and_contexts(gpu):
         assert np.array_equal(g, fd.cpu().numpy())
 
 
+def test_auto_schedule_picks_by_batch_size(gpu, O):
+    """boltz_set_schedule(6) / set_schedule("auto"): the K2 schedule is picked per
+    call from the batch size (N <= 16: cell up to 4 cells, latency8 up to 64,
+    latency up to 256, else the throughput / mirror schedule), which is what
+    the reference-typed shim runs under, since the reference passes one cell
+    per call.  Each batch size is bitwise the explicit
+    schedule's result, host and device memory, and one cell matches the oracle."""
+    import torch
+    n, L = 16, 6.0
+    grid = VelocityGrid.create(n, L)
+    f = scenarios.mixture_cells(grid, 300, seed=61)
+    G = table(n, L, 1.0)
+    with _op(n, L) as op:
+        for cells, explicit in ((1, "cell"), (4, "cell"), (5, "latency8"), (64, "latency8"), (65, "latency"),
+                                (256, "latency"), (257, "throughput")):
+            fd = torch.from_numpy(f[:cells]).to(gpu)
+            op.set_schedule(explicit)
+            ref = op.collide(fd).cpu().numpy()
+            op.set_schedule("auto")
+            assert np.array_equal(op.collide(fd).cpu().numpy(), ref), (cells, explicit)
+            assert np.array_equal(op.collide(f[:cells].copy()), ref), (cells, explicit)   # host memory
+        q1 = op.collide(f[:1].copy())
+        ref1, _ = O.collide(n, L, G, f[0], 1.0, nthreads=8)
+        assert rel_max(q1[0], ref1) < TOL_Q
+        g = f[:1].copy()
+        op.collision_rk2(g, 0.01)
+        assert rel_max(g[0], O.collision_rk2(n, L, G, f[:1], 0.01, 1.0, nthreads=8)[0]) < 1e-12
+        op.set_schedule("throughput")
+    with _op(24, 8.0) as op24:                      # N > 16: auto is the throughput schedule
+        f24 = scenarios.mixture_cells(VelocityGrid.create(24, 8.0), 3, seed=62)
+        ref = op24.collide(f24.copy())
+        op24.set_schedule("auto")
+        assert np.array_equal(op24.collide(f24.copy()), ref)
+
+
 def test_joint_lpt_tail_ragged_batch(gpu, O):
     """N=16 at 4128 cells: 33 cell-group columns, so the mirror kernel's joint
     longest-first tail (conv.cuh lpt_unit, the last 4 columns) runs with a
