@@ -1810,6 +1810,10 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
     bool bounce_in = is_pageable(in), bounce_out = is_pageable(out) || (max_imag && is_pageable(max_imag));
     if (const char* e = std::getenv("BOLTZ_BOUNCE"))
         if (std::atoi(e) == 0) bounce_in = bounce_out = false;
+    // a few cells (<= 512 KiB each way): the driver's own staging of small pageable copies is as fast as
+    // the ring and needs no thread hand-offs (N=16, 16 cells: 202 against 227 us per collide; 64 cells:
+    // 470 against 375, so the ring from there on; profiles/r2_small_bounce_ab.txt)
+    if ((size_t)ncells * (size_t)std::max(in_elems, out_elems) * 8 <= (512u << 10)) bounce_in = bounce_out = false;
     if (bounce_in || bounce_out) {
         ensure_bounce(c, chunk);
         return run_host_bounced(c, in, out, in_elems, out_elems, s, max_imag, fn, bounds, two, bounce_in,
