@@ -1820,6 +1820,15 @@ int run_host_pipelined(boltz_ctx* c, const double* in, double* out, int64_t ncel
                                 bounce_out);
     }
     CK(cudaMemsetAsync(c->dFlag, 0, sizeof(int), s));
+    if (nchunks == 1) {
+        // one chunk has nothing to overlap: copy in, compute and copy out on the caller's stream, with no
+        // cross-stream events (a one-cell call is a handful of launches; each hand-off costs microseconds)
+        CK(cudaMemcpyAsync(c->dStageIn[0], in, (size_t)ncells * in_elems * 8, cudaMemcpyHostToDevice, s));
+        fn(c->dStageIn[0], c->dStageOut[0], ncells, s);
+        if (max_imag) CK(cudaMemcpyAsync(max_imag, c->dMaxIm, (size_t)ncells * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(out, c->dStageOut[0], (size_t)ncells * out_elems * 8, cudaMemcpyDeviceToHost, s));
+        return check_flag(c, s);
+    }
     if (two) {
         CK(cudaEventRecord(c->ev_fork, s));
         CK(cudaStreamWaitEvent(c->comp2, c->ev_fork, 0));
