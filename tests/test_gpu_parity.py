@@ -694,6 +694,13 @@ def test_auto_schedule_picks_by_batch_size(gpu, O):
         g = f[:1].copy()
         op.collision_rk2(g, 0.01)
         assert rel_max(g[0], O.collision_rk2(n, L, G, f[:1], 0.01, 1.0, nthreads=8)[0]) < 1e-12
+        # a chunked host call under auto: its small chunks run segmented, the large ones mirrored,
+        # on the two workspace sets of the host pipeline
+        f4 = scenarios.mixture_cells(grid, 1300, seed=63)
+        q4 = op.collide(f4.copy())
+        for c in (0, 255, 300, 1299):
+            ref, _ = O.collide(n, L, G, f4[c], 1.0, nthreads=8)
+            assert rel_max(q4[c], ref) < TOL_Q, c
         op.set_schedule("throughput")
     with _op(24, 8.0) as op24:                      # N > 16: auto is the throughput schedule
         f24 = scenarios.mixture_cells(VelocityGrid.create(24, 8.0), 3, seed=62)
